@@ -1,0 +1,179 @@
+/*
+ * qlrt_b200.h -- C ABI of the B200-native NF4 / double-quant / QLoRA-linear
+ * hot path.  Every entry point takes DEVICE pointers, element counts and a
+ * cudaStream_t (passed as void*), never allocates (callers own all buffers,
+ * including the documented workspaces) and returns a qlrt_status.  Launches
+ * are stream-ordered and reentrant; there is no global mutable state.
+ *
+ * Each function cites the reference (qlrt 0.1.0, /root/reference/pkg/src/qlrt)
+ * interface it replaces.  The Python host mirror binds these with ctypes
+ * (paper_2305_14314_b200/_native.py); INTEGRATION.md shows the binding.
+ */
+#ifndef QLRT_B200_H
+#define QLRT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QLRT_OK = 0,
+  QLRT_ERR_ARG = 1,        /* ValueError in the reference                         */
+  QLRT_ERR_CUDA = 2,       /* launch / runtime failure                            */
+  QLRT_ERR_UNSUPPORTED = 3 /* shape/layout outside what the kernel was built for  */
+} qlrt_status;
+
+typedef enum { QLRT_F32 = 0, QLRT_BF16 = 1, QLRT_F64 = 2 } qlrt_dtype;
+
+/* A 4-bit codebook as the kernels consume it (codebooks.py:125-176).
+ * values: the 16-entry decode table (spares duplicate 0.0);
+ * mids: the n_mids = n_emitted-1 fp64 decision boundaries;
+ * lo/hi: fp32 brackets around each midpoint -- outside [lo,hi] the fp32 fast
+ * path decides the code, inside it the kernel re-decides in fp64;
+ * pad_code: code of padding and of all-zero blocks (blockquant.py:173-179). */
+typedef struct {
+  double values[16];
+  double mids[15];
+  float lo[16];
+  float hi[16];
+  int n_mids;
+  int pad_code;
+} qlrt_codebook4;
+
+/* 8-bit float layout of the double quantizer (doublequant.py:33-51). */
+typedef struct {
+  int exp_bits;
+  int mant_bits;
+  int bias;
+} qlrt_fp8spec;
+
+/* ---- quantization (blockquant.py:132-195, doublequant.py:148-187) ------- */
+
+/* Phase A of quantize(): per-block float32 absmax, nearest codes (ties away
+ * from zero, fp64-exact), 2-codes-per-byte packing, padding/zero blocks ->
+ * pad_code, first non-finite flat index (INT64_MAX if none).
+ * x: n elements of x_dtype (F32, BF16 or F64 -- the reference's own dtype).  codes: ceil(nb*blocksize/2) bytes.
+ * absmax: nb floats.  first_bad: one int64 on the device. */
+qlrt_status qlrt_quantize4(const void* x, int x_dtype, int64_t n, int blocksize,
+                           const qlrt_codebook4* cb, uint8_t* codes, float* absmax,
+                           int64_t* first_bad, void* stream);
+
+/* Bytes of scratch qlrt_dq_compress needs for nb constants. */
+size_t qlrt_dq_workspace_bytes(int64_t nb);
+
+/* dq_compress(): mu = f32(numpy-order mean), per-blocksize2 fp64 absmax,
+ * c1 = f32(A/max), codes = nearest 8-bit float (ties away, clamp). */
+qlrt_status qlrt_dq_compress(const float* absmax, int64_t nb, int blocksize2,
+                             qlrt_fp8spec spec, void* workspace, float* mu, float* c1,
+                             uint8_t* dq_codes, void* stream);
+
+/* dq_decompress() (doublequant.py:190-195): nb float32 constants. */
+qlrt_status qlrt_dq_decompress(const uint8_t* dq_codes, const float* c1, const float* mu,
+                               int64_t nb, int blocksize2, qlrt_fp8spec spec, float* out,
+                               void* stream);
+
+/* dequantize() (blockquant.py:198-213): out[i] = f32(values[code_i] * f64(c_b)),
+ * written as F64 (the reference's float64, bit-exact), F32 or BF16 (bf16 of the f32).  Either absmax (plain constants)
+ * or (dq_codes, c1, mu) must be given (4-bit codes cannot leave the table). */
+qlrt_status qlrt_dequantize4(const uint8_t* codes, int64_t n, int blocksize,
+                             const qlrt_codebook4* cb, const float* absmax,
+                             const uint8_t* dq_codes, const float* c1, const float* mu,
+                             int blocksize2, qlrt_fp8spec spec, void* out, int out_dtype,
+                             void* stream);
+
+/* encode_fp8 / decode_fp8 (doublequant.py:103-121) on arbitrary fp64 values. */
+qlrt_status qlrt_fp8_encode(const double* x, int64_t n, qlrt_fp8spec spec, uint8_t* out, void* stream);
+qlrt_status qlrt_fp8_decode(const uint8_t* codes, int64_t n, qlrt_fp8spec spec, double* out, void* stream);
+
+/* pack_codes / unpack_codes (blockquant.py:81-115) for k = 4. */
+qlrt_status qlrt_pack4(const uint8_t* codes, int64_t count, uint8_t* packed, void* stream);
+qlrt_status qlrt_unpack4(const uint8_t* packed, int64_t count, uint8_t* codes, void* stream);
+
+/* ---- frozen NF4 linear with LoRA (qlora.py:117-167) ---------------------- */
+
+/* The quantized base W[K_in, N_out] (row-major, blocks of 64 along N_out,
+ * qlora.py:110-115) in the form the fused kernels read. */
+typedef struct {
+  const uint8_t* codes;    /* K_in*N_out/2 bytes                         */
+  const uint8_t* dq_codes; /* K_in*N_out/64 bytes                        */
+  const float* c1;         /* ceil(nb/blocksize2) floats                 */
+  const float* mu;         /* 1 float (device)                           */
+  int64_t k_in, n_out;
+  int blocksize2;
+  qlrt_fp8spec spec;
+  double values[16];       /* codebook decode table                      */
+} qlrt_nf4_weight;
+
+/* Workspace bytes for the linear entry points (split-K partial sums). */
+size_t qlrt_linear_workspace_bytes(int64_t m, int64_t k_in, int64_t n_out, int rank);
+
+/* forward (qlora.py:124-148):
+ *   Ts = s * Xa l1 as a bf16 hi/lo pair [M, 2r] (Ts[:, :r] + Ts[:, r:]; kept for backward)
+ *   Y  = X W + Ts_hi l2                 [M, N]   bf16 out, fp32 accumulate
+ * X bf16 [M,K]; Xa = the adapter input (X with the dropout mask applied,
+ * qlora.py:137-143; NULL -> X); l1 bf16 [K,r], l2 bf16 [r,N]; rank % 8 == 0
+ * (callers zero-pad), rank == 0 -> no adapter.  N % 64 == 0, K % 8 == 0. */
+qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const void* xa,
+                                int64_t m, const void* l1, const void* l2, int rank, float s,
+                                void* ts_out, void* y, void* workspace, void* stream);
+
+/* backward (qlora.py:150-167):
+ *   dT  = s * dY l2^T as a bf16 hi/lo pair [M, 2r]
+ *   dX  = dY W^T + dT_hi l1^T           [M, K]  bf16
+ *   dl2 = (Ts_hi + Ts_lo)^T dY          [r, N]  fp32   (= s T^T dY)
+ *   dl1 = Xa^T (dT_hi + dT_lo)          [K, r]  fp32   (= s Xa^T dY l2^T)
+ * The hi/lo pairs keep the adapter gradients at ~16-bit operand precision.
+ * (x is the adapter input Xa; with dropout the caller masks the adapter part
+ * of dX itself and passes rank = 0 semantics through qlrt_gemm_bf16.) */
+qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_t m,
+                                const void* x, const void* ts, const void* l1,
+                                const void* l2, int rank, float s, void* dt_out, void* dx,
+                                float* dl1, float* dl2, void* workspace, void* stream);
+
+/* batch-1 GEMV variant of forward (M = 1), HBM-bound on the packed codes:
+ *   y[N] = x[K] W + s (x l1) l2          fp32 accumulate, bf16 out. */
+qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* l1,
+                          const void* l2, int rank, float s, void* y, void* workspace,
+                          void* stream);
+
+/* Plain bf16 GEMM on the same tcgen05 engine (test + building block):
+ * D[M,N] = alpha * A[M,K] B[K,N]; a_mn/b_mn select MN-major storage
+ * (A stored [K,M] / B stored [K,N]) vs K-major (A [M,K] / B [N,K]).
+ * out_f32 selects fp32 vs bf16 output, out_t stores D^T ([N,M]). */
+qlrt_status qlrt_gemm_bf16(const void* a, const void* b, void* d, int64_t m, int64_t n,
+                           int64_t k, int a_mn, int b_mn, float alpha, int out_f32,
+                           int out_t, void* workspace, size_t workspace_bytes,
+                           void* stream);
+
+/* ---- optimizer (training.py:398-442) ------------------------------------ */
+
+/* Bit-exact fp32 Adam (training.py:434-440 op order); also refreshes the
+ * bf16 shadow copy used by the GEMMs when p_bf16 != NULL.  The constants are
+ * the float32-rounded values numpy 2 uses (b1, 1-b1, b2, 1-b2, bc1, bc2,
+ * eps, lr). */
+qlrt_status qlrt_adam_step(float* p, const float* g, float* m, float* v, int64_t n,
+                           float b1, float omb1, float b2, float omb2, float bc1,
+                           float bc2, float eps, float lr, void* p_bf16, void* stream);
+
+/* sum of squares in fp64 of n floats, accumulated into acc[0] (device).
+ * acc must have QLRT_SUMSQ_SCRATCH bytes: acc[0] result, then scratch. */
+#define QLRT_SUMSQ_SCRATCH (8 + 8 * 296 + 8)
+qlrt_status qlrt_sumsq_f64(const float* g, int64_t n, double* acc, void* stream);
+
+/* g *= scale (float32), for clip_global_norm. */
+qlrt_status qlrt_scale_f32(float* g, int64_t n, float scale, void* stream);
+
+/* Paged optimizer state: advise + prefetch a managed range to a device
+ * (device >= 0) or to the host (device < 0) on the given stream. */
+qlrt_status qlrt_prefetch(void* ptr, size_t bytes, int device, void* stream);
+
+/* Library identification: returns the compiled arch string ("sm_100a"). */
+const char* qlrt_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QLRT_B200_H */

@@ -1,0 +1,109 @@
+"""ctypes binding of the C ABI in ``include/qlrt_b200.h``.
+
+The CUDA library ``_lib/libqlrt_b200.so`` is built in-tree for sm_100a by
+``tools/build_lib.sh`` (``__graft_entry__.build()``).  There is no CPU
+fallback: every product entry point goes through this module and raises
+``RuntimeError`` when the library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_double, c_float, c_int, c_int64, c_size_t, c_uint8, c_void_p
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libqlrt_b200.so")
+
+QLRT_OK, QLRT_ERR_ARG, QLRT_ERR_CUDA, QLRT_ERR_UNSUPPORTED = 0, 1, 2, 3
+F32, BF16, F64 = 0, 1, 2
+SUMSQ_SCRATCH = 8 + 8 * 296 + 8
+
+
+class Codebook4(ctypes.Structure):
+    _fields_ = [("values", c_double * 16), ("mids", c_double * 15), ("lo", c_float * 16),
+                ("hi", c_float * 16), ("n_mids", c_int), ("pad_code", c_int)]
+
+
+class Fp8SpecC(ctypes.Structure):
+    _fields_ = [("exp_bits", c_int), ("mant_bits", c_int), ("bias", c_int)]
+
+
+class NF4Weight(ctypes.Structure):
+    _fields_ = [("codes", c_void_p), ("dq_codes", c_void_p), ("c1", c_void_p), ("mu", c_void_p),
+                ("k_in", c_int64), ("n_out", c_int64), ("blocksize2", c_int),
+                ("spec", Fp8SpecC), ("values", c_double * 16)]
+
+
+_SIGS = {
+    "qlrt_quantize4": [c_void_p, c_int, c_int64, c_int, POINTER(Codebook4), c_void_p, c_void_p, c_void_p, c_void_p],
+    "qlrt_dq_workspace_bytes": [c_int64],
+    "qlrt_dq_compress": [c_void_p, c_int64, c_int, Fp8SpecC, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    "qlrt_dq_decompress": [c_void_p, c_void_p, c_void_p, c_int64, c_int, Fp8SpecC, c_void_p, c_void_p],
+    "qlrt_dequantize4": [c_void_p, c_int64, c_int, POINTER(Codebook4), c_void_p, c_void_p, c_void_p, c_void_p,
+                         c_int, Fp8SpecC, c_void_p, c_int, c_void_p],
+    "qlrt_fp8_encode": [c_void_p, c_int64, Fp8SpecC, c_void_p, c_void_p],
+    "qlrt_fp8_decode": [c_void_p, c_int64, Fp8SpecC, c_void_p, c_void_p],
+    "qlrt_pack4": [c_void_p, c_int64, c_void_p, c_void_p],
+    "qlrt_unpack4": [c_void_p, c_int64, c_void_p, c_void_p],
+    "qlrt_linear_workspace_bytes": [c_int64, c_int64, c_int64, c_int],
+    "qlrt_nf4_linear_fwd": [POINTER(NF4Weight), c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int, c_float,
+                            c_void_p, c_void_p, c_void_p, c_void_p],
+    "qlrt_nf4_linear_bwd": [POINTER(NF4Weight), c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                            c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    "qlrt_nf4_gemv": [POINTER(NF4Weight), c_void_p, c_void_p, c_void_p, c_int, c_float, c_void_p, c_void_p, c_void_p],
+    "qlrt_gemm_bf16": [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_int, c_float, c_int, c_int,
+                       c_void_p, c_size_t, c_void_p],
+    "qlrt_adam_step": [c_void_p, c_void_p, c_void_p, c_void_p, c_int64] + [c_float] * 8 + [c_void_p, c_void_p],
+    "qlrt_sumsq_f64": [c_void_p, c_int64, c_void_p, c_void_p],
+    "qlrt_scale_f32": [c_void_p, c_int64, c_float, c_void_p],
+    "qlrt_prefetch": [c_void_p, c_size_t, c_int, c_void_p],
+    "qlrt_build_info": [],
+}
+_RESTYPE = {"qlrt_dq_workspace_bytes": c_size_t, "qlrt_linear_workspace_bytes": c_size_t,
+            "qlrt_build_info": ctypes.c_char_p}
+
+EXPORTS = tuple(_SIGS)
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load (once) and type the C ABI.  Raises if the .so is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise RuntimeError(f"qlrt_b200 CUDA library not built: {path} (run __graft_entry__.build())")
+        lib = ctypes.CDLL(path)
+        for name, args in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPE.get(name, c_int)
+        _lib = lib
+    return _lib
+
+
+def lib() -> ctypes.CDLL:
+    """The library, for a call that will launch kernels: also requires CUDA."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("qlrt_b200 requires a CUDA (sm_100a) device; there is no CPU fallback")
+    return load_library()
+
+
+def stream_ptr(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def check(status: int, what: str) -> None:
+    if status == QLRT_OK:
+        return
+    names = {QLRT_ERR_ARG: "invalid argument", QLRT_ERR_CUDA: "CUDA error",
+             QLRT_ERR_UNSUPPORTED: "unsupported shape/layout"}
+    if status == QLRT_ERR_ARG:
+        raise ValueError(f"{what}: {names[status]}")
+    raise RuntimeError(f"{what}: {names.get(status, status)}")

@@ -1,0 +1,804 @@
+// tcgen05 / TMEM / TMA GEMM engine for sm_100a with an in-kernel NF4
+// double-dequant producer -- the frozen 4-bit linear of QLoRA
+// (reference: QLinear.forward / backward, pkg/src/qlrt/qlora.py:117-167).
+//
+//   D[M, N] (fp32 in TMEM) = sum_k A[M, k] B[k, N]  (+ an optional second,
+//   "augmented" K segment A2 B2 -- the LoRA term folded into the same
+//   accumulator: Y^T = W^T X^T + l2^T (sT)^T, dX^T = W dY^T + l1 dT^T).
+//
+// One CTA per SM, persistent over 128 x BN output tiles.  Warp roles:
+//   warp 0      TMA producer (B tiles; A tiles when A is a bf16 tensor)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5   epilogue: tcgen05.ld -> registers -> global (fp32/bf16,
+//               row-major or transposed), double-buffered TMEM accumulators
+//   warps 6-13  (NF4 only) dequant producer: packed codes + DQ constants from
+//               global -> per-block 16-entry bf16 table -> prmt lookups ->
+//               128B-swizzled UMMA tile in shared memory
+// The W tile is always the A operand (M = 128 W rows/cols), so each
+// dequantized weight feeds BN = 256 token columns of MMA.
+#include "qlrt_common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace qlrt {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;              // one 128B swizzle row of bf16
+constexpr int A_STAGE = BM * BK * 2;  // 16 KB
+constexpr int kTmaWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2, kNumEpiWarps = 4, kXfWarp0 = 6;
+constexpr int kNumXfWarps = 8;
+
+struct Args {
+  int M, N;             // output extent (UMMA M rows, N cols)
+  int k_iters;          // main segment K / 64
+  int k_iters_aug;      // augmented segment K / 64 (0 = none)
+  int splits;           // split-K over the main segment (>1 -> fp32 partials)
+  int a_mn, b_mn;       // main segment operand majorness (A ignored for NF4)
+  int a2_mn, b2_mn;     // augmented segment majorness
+  // NF4 A source (nf4_mode 1: A = W^T (fwd), 2: A = W (bwd))
+  int nf4_mode;
+  const uint8_t* codes;
+  const uint8_t* dq_codes;
+  const float* c1;
+  const float* mu;
+  const float* absmax;  // plain constants if dq_codes == nullptr
+  int64_t w_rows, w_cols;
+  int bs2;
+  qlrt_fp8spec spec;
+  double values[16];
+  // output
+  void* out;
+  int64_t ldo;
+  int out_f32, out_t;
+  float alpha;
+  float* ws;            // split-K partials [splits][M][N]
+  int to_ws;            // force fp32 partials to ws (finished by the reduce kernel)
+  int out_split;        // bf16 out: also store lo = bf16(v - hi) at column offset out_split
+  int fold;             // reduce: out[:, n] = D[:, n] + D[:, n + fold] for n < fold
+};
+
+template <int BN>
+struct Smem {
+  static constexpr int B_STAGE = BN * BK * 2;
+  static constexpr int STAGE = A_STAGE + B_STAGE;
+  static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);  // even: a stage is always refilled by the same dequant group
+  static constexpr int BAR_OFF = STAGES * STAGE;
+  // full[S], afull[S], empty[S], tmem_full[2], tmem_empty[2], tmem_ptr
+  static constexpr int BYTES = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
+};
+
+__device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int& mt, int& nt, int& z) {
+  const int per = m_tiles * n_tiles;
+  z = t / per;
+  const int r = t - z * per;
+  mt = r / n_tiles;
+  nt = r - mt * n_tiles;
+}
+
+// ---------------------------------------------------------------------------
+// NF4 -> bf16 tile producer helpers
+// ---------------------------------------------------------------------------
+// 16-entry table bf16(f32(v_i * c)) split into lo/hi byte planes (4 regs each)
+__device__ __forceinline__ void build_planes(const double* vals, float c, uint32_t (&L)[4],
+                                             uint32_t (&H)[4]) {
+  const double cd = (double)c;
+  uint32_t P[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float a = __double2float_rn(__dmul_rn(vals[2 * j], cd));
+    float b = __double2float_rn(__dmul_rn(vals[2 * j + 1], cd));
+    P[j] = pack_bf16x2(a, b);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    L[q] = ptx::prmt(P[2 * q], P[2 * q + 1], 0x6420);
+    H[q] = ptx::prmt(P[2 * q], P[2 * q + 1], 0x7531);
+  }
+}
+
+// 4 codes (nibbles of the low 16 bits of w) -> 4 bf16 packed in 2 words
+__device__ __forceinline__ void lookup4(uint32_t w, const uint32_t (&L)[4], const uint32_t (&H)[4],
+                                        uint32_t& o0, uint32_t& o1) {
+  const uint32_t sel = w & 0x7777u;
+  const uint32_t bsel = ((w >> 1) & 0x4444u) | 0x3210u;
+  const uint32_t lo = ptx::prmt(ptx::prmt(L[0], L[1], sel), ptx::prmt(L[2], L[3], sel), bsel);
+  const uint32_t hi = ptx::prmt(ptx::prmt(H[0], H[1], sel), ptx::prmt(H[2], H[3], sel), bsel);
+  o0 = ptx::prmt(lo, hi, 0x5140);
+  o1 = ptx::prmt(lo, hi, 0x7362);
+}
+
+// one accumulator row segment of EC fp32 values -> global
+template <int EC>
+__device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[EC], int64_t m, int64_t n0, int z) {
+  const bool full_chunk = n0 + EC <= p.N;
+  if (p.splits > 1 || p.to_ws) {
+    float* dst = p.ws + ((int64_t)z * p.M + m) * p.N + n0;
+    if (full_chunk && (p.N & 3) == 0) {
+#pragma unroll
+      for (int j = 0; j < EC; j += 4)
+        *reinterpret_cast<float4*>(dst + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                          __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+    } else {
+      for (int j = 0; j < EC && n0 + j < p.N; ++j) dst[j] = __uint_as_float(r[j]);
+    }
+    return;
+  }
+  const float a = p.alpha;
+  if (p.out_t) {  // D^T: out[n][m]; lanes are consecutive m -> coalesced per column
+    if (p.out_f32) {
+      float* o = static_cast<float*>(p.out);
+#pragma unroll
+      for (int j = 0; j < EC; ++j)
+        if (n0 + j < p.N) o[(n0 + j) * p.ldo + m] = __uint_as_float(r[j]) * a;
+    } else {
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out);
+#pragma unroll
+      for (int j = 0; j < EC; ++j)
+        if (n0 + j < p.N) o[(n0 + j) * p.ldo + m] = __float2bfloat16_rn(__uint_as_float(r[j]) * a);
+    }
+    return;
+  }
+  if (p.out_f32) {
+    float* o = static_cast<float*>(p.out) + m * p.ldo + n0;
+    if (full_chunk && (p.ldo & 3) == 0) {
+#pragma unroll
+      for (int j = 0; j < EC; j += 4)
+        *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(r[j]) * a, __uint_as_float(r[j + 1]) * a,
+                                                        __uint_as_float(r[j + 2]) * a, __uint_as_float(r[j + 3]) * a);
+    } else {
+      for (int j = 0; j < EC && n0 + j < p.N; ++j) o[j] = __uint_as_float(r[j]) * a;
+    }
+  } else if (p.out_split) {  // bf16 hi/lo pair: v ~= hi + lo to ~16 mantissa bits
+    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + m * p.ldo + n0;
+    for (int j = 0; j < EC && n0 + j < p.N; ++j) {
+      const float v = __uint_as_float(r[j]) * a;
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      o[j] = hi;
+      o[j + p.out_split] = __float2bfloat16_rn(v - __bfloat162float(hi));
+    }
+  } else {
+    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + m * p.ldo + n0;
+    if (full_chunk && (p.ldo & 7) == 0) {
+#pragma unroll
+      for (int j = 0; j < EC; j += 8)
+        *reinterpret_cast<uint4*>(o + j) =
+            make_uint4(pack_bf16x2(__uint_as_float(r[j]) * a, __uint_as_float(r[j + 1]) * a),
+                       pack_bf16x2(__uint_as_float(r[j + 2]) * a, __uint_as_float(r[j + 3]) * a),
+                       pack_bf16x2(__uint_as_float(r[j + 4]) * a, __uint_as_float(r[j + 5]) * a),
+                       pack_bf16x2(__uint_as_float(r[j + 6]) * a, __uint_as_float(r[j + 7]) * a));
+    } else {
+      for (int j = 0; j < EC && n0 + j < p.N; ++j) o[j] = __float2bfloat16_rn(__uint_as_float(r[j]) * a);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+template <int BN, bool NF4>
+__global__ void __launch_bounds__(NF4 ? 448 : 192, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
+                const __grid_constant__ Args p) {
+  using L = Smem<BN>;
+  constexpr int STAGES = L::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* full = bars;
+  uint64_t* afull = bars + STAGES;
+  uint64_t* empty = bars + 2 * STAGES;
+  uint64_t* tfull = bars + 3 * STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  const int m_tiles = (p.M + BM - 1) / BM;
+  const int n_tiles = (p.N + BN - 1) / BN;
+  const int n_tiles_total = m_tiles * n_tiles * p.splits;
+  const int kc = (p.k_iters + p.splits - 1) / p.splits;
+
+  if (warp == kTmaWarp && lane == 0) {
+    ptx::prefetch_tmap(&tmB);
+    if (!NF4) ptx::prefetch_tmap(&tmA);
+    if (p.k_iters_aug) { ptx::prefetch_tmap(&tmA2); ptx::prefetch_tmap(&tmB2); }
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&afull[s], NF4 ? 128 : 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], kNumEpiWarps * 32);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == kMmaWarp) ptx::tmem_alloc(tmem_slot, 2 * BN < 32 ? 32 : 2 * BN);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == kTmaWarp) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+        int mt, nt, z;
+        tile_coords(t, m_tiles, n_tiles, mt, nt, z);
+        const int kb = z * kc;
+        const int nk = min(kc, p.k_iters - kb);
+        const int total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
+        for (int i = 0; i < total; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          const bool aug = i >= nk;
+          const CUtensorMap* ma = aug ? &tmA2 : &tmA;
+          const CUtensorMap* mb = aug ? &tmB2 : &tmB;
+          const int amn = aug ? p.a2_mn : p.a_mn;
+          const int bmn = aug ? p.b2_mn : p.b_mn;
+          const int k0 = (aug ? (i - nk) : (kb + i)) * BK;
+          const bool a_tma = aug || !NF4;
+          ptx::mbar_arrive_expect_tx(&full[s], L::B_STAGE + (a_tma ? A_STAGE : 0));
+          uint8_t* a_dst = sA + s * A_STAGE;
+          uint8_t* b_dst = sB + s * L::B_STAGE;
+          if (a_tma) {
+            if (amn) {
+              ptx::tma_load_2d(ma, &full[s], a_dst, mt * BM, k0);
+              ptx::tma_load_2d(ma, &full[s], a_dst + 8192, mt * BM + 64, k0);
+            } else {
+              ptx::tma_load_2d(ma, &full[s], a_dst, k0, mt * BM);
+            }
+          }
+          if (bmn) {
+#pragma unroll
+            for (int j = 0; j < (BN + 63) / 64; ++j)
+              ptx::tma_load_2d(mb, &full[s], b_dst + j * 8192, nt * BN + j * 64, k0);
+          } else {
+            ptx::tma_load_2d(mb, &full[s], b_dst, k0, nt * BN);
+          }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ======================= MMA issuer =======================
+    uint32_t it = 0, local = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++local) {
+      int mt, nt, z;
+      tile_coords(t, m_tiles, n_tiles, mt, nt, z);
+      const int kb = z * kc;
+      const int nk = min(kc, p.k_iters - kb);
+      const int total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
+      const uint32_t acc = local & 1;
+      ptx::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int i = 0; i < total; ++i, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        const bool aug = i >= nk;
+        ptx::mbar_wait(&full[s], ph);
+        if (NF4) ptx::mbar_wait(&afull[s], ph);
+        ptx::tc_fence_after();
+        const int amn = aug ? p.a2_mn : (NF4 ? (p.nf4_mode == 1) : p.a_mn);
+        const int bmn = aug ? p.b2_mn : p.b_mn;
+        const uint32_t idesc = ptx::idesc_bf16(BM, BN, amn, bmn);
+        const uint32_t a_addr = ptx::smem_u32(sA + s * A_STAGE);
+        const uint32_t b_addr = ptx::smem_u32(sB + s * L::B_STAGE);
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = amn ? ptx::sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
+                                    : ptx::sdesc_sw128(a_addr + kk * 32, 16, 1024);
+            const uint64_t bd = bmn ? ptx::sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
+                                    : ptx::sdesc_sw128(b_addr + kk * 32, 16, 1024);
+            ptx::umma_bf16(d_tmem, ad, bd, idesc, (i | kk) != 0);
+          }
+          ptx::umma_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) ptx::umma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpiWarps) {
+    // ======================= epilogue =======================
+    constexpr int EC = BN < 32 ? BN : 32;   // columns per tcgen05.ld
+    const int quarter = warp & 3;           // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;    // accumulator row (M index within tile)
+    uint32_t local = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++local) {
+      int mt, nt, z;
+      tile_coords(t, m_tiles, n_tiles, mt, nt, z);
+      const uint32_t acc = local & 1;
+      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::tc_fence_after();
+      const int64_t m = (int64_t)mt * BM + row;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += EC) {
+        uint32_t r[EC];
+        ptx::tmem_ld<EC>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, r);
+        const int64_t n0 = (int64_t)nt * BN + c0;
+        if (m < p.M) store_chunk<EC>(p, r, m, n0, z);
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+    }
+  } else if (NF4 && warp >= kXfWarp0 && warp < kXfWarp0 + kNumXfWarps) {
+    // ======================= NF4 dequant producer =======================
+    const int xw = warp - kXfWarp0;
+    const int grp = xw >> 2;                 // two groups alternate stages
+    const int item = (xw & 3) * 32 + lane;   // 0..127: one 64-element W block per stage
+    double vals[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) vals[i] = p.values[i];
+    const float mu = p.dq_codes ? *p.mu : 0.0f;
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+      int mt, nt, z;
+      tile_coords(t, m_tiles, n_tiles, mt, nt, z);
+      const int kb = z * kc;
+      const int nk = min(kc, p.k_iters - kb);
+      const int total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
+      for (int i = 0; i < total; ++i) {
+        const uint32_t my_it = it + i;
+        if ((int)(my_it & 1) != grp) continue;
+        const int s = my_it % STAGES;
+        const uint32_t ph = (my_it / STAGES) & 1;
+        if (i >= nk) {  // augmented (TMA-fed) stage: keep afull's phase in step
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          ptx::mbar_arrive(&afull[s]);
+          continue;
+        }
+        const int64_t kg = (int64_t)(kb + i) * BK;
+        int64_t wr, wc;
+        uint32_t soff;
+        if (p.nf4_mode == 1) {  // A = W^T: M = W cols, K = W rows; MN-major image
+          const int h = item >> 6, r = item & 63;
+          wr = kg + r;
+          wc = (int64_t)mt * BM + h * 64;
+          soff = h * 8192 + r * 128;
+        } else {                // A = W: M = W rows, K = W cols; K-major image
+          wr = (int64_t)mt * BM + item;
+          wc = kg;
+          soff = item * 128;
+        }
+        const bool live = wr < p.w_rows && wc < p.w_cols;
+        uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0;
+        float c = 0.0f;
+        if (live) {
+          const int64_t e0 = wr * p.w_cols + wc;
+          const uint8_t* src = p.codes + (e0 >> 1);
+          w0 = ptx::ld_nc_v4(src);
+          w1 = ptx::ld_nc_v4(src + 16);
+          const int64_t blk = e0 >> 6;
+          c = p.dq_codes ? dq_constant(__ldg(p.dq_codes + blk), __ldg(p.c1 + blk / p.bs2), mu, p.spec)
+                         : __ldg(p.absmax + blk);
+        }
+        uint32_t Lp[4], Hp[4];
+        build_planes(vals, c, Lp, Hp);
+        ptx::mbar_wait(&empty[s], ph ^ 1);
+        const uint32_t base = ptx::smem_u32(sA + s * A_STAGE) + soff;
+        const uint32_t swz = (soff >> 7) & 7;
+        const uint32_t words[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint32_t o0, o1, o2, o3;
+          lookup4(words[ch], Lp, Hp, o0, o1);
+          lookup4(words[ch] >> 16, Lp, Hp, o2, o3);
+          ptx::st_shared_v4(base + ((ch ^ swz) << 4), o0, o1, o2, o3);
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&afull[s]);
+      }
+      it += total;
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, 2 * BN < 32 ? 32 : 2 * BN);
+  }
+}
+
+
+// split-K reduction: out = alpha * sum_z ws[z]  (fixed order -> deterministic);
+// fold > 0 also adds column n + fold into column n (hi/lo operand pairs);
+// out_split writes a bf16 hi/lo pair.
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, int fold, float alpha,
+                                     void* __restrict__ out, int64_t ldo, int out_f32, int out_t, int out_split) {
+  const int64_t total = (int64_t)M * N;
+  const int NO = fold ? fold : N;
+  const int64_t total_o = (int64_t)M * NO;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total_o;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / NO, n = i - m * NO;
+    const int64_t src = m * N + n;
+    float acc = 0.0f;
+    for (int z = 0; z < splits; ++z) {
+      acc += ws[(int64_t)z * total + src];
+      if (fold) acc += ws[(int64_t)z * total + src + fold];
+    }
+    acc *= alpha;
+    const int64_t o = out_t ? n * ldo + m : m * ldo + n;
+    if (out_f32) {
+      static_cast<float*>(out)[o] = acc;
+    } else {
+      const __nv_bfloat16 hi = __float2bfloat16_rn(acc);
+      static_cast<__nv_bfloat16*>(out)[o] = hi;
+      if (out_split) static_cast<__nv_bfloat16*>(out)[o + out_split] = __float2bfloat16_rn(acc - __bfloat162float(hi));
+    }
+  }
+}
+
+// GEMV finish: y[n] = bf16( sum_z ws[z][n] + s * sum_j t[j] l2[j][n] )
+__global__ void gemv_finish_kernel(const float* __restrict__ ws, int splits, int N,
+                                   const float* __restrict__ t, const __nv_bfloat16* __restrict__ l2, int rank,
+                                   float s, __nv_bfloat16* __restrict__ y) {
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    float acc = 0.0f;
+    for (int z = 0; z < splits; ++z) acc += ws[(int64_t)z * N + n];
+    if (rank > 0) {
+      float lr = 0.0f;
+      for (int j = 0; j < rank; ++j) lr = fmaf(t[j], __bfloat162float(l2[(int64_t)j * N + n]), lr);
+      acc += s * lr;
+    }
+    y[n] = __float2bfloat16_rn(acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// bf16 matrix stored row-major [outer][inner] with row pitch ld (elements);
+// box = 64 inner x box_outer, 128B swizzle, out-of-bounds -> 0 (pads K, M, N).
+static bool make_tmap(CUtensorMap* m, const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || (((uintptr_t)base) & 15) || ((ld * 2) & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// One GEMM operand.  K-major: stored [rows][K] (pitch ld); MN-major: stored [K][rows].
+struct Operand {
+  const void* ptr = nullptr;
+  int64_t ld = 0;
+  int mn = 0;
+};
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
+  }
+  return n;
+}
+
+template <int BN, bool NF4>
+static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2, const CUtensorMap& b2,
+                            const Args& args, cudaStream_t s) {
+  using L = Smem<BN>;
+  auto kern = gemm_kernel<BN, NF4>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES) != cudaSuccess)
+      return QLRT_ERR_CUDA;
+    attr = true;
+  }
+  const int m_tiles = (args.M + BM - 1) / BM, n_tiles = (args.N + BN - 1) / BN;
+  const int tiles = m_tiles * n_tiles * args.splits;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, NF4 ? 448 : 192, L::BYTES, s>>>(a, b, a2, b2, args);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+static int effective_splits(int splits, int k_iters) {
+  int sp = splits < 1 ? 1 : (splits > k_iters ? k_iters : splits);
+  while (sp > 1 && (int64_t)(sp - 1) * ((k_iters + sp - 1) / sp) >= k_iters) --sp;  // every split owns >= 1 iter
+  return sp;
+}
+
+// D[M,N] = A B (+ A2 B2).  K / K2 are true extents (TMA zero-fills the pad to 64).
+// args.nf4_mode != 0 makes A the quantized weight (A operand ignored).
+static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand* A2, const Operand* B2, int64_t K,
+                       int64_t K2, Args args, cudaStream_t s) {
+  CUtensorMap ta{}, tb{}, ta2{}, tb2{};
+  const bool nf4 = args.nf4_mode != 0;
+  const int64_t M = args.M, N = args.N;
+  if (bn < 64 && (B.mn || (B2 && B2->mn))) return QLRT_ERR_UNSUPPORTED;
+  if (!nf4 && !(A.mn ? make_tmap(&ta, A.ptr, M, K, A.ld, 64) : make_tmap(&ta, A.ptr, K, M, A.ld, BM)))
+    return QLRT_ERR_UNSUPPORTED;
+  if (!(B.mn ? make_tmap(&tb, B.ptr, N, K, B.ld, 64) : make_tmap(&tb, B.ptr, K, N, B.ld, bn)))
+    return QLRT_ERR_UNSUPPORTED;
+  if (K2) {
+    if (!(A2->mn ? make_tmap(&ta2, A2->ptr, M, K2, A2->ld, 64) : make_tmap(&ta2, A2->ptr, K2, M, A2->ld, BM)))
+      return QLRT_ERR_UNSUPPORTED;
+    if (!(B2->mn ? make_tmap(&tb2, B2->ptr, N, K2, B2->ld, 64) : make_tmap(&tb2, B2->ptr, K2, N, B2->ld, bn)))
+      return QLRT_ERR_UNSUPPORTED;
+  } else {
+    ta2 = nf4 ? tb : ta;
+    tb2 = tb;
+  }
+  args.k_iters = (int)((K + BK - 1) / BK);
+  args.k_iters_aug = (int)((K2 + BK - 1) / BK);
+  args.a_mn = A.mn;
+  args.b_mn = B.mn;
+  args.a2_mn = A2 ? A2->mn : 0;
+  args.b2_mn = B2 ? B2->mn : 0;
+  args.splits = effective_splits(args.splits, args.k_iters);
+  if (args.splits > 1 && K2) return QLRT_ERR_UNSUPPORTED;
+  switch (bn) {
+    case 256: return nf4 ? launch_t<256, true>(ta, tb, ta2, tb2, args, s) : launch_t<256, false>(ta, tb, ta2, tb2, args, s);
+    case 128: return nf4 ? launch_t<128, true>(ta, tb, ta2, tb2, args, s) : launch_t<128, false>(ta, tb, ta2, tb2, args, s);
+    case 64: return nf4 ? launch_t<64, true>(ta, tb, ta2, tb2, args, s) : launch_t<64, false>(ta, tb, ta2, tb2, args, s);
+    case 16: return nf4 ? launch_t<16, true>(ta, tb, ta2, tb2, args, s) : launch_t<16, false>(ta, tb, ta2, tb2, args, s);
+  }
+  return QLRT_ERR_UNSUPPORTED;
+}
+
+static qlrt_status reduce(const Args& args, cudaStream_t s) {
+  const int64_t total = (int64_t)args.M * (args.fold ? args.fold : args.N);
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  splitk_reduce_kernel<<<(int)g, 256, 0, s>>>(args.ws, args.splits, args.M, args.N, args.fold, args.alpha, args.out,
+                                              args.ldo, args.out_f32, args.out_t, args.out_split);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+// split count that fills the machine for a tile grid, bounded by workspace
+static int pick_splits(int64_t tiles, int64_t k_iters, int64_t per_split_bytes, size_t ws_bytes) {
+  if (tiles >= 74 || k_iters < 8) return 1;
+  int64_t sp = 148 / tiles;
+  if (sp > k_iters / 4) sp = k_iters / 4;
+  if (sp > 16) sp = 16;
+  if (per_split_bytes > 0 && (int64_t)ws_bytes / per_split_bytes < sp) sp = (int64_t)ws_bytes / per_split_bytes;
+  return sp < 1 ? 1 : (int)sp;
+}
+
+// D = alpha A B with automatic split-K (skinny LoRA GEMMs).  fold: see the
+// reduce kernel (forces the fp32 workspace route); out_split: bf16 hi/lo.
+static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, int64_t N, int64_t K, float alpha,
+                         void* out, int64_t ldo, int out_f32, int out_t, float* ws, size_t ws_bytes, cudaStream_t s,
+                         int fold = 0, int out_split = 0) {
+  Args a{};
+  a.M = (int)M;
+  a.N = (int)N;
+  a.out = out;
+  a.ldo = ldo;
+  a.out_f32 = out_f32;
+  a.out_t = out_t;
+  a.alpha = alpha;
+  a.ws = ws;
+  a.bs2 = 1;
+  a.fold = fold;
+  a.out_split = out_split;
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+  const int64_t kit = (K + BK - 1) / BK;
+  a.splits = effective_splits(ws ? pick_splits(tiles, kit, M * N * 4, ws_bytes) : 1, (int)kit);
+  a.to_ws = fold != 0 || (out_split && out_t);
+  if ((a.to_ws || a.splits > 1) && (!ws || (size_t)(M * N * 4) * a.splits > ws_bytes)) return QLRT_ERR_ARG;
+  qlrt_status st = run(bn, A, B, nullptr, nullptr, K, 0, a, s);
+  if (st != QLRT_OK || (a.splits == 1 && !a.to_ws)) return st;
+  return reduce(a, s);
+}
+
+static void fill_nf4(Args& a, const qlrt_nf4_weight* w, int mode) {
+  a.nf4_mode = mode;
+  a.codes = w->codes;
+  a.dq_codes = w->dq_codes;
+  a.c1 = w->c1;
+  a.mu = w->mu;
+  a.absmax = nullptr;
+  a.w_rows = w->k_in;
+  a.w_cols = w->n_out;
+  a.bs2 = w->blocksize2;
+  a.spec = w->spec;
+  for (int i = 0; i < 16; ++i) a.values[i] = w->values[i];
+}
+
+static bool weight_ok(const qlrt_nf4_weight* w) {
+  return w && w->codes && w->dq_codes && w->c1 && w->mu && w->k_in > 0 && w->n_out > 0 && (w->n_out % 64) == 0 &&
+         (((uintptr_t)w->codes) & 15) == 0 && w->blocksize2 > 0;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace gemm
+}  // namespace qlrt
+
+using namespace qlrt;
+using gemm::Operand;
+
+extern "C" {
+
+size_t qlrt_linear_workspace_bytes(int64_t m, int64_t k_in, int64_t n_out, int rank) {
+  // split-K partials of the skinny adapter GEMMs (<= 16 splits each) + GEMV scratch
+  int64_t r = rank > 0 ? rank : 1;
+  int64_t a = 16 * m * 2 * r, b = 16 * k_in * 2 * r, c = 16 * 2 * r * n_out;
+  int64_t mx = a > b ? a : b;
+  mx = mx > c ? mx : c;
+  int64_t gemv = 32 * (n_out > k_in ? n_out : k_in) + 64 * ((r + 63) / 64) + 16 * r + 256;
+  mx = mx > gemv ? mx : gemv;
+  return gemm::align256((size_t)mx * 4) + 4096;
+}
+
+qlrt_status qlrt_gemm_bf16(const void* a, const void* b, void* d, int64_t m, int64_t n, int64_t k, int a_mn, int b_mn,
+                           float alpha, int out_f32, int out_t, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!a || !b || !d || m <= 0 || n <= 0 || k <= 0) return QLRT_ERR_ARG;
+  Operand A, B;
+  A.ptr = a; A.mn = a_mn; A.ld = a_mn ? m : k;
+  B.ptr = b; B.mn = b_mn; B.ld = b_mn ? n : k;
+  const int bn = n <= 64 ? 64 : (n <= 128 ? 128 : 256);
+  return gemm::plain(bn, A, B, m, n, k, alpha, d, out_t ? m : n, out_f32, out_t, (float*)workspace, workspace_bytes,
+                     (cudaStream_t)stream);
+}
+
+qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const void* xa, int64_t m, const void* l1,
+                                const void* l2, int rank, float s, void* ts_out, void* y, void* workspace,
+                                void* stream) {
+  if (!gemm::weight_ok(w) || !x || !y || m <= 0 || rank < 0) return QLRT_ERR_ARG;
+  if (rank > 0 && (!l1 || !l2 || !ts_out || (rank % 8))) return QLRT_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t K = w->k_in, N = w->n_out;
+  const size_t ws_bytes = qlrt_linear_workspace_bytes(m, K, N, rank);
+  qlrt_status rc;
+  if (rank > 0) {
+    // Ts[m, 0:r] + Ts[m, r:2r] = s * Xa l1 as a bf16 hi/lo pair:
+    //   A = Xa (K-major, [m][K]), B = l1 (MN-major, [K][r])
+    Operand A{xa ? xa : x, K, 0}, B{l1, rank, 1};
+    rc = gemm::plain(64, A, B, m, rank, K, s, ts_out, 2 * rank, 0, 0, (float*)workspace, ws_bytes, st, 0, rank);
+    if (rc != QLRT_OK) return rc;
+  }
+  // Y^T[N, m] = W^T X^T (+ l2^T Ts^T): A = NF4 (MN-major image), B = X (K-major)
+  gemm::Args a{};
+  a.M = (int)N;
+  a.N = (int)m;
+  a.splits = 1;
+  a.out = y;
+  a.ldo = N;
+  a.out_f32 = 0;
+  a.out_t = 1;
+  a.alpha = 1.0f;
+  gemm::fill_nf4(a, w, 1);
+  Operand none{}, B{x, K, 0};
+  Operand A2{l2, N, 1}, B2{ts_out, 2 * rank, 0};  // the hi half (K2 = r, pitch 2r)
+  return gemm::run(256, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, K, rank, a, st);
+}
+
+qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_t m, const void* x, const void* ts,
+                                const void* l1, const void* l2, int rank, float s, void* dt_out, void* dx, float* dl1,
+                                float* dl2, void* workspace, void* stream) {
+  if (!gemm::weight_ok(w) || !dy || !dx || m <= 0 || rank < 0) return QLRT_ERR_ARG;
+  if (rank > 0 && (!x || !ts || !l1 || !l2 || !dt_out || !dl1 || !dl2 || (rank % 8))) return QLRT_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t K = w->k_in, N = w->n_out;
+  const size_t ws_bytes = qlrt_linear_workspace_bytes(m, K, N, rank);
+  qlrt_status rc;
+  if (rank > 0) {
+    // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):
+    //   A = dY (K-major [m][N]), B = l2 (K-major [r][N])
+    Operand A{dy, N, 0}, B{l2, N, 0};
+    rc = gemm::plain(64, A, B, m, rank, N, s, dt_out, 2 * rank, 0, 0, (float*)workspace, ws_bytes, st, 0, rank);
+    if (rc != QLRT_OK) return rc;
+  }
+  // dX^T[K, m] = W dY^T (+ l1 dT^T): A = NF4 (K-major image), B = dY (K-major)
+  gemm::Args a{};
+  a.M = (int)K;
+  a.N = (int)m;
+  a.splits = 1;
+  a.out = dx;
+  a.ldo = K;
+  a.out_f32 = 0;
+  a.out_t = 1;
+  a.alpha = 1.0f;
+  gemm::fill_nf4(a, w, 2);
+  Operand none{}, B{dy, N, 0};
+  Operand A2{l1, rank, 0}, B2{dt_out, 2 * rank, 0};
+  rc = gemm::run(256, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, N, rank, a, st);
+  if (rc != QLRT_OK || rank == 0) return rc;
+  // dl2^T[N, r] = dY^T (Ts_hi + Ts_lo): A = dY (MN-major [m][N]), B = [Ts_hi | Ts_lo] (MN-major [m][2r]);
+  // the pair is folded in the reduction, stored transposed into dl2[r][N]
+  {
+    Operand A{dy, N, 1}, B{ts, 2 * rank, 1};
+    rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, N, 2 * rank, m, 1.0f, dl2, N, 1, 1, (float*)workspace,
+                     ws_bytes, st, rank);
+    if (rc != QLRT_OK) return rc;
+  }
+  // dl1[K, r] = Xa^T (dT_hi + dT_lo): A = Xa (MN-major [m][K]), B = [dT_hi | dT_lo] (MN-major [m][2r])
+  {
+    Operand A{x, K, 1}, B{dt_out, 2 * rank, 1};
+    rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, K, 2 * rank, m, 1.0f, dl1, rank, 1, 0, (float*)workspace,
+                     ws_bytes, st, rank);
+  }
+  return rc;
+}
+
+qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* l1, const void* l2, int rank, float s,
+                          void* y, void* workspace, void* stream) {
+  if (!gemm::weight_ok(w) || !x || !y || rank < 0 || !workspace) return QLRT_ERR_ARG;
+  if (rank > 0 && (!l1 || !l2 || (rank % 8))) return QLRT_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t K = w->k_in, N = w->n_out;
+  float* ws = (float*)workspace;
+  // y^T[N, 1] = W^T x^T with split-K over K_in (BN = 16: one live column)
+  const int m_tiles = (int)((N + 127) / 128);
+  const int kit = (int)((K + 63) / 64);
+  int best = 1;
+  double best_eff = 0.0;
+  for (int sp = 1; sp <= 32 && sp <= kit / 2; ++sp) {  // fill whole waves of 148 SMs
+    int tiles = m_tiles * sp;
+    double eff = (double)tiles / (double)(((tiles + 147) / 148) * 148);
+    if (tiles >= 148 && eff > best_eff + 1e-9) { best = sp; best_eff = eff; }
+    if (tiles < 148) { best = sp; best_eff = eff; }
+  }
+  gemm::Args a{};
+  a.M = (int)N;
+  a.N = 1;
+  a.splits = gemm::effective_splits(best, kit);
+  a.ws = ws;
+  a.out_f32 = 1;
+  a.alpha = 1.0f;
+  gemm::fill_nf4(a, w, 1);
+  Operand none{}, B{x, K, 0};
+  qlrt_status rc = gemm::run(16, none, B, nullptr, nullptr, K, 0, a, st);
+  if (rc != QLRT_OK) return rc;
+  float* t = ws + (size_t)32 * (N > K ? N : K);
+  float* tws = t + 64 * ((rank + 63) / 64);
+  if (rank > 0) {
+    // t^T[r, 1] = l1^T x^T: A = l1 (MN-major [K][r]), B = x (K-major [1][K]), fp32, scaled later
+    Operand A{l1, rank, 1}, B2{x, K, 0};
+    gemm::Args b{};
+    b.M = rank;
+    b.N = 1;
+    b.out = t;
+    b.ldo = 1;
+    b.out_f32 = 1;
+    b.alpha = 1.0f;
+    b.ws = tws;
+    b.bs2 = 1;
+    b.splits = gemm::effective_splits(kit >= 64 ? 16 : 1, kit);
+    rc = gemm::run(16, A, B2, nullptr, nullptr, K, 0, b, st);
+    if (rc != QLRT_OK) return rc;
+    if (b.splits > 1 && (rc = gemm::reduce(b, st)) != QLRT_OK) return rc;
+  }
+  gemm::gemv_finish_kernel<<<(int)((N + 255) / 256), 256, 0, st>>>(ws, a.splits, (int)N, t,
+                                                                 (const __nv_bfloat16*)l2, rank, s,
+                                                                 (__nv_bfloat16*)y);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+}  // extern "C"

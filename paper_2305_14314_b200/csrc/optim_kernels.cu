@@ -1,0 +1,154 @@
+// Optimizer-side kernels: bit-exact fp32 Adam (reference AdamOptimizer.step,
+// pkg/src/qlrt/training.py:426-442), the fp64 sum of squares and in-place
+// scale of clip_global_norm (training.py:398-413), and the unified-memory
+// prefetch that backs the paged moment store (paging.py's Pager, B200-native).
+#include "qlrt_common.cuh"
+
+namespace qlrt {
+
+// One element, in the reference's op order with IEEE round-to-nearest on
+// every step and no FMA contraction:
+//   m *= b1; m += (1-b1)*g; v *= b2; v += (1-b2)*(g*g);
+//   step = (m/bc1) / (sqrt(v/bc2) + eps); p -= lr*step
+__device__ __forceinline__ void adam_one(float& p, float g, float& m, float& v, float b1, float omb1, float b2,
+                                         float omb2, float bc1, float bc2, float eps, float lr) {
+  m = __fmul_rn(m, b1);
+  m = __fadd_rn(m, __fmul_rn(omb1, g));
+  v = __fmul_rn(v, b2);
+  v = __fadd_rn(v, __fmul_rn(omb2, __fmul_rn(g, g)));
+  const float step = __fdiv_rn(__fdiv_rn(m, bc1), __fadd_rn(__fsqrt_rn(__fdiv_rn(v, bc2)), eps));
+  p = __fsub_rn(p, __fmul_rn(lr, step));
+}
+
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                                   float* __restrict__ m, float* __restrict__ v, int64_t n, float b1,
+                                                   float omb1, float b2, float omb2, float bc1, float bc2, float eps,
+                                                   float lr, __nv_bfloat16* __restrict__ pb) {
+  const int64_t n4 = n >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool vec = ((((uintptr_t)p) | ((uintptr_t)g) | ((uintptr_t)m) | ((uintptr_t)v)) & 15) == 0 &&
+                   (!pb || (((uintptr_t)pb) & 7) == 0);
+  int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec) {
+    for (int64_t i = i0; i < n4; i += stride) {
+      float4 P = reinterpret_cast<float4*>(p)[i];
+      const float4 G = reinterpret_cast<const float4*>(g)[i];
+      float4 Mv = reinterpret_cast<float4*>(m)[i];
+      float4 Vv = reinterpret_cast<float4*>(v)[i];
+      adam_one(P.x, G.x, Mv.x, Vv.x, b1, omb1, b2, omb2, bc1, bc2, eps, lr);
+      adam_one(P.y, G.y, Mv.y, Vv.y, b1, omb1, b2, omb2, bc1, bc2, eps, lr);
+      adam_one(P.z, G.z, Mv.z, Vv.z, b1, omb1, b2, omb2, bc1, bc2, eps, lr);
+      adam_one(P.w, G.w, Mv.w, Vv.w, b1, omb1, b2, omb2, bc1, bc2, eps, lr);
+      reinterpret_cast<float4*>(p)[i] = P;
+      reinterpret_cast<float4*>(m)[i] = Mv;
+      reinterpret_cast<float4*>(v)[i] = Vv;
+      if (pb) reinterpret_cast<uint2*>(pb)[i] = make_uint2(pack_bf16x2(P.x, P.y), pack_bf16x2(P.z, P.w));
+    }
+    for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      float P = p[i], Mv = m[i], Vv = v[i];
+      adam_one(P, g[i], Mv, Vv, b1, omb1, b2, omb2, bc1, bc2, eps, lr);
+      p[i] = P; m[i] = Mv; v[i] = Vv;
+      if (pb) pb[i] = __float2bfloat16_rn(P);
+    }
+  } else {
+    for (int64_t i = i0; i < n; i += stride) {
+      float P = p[i], Mv = m[i], Vv = v[i];
+      adam_one(P, g[i], Mv, Vv, b1, omb1, b2, omb2, bc1, bc2, eps, lr);
+      p[i] = P; m[i] = Mv; v[i] = Vv;
+      if (pb) pb[i] = __float2bfloat16_rn(P);
+    }
+  }
+}
+
+// fp64 sum of squares: per-thread sequential over a grid-stride range, then
+// a fixed-shape tree per CTA and a fixed-order add of CTA partials by the
+// last CTA (deterministic for a given n and grid).
+__global__ void __launch_bounds__(256) sumsq_kernel(const float* __restrict__ g, int64_t n,
+                                                    double* __restrict__ partials, unsigned* __restrict__ counter,
+                                                    double* __restrict__ acc) {
+  __shared__ double red[256];
+  __shared__ bool last;
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = (double)g[i];
+    s = __dadd_rn(s, __dmul_rn(d, d));
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = red[0];
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double t = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) t = __dadd_rn(t, ((volatile double*)partials)[b]);
+    *acc = __dadd_rn(*acc, t);
+    *counter = 0u;
+  }
+}
+
+__global__ void scale_kernel(float* __restrict__ g, int64_t n, float scale) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    g[i] = __fmul_rn(g[i], scale);
+}
+
+}  // namespace qlrt
+
+using namespace qlrt;
+
+extern "C" {
+
+qlrt_status qlrt_adam_step(float* p, const float* g, float* m, float* v, int64_t n, float b1, float omb1, float b2,
+                           float omb2, float bc1, float bc2, float eps, float lr, void* p_bf16, void* stream) {
+  if (!p || !g || !m || !v || n <= 0) return QLRT_ERR_ARG;
+  int64_t blocks = (n / 4 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  adam_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(p, g, m, v, n, b1, omb1, b2, omb2, bc1, bc2, eps, lr,
+                                                            (__nv_bfloat16*)p_bf16);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+// acc must point to a device double; the scratch (partials + counter) lives
+// right after it: caller passes a buffer of >= 8 + 8*148*2 + 8 bytes.
+qlrt_status qlrt_sumsq_f64(const float* g, int64_t n, double* acc, void* stream) {
+  if (!g || !acc || n <= 0) return QLRT_ERR_ARG;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 296) blocks = 296;
+  double* partials = acc + 1;
+  unsigned* counter = reinterpret_cast<unsigned*>(acc + 1 + 296);
+  sumsq_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(g, n, partials, counter, acc);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_scale_f32(float* g, int64_t n, float scale, void* stream) {
+  if (!g || n <= 0) return QLRT_ERR_ARG;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  scale_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(g, n, scale);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_prefetch(void* ptr, size_t bytes, int device, void* stream) {
+  if (!ptr || !bytes) return QLRT_ERR_ARG;
+  const int dst = device >= 0 ? device : cudaCpuDeviceId;
+  if (device >= 0) cudaMemAdvise(ptr, bytes, cudaMemAdviseSetPreferredLocation, device);
+  cudaError_t e = cudaMemPrefetchAsync(ptr, bytes, dst, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return QLRT_ERR_CUDA;
+  }
+  return QLRT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// Shared helpers for the qlrt_b200 kernels (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include "qlrt_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "qlrt_b200 kernels are written for sm_100a (B200) only"
+#endif
+
+#define QLRT_CHECK_LAUNCH()                                    \
+  do {                                                         \
+    cudaError_t _e = cudaGetLastError();                       \
+    if (_e != cudaSuccess) return QLRT_ERR_CUDA;               \
+  } while (0)
+
+namespace qlrt {
+
+constexpr int kNumSMs = 148;
+
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---- 8-bit float of the double quantizer (doublequant.py:33-121) ----------
+// decode: exact dyadic value of every byte (no NaN/Inf; 0x80 is -0.0)
+__device__ __forceinline__ double fp8_decode(unsigned b, int E, int M, int B) {
+  unsigned e = (b >> M) & ((1u << E) - 1u);
+  unsigned m = b & ((1u << M) - 1u);
+  double mag = (e == 0) ? ldexp((double)m, 1 - B - M)
+                        : ldexp((double)((1u << M) + m), (int)e - B - M);
+  return (b >> 7) ? -mag : mag;
+}
+
+__host__ __device__ inline double fp8_max_value(int E, int M, int B) {
+  // (2 - 2^-M) * 2^(2^E - 1 - B)
+  double top = 2.0 - 1.0 / (double)(1 << M);
+  int ex = (1 << E) - 1 - B;
+  double p = 1.0;
+  if (ex >= 0) for (int i = 0; i < ex; ++i) p *= 2.0;
+  else for (int i = 0; i < -ex; ++i) p *= 0.5;
+  return top * p;
+}
+
+// encode: nearest grid value, ties away from zero, clamp at +-max
+// (doublequant.py:103-113).  Exact in fp64: within a binade the grid is
+// uniform, so round-half-up of the scaled mantissa is the midpoint rule.
+__device__ __forceinline__ unsigned fp8_encode(double q, int E, int M, int B, double maxv) {
+  double a = fabs(q);
+  unsigned mag;
+  if (a >= maxv) {
+    mag = 0x7Fu;
+  } else if (a < ldexp(1.0, 1 - B)) {
+    mag = (unsigned)floor(ldexp(a, B + M - 1) + 0.5);
+  } else {
+    int ex;
+    double f = frexp(a, &ex);                      // a = f 2^ex, f in [0.5,1)
+    double mr = (ldexp(f, 1) - 1.0) * (double)(1 << M);
+    mag = ((unsigned)(ex - 1 + B) << M) + (unsigned)floor(mr + 0.5);
+  }
+  if (mag == 0u) return 0u;
+  return (q < 0.0 ? 0x80u : 0u) | mag;
+}
+
+// reconstruct one first-level constant (doublequant.py:190-195): two
+// separate fp64 roundings (no FMA contraction), clamp at 0, round to f32.
+__device__ __forceinline__ float dq_constant(unsigned code, float c1, float mu,
+                                             const qlrt_fp8spec& sp) {
+  double d = fp8_decode(code, sp.exp_bits, sp.mant_bits, sp.bias);
+  double r = __dadd_rn(__dmul_rn(d, (double)c1), (double)mu);
+  r = r > 0.0 ? r : 0.0;
+  return __double2float_rn(r);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+}  // namespace qlrt

@@ -1,0 +1,626 @@
+// NF4 (any 4-bit codebook) block-wise quantize, double quantization and
+// double-dequantize for sm_100a.  Restates, bit-exactly, the reference's
+//   blockquant.quantize / dequantize / pack_codes / unpack_codes
+//   (pkg/src/qlrt/blockquant.py:81-213) and
+//   doublequant.dq_compress / dq_decompress (pkg/src/qlrt/doublequant.py:148-195).
+// All kernels are HBM-bound streaming kernels: 128-bit coalesced loads and
+// stores, grids sized in multiples of the 148 SMs.
+#include "qlrt_common.cuh"
+
+namespace qlrt {
+
+// ---------------------------------------------------------------------------
+// code search: #{mids <= q} for q >= 0 (incl. -0.0), #{mids < q} for q < 0
+// (blockquant.py:123-129).  Fast path in fp32 against brackets [lo_i, hi_i]
+// that contain each midpoint with a wide margin; inside a bracket the code is
+// re-decided from the fp64 quotient x / f64(c), exactly as the reference.
+// ---------------------------------------------------------------------------
+struct CodeTables {
+  float lo[16];   // lo[n_mids..15] = +inf
+  float hi[16];
+  double mids[15];
+  int n_mids;
+};
+
+__device__ __forceinline__ unsigned exact_code(double x, float c, const CodeTables& t) {
+  double q = __ddiv_rn(x, (double)c);
+  unsigned k = 0;
+  if (q >= 0.0) {
+    for (int i = 0; i < t.n_mids; ++i) k += (t.mids[i] <= q) ? 1u : 0u;
+  } else {
+    for (int i = 0; i < t.n_mids; ++i) k += (t.mids[i] < q) ? 1u : 0u;
+  }
+  return k;
+}
+
+__device__ __forceinline__ unsigned fast_code(double xd, float r, float c, const CodeTables& t) {
+  // for fp64 inputs the fp32 rounding of x (2^-24 rel.) is far inside the bracket margin
+  float q = __double2float_rn(xd) * r;
+  unsigned j = (q > t.lo[7]) ? 8u : 0u;
+  j += (q > t.lo[j + 3]) ? 4u : 0u;
+  j += (q > t.lo[j + 1]) ? 2u : 0u;
+  j += (q > t.lo[j]) ? 1u : 0u;
+  // q in (lo[j-1], lo[j]]: certain unless it sits inside bracket j-1
+  if (j > 0 && q < t.hi[j - 1]) return exact_code(xd, c, t);
+  return j;
+}
+
+template <typename T> struct AccT { using type = float; };
+template <> struct AccT<double> { using type = double; };
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* __restrict__ x, int64_t i, int64_t n, typename AccT<T>::type v[8]);
+
+template <>
+__device__ __forceinline__ void load8<float>(const float* __restrict__ x, int64_t i, int64_t n, float v[8]) {
+  if (i + 8 <= n) {
+    float4 a = __ldg(reinterpret_cast<const float4*>(x + i));
+    float4 b = __ldg(reinterpret_cast<const float4*>(x + i + 4));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (i + j < n) ? x[i + j] : 0.0f;
+  }
+}
+
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* __restrict__ x, int64_t i, int64_t n,
+                                                     float v[8]) {
+  if (i + 8 <= n) {
+    uint4 a = __ldg(reinterpret_cast<const uint4*>(x + i));
+    uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[2 * j] = __uint_as_float(w[j] << 16);
+      v[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (i + j < n) ? __bfloat162float(x[i + j]) : 0.0f;
+  }
+}
+
+template <>
+__device__ __forceinline__ void load8<double>(const double* __restrict__ x, int64_t i, int64_t n, double v[8]) {
+  if (i + 8 <= n) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double2 a = __ldg(reinterpret_cast<const double2*>(x + i) + j);
+      v[2 * j] = a.x;
+      v[2 * j + 1] = a.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (i + j < n) ? x[i + j] : 0.0;
+  }
+}
+
+__device__ __forceinline__ bool finite_v(float a) { return fabsf(a) <= 3.402823466e38f; }
+__device__ __forceinline__ bool finite_v(double a) { return fabs(a) <= 1.7976931348623157e308; }
+__device__ __forceinline__ float to_f32_const(float m) { return m; }
+__device__ __forceinline__ float to_f32_const(double m) { return __double2float_rn(m); }
+
+// Phase A, blocksize 64: 8 consecutive lanes own one 64-block, 8 elements
+// each (two 16B loads for fp32, one for bf16); absmax by 3 xor-shuffles;
+// 8 codes -> one 32-bit packed store.
+template <typename T>
+__global__ void __launch_bounds__(256) quantize64_kernel(const T* __restrict__ x, int64_t n,
+                                                         int64_t n_groups, qlrt_codebook4 cb,
+                                                         uint32_t* __restrict__ codes,
+                                                         float* __restrict__ absmax,
+                                                         unsigned long long* __restrict__ first_bad) {
+  __shared__ CodeTables t;
+  if (threadIdx.x < 16) {
+    t.lo[threadIdx.x] = cb.lo[threadIdx.x];
+    t.hi[threadIdx.x] = cb.hi[threadIdx.x];
+    if (threadIdx.x < 15) t.mids[threadIdx.x] = cb.mids[threadIdx.x];
+  }
+  if (threadIdx.x == 0) t.n_mids = cb.n_mids;
+  __syncthreads();
+  const unsigned pad = (unsigned)cb.pad_code;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count: every lane reaches the shuffles
+  for (int64_t gb = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); gb < n_groups;
+       gb += stride) {
+    const int64_t g = gb + lane;
+    const bool act = g < n_groups;  // n_groups % 8 == 0: 8-lane groups are all-in or all-out
+    const int64_t i0 = g * 8;
+    using V = typename AccT<T>::type;
+    V v[8];
+    if (act) {
+      load8<T>(x, i0, n, v);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (V)0;
+    }
+    V m = (V)0;
+    bool finite = true;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      finite &= finite_v(v[j]);  // false for inf and NaN
+      m = fmax(m, fabs(v[j]));
+    }
+    if (!finite) {
+      unsigned long long bad = ~0ull;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (!finite_v(v[j]) && i0 + j < n) bad = min(bad, (unsigned long long)(i0 + j));
+      atomicMin(first_bad, bad);
+    }
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 4));
+    if (!act) continue;
+    const float c = to_f32_const(m);  // f32(absmax) (blockquant.py:166)
+    uint32_t word = 0;
+    if (c > 0.0f) {
+      const float r = __frcp_rn(c);
+      const bool fast_ok = r <= 3.402823466e38f;  // subnormal c: 1/c overflows
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        unsigned k = pad;
+        if (i0 + j < n) k = fast_ok ? fast_code((double)v[j], r, c, t) : exact_code((double)v[j], c, t);
+        word |= k << (4 * j);
+      }
+    } else {
+      word = pad * 0x11111111u;
+    }
+    codes[g] = word;
+    if ((threadIdx.x & 7) == 0) absmax[g >> 3] = c;
+  }
+}
+
+// Generic blocksize: absmax per block (one warp per block) ...
+template <typename T>
+__global__ void absmax_generic_kernel(const T* __restrict__ x, int64_t n, int bs, int64_t nb,
+                                      float* __restrict__ absmax,
+                                      unsigned long long* __restrict__ first_bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b = warp; b < nb; b += nwarps) {
+    double m = 0.0;
+    unsigned long long bad = ~0ull;
+    for (int64_t i = b * bs + lane; i < min((b + 1) * bs, n); i += 32) {
+      double a = fabs((double)x[i]);
+      if (!(a <= 1.7976931348623157e308)) bad = min(bad, (unsigned long long)i);
+      m = fmax(m, a);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+    }
+    if (lane == 0) {
+      absmax[b] = __double2float_rn(m);
+      if (bad != ~0ull) atomicMin(first_bad, bad);
+    }
+  }
+}
+
+// ... then one thread per packed byte (two elements, possibly two blocks).
+template <typename T>
+__global__ void codes_generic_kernel(const T* __restrict__ x, int64_t n, int bs, int64_t n_pad,
+                                     qlrt_codebook4 cb, const float* __restrict__ absmax,
+                                     uint8_t* __restrict__ codes) {
+  __shared__ CodeTables t;
+  if (threadIdx.x < 16) {
+    t.lo[threadIdx.x] = cb.lo[threadIdx.x];
+    t.hi[threadIdx.x] = cb.hi[threadIdx.x];
+    if (threadIdx.x < 15) t.mids[threadIdx.x] = cb.mids[threadIdx.x];
+  }
+  if (threadIdx.x == 0) t.n_mids = cb.n_mids;
+  __syncthreads();
+  const int64_t nbytes = (n_pad + 1) / 2;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbytes;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    unsigned byte = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int64_t i = 2 * b + h;
+      unsigned k = 0;  // odd tail nibble of pack_codes is 0
+      if (i < n_pad) {
+        float c = absmax[i / bs];
+        if (i < n && c > 0.0f) {
+          float r = __frcp_rn(c);
+          const double xd = (double)x[i];
+          k = (r <= 3.402823466e38f) ? fast_code(xd, r, c, t) : exact_code(xd, c, t);
+        } else {
+          k = (unsigned)cb.pad_code;
+        }
+      }
+      byte |= k << (4 * h);
+    }
+    codes[b] = (uint8_t)byte;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// double quantization (doublequant.py:148-187)
+// ---------------------------------------------------------------------------
+
+// numpy pairwise_sum (loops_utils.h.src) of float32 values widened to fp64;
+// recursive form for the (at most one) partial 8192-chunk.
+__device__ double pairwise_seq(const float* a, int n) {
+  if (n < 8) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s = __dadd_rn(s, (double)a[i]);
+    return s;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = (double)a[j];
+    int m = n - n % 8;
+    for (int i = 8; i < m; i += 8)
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], (double)a[i + j]);
+    double s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (int i = m; i < n; ++i) s = __dadd_rn(s, (double)a[i]);
+    return s;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  double l = pairwise_seq(a, n2);
+  double r = pairwise_seq(a + n2, n - n2);
+  return __dadd_rn(l, r);
+}
+
+// One CTA (64 threads) per 8192-constant buffer chunk.  A full chunk is a
+// perfect pairwise tree of 64 leaves of 128 (8 strided accumulators each).
+__global__ void __launch_bounds__(64) dq_chunk_sums_kernel(const float* __restrict__ c,
+                                                           int64_t nb,
+                                                           double* __restrict__ chunk_sums) {
+  __shared__ double leaf[64];
+  const int64_t base = (int64_t)blockIdx.x * 8192;
+  const int len = (int)min((int64_t)8192, nb - base);
+  if (len < 8192) {
+    if (threadIdx.x == 0) chunk_sums[blockIdx.x] = pairwise_seq(c + base, len);
+    return;
+  }
+  const float* a = c + base + threadIdx.x * 128;
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = (double)a[j];
+  for (int i = 8; i < 128; i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], (double)a[i + j]);
+  leaf[threadIdx.x] = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                                __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  __syncthreads();
+  for (int w = 32; w >= 1; w >>= 1) {
+    double s = 0.0;
+    if (threadIdx.x < w) s = __dadd_rn(leaf[2 * threadIdx.x], leaf[2 * threadIdx.x + 1]);
+    __syncthreads();
+    if (threadIdx.x < w) leaf[threadIdx.x] = s;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) chunk_sums[blockIdx.x] = leaf[0];
+}
+
+// One CTA per second-level block: mu from the chunk sums (added in order
+// from 0.0, then / nb in fp64, then f32), centring, fp64 absmax,
+// c1 = f32(A / max), codes = encode(centered / f64(c1)).
+__global__ void __launch_bounds__(256) dq_encode_kernel(const float* __restrict__ c, int64_t nb,
+                                                        int bs2, int64_t n_chunks,
+                                                        const double* __restrict__ chunk_sums,
+                                                        qlrt_fp8spec sp, float* __restrict__ mu_out,
+                                                        float* __restrict__ c1,
+                                                        uint8_t* __restrict__ codes) {
+  __shared__ double s_mu;
+  __shared__ double s_red[8];
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < n_chunks; ++i) acc = __dadd_rn(acc, chunk_sums[i]);
+    float mu = __double2float_rn(__ddiv_rn(acc, (double)nb));
+    s_mu = (double)mu;
+    if (blockIdx.x == 0) *mu_out = mu;
+  }
+  __syncthreads();
+  const double mu = s_mu;
+  const int64_t b0 = (int64_t)blockIdx.x * bs2;
+  const int64_t b1 = min(b0 + bs2, nb);
+  double amax = 0.0;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x)
+    amax = fmax(amax, fabs(__dsub_rn((double)c[i], mu)));
+  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  amax = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) amax = fmax(amax, s_red[w]);
+  const double maxv = fp8_max_value(sp.exp_bits, sp.mant_bits, sp.bias);
+  float scale = 0.0f;
+  if (amax > 0.0) scale = __double2float_rn(__ddiv_rn(amax, maxv));
+  if (threadIdx.x == 0) c1[blockIdx.x] = scale;  // 0 for flat / underflowing blocks
+  const double sd = (double)scale;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+    unsigned code = 0u;
+    if (scale != 0.0f)
+      code = fp8_encode(__ddiv_rn(__dsub_rn((double)c[i], mu), sd), sp.exp_bits, sp.mant_bits,
+                        sp.bias, maxv);
+    codes[i] = (uint8_t)code;
+  }
+}
+
+__global__ void dq_decompress_kernel(const uint8_t* __restrict__ codes,
+                                     const float* __restrict__ c1, const float* __restrict__ mu,
+                                     int64_t nb, int bs2, qlrt_fp8spec sp,
+                                     float* __restrict__ out) {
+  const float m = *mu;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = dq_constant(codes[i], c1[i / bs2], m, sp);
+}
+
+// ---------------------------------------------------------------------------
+// dequantize (blockquant.py:198-213): out = f32(values[code] * f64(c)).
+// blocksize 64 fast path: one thread = 32 elements = 16 code bytes (one 16B
+// load), the block constant rebuilt from its DQ byte in fp64, the fp64
+// product from a 16-entry smem table (conflict-free: 16 doubles, 32 banks).
+// ---------------------------------------------------------------------------
+template <int OUT>
+__global__ void __launch_bounds__(256) dequant64_kernel(const uint4* __restrict__ codes,
+                                                        int64_t n, qlrt_codebook4 cb,
+                                                        const float* __restrict__ absmax,
+                                                        const uint8_t* __restrict__ dq_codes,
+                                                        const float* __restrict__ c1,
+                                                        const float* __restrict__ mu, int bs2,
+                                                        qlrt_fp8spec sp, void* __restrict__ out) {
+  __shared__ double vals[16];
+  if (threadIdx.x < 16) vals[threadIdx.x] = cb.values[threadIdx.x];
+  __syncthreads();
+  const float mu_v = dq_codes ? *mu : 0.0f;
+  const int64_t n_chunks = cdiv(n, 32);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_chunks;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = t >> 1;
+    float c;
+    if (dq_codes) c = dq_constant(__ldg(dq_codes + blk), __ldg(c1 + blk / bs2), mu_v, sp);
+    else c = __ldg(absmax + blk);
+    const double cd = (double)c;
+    const int64_t e0 = t * 32;
+    uint4 w;
+    if (e0 + 32 <= n) {
+      w = __ldg(codes + t);
+    } else {
+      const uint8_t* cb8 = reinterpret_cast<const uint8_t*>(codes) + t * 16;
+      uint8_t tmp[16];
+      for (int j = 0; j < 16; ++j) tmp[j] = (e0 + 2 * j < n) ? cb8[j] : 0;
+      w = *reinterpret_cast<uint4*>(tmp);
+    }
+    uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    if constexpr (OUT == QLRT_F64) {  // the reference's own float64 output, bit-exact
+      double* o = static_cast<double*>(out) + e0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (e0 + q * 8 + j < n) o[q * 8 + j] = __dmul_rn(vals[(ws[q] >> (4 * j)) & 15u], cd);
+    } else {
+    float f[32];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        f[q * 8 + j] = __double2float_rn(__dmul_rn(vals[(ws[q] >> (4 * j)) & 15u], cd));
+    if (e0 + 32 <= n) {
+      if (OUT == QLRT_BF16) {
+        uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + e0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          o[q] = make_uint4(pack_bf16x2(f[8 * q], f[8 * q + 1]), pack_bf16x2(f[8 * q + 2], f[8 * q + 3]),
+                            pack_bf16x2(f[8 * q + 4], f[8 * q + 5]), pack_bf16x2(f[8 * q + 6], f[8 * q + 7]));
+      } else {
+        float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + e0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) o[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+      }
+    } else {
+      for (int j = 0; j < 32; ++j) {
+        if (e0 + j >= n) break;
+        if (OUT == QLRT_BF16) static_cast<__nv_bfloat16*>(out)[e0 + j] = __float2bfloat16_rn(f[j]);
+        else static_cast<float*>(out)[e0 + j] = f[j];
+      }
+    }
+    }
+  }
+}
+
+// generic blocksize: one thread per element
+template <int OUT>
+__global__ void dequant_generic_kernel(const uint8_t* __restrict__ codes, int64_t n, int bs,
+                                       qlrt_codebook4 cb, const float* __restrict__ absmax,
+                                       const uint8_t* __restrict__ dq_codes,
+                                       const float* __restrict__ c1, const float* __restrict__ mu,
+                                       int bs2, qlrt_fp8spec sp, void* __restrict__ out) {
+  __shared__ double vals[16];
+  if (threadIdx.x < 16) vals[threadIdx.x] = cb.values[threadIdx.x];
+  __syncthreads();
+  const float mu_v = dq_codes ? *mu : 0.0f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = i / bs;
+    float c = dq_codes ? dq_constant(dq_codes[blk], c1[blk / bs2], mu_v, sp) : absmax[blk];
+    unsigned code = (codes[i >> 1] >> (4 * (i & 1))) & 15u;
+    const double d = __dmul_rn(vals[code], (double)c);
+    if (OUT == QLRT_F64) static_cast<double*>(out)[i] = d;
+    else if (OUT == QLRT_BF16) static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(__double2float_rn(d));
+    else static_cast<float*>(out)[i] = __double2float_rn(d);
+  }
+}
+
+__global__ void fp8_encode_kernel(const double* __restrict__ x, int64_t n, qlrt_fp8spec sp,
+                                  uint8_t* __restrict__ out) {
+  const double maxv = fp8_max_value(sp.exp_bits, sp.mant_bits, sp.bias);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (uint8_t)fp8_encode(x[i], sp.exp_bits, sp.mant_bits, sp.bias, maxv);
+}
+
+__global__ void fp8_decode_kernel(const uint8_t* __restrict__ c, int64_t n, qlrt_fp8spec sp,
+                                  double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = fp8_decode(c[i], sp.exp_bits, sp.mant_bits, sp.bias);
+}
+
+__global__ void pack4_kernel(const uint8_t* __restrict__ codes, int64_t count,
+                             uint8_t* __restrict__ packed) {
+  const int64_t nbytes = (count + 1) / 2;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbytes;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    unsigned lo = codes[2 * b] & 15u;
+    unsigned hi = (2 * b + 1 < count) ? (codes[2 * b + 1] & 15u) : 0u;
+    packed[b] = (uint8_t)(lo | (hi << 4));
+  }
+}
+
+__global__ void unpack4_kernel(const uint8_t* __restrict__ packed, int64_t count,
+                               uint8_t* __restrict__ codes) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    codes[i] = (packed[i >> 1] >> (4 * (i & 1))) & 15u;
+}
+
+static inline int grid_for(int64_t work, int threads, int per_sm = 8) {
+  int64_t g = cdiv(work, threads);
+  int64_t cap = (int64_t)kNumSMs * per_sm;
+  return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
+}
+
+}  // namespace qlrt
+
+using namespace qlrt;
+
+extern "C" {
+
+qlrt_status qlrt_quantize4(const void* x, int x_dtype, int64_t n, int blocksize,
+                           const qlrt_codebook4* cb, uint8_t* codes, float* absmax,
+                           int64_t* first_bad, void* stream) {
+  if (n <= 0 || blocksize < 1 || !cb || !x || !codes || !absmax || !first_bad) return QLRT_ERR_ARG;
+  if (x_dtype != QLRT_F32 && x_dtype != QLRT_BF16 && x_dtype != QLRT_F64) return QLRT_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nb = cdiv(n, blocksize);
+  // sentinel 0x7F7F...7F (> any index); memset is graph-capturable
+  if (cudaMemsetAsync(first_bad, 0x7F, 8, s) != cudaSuccess) return QLRT_ERR_CUDA;
+  auto* fb = reinterpret_cast<unsigned long long*>(first_bad);
+  const bool aligned = (((uintptr_t)x) & 15) == 0 && (((uintptr_t)codes) & 3) == 0;
+  if (blocksize == 64 && aligned) {
+    const int64_t n_groups = nb * 8;
+    const int grid = grid_for(n_groups, 256, 8);
+    if (x_dtype == QLRT_F32)
+      quantize64_kernel<float><<<grid, 256, 0, s>>>((const float*)x, n, n_groups, *cb, (uint32_t*)codes, absmax, fb);
+    else if (x_dtype == QLRT_BF16)
+      quantize64_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, n, n_groups, *cb,
+                                                            (uint32_t*)codes, absmax, fb);
+    else
+      quantize64_kernel<double><<<grid, 256, 0, s>>>((const double*)x, n, n_groups, *cb, (uint32_t*)codes, absmax, fb);
+  } else {
+    const int ga = grid_for(nb * 32, 256, 8);
+    const int gc = grid_for(cdiv(nb * blocksize, 2), 256, 8);
+    if (x_dtype == QLRT_F32) {
+      absmax_generic_kernel<float><<<ga, 256, 0, s>>>((const float*)x, n, blocksize, nb, absmax, fb);
+      codes_generic_kernel<float><<<gc, 256, 0, s>>>((const float*)x, n, blocksize, nb * blocksize, *cb, absmax, codes);
+    } else if (x_dtype == QLRT_BF16) {
+      absmax_generic_kernel<__nv_bfloat16><<<ga, 256, 0, s>>>((const __nv_bfloat16*)x, n, blocksize, nb, absmax, fb);
+      codes_generic_kernel<__nv_bfloat16><<<gc, 256, 0, s>>>((const __nv_bfloat16*)x, n, blocksize, nb * blocksize,
+                                                             *cb, absmax, codes);
+    } else {
+      absmax_generic_kernel<double><<<ga, 256, 0, s>>>((const double*)x, n, blocksize, nb, absmax, fb);
+      codes_generic_kernel<double><<<gc, 256, 0, s>>>((const double*)x, n, blocksize, nb * blocksize, *cb, absmax,
+                                                      codes);
+    }
+  }
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+size_t qlrt_dq_workspace_bytes(int64_t nb) { return (size_t)cdiv(nb, 8192) * sizeof(double); }
+
+qlrt_status qlrt_dq_compress(const float* absmax, int64_t nb, int blocksize2, qlrt_fp8spec spec,
+                             void* workspace, float* mu, float* c1, uint8_t* dq_codes,
+                             void* stream) {
+  if (nb <= 0 || blocksize2 < 1 || !absmax || !workspace || !mu || !c1 || !dq_codes)
+    return QLRT_ERR_ARG;
+  if (spec.exp_bits + spec.mant_bits != 7 || spec.exp_bits < 1 || spec.bias < 0) return QLRT_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n_chunks = cdiv(nb, 8192);
+  double* sums = (double*)workspace;
+  dq_chunk_sums_kernel<<<(unsigned)n_chunks, 64, 0, s>>>(absmax, nb, sums);
+  const int64_t n2 = cdiv(nb, blocksize2);
+  dq_encode_kernel<<<(unsigned)n2, 256, 0, s>>>(absmax, nb, blocksize2, n_chunks, sums, spec, mu,
+                                                c1, dq_codes);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_dq_decompress(const uint8_t* dq_codes, const float* c1, const float* mu,
+                               int64_t nb, int blocksize2, qlrt_fp8spec spec, float* out,
+                               void* stream) {
+  if (nb <= 0 || blocksize2 < 1 || !dq_codes || !c1 || !mu || !out) return QLRT_ERR_ARG;
+  dq_decompress_kernel<<<grid_for(nb, 256), 256, 0, (cudaStream_t)stream>>>(dq_codes, c1, mu, nb,
+                                                                            blocksize2, spec, out);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_dequantize4(const uint8_t* codes, int64_t n, int blocksize,
+                             const qlrt_codebook4* cb, const float* absmax,
+                             const uint8_t* dq_codes, const float* c1, const float* mu,
+                             int blocksize2, qlrt_fp8spec spec, void* out, int out_dtype,
+                             void* stream) {
+  if (n <= 0 || blocksize < 1 || !codes || !cb || !out) return QLRT_ERR_ARG;
+  if (!absmax && !(dq_codes && c1 && mu)) return QLRT_ERR_ARG;
+  if (out_dtype != QLRT_F32 && out_dtype != QLRT_BF16 && out_dtype != QLRT_F64) return QLRT_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool aligned = (((uintptr_t)codes) & 15) == 0 && (((uintptr_t)out) & 15) == 0;
+  if (blocksize == 64 && aligned) {
+    const int g = grid_for(cdiv(n, 32), 256, 8);
+#define QLRT_DQ64(O) dequant64_kernel<O><<<g, 256, 0, s>>>((const uint4*)codes, n, *cb, absmax, dq_codes, c1, mu, \
+                                                           blocksize2, spec, out)
+    if (out_dtype == QLRT_BF16) QLRT_DQ64(QLRT_BF16);
+    else if (out_dtype == QLRT_F32) QLRT_DQ64(QLRT_F32);
+    else QLRT_DQ64(QLRT_F64);
+#undef QLRT_DQ64
+  } else {
+    const int g = grid_for(n, 256, 8);
+#define QLRT_DQG(O) dequant_generic_kernel<O><<<g, 256, 0, s>>>(codes, n, blocksize, *cb, absmax, dq_codes, c1, mu, \
+                                                                blocksize2, spec, out)
+    if (out_dtype == QLRT_BF16) QLRT_DQG(QLRT_BF16);
+    else if (out_dtype == QLRT_F32) QLRT_DQG(QLRT_F32);
+    else QLRT_DQG(QLRT_F64);
+#undef QLRT_DQG
+  }
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_fp8_encode(const double* x, int64_t n, qlrt_fp8spec spec, uint8_t* out, void* stream) {
+  if (!x || !out || n <= 0 || spec.exp_bits + spec.mant_bits != 7) return QLRT_ERR_ARG;
+  fp8_encode_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, n, spec, out);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_fp8_decode(const uint8_t* codes, int64_t n, qlrt_fp8spec spec, double* out, void* stream) {
+  if (!codes || !out || n <= 0 || spec.exp_bits + spec.mant_bits != 7) return QLRT_ERR_ARG;
+  fp8_decode_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(codes, n, spec, out);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_pack4(const uint8_t* codes, int64_t count, uint8_t* packed, void* stream) {
+  if (count <= 0 || !codes || !packed) return QLRT_ERR_ARG;
+  pack4_kernel<<<grid_for(cdiv(count, 2), 256), 256, 0, (cudaStream_t)stream>>>(codes, count, packed);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_unpack4(const uint8_t* packed, int64_t count, uint8_t* codes, void* stream) {
+  if (count <= 0 || !codes || !packed) return QLRT_ERR_ARG;
+  unpack4_kernel<<<grid_for(count, 256), 256, 0, (cudaStream_t)stream>>>(packed, count, codes);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+const char* qlrt_build_info(void) { return "qlrt_b200 sm_100a"; }
+
+}  // extern "C"

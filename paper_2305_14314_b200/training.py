@@ -1,0 +1,183 @@
+"""Optimizer step of the QLoRA finetune on the GPU -- mirror of the reference's
+``TrainConfig`` / ``clip_global_norm`` / ``AdamOptimizer`` / moment stores
+(pkg/src/qlrt/training.py:62-90, 354-442).
+
+* ``AdamOptimizer.step`` launches one bit-exact fp32 Adam kernel per
+  parameter (the reference's op order with the float32-rounded constants
+  numpy 2 uses under NEP 50), which also refreshes the bf16 operand copies.
+* ``PlainMomentStore`` keeps moments as device tensors; ``PagedMomentStore``
+  keeps them in unified-memory slabs under a :class:`Pager` budget.  Both run
+  the same kernel on the same bytes, so paged == plain bit for bit.
+* ``clip_global_norm`` sums squares in fp64 on the device and scales in
+  place with the float32-rounded factor (training.py:398-413).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from ._native import SUMSQ_SCRATCH, check, lib, ptr, stream_ptr
+from .errors import TrainingDivergedError
+from .paging import Pager
+
+OPTIMIZERS = ("plain", "paged")
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    """training.py:62-90 (the optimizer-relevant fields and defaults)."""
+
+    learning_rate: float = 0.01
+    batch_size: int = 64
+    steps: int = 500
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.999
+    adam_eps: float = 1e-8
+    max_grad_norm: float = 0.3
+    lr_schedule: str = "constant"
+    seed: int = 0
+
+    def validate(self) -> None:
+        if not (self.learning_rate > 0 and math.isfinite(self.learning_rate)):
+            raise ValueError("learning_rate must be positive and finite")
+        if self.batch_size < 1:
+            raise ValueError("batch_size must be at least 1")
+        if self.steps < 1:
+            raise ValueError("steps must be at least 1")
+        for name in ("adam_beta1", "adam_beta2"):
+            if not 0.0 <= getattr(self, name) < 1.0:
+                raise ValueError(f"{name} must lie in [0, 1)")
+        if self.adam_eps <= 0:
+            raise ValueError("adam_eps must be positive")
+        if self.max_grad_norm <= 0:
+            raise ValueError("max_grad_norm must be positive")
+        if self.lr_schedule != "constant":
+            raise ValueError("only the constant lr schedule is supported")
+
+
+class PlainMomentStore:
+    """Adam moments as resident device tensors (training.py:354-368)."""
+
+    def __init__(self):
+        self._state: dict[str, tuple[torch.Tensor, torch.Tensor]] = {}
+
+    def update(self, name: str, param: torch.Tensor, fn) -> None:
+        st = self._state.get(name)
+        if st is None:
+            st = (torch.zeros_like(param), torch.zeros_like(param))
+            self._state[name] = st
+        fn(*st)
+
+    def close(self) -> None:
+        pass
+
+
+class PagedMomentStore:
+    """Moments in pager slabs: first moment then second, one slab per
+    parameter (training.py:371-395), resident on demand."""
+
+    def __init__(self, pager: Pager):
+        self.pager = pager
+        self._slabs = {}
+
+    def update(self, name: str, param: torch.Tensor, fn) -> None:
+        slab = self._slabs.get(name)
+        if slab is None:
+            slab = self.pager.alloc(2 * param.numel() * param.element_size())
+            self._slabs[name] = slab
+
+        def run(view: torch.Tensor) -> None:
+            flat = view.view(param.dtype)
+            fn(flat[: param.numel()].view(param.shape), flat[param.numel():].view(param.shape))
+
+        self.pager.with_slab(slab, run)
+
+    def close(self) -> None:
+        self.pager.flush()
+
+
+def _sumsq_scratch(device) -> torch.Tensor:
+    return torch.zeros(SUMSQ_SCRATCH // 8, dtype=torch.float64, device=device)
+
+
+def global_sumsq(grads: dict, order: list) -> torch.Tensor:
+    """Device fp64 sum of squares over ``order`` (no host sync)."""
+    dev = grads[order[0]].device
+    acc = _sumsq_scratch(dev)
+    for name in order:
+        g = grads[name]
+        if not g.is_contiguous():
+            g = g.contiguous()
+        if g.numel():
+            check(lib().qlrt_sumsq_f64(ptr(g), g.numel(), ptr(acc), stream_ptr()), "clip_global_norm")
+    return acc[:1]
+
+
+def clip_global_norm(grads: dict, order: list, max_norm: float) -> float:
+    """Scale every gradient in place when the joint 2-norm exceeds ``max_norm``;
+    returns the pre-clip norm (training.py:398-413)."""
+    norm = math.sqrt(float(global_sumsq(grads, order).item()))
+    if norm > max_norm and norm > 0.0:
+        scale = float(np.float32(max_norm / norm))
+        for name in order:
+            g = grads[name]
+            if g.is_contiguous():
+                check(lib().qlrt_scale_f32(ptr(g), g.numel(), scale, stream_ptr()), "clip_global_norm")
+            else:
+                g.mul_(scale)
+    return norm
+
+
+class AdamOptimizer:
+    """Adam with bias correction; moments live wherever ``store`` puts them
+    (training.py:416-442).  ``params`` maps names to float32 device tensors;
+    ``shadows`` optionally maps names to bf16 copies refreshed by the kernel."""
+
+    def __init__(self, params: dict, cfg: TrainConfig, store, shadows: dict | None = None):
+        self.params = params
+        self.cfg = cfg
+        self.store = store
+        self.shadows = shadows or {}
+        self.t = 0
+
+    def constants(self):
+        """The float32 values numpy 2 (NEP 50) uses in the reference's update."""
+        c = self.cfg
+        f = np.float32
+        bc1 = 1.0 - c.adam_beta1 ** self.t
+        bc2 = 1.0 - c.adam_beta2 ** self.t
+        return tuple(float(f(v)) for v in (c.adam_beta1, 1.0 - c.adam_beta1, c.adam_beta2, 1.0 - c.adam_beta2,
+                                           bc1, bc2, c.adam_eps, c.learning_rate))
+
+    def step(self, grads: dict) -> None:
+        self.t += 1
+        consts = self.constants()
+        for name, p in self.params.items():
+            g = grads[name]
+            if not g.is_contiguous():
+                g = g.contiguous()
+            if p.dtype != torch.float32 or g.dtype != torch.float32:
+                raise ValueError("AdamOptimizer expects float32 parameters and gradients")
+            shadow = self.shadows.get(name)
+
+            def upd(m, v, p=p, g=g, shadow=shadow):
+                check(lib().qlrt_adam_step(ptr(p), ptr(g), ptr(m), ptr(v), p.numel(), *consts, ptr(shadow),
+                                           stream_ptr()), "AdamOptimizer.step")
+
+            self.store.update(name, p, upd)
+
+
+def check_finite(loss: float, norm: float, step: int) -> None:
+    """The trainer's divergence guard (training.py:496-503)."""
+    if not math.isfinite(loss):
+        raise TrainingDivergedError(f"non-finite loss at step {step}")
+    if not math.isfinite(norm):
+        raise TrainingDivergedError(f"non-finite gradient norm at step {step}")
+
+
+__all__ = ["TrainConfig", "PlainMomentStore", "PagedMomentStore", "AdamOptimizer", "clip_global_norm",
+           "global_sumsq", "check_finite", "OPTIMIZERS"]

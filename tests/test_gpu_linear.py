@@ -1,0 +1,216 @@
+"""GPU parity for the tcgen05 engine and the fused NF4 linear + LoRA.
+
+Tolerance (BASELINE.json north star): bf16 outputs vs the bf16-rounded fp64
+oracle -- max|d|/max|ref| <= 1e-2 and mean|d|/mean|ref| <= 1e-3.  The oracle
+is the reference QLinear in float64 over W = bf16(f32(dequantize(q))) with
+bf16-representable X, dY, l1, l2.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+MAX_REL, MEAN_REL = 1e-2, 1e-3
+
+
+def rel_errs(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    d = np.abs(got - ref)
+    return float(d.max() / np.abs(ref).max()), float(d.mean() / np.abs(ref).mean())
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).float().numpy()
+
+
+def assert_tol(got, ref, what):
+    mx, mn = rel_errs(got, ref)
+    assert mx <= MAX_REL and mn <= MEAN_REL, f"{what}: max-rel {mx:.3e} mean-rel {mn:.3e}"
+
+
+# ---------------------------------------------------------------------------
+# plain bf16 GEMM on the engine, every operand layout
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("m,n,k", [(256, 512, 1024), (200, 296, 320), (128, 64, 4096), (1000, 128, 192),
+                                   (64, 1, 512), (2048, 64, 11008)])
+@pytest.mark.parametrize("a_t,b_t", [(False, False), (True, False), (False, True), (True, True)])
+def test_gemm_layouts(m, n, k, a_t, b_t, qb, cuda):
+    if n < 16 and not b_t:
+        pytest.skip("MN-major B needs N >= 64 (swizzle atom)")
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n)
+    a = torch.randn(m, k, device="cuda", generator=g).bfloat16()
+    b = torch.randn(k, n, device="cuda", generator=g).bfloat16()
+    ref = a.float() @ b.float()
+    A = a.t().contiguous() if a_t else a
+    B = b.t().contiguous() if b_t else b
+    out = qb.gemm_bf16(A, B, a_t=a_t, b_t=b_t, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    err = (out - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-5, err
+    out16 = qb.gemm_bf16(A, B, a_t=a_t, b_t=b_t, alpha=0.5)
+    assert torch.equal(out16, (out * 0.5).bfloat16())
+
+
+# ---------------------------------------------------------------------------
+# fused NF4 linear + LoRA vs the golden reference cases
+# ---------------------------------------------------------------------------
+
+def _layer_from_golden(golden, i, case, qb):
+    g = lambda k: golden[f"ql/{i}/{k}"]  # noqa: E731
+    q = qb.quantize(g("w"), qb.get_codebook("nf4"), 64, double_quant=True)
+    assert np.array_equal(q.codes.cpu().numpy(), g("codes"))
+    ad = qb.LoraAdapter(rank=case["rank"], alpha=case["alpha"],
+                        l1=torch.from_numpy(g("l1").astype(np.float32)).cuda(),
+                        l2=torch.from_numpy(g("l2").astype(np.float32)).cuda())
+    return qb.QLinear(q, [ad])
+
+
+def test_golden_qlinear_fwd_bwd(golden, golden_meta, qb, cuda):
+    for i, case in enumerate(golden_meta["qlinear_cases"]):
+        g = lambda k: golden[f"ql/{i}/{k}"]  # noqa: E731
+        lin = _layer_from_golden(golden, i, case, qb)
+        assert lin.fused()
+        y, cache = lin.forward(torch.from_numpy(g("x").astype(np.float32)))
+        dx, grads = lin.backward(torch.from_numpy(g("dy").astype(np.float32)), cache)
+        torch.cuda.synchronize()
+        assert_tol(y.float().cpu().numpy(), bf16_round(g("y")), f"case {i} y")
+        assert_tol(dx.float().cpu().numpy(), bf16_round(g("dx")), f"case {i} dx")
+        assert_tol(grads["adapter0.l1"].cpu().numpy(), g("dl1"), f"case {i} dl1")
+        assert_tol(grads["adapter0.l2"].cpu().numpy(), g("dl2"), f"case {i} dl2")
+        assert set(grads) == {"adapter0.l1", "adapter0.l2"}
+
+
+def _oracle_case(oracle, m, k, n, r, seed):
+    """Config-C2-style inputs and the fp64 oracle over bf16-rounded operands."""
+    rng = np.random.default_rng(seed)
+    w = (0.02 * rng.standard_normal((k, n))).astype(np.float32)
+    q = oracle.quantize(w, oracle.get_codebook("nf4"), 64, double_quant=True)
+    wd = bf16_round(oracle.dequantize(q).astype(np.float32)).astype(np.float64)
+    x = bf16_round(rng.standard_normal((m, k)))
+    dy = bf16_round(rng.standard_normal((m, n)))
+    l1 = bf16_round(rng.standard_normal((k, r)) / np.sqrt(r))
+    l2 = bf16_round(0.01 * rng.standard_normal((r, n)))
+    ad = oracle.LoraAdapter(r, 16.0, l1.astype(np.float64), l2.astype(np.float64))
+    y, cache = oracle.qlinear_forward(wd, [ad], x.astype(np.float64))
+    dx, grads = oracle.qlinear_backward([ad], dy.astype(np.float64), cache)
+    return w, x, dy, l1, l2, y, dx, grads
+
+
+@pytest.mark.parametrize("m,k,n,r", [(512, 1024, 2048, 64), (300, 512, 704, 16), (2048, 4096, 1024, 64)])
+def test_fused_linear_vs_oracle(m, k, n, r, oracle, qb, cuda):
+    w, x, dy, l1, l2, y, dx, grads = _oracle_case(oracle, m, k, n, r, seed=m + n)
+    q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)
+    ad = qb.LoraAdapter(r, 16.0, torch.from_numpy(l1).cuda(), torch.from_numpy(l2).cuda())
+    lin = qb.QLinear(q, [ad])
+    yg, cache = lin.forward(torch.from_numpy(x))
+    dxg, gg = lin.backward(torch.from_numpy(dy), cache)
+    torch.cuda.synchronize()
+    assert_tol(yg.float().cpu().numpy(), bf16_round(y), "y")
+    assert_tol(dxg.float().cpu().numpy(), bf16_round(dx), "dx")
+    assert_tol(gg["adapter0.l1"].cpu().numpy(), grads["adapter0.l1"], "dl1")
+    assert_tol(gg["adapter0.l2"].cpu().numpy(), grads["adapter0.l2"], "dl2")
+
+
+def test_c2_shape_vs_torch_fp32(qb, cuda):
+    """Config C2 at full size (4096 -> 11008, r = 64, 4x512 tokens) against a
+    plain PyTorch fp32 reference of the same bf16 operands (the fp64 oracle
+    takes minutes at this size)."""
+    m, k, n, r, s = 2048, 4096, 11008, 64, 0.25
+    g = torch.Generator(device="cuda").manual_seed(0)
+    w = torch.randn(k, n, device="cuda", generator=g) * 0.02
+    q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)
+    wd = qb.dequantize(q, torch.bfloat16).float()
+    x = torch.randn(m, k, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(m, n, device="cuda", generator=g).bfloat16()
+    l1 = (torch.randn(k, r, device="cuda", generator=g) / 8).bfloat16().float()
+    l2 = (torch.randn(r, n, device="cuda", generator=g) * 0.01).bfloat16().float()
+    lin = qb.QLinear(q, [qb.LoraAdapter(r, 16.0, l1.clone(), l2.clone())])
+    y, cache = lin.forward(x)
+    dx, gr = lin.backward(dy, cache)
+    t = x.float() @ l1
+    y_ref = x.float() @ wd + s * t @ l2
+    dt = s * dy.float() @ l2.t()
+    dx_ref = dy.float() @ wd.t() + dt @ l1.t()
+    dl2_ref = s * t.t() @ dy.float()
+    dl1_ref = x.float().t() @ dt
+    for got, ref, what in ((y.float(), y_ref.bfloat16().float(), "y"), (dx.float(), dx_ref.bfloat16().float(), "dx"),
+                           (gr["adapter0.l1"], dl1_ref, "dl1"), (gr["adapter0.l2"], dl2_ref, "dl2")):
+        d = (got - ref).abs()
+        mx = (d.max() / ref.abs().max()).item()
+        mn = (d.mean() / ref.abs().mean()).item()
+        assert mx <= MAX_REL and mn <= MEAN_REL, f"{what}: {mx:.3e} {mn:.3e}"
+
+
+def test_no_adapter_dx_is_dy_wT(qb, cuda):
+    """qlora tests :182-194 -- without adapters dX = dY W^T and grads == {}."""
+    g = torch.Generator(device="cuda").manual_seed(4)
+    w = torch.randn(512, 384, device="cuda", generator=g)
+    q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)
+    lin = qb.QLinear(q, [])
+    x = torch.randn(64, 512, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(64, 384, device="cuda", generator=g).bfloat16()
+    y, cache = lin.forward(x)
+    dx, grads = lin.backward(dy, cache)
+    wd = qb.dequantize(q, torch.bfloat16).float()
+    assert grads == {}
+    ref = (dy.float() @ wd.t()).bfloat16().float()
+    d = (dx.float() - ref).abs()
+    assert (d.mean() / ref.abs().mean()).item() <= MEAN_REL
+    ref_y = (x.float() @ wd).bfloat16().float()
+    assert ((y.float() - ref_y).abs().mean() / ref_y.abs().mean()).item() <= MEAN_REL
+
+
+def test_fresh_adapter_is_exact_noop(qb, cuda):
+    rng = np.random.default_rng(3)
+    q = qb.quantize(rng.normal(size=(256, 128)), qb.get_codebook("nf4"), 64, double_quant=True)
+    x = torch.from_numpy(rng.normal(size=(40, 256)).astype(np.float32))
+    plain = qb.QLinear(q, [])
+    adapted = qb.QLinear(q, [qb.lora_init(256, 128, 8, 16.0, rng)])
+    assert torch.equal(plain.forward(x)[0], adapted.forward(x)[0])
+
+
+@pytest.mark.parametrize("k,n", [(8192, 8192), (4096, 11008)])
+def test_gemv_batch1(k, n, oracle, qb, cuda):
+    """Batch-1 GEMV vs the fp64 oracle over the reference's float32 weight."""
+    rng = np.random.default_rng(k + n)
+    w = (0.02 * rng.standard_normal((k, n))).astype(np.float32)
+    q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)
+    wd = qb.dequantize(q, torch.float64).cpu().numpy()
+    x = bf16_round(rng.standard_normal((1, k)))
+    r = 64
+    l1 = bf16_round(rng.standard_normal((k, r)) / 8)
+    l2 = bf16_round(0.01 * rng.standard_normal((r, n)))
+    lin = qb.QLinear(q, [qb.LoraAdapter(r, 16.0, torch.from_numpy(l1).cuda(), torch.from_numpy(l2).cuda())])
+    y, _ = lin.forward(torch.from_numpy(x))
+    ref = x.astype(np.float64) @ wd + 0.25 * (x.astype(np.float64) @ l1) @ l2
+    assert_tol(y.float().cpu().numpy(), bf16_round(ref), "gemv")
+
+
+def test_unfused_shape_path(oracle, qb, cuda):
+    """out_dim % 64 != 0 / non-DQ bases route through dequantize + engine GEMMs."""
+    rng = np.random.default_rng(5)
+    w = (0.05 * rng.standard_normal((96, 100))).astype(np.float32)
+    q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=False)
+    ad = qb.LoraAdapter(4, 8.0, torch.from_numpy((rng.standard_normal((96, 4)) / 2).astype(np.float32)).cuda(),
+                        torch.from_numpy((0.1 * rng.standard_normal((4, 100))).astype(np.float32)).cuda())
+    lin = qb.QLinear(q, [ad])
+    assert not lin.fused()
+    x = bf16_round(rng.standard_normal((17, 96)))
+    dy = bf16_round(rng.standard_normal((17, 100)))
+    y, cache = lin.forward(torch.from_numpy(x))
+    dx, gr = lin.backward(torch.from_numpy(dy), cache)
+    qo = oracle.quantize(w, oracle.get_codebook("nf4"), 64)
+    wd = bf16_round(oracle.dequantize(qo).astype(np.float32)).astype(np.float64)
+    oad = oracle.LoraAdapter(4, 8.0, bf16_round(ad.l1.cpu().numpy()).astype(np.float64),
+                             bf16_round(ad.l2.cpu().numpy()).astype(np.float64))
+    yr, c = oracle.qlinear_forward(wd, [oad], x.astype(np.float64))
+    dxr, grr = oracle.qlinear_backward([oad], dy.astype(np.float64), c)
+    assert_tol(y.float().cpu().numpy(), bf16_round(yr), "y")
+    assert_tol(dx.float().cpu().numpy(), bf16_round(dxr), "dx")
+    assert_tol(gr["adapter0.l1"].cpu().numpy(), grr["adapter0.l1"], "dl1")

@@ -1,0 +1,18 @@
+#!/usr/bin/env bash
+# Build the sm_100a CUDA library in-tree: paper_2305_14314_b200/_lib/libqlrt_b200.so
+set -euo pipefail
+ROOT="$(cd "$(dirname "$0")/.." && pwd)"
+SRC="$ROOT/paper_2305_14314_b200/csrc"
+OUT="$ROOT/paper_2305_14314_b200/_lib"
+mkdir -p "$OUT"
+NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
+FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$ROOT/include -I$SRC ${QLRT_NVCC_EXTRA:-}"
+objs=()
+for f in quant_kernels gemm_sm100 optim_kernels; do
+  "$NVCC" $FLAGS -c "$SRC/$f.cu" -o "$OUT/$f.o" &
+  objs+=("$OUT/$f.o")
+done
+wait
+"$NVCC" -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT/libqlrt_b200.so" "${objs[@]}" -lcudart
+rm -f "${objs[@]}"
+echo "built $OUT/libqlrt_b200.so"

@@ -112,7 +112,8 @@ size_t qlrt_linear_workspace_bytes(int64_t m, int64_t k_in, int64_t n_out, int r
 
 /* forward (qlora.py:124-148):
  *   Ts = s * Xa l1 as a bf16 hi/lo pair [M, 2r] (Ts[:, :r] + Ts[:, r:]; kept for backward)
- *   Y  = X W + Ts_hi l2                 [M, N]   bf16 out, fp32 accumulate
+ *   Y  = X W + (Ts_hi + Ts_lo) l2       [M, N]   bf16 out, fp32 accumulate
+ *        (one augmented K = 2r segment of the same tcgen05 accumulator)
  * X bf16 [M,K]; Xa = the adapter input (X with the dropout mask applied,
  * qlora.py:137-143; NULL -> X); l1 bf16 [K,r], l2 bf16 [r,N]; rank % 8 == 0
  * (callers zero-pad), rank == 0 -> no adapter.  N % 64 == 0, K % 8 == 0. */
@@ -122,7 +123,7 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
 
 /* backward (qlora.py:150-167):
  *   dT  = s * dY l2^T as a bf16 hi/lo pair [M, 2r]
- *   dX  = dY W^T + dT_hi l1^T           [M, K]  bf16
+ *   dX  = dY W^T + (dT_hi + dT_lo) l1^T [M, K]  bf16
  *   dl2 = (Ts_hi + Ts_lo)^T dY          [r, N]  fp32   (= s T^T dY)
  *   dl1 = Xa^T (dT_hi + dT_lo)          [K, r]  fp32   (= s Xa^T dY l2^T)
  * The hi/lo pairs keep the adapter gradients at ~16-bit operand precision.

@@ -636,6 +636,16 @@ static bool weight_ok(const qlrt_nf4_weight* w) {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// bytes of the doubled adapter operand ([l1|l1] or [l2;l2], bf16)
+static size_t dbl_bytes(int64_t k_in, int64_t n_out, int rank) {
+  const int64_t mx = k_in > n_out ? k_in : n_out;
+  return align256((size_t)mx * 2 * rank * 2);
+}
+// the doubled-operand region sits at the end of the linear workspace
+static void* dbl_region(void* ws, size_t ws_bytes, int64_t k_in, int64_t n_out, int rank) {
+  return (uint8_t*)ws + (ws_bytes - dbl_bytes(k_in, n_out, rank));
+}
+
 }  // namespace gemm
 }  // namespace qlrt
 
@@ -652,7 +662,7 @@ size_t qlrt_linear_workspace_bytes(int64_t m, int64_t k_in, int64_t n_out, int r
   mx = mx > c ? mx : c;
   int64_t gemv = 32 * (n_out > k_in ? n_out : k_in) + 64 * ((r + 63) / 64) + 16 * r + 256;
   mx = mx > gemv ? mx : gemv;
-  return gemm::align256((size_t)mx * 4) + 4096;
+  return gemm::align256((size_t)mx * 4) + 4096 + gemm::dbl_bytes(k_in, n_out, rank > 0 ? rank : 0);
 }
 
 qlrt_status qlrt_gemm_bf16(const void* a, const void* b, void* d, int64_t m, int64_t n, int64_t k, int a_mn, int b_mn,
@@ -674,12 +684,13 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t K = w->k_in, N = w->n_out;
   const size_t ws_bytes = qlrt_linear_workspace_bytes(m, K, N, rank);
+  const size_t part_bytes = ws_bytes - gemm::dbl_bytes(K, N, rank);
   qlrt_status rc;
   if (rank > 0) {
     // Ts[m, 0:r] + Ts[m, r:2r] = s * Xa l1 as a bf16 hi/lo pair:
     //   A = Xa (K-major, [m][K]), B = l1 (MN-major, [K][r])
     Operand A{xa ? xa : x, K, 0}, B{l1, rank, 1};
-    rc = gemm::plain(64, A, B, m, rank, K, s, ts_out, 2 * rank, 0, 0, (float*)workspace, ws_bytes, st, 0, rank);
+    rc = gemm::plain(64, A, B, m, rank, K, s, ts_out, 2 * rank, 0, 0, (float*)workspace, part_bytes, st, 0, rank);
     if (rc != QLRT_OK) return rc;
   }
   // Y^T[N, m] = W^T X^T (+ l2^T Ts^T): A = NF4 (MN-major image), B = X (K-major)
@@ -694,8 +705,15 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   a.alpha = 1.0f;
   gemm::fill_nf4(a, w, 1);
   Operand none{}, B{x, K, 0};
-  Operand A2{l2, N, 1}, B2{ts_out, 2 * rank, 0};  // the hi half (K2 = r, pitch 2r)
-  return gemm::run(256, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, K, rank, a, st);
+  // augmented segment K2 = 2r: [l2 ; l2]^T [Ts_hi | Ts_lo]^T, i.e. the pair at ~16-bit precision
+  __nv_bfloat16* l2d = (__nv_bfloat16*)gemm::dbl_region(workspace, ws_bytes, K, N, rank);
+  if (rank) {
+    if (cudaMemcpyAsync(l2d, l2, (size_t)rank * N * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(l2d + (size_t)rank * N, l2, (size_t)rank * N * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return QLRT_ERR_CUDA;
+  }
+  Operand A2{l2d, N, 1}, B2{ts_out, 2 * rank, 0};
+  return gemm::run(256, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, K, 2 * rank, a, st);
 }
 
 qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_t m, const void* x, const void* ts,
@@ -706,12 +724,13 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t K = w->k_in, N = w->n_out;
   const size_t ws_bytes = qlrt_linear_workspace_bytes(m, K, N, rank);
+  const size_t part_bytes = ws_bytes - gemm::dbl_bytes(K, N, rank);
   qlrt_status rc;
   if (rank > 0) {
     // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):
     //   A = dY (K-major [m][N]), B = l2 (K-major [r][N])
     Operand A{dy, N, 0}, B{l2, N, 0};
-    rc = gemm::plain(64, A, B, m, rank, N, s, dt_out, 2 * rank, 0, 0, (float*)workspace, ws_bytes, st, 0, rank);
+    rc = gemm::plain(64, A, B, m, rank, N, s, dt_out, 2 * rank, 0, 0, (float*)workspace, part_bytes, st, 0, rank);
     if (rc != QLRT_OK) return rc;
   }
   // dX^T[K, m] = W dY^T (+ l1 dT^T): A = NF4 (K-major image), B = dY (K-major)
@@ -726,22 +745,30 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   a.alpha = 1.0f;
   gemm::fill_nf4(a, w, 2);
   Operand none{}, B{dy, N, 0};
-  Operand A2{l1, rank, 0}, B2{dt_out, 2 * rank, 0};
-  rc = gemm::run(256, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, N, rank, a, st);
+  // augmented segment K2 = 2r: [l1 | l1] [dT_hi | dT_lo]^T
+  __nv_bfloat16* l1d = (__nv_bfloat16*)gemm::dbl_region(workspace, ws_bytes, K, N, rank);
+  if (rank) {
+    for (int h = 0; h < 2; ++h)
+      if (cudaMemcpy2DAsync(l1d + h * rank, (size_t)4 * rank, l1, (size_t)2 * rank, (size_t)2 * rank, (size_t)K,
+                            cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return QLRT_ERR_CUDA;
+  }
+  Operand A2{l1d, 2 * rank, 0}, B2{dt_out, 2 * rank, 0};
+  rc = gemm::run(256, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, N, 2 * rank, a, st);
   if (rc != QLRT_OK || rank == 0) return rc;
   // dl2^T[N, r] = dY^T (Ts_hi + Ts_lo): A = dY (MN-major [m][N]), B = [Ts_hi | Ts_lo] (MN-major [m][2r]);
   // the pair is folded in the reduction, stored transposed into dl2[r][N]
   {
     Operand A{dy, N, 1}, B{ts, 2 * rank, 1};
     rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, N, 2 * rank, m, 1.0f, dl2, N, 1, 1, (float*)workspace,
-                     ws_bytes, st, rank);
+                     part_bytes, st, rank);
     if (rc != QLRT_OK) return rc;
   }
   // dl1[K, r] = Xa^T (dT_hi + dT_lo): A = Xa (MN-major [m][K]), B = [dT_hi | dT_lo] (MN-major [m][2r])
   {
     Operand A{x, K, 1}, B{dt_out, 2 * rank, 1};
     rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, K, 2 * rank, m, 1.0f, dl1, rank, 1, 0, (float*)workspace,
-                     ws_bytes, st, rank);
+                     part_bytes, st, rank);
   }
   return rc;
 }

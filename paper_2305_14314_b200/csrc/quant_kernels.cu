@@ -240,30 +240,59 @@ __global__ void codes_generic_kernel(const T* __restrict__ x, int64_t n, int bs,
 // double quantization (doublequant.py:148-187)
 // ---------------------------------------------------------------------------
 
-// numpy pairwise_sum (loops_utils.h.src) of float32 values widened to fp64;
-// recursive form for the (at most one) partial 8192-chunk.
-__device__ double pairwise_seq(const float* a, int n) {
+// numpy pairwise_sum (loops_utils.h.src) of float32 values widened to fp64,
+// for the (at most one) partial 8192-chunk.  The recursion
+//   n <  8   : sequential;   n <= 128 : 8 strided accumulators + tail;
+//   otherwise: split at n/2 - (n/2 % 8), left + right
+// runs on an explicit stack (no device recursion / dynamic stack).
+__device__ double pairwise_leaf(const float* a, int n) {
   if (n < 8) {
     double s = 0.0;
     for (int i = 0; i < n; ++i) s = __dadd_rn(s, (double)a[i]);
     return s;
   }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = (double)a[j];
-    int m = n - n % 8;
-    for (int i = 8; i < m; i += 8)
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], (double)a[i + j]);
-    double s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (int i = m; i < n; ++i) s = __dadd_rn(s, (double)a[i]);
-    return s;
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = (double)a[j];
+  const int m = n - n % 8;
+  for (int i = 8; i < m; i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], (double)a[i + j]);
+  double s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                       __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (int i = m; i < n; ++i) s = __dadd_rn(s, (double)a[i]);
+  return s;
+}
+
+__device__ double pairwise_seq(const float* a, int n) {
+  int off[32], len[32], stage[32];
+  double left[32];
+  int sp = 0;
+  off[0] = 0; len[0] = n; stage[0] = 0;
+  double ret = 0.0;
+  while (true) {
+    const int L = len[sp];
+    if (L <= 128) {
+      ret = pairwise_leaf(a + off[sp], L);
+      if (sp == 0) return ret;
+      --sp;
+      continue;
+    }
+    int n2 = L / 2;
+    n2 -= n2 % 8;
+    if (stage[sp] == 0) {
+      stage[sp] = 1;
+      ++sp;
+      off[sp] = off[sp - 1]; len[sp] = n2; stage[sp] = 0;
+    } else if (stage[sp] == 1) {
+      left[sp] = ret;
+      stage[sp] = 2;
+      ++sp;
+      off[sp] = off[sp - 1] + n2; len[sp] = L - n2; stage[sp] = 0;
+    } else {
+      ret = __dadd_rn(left[sp], ret);
+      if (sp == 0) return ret;
+      --sp;
+    }
   }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  double l = pairwise_seq(a, n2);
-  double r = pairwise_seq(a + n2, n - n2);
-  return __dadd_rn(l, r);
 }
 
 // One CTA (64 threads) per 8192-constant buffer chunk.  A full chunk is a

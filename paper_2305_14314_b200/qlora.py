@@ -184,7 +184,8 @@ class QLinear:
             if ad is not None:
                 l1b, l2b = ad.bf16_operands()
                 _split_into(gemm_bf16(xa, l1b, alpha=ad.scaling, out_dtype=torch.float32), ts)
-                y += gemm_bf16(ts[:, :rp], l2b)
+                y.copy_((y.float() + gemm_bf16(ts[:, :rp], l2b, out_dtype=torch.float32)
+                         + gemm_bf16(ts[:, rp:], l2b, out_dtype=torch.float32)).to(self.dtype))
         cache = {"x": x2, "xa": xa, "ts": ts, "mask": mask, "lead": lead}
         return y.reshape(*lead, self.out_dim), cache
 
@@ -221,7 +222,8 @@ class QLinear:
                 gemm_bf16(d_y, w, out=d_x, b_t=True)
             if ad is not None:
                 _split_into(gemm_bf16(d_y, l2b, alpha=ad.scaling, b_t=True, out_dtype=torch.float32), dt)
-                d_xa = gemm_bf16(dt[:, :rp], l1b, b_t=True, out_dtype=torch.float32)
+                d_xa = (gemm_bf16(dt[:, :rp], l1b, b_t=True, out_dtype=torch.float32)
+                        + gemm_bf16(dt[:, rp:], l1b, b_t=True, out_dtype=torch.float32))
                 if mask is not None:
                     d_xa = d_xa * mask
                 d_x.copy_((d_x.float() + d_xa).to(self.dtype))

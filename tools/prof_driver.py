@@ -1,0 +1,44 @@
+"""Small drivers for ncu captures: one op family per invocation."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2305_14314_b200 as qb  # noqa: E402
+
+
+def main(which: str) -> None:
+    dev = torch.device("cuda", 0)
+    cb = qb.get_codebook("nf4")
+    if which in ("gemm_fwd", "gemm_bwd", "linear"):
+        w = torch.randn(4096, 11008, device=dev) * 0.02
+        q = qb.quantize(w, cb, 64, double_quant=True)
+        x = torch.randn(2048, 4096, device=dev).bfloat16()
+        dy = torch.randn(2048, 11008, device=dev).bfloat16()
+        ad = qb.LoraAdapter(64, 16.0, torch.randn(4096, 64, device=dev) / 8, torch.randn(64, 11008, device=dev) * .01)
+        lin = qb.QLinear(q, [ad] if which == "linear" else [])
+        for _ in range(4):
+            y, c = lin.forward(x)
+            if which != "gemm_fwd":
+                lin.backward(dy, c)
+    elif which == "dequant":
+        x = torch.randn(4096, 4096, device=dev)
+        q = qb.quantize(x, cb, 64, double_quant=True)
+        for _ in range(4):
+            qb.dequantize(q, torch.bfloat16)
+    elif which == "quantize":
+        x = torch.randn(4096, 4096, device=dev)
+        for _ in range(4):
+            qb.quantize(x, cb, 64, double_quant=True)
+    elif which == "gemv":
+        w = torch.randn(8192, 22016, device=dev) * 0.02
+        lin = qb.QLinear(qb.quantize(w, cb, 64, double_quant=True), [])
+        xv = torch.randn(1, 8192, device=dev).bfloat16()
+        for _ in range(4):
+            lin.forward(xv)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])

@@ -106,13 +106,11 @@ def unpack_codes(packed, k: int, count: int) -> torch.Tensor:
     return out
 
 
-def quantize(x, codebook: Codebook, blocksize: int = 64, double_quant: bool = False, blocksize2: int = 256,
-             fp8_spec: Fp8Spec | None = None) -> BlockQuantized:
-    """Block-wise absmax quantization against ``codebook`` (blockquant.py:132-195).
-
-    Raises ``ValueError`` for an empty tensor, ``blocksize < 1`` and the first
-    non-finite flat index -- the reference's messages.
-    """
+def quantize_async(x, codebook: Codebook, blocksize: int = 64, double_quant: bool = False, blocksize2: int = 256,
+                   fp8_spec: Fp8Spec | None = None):
+    """Launch-only quantize (no host sync, CUDA-graph capturable): returns the
+    ``BlockQuantized`` and the device int64 holding the first non-finite flat
+    index (0x7F7F... when none).  :func:`quantize` adds the check."""
     L = lib()  # no CUDA library / device -> RuntimeError before touching the data
     shape = tuple(x.shape) if hasattr(x, "shape") else ()
     xt = _as_input(x)
@@ -122,6 +120,8 @@ def quantize(x, codebook: Codebook, blocksize: int = 64, double_quant: bool = Fa
         raise ValueError(f"blocksize must be >= 1, got {blocksize}")
     if codebook.bits != 4:
         raise ValueError(f"the GPU quantizer handles 4-bit codebooks only, got k={codebook.bits}")
+    if double_quant and blocksize2 < 1:
+        raise ValueError(f"blocksize2 must be >= 1, got {blocksize2}")
     n = xt.numel()
     nb = (n + blocksize - 1) // blocksize
     n_pad = nb * blocksize
@@ -130,17 +130,25 @@ def quantize(x, codebook: Codebook, blocksize: int = 64, double_quant: bool = Fa
     bad = torch.empty(1, dtype=torch.int64, device=xt.device)
     check(L.qlrt_quantize4(ptr(xt), _IN_DTYPES[xt.dtype], n, blocksize, codebook.to_c(), ptr(codes), ptr(absmax),
                            ptr(bad), stream_ptr()), "quantize")
-    first = int(bad.item())
-    if first < n:
-        raise ValueError(f"non-finite input at flat index {first}")
     codes = codes[: (n_pad + 1) // 2]
-    dq = None
-    if double_quant:
-        if blocksize2 < 1:
-            raise ValueError(f"blocksize2 must be >= 1, got {blocksize2}")
-        dq = _dq_compress_unchecked(absmax, blocksize2, fp8_spec or Fp8Spec())
-    return BlockQuantized(shape=shape, blocksize=blocksize, codebook=codebook, codes=codes,
-                          constants=None if double_quant else absmax, dq=dq)
+    dq = _dq_compress_unchecked(absmax, blocksize2, fp8_spec or Fp8Spec()) if double_quant else None
+    q = BlockQuantized(shape=shape, blocksize=blocksize, codebook=codebook, codes=codes,
+                       constants=None if double_quant else absmax, dq=dq)
+    return q, bad
+
+
+def quantize(x, codebook: Codebook, blocksize: int = 64, double_quant: bool = False, blocksize2: int = 256,
+             fp8_spec: Fp8Spec | None = None) -> BlockQuantized:
+    """Block-wise absmax quantization against ``codebook`` (blockquant.py:132-195).
+
+    Raises ``ValueError`` for an empty tensor, ``blocksize < 1`` and the first
+    non-finite flat index -- the reference's messages (one host sync).
+    """
+    q, bad = quantize_async(x, codebook, blocksize, double_quant, blocksize2, fp8_spec)
+    first = int(bad.item())
+    if first < q.numel:
+        raise ValueError(f"non-finite input at flat index {first}")
+    return q
 
 
 def dequantize(q: BlockQuantized, dtype: torch.dtype = torch.float64) -> torch.Tensor:
@@ -174,4 +182,4 @@ def dequantize(q: BlockQuantized, dtype: torch.dtype = torch.float64) -> torch.T
     return out.reshape(q.shape)
 
 
-__all__ = ["BlockQuantized", "quantize", "dequantize", "pack_codes", "unpack_codes"]
+__all__ = ["BlockQuantized", "quantize", "quantize_async", "dequantize", "pack_codes", "unpack_codes"]

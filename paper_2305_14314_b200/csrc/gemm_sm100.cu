@@ -44,6 +44,7 @@ struct Args {
   const float* absmax;  // plain constants if dq_codes == nullptr
   int64_t w_rows, w_cols;
   int bs2;
+  int bs2_shift;        // log2(bs2) when bs2 is a power of two, else -1
   qlrt_fp8spec spec;
   double values[16];
   // output
@@ -57,14 +58,22 @@ struct Args {
   int fold;             // reduce: out[:, n] = D[:, n] + D[:, n + fold] for n < fold
 };
 
-template <int BN>
+template <int BN, bool NF4>
 struct Smem {
   static constexpr int B_STAGE = BN * BK * 2;
-  static constexpr int STAGE = A_STAGE + B_STAGE;
-  static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);  // even: a stage is always refilled by the same dequant group
-  static constexpr int BAR_OFF = STAGES * STAGE;
+  static constexpr int C_STAGE = NF4 ? 4096 : 0;  // packed NF4 codes of one A stage (128 x 64 nibbles)
+  static constexpr int STAGE = A_STAGE + B_STAGE + C_STAGE;
+  static constexpr int EPI_BYTES = kNumEpiWarps * 32 * 32 * 2;  // 32x32 bf16 transpose tile per warp
+  // as many stages as fit in ~220 KB, at most 8, even (a stage is always
+  // refilled by the same dequant group)
+  static constexpr int FIT = (220 * 1024 - EPI_BYTES) / STAGE;
+  static constexpr int STAGES = (FIT > 8 ? 8 : FIT) & ~1;
+  static constexpr int C_OFF = STAGES * (A_STAGE + B_STAGE);
+  static constexpr int EPI_OFF = STAGES * STAGE;
+  static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
   // full[S], afull[S], empty[S], tmem_full[2], tmem_empty[2], tmem_ptr
   static constexpr int BYTES = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
+  static_assert(STAGES >= 2 && BYTES <= 232448, "shared memory budget");
 };
 
 __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int& mt, int& nt, int& z) {
@@ -75,20 +84,30 @@ __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int
   nt = r - mt * n_tiles;
 }
 
+// exact decode of the DQ 8-bit float by assembling the fp64 bit pattern
+__device__ __forceinline__ double fp8_decode_bits(unsigned b, const qlrt_fp8spec& sp, double sub_scale) {
+  const unsigned M = sp.mant_bits;
+  const unsigned e = (b >> M) & ((1u << sp.exp_bits) - 1u);
+  const unsigned m = b & ((1u << M) - 1u);
+  double mag;
+  if (e == 0) {
+    mag = (double)m * sub_scale;  // m * 2^(1-B-M), exact
+  } else {
+    const unsigned long long bits = ((unsigned long long)(e - sp.bias + 1023) << 52) |
+                                    ((unsigned long long)m << (52 - M));
+    mag = __longlong_as_double((long long)bits);
+  }
+  return (b >> 7) ? -mag : mag;
+}
+
 // ---------------------------------------------------------------------------
 // NF4 -> bf16 tile producer helpers
 // ---------------------------------------------------------------------------
-// 16-entry table bf16(f32(v_i * c)) split into lo/hi byte planes (4 regs each)
-__device__ __forceinline__ void build_planes(const double* vals, float c, uint32_t (&L)[4],
-                                             uint32_t (&H)[4]) {
-  const double cd = (double)c;
+// 16-entry table bf16(v_i * c) (fp32 product) split into lo/hi byte planes (4 regs each)
+__device__ __forceinline__ void build_planes(const float (&v)[16], float c, uint32_t (&L)[4], uint32_t (&H)[4]) {
   uint32_t P[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    float a = __double2float_rn(__dmul_rn(vals[2 * j], cd));
-    float b = __double2float_rn(__dmul_rn(vals[2 * j + 1], cd));
-    P[j] = pack_bf16x2(a, b);
-  }
+  for (int j = 0; j < 8; ++j) P[j] = pack_bf16x2(v[2 * j] * c, v[2 * j + 1] * c);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     L[q] = ptx::prmt(P[2 * q], P[2 * q + 1], 0x6420);
@@ -179,13 +198,15 @@ template <int BN, bool NF4>
 __global__ void __launch_bounds__(NF4 ? 448 : 192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
-                const __grid_constant__ Args p) {
-  using L = Smem<BN>;
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ Args p) {
+  using L = Smem<BN, NF4>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE;
+  uint8_t* sC = smem + L::C_OFF;                       // packed codes per stage (NF4)
+  __nv_bfloat16* sE = reinterpret_cast<__nv_bfloat16*>(smem + L::EPI_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* full = bars;
   uint64_t* afull = bars + STAGES;
@@ -205,6 +226,7 @@ __global__ void __launch_bounds__(NF4 ? 448 : 192, 1)
   if (warp == kTmaWarp && lane == 0) {
     ptx::prefetch_tmap(&tmB);
     if (!NF4) ptx::prefetch_tmap(&tmA);
+    if (NF4) ptx::prefetch_tmap(&tmC);
     if (p.k_iters_aug) { ptx::prefetch_tmap(&tmA2); ptx::prefetch_tmap(&tmB2); }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
@@ -244,9 +266,15 @@ __global__ void __launch_bounds__(NF4 ? 448 : 192, 1)
           const int bmn = aug ? p.b2_mn : p.b_mn;
           const int k0 = (aug ? (i - nk) : (kb + i)) * BK;
           const bool a_tma = aug || !NF4;
-          ptx::mbar_arrive_expect_tx(&full[s], L::B_STAGE + (a_tma ? A_STAGE : 0));
+          ptx::mbar_arrive_expect_tx(&full[s], L::B_STAGE + (a_tma ? A_STAGE : L::C_STAGE));
           uint8_t* a_dst = sA + s * A_STAGE;
           uint8_t* b_dst = sB + s * L::B_STAGE;
+          if (!a_tma) {
+            // packed NF4 codes of the A tile: fwd  W[k0:k0+64, m0:m0+128] -> 64 rows x 64 B
+            //                                 bwd  W[m0:m0+128, k0:k0+64] -> 128 rows x 32 B
+            if (p.nf4_mode == 1) ptx::tma_load_2d(&tmC, &full[s], sC + s * L::C_STAGE, mt * BM / 2, k0);
+            else ptx::tma_load_2d(&tmC, &full[s], sC + s * L::C_STAGE, k0 / 2, mt * BM);
+          }
           if (a_tma) {
             if (amn) {
               ptx::tma_load_2d(ma, &full[s], a_dst, mt * BM, k0);
@@ -324,7 +352,33 @@ __global__ void __launch_bounds__(NF4 ? 448 : 192, 1)
         uint32_t r[EC];
         ptx::tmem_ld<EC>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, r);
         const int64_t n0 = (int64_t)nt * BN + c0;
-        if (m < p.M) store_chunk<EC>(p, r, m, n0, z);
+        if (EC == 32 && p.out_t && !p.out_f32 && p.splits == 1 && !p.to_ws) {
+          // D^T tile through shared memory: row j = token n0+j, 32 features per row,
+          // then 16B vector stores (4 lanes cover one 64B output row segment)
+          __nv_bfloat16* st = sE + (warp - kEpiWarp0) * 32 * 32;
+#pragma unroll
+          for (int j = 0; j < EC; ++j) st[j * 32 + lane] = __float2bfloat16_rn(__uint_as_float(r[j]) * p.alpha);
+          __syncwarp();
+          const int64_t mcol = (int64_t)mt * BM + quarter * 32 + (lane & 3) * 8;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int rr = q * 8 + (lane >> 2);
+            const int64_t n = n0 + rr;
+            const uint4 v = *reinterpret_cast<const uint4*>(st + rr * 32 + (lane & 3) * 8);
+            if (n < p.N) {
+              __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + n * p.ldo + mcol;
+              if (mcol + 8 <= p.M && (p.ldo & 7) == 0) {
+                *reinterpret_cast<uint4*>(o) = v;
+              } else {
+                const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+                for (int u = 0; u < 8 && mcol + u < p.M; ++u) o[u] = e[u];
+              }
+            }
+          }
+          __syncwarp();
+        } else if (m < p.M) {
+          store_chunk<EC>(p, r, m, n0, z);
+        }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
@@ -334,69 +388,106 @@ __global__ void __launch_bounds__(NF4 ? 448 : 192, 1)
     const int xw = warp - kXfWarp0;
     const int grp = xw >> 2;                 // two groups alternate stages
     const int item = (xw & 3) * 32 + lane;   // 0..127: one 64-element W block per stage
-    double vals[16];
+    float vals[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) vals[i] = p.values[i];
+    for (int i = 0; i < 16; ++i) vals[i] = (float)p.values[i];
     const float mu = p.dq_codes ? *p.mu : 0.0f;
-    uint32_t it = 0;
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
-      int mt, nt, z;
-      tile_coords(t, m_tiles, n_tiles, mt, nt, z);
-      const int kb = z * kc;
-      const int nk = min(kc, p.k_iters - kb);
-      const int total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
-      for (int i = 0; i < total; ++i) {
-        const uint32_t my_it = it + i;
-        if ((int)(my_it & 1) != grp) continue;
-        const int s = my_it % STAGES;
-        const uint32_t ph = (my_it / STAGES) & 1;
-        if (i >= nk) {  // augmented (TMA-fed) stage: keep afull's phase in step
-          ptx::mbar_wait(&empty[s], ph ^ 1);
-          ptx::mbar_arrive(&afull[s]);
-          continue;
+    const double sub_scale = ldexp(1.0, 1 - p.spec.bias - p.spec.mant_bits);
+    // fwd: item -> (h = item & 1, r = item >> 1): A image at h*8192 + r*128,
+    //      codes at r*64 + h*32 (W row k0+r, cols m0+64h..+64)
+    // bwd: item -> W row m0+item, cols k0..k0+64: A image item*128, codes item*32
+    const int h = item & 1, rr = item >> 1;
+    const uint32_t soff = p.nf4_mode == 1 ? (uint32_t)(h * 8192 + rr * 128) : (uint32_t)(item * 128);
+    const uint32_t coff = (uint32_t)item * 32;
+    const uint32_t swz = (soff >> 7) & 7;
+    // cursor over (tile, k-iteration); this group handles global iterations it with it % 2 == grp
+    int t = blockIdx.x, i = 0, total = 0, nk = 0, mt = 0, kb = 0;
+    auto enter = [&](int tt) {
+      int nt_, z_;
+      tile_coords(tt, m_tiles, n_tiles, mt, nt_, z_);
+      kb = z_ * kc;
+      nk = min(kc, p.k_iters - kb);
+      total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
+    };
+    // block constant of this thread's item in iteration (mt, kb + i): loads only
+    auto fetch = [&](int mt_, int kk, uint32_t& dqb, float& c1v, bool& live) {
+      const int64_t kg = (int64_t)kk * BK;
+      const int64_t wr = p.nf4_mode == 1 ? kg + rr : (int64_t)mt_ * BM + item;
+      const int64_t wc = p.nf4_mode == 1 ? (int64_t)mt_ * BM + h * 64 : kg;
+      live = wr < p.w_rows && wc < p.w_cols;
+      dqb = 0;
+      c1v = 0.0f;
+      if (live) {
+        const int64_t blk = (wr * p.w_cols + wc) >> 6;
+        if (p.dq_codes) {
+          dqb = __ldg(p.dq_codes + blk);
+          c1v = __ldg(p.c1 + (p.bs2_shift >= 0 ? (blk >> p.bs2_shift) : blk / p.bs2));
+        } else {
+          c1v = __ldg(p.absmax + blk);
         }
-        const int64_t kg = (int64_t)(kb + i) * BK;
-        int64_t wr, wc;
-        uint32_t soff;
-        if (p.nf4_mode == 1) {  // A = W^T: M = W cols, K = W rows; MN-major image
-          const int h = item >> 6, r = item & 63;
-          wr = kg + r;
-          wc = (int64_t)mt * BM + h * 64;
-          soff = h * 8192 + r * 128;
-        } else {                // A = W: M = W rows, K = W cols; K-major image
-          wr = (int64_t)mt * BM + item;
-          wc = kg;
-          soff = item * 128;
-        }
-        const bool live = wr < p.w_rows && wc < p.w_cols;
-        uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0;
-        float c = 0.0f;
-        if (live) {
-          const int64_t e0 = wr * p.w_cols + wc;
-          const uint8_t* src = p.codes + (e0 >> 1);
-          w0 = ptx::ld_nc_v4(src);
-          w1 = ptx::ld_nc_v4(src + 16);
-          const int64_t blk = e0 >> 6;
-          c = p.dq_codes ? dq_constant(__ldg(p.dq_codes + blk), __ldg(p.c1 + blk / p.bs2), mu, p.spec)
-                         : __ldg(p.absmax + blk);
-        }
-        uint32_t Lp[4], Hp[4];
-        build_planes(vals, c, Lp, Hp);
-        ptx::mbar_wait(&empty[s], ph ^ 1);
-        const uint32_t base = ptx::smem_u32(sA + s * A_STAGE) + soff;
-        const uint32_t swz = (soff >> 7) & 7;
-        const uint32_t words[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          uint32_t o0, o1, o2, o3;
-          lookup4(words[ch], Lp, Hp, o0, o1);
-          lookup4(words[ch] >> 16, Lp, Hp, o2, o3);
-          ptx::st_shared_v4(base + ((ch ^ swz) << 4), o0, o1, o2, o3);
-        }
-        ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&afull[s]);
       }
-      it += total;
+    };
+    if (t < n_tiles_total) enter(t);
+    uint32_t it = 0;
+    // advance to the first handled iteration
+    auto step = [&]() {
+      ++it;
+      if (++i >= total) {
+        i = 0;
+        t += gridDim.x;
+        if (t < n_tiles_total) enter(t);
+      }
+    };
+    if ((int)(it & 1) != grp && t < n_tiles_total) step();
+    uint32_t dqb = 0;
+    float c1v = 0.0f;
+    bool live = false;
+    if (t < n_tiles_total && i < nk) fetch(mt, kb + i, dqb, c1v, live);
+    while (t < n_tiles_total) {
+      const int s = it % STAGES;
+      const uint32_t ph = (it / STAGES) & 1;
+      const bool main_it = i < nk;
+      const int cur_mt = mt;
+      (void)cur_mt;
+      const uint32_t cur_dqb = dqb;
+      const float cur_c1 = c1v;
+      const bool cur_live = live;
+      // move the cursor two iterations ahead and prefetch that item's constant
+      step();
+      if (t < n_tiles_total) step();
+      if (t < n_tiles_total && i < nk) fetch(mt, kb + i, dqb, c1v, live);
+      if (!main_it) {  // augmented (TMA-fed) stage: keep afull's phase in step
+        ptx::mbar_wait(&empty[s], ph ^ 1);
+        ptx::mbar_arrive(&afull[s]);
+        continue;
+      }
+      float c = 0.0f;
+      if (cur_live) {
+        if (p.dq_codes) {
+          double d = fp8_decode_bits(cur_dqb, p.spec, sub_scale);
+          double rcon = __dadd_rn(__dmul_rn(d, (double)cur_c1), (double)mu);
+          c = __double2float_rn(rcon > 0.0 ? rcon : 0.0);
+        } else {
+          c = cur_c1;
+        }
+      }
+      uint32_t Lp[4], Hp[4];
+      build_planes(vals, c, Lp, Hp);
+      ptx::mbar_wait(&full[s], ph);  // codes (and B) landed; implies the A slot is free
+      const uint8_t* cs = sC + s * L::C_STAGE + coff;
+      const uint4 w0 = *reinterpret_cast<const uint4*>(cs);
+      const uint4 w1 = *reinterpret_cast<const uint4*>(cs + 16);
+      const uint32_t base = ptx::smem_u32(sA + s * A_STAGE) + soff;
+      const uint32_t words[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        uint32_t o0, o1, o2, o3;
+        lookup4(words[ch], Lp, Hp, o0, o1);
+        lookup4(words[ch] >> 16, Lp, Hp, o2, o3);
+        ptx::st_shared_v4(base + ((ch ^ swz) << 4), o0, o1, o2, o3);
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::mbar_arrive(&afull[s]);
     }
   }
 
@@ -488,6 +579,21 @@ static bool make_tmap(CUtensorMap* m, const void* base, int64_t inner, int64_t o
   return r == CUDA_SUCCESS;
 }
 
+// packed NF4 codes viewed as a uint8 matrix [rows][bytes], no swizzle
+static bool make_tmap_u8(CUtensorMap* m, const void* base, int64_t inner_bytes, int64_t rows, int box_inner,
+                         int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || (((uintptr_t)base) & 15) || (inner_bytes & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner_bytes, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)inner_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // One GEMM operand.  K-major: stored [rows][K] (pitch ld); MN-major: stored [K][rows].
 struct Operand {
   const void* ptr = nullptr;
@@ -507,8 +613,8 @@ static int num_sms() {
 
 template <int BN, bool NF4>
 static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2, const CUtensorMap& b2,
-                            const Args& args, cudaStream_t s) {
-  using L = Smem<BN>;
+                            const CUtensorMap& c, const Args& args, cudaStream_t s) {
+  using L = Smem<BN, NF4>;
   auto kern = gemm_kernel<BN, NF4>;
   static bool attr = false;
   if (!attr) {
@@ -519,7 +625,7 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
   const int m_tiles = (args.M + BM - 1) / BM, n_tiles = (args.N + BN - 1) / BN;
   const int tiles = m_tiles * n_tiles * args.splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, NF4 ? 448 : 192, L::BYTES, s>>>(a, b, a2, b2, args);
+  kern<<<grid, NF4 ? 448 : 192, L::BYTES, s>>>(a, b, a2, b2, c, args);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }
@@ -534,8 +640,17 @@ static int effective_splits(int splits, int k_iters) {
 // args.nf4_mode != 0 makes A the quantized weight (A operand ignored).
 static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand* A2, const Operand* B2, int64_t K,
                        int64_t K2, Args args, cudaStream_t s) {
-  CUtensorMap ta{}, tb{}, ta2{}, tb2{};
+  CUtensorMap ta{}, tb{}, ta2{}, tb2{}, tc{};
   const bool nf4 = args.nf4_mode != 0;
+  if (nf4) {
+    // packed codes as a uint8 matrix [w_rows][w_cols/2]
+    const bool ok = args.nf4_mode == 1 ? make_tmap_u8(&tc, args.codes, args.w_cols / 2, args.w_rows, 64, 64)
+                                       : make_tmap_u8(&tc, args.codes, args.w_cols / 2, args.w_rows, 32, 128);
+    if (!ok) return QLRT_ERR_UNSUPPORTED;
+    args.bs2_shift = (args.bs2 > 0 && (args.bs2 & (args.bs2 - 1)) == 0) ? __builtin_ctz((unsigned)args.bs2) : -1;
+  } else {
+    tc = tb;
+  }
   const int64_t M = args.M, N = args.N;
   if (bn < 64 && (B.mn || (B2 && B2->mn))) return QLRT_ERR_UNSUPPORTED;
   if (!nf4 && !(A.mn ? make_tmap(&ta, A.ptr, M, K, A.ld, 64) : make_tmap(&ta, A.ptr, K, M, A.ld, BM)))
@@ -560,10 +675,10 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   args.splits = effective_splits(args.splits, args.k_iters);
   if (args.splits > 1 && K2) return QLRT_ERR_UNSUPPORTED;
   switch (bn) {
-    case 256: return nf4 ? launch_t<256, true>(ta, tb, ta2, tb2, args, s) : launch_t<256, false>(ta, tb, ta2, tb2, args, s);
-    case 128: return nf4 ? launch_t<128, true>(ta, tb, ta2, tb2, args, s) : launch_t<128, false>(ta, tb, ta2, tb2, args, s);
-    case 64: return nf4 ? launch_t<64, true>(ta, tb, ta2, tb2, args, s) : launch_t<64, false>(ta, tb, ta2, tb2, args, s);
-    case 16: return nf4 ? launch_t<16, true>(ta, tb, ta2, tb2, args, s) : launch_t<16, false>(ta, tb, ta2, tb2, args, s);
+    case 256: return nf4 ? launch_t<256, true>(ta, tb, ta2, tb2, tc, args, s) : launch_t<256, false>(ta, tb, ta2, tb2, tc, args, s);
+    case 128: return nf4 ? launch_t<128, true>(ta, tb, ta2, tb2, tc, args, s) : launch_t<128, false>(ta, tb, ta2, tb2, tc, args, s);
+    case 64: return nf4 ? launch_t<64, true>(ta, tb, ta2, tb2, tc, args, s) : launch_t<64, false>(ta, tb, ta2, tb2, tc, args, s);
+    case 16: return nf4 ? launch_t<16, true>(ta, tb, ta2, tb2, tc, args, s) : launch_t<16, false>(ta, tb, ta2, tb2, tc, args, s);
   }
   return QLRT_ERR_UNSUPPORTED;
 }

@@ -5,6 +5,8 @@
 //   doublequant.dq_compress / dq_decompress (pkg/src/qlrt/doublequant.py:148-195).
 // All kernels are HBM-bound streaming kernels: 128-bit coalesced loads and
 // stores, grids sized in multiples of the 148 SMs.
+#include <type_traits>
+
 #include "qlrt_common.cuh"
 
 namespace qlrt {
@@ -383,74 +385,77 @@ __global__ void dq_decompress_kernel(const uint8_t* __restrict__ codes,
 
 // ---------------------------------------------------------------------------
 // dequantize (blockquant.py:198-213): out = f32(values[code] * f64(c)).
-// blocksize 64 fast path: one thread = 32 elements = 16 code bytes (one 16B
-// load), the block constant rebuilt from its DQ byte in fp64, the fp64
-// product from a 16-entry smem table (conflict-free: 16 doubles, 32 banks).
+// blocksize 64 fast path: one thread = one 64-block (32 code bytes in two
+// 16B loads, its DQ byte and c1 in flight together).  The block's 16 exact
+// products f64(v_i) * f64(c) are computed once (16 DMUL) into a per-thread
+// column of a [code][thread] shared table (conflict-free), then each element
+// is one table read.
 // ---------------------------------------------------------------------------
 template <int OUT>
-__global__ void __launch_bounds__(256) dequant64_kernel(const uint4* __restrict__ codes,
-                                                        int64_t n, qlrt_codebook4 cb,
+__global__ void __launch_bounds__(256) dequant64_kernel(const uint4* __restrict__ codes, int64_t n, qlrt_codebook4 cb,
                                                         const float* __restrict__ absmax,
                                                         const uint8_t* __restrict__ dq_codes,
-                                                        const float* __restrict__ c1,
-                                                        const float* __restrict__ mu, int bs2,
-                                                        qlrt_fp8spec sp, void* __restrict__ out) {
-  __shared__ double vals[16];
-  if (threadIdx.x < 16) vals[threadIdx.x] = cb.values[threadIdx.x];
-  __syncthreads();
+                                                        const float* __restrict__ c1, const float* __restrict__ mu,
+                                                        int bs2, qlrt_fp8spec sp, void* __restrict__ out) {
+  using LT = typename std::conditional<OUT == QLRT_F64, double, float>::type;
+  __shared__ LT lut[16 * 256];
   const float mu_v = dq_codes ? *mu : 0.0f;
-  const int64_t n_chunks = cdiv(n, 32);
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_chunks;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t blk = t >> 1;
-    float c;
-    if (dq_codes) c = dq_constant(__ldg(dq_codes + blk), __ldg(c1 + blk / bs2), mu_v, sp);
-    else c = __ldg(absmax + blk);
+  const int64_t nb = cdiv(n, 64);
+  LT* col = lut + threadIdx.x;
+  for (int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; blk < nb;
+       blk += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w0 = __ldg(codes + 2 * blk);
+    const uint4 w1 = __ldg(codes + 2 * blk + 1);
+    const float c = dq_codes ? dq_constant(__ldg(dq_codes + blk), __ldg(c1 + blk / bs2), mu_v, sp)
+                             : __ldg(absmax + blk);
     const double cd = (double)c;
-    const int64_t e0 = t * 32;
-    uint4 w;
-    if (e0 + 32 <= n) {
-      w = __ldg(codes + t);
-    } else {
-      const uint8_t* cb8 = reinterpret_cast<const uint8_t*>(codes) + t * 16;
-      uint8_t tmp[16];
-      for (int j = 0; j < 16; ++j) tmp[j] = (e0 + 2 * j < n) ? cb8[j] : 0;
-      w = *reinterpret_cast<uint4*>(tmp);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const double d = __dmul_rn(cb.values[i], cd);
+      if constexpr (OUT == QLRT_F64) col[i * 256] = d;
+      else col[i * 256] = __double2float_rn(d);
     }
-    uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-    if constexpr (OUT == QLRT_F64) {  // the reference's own float64 output, bit-exact
-      double* o = static_cast<double*>(out) + e0;
+    const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    const int64_t e0 = blk * 64;
+    const bool full_blk = e0 + 64 <= n;
+    if constexpr (OUT == QLRT_BF16) {
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + e0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t w = ws[q];
+        uint32_t pk[4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (e0 + q * 8 + j < n) o[q * 8 + j] = __dmul_rn(vals[(ws[q] >> (4 * j)) & 15u], cd);
-    } else {
-    float f[32];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        f[q * 8 + j] = __double2float_rn(__dmul_rn(vals[(ws[q] >> (4 * j)) & 15u], cd));
-    if (e0 + 32 <= n) {
-      if (OUT == QLRT_BF16) {
-        uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + e0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          o[q] = make_uint4(pack_bf16x2(f[8 * q], f[8 * q + 1]), pack_bf16x2(f[8 * q + 2], f[8 * q + 3]),
-                            pack_bf16x2(f[8 * q + 4], f[8 * q + 5]), pack_bf16x2(f[8 * q + 6], f[8 * q + 7]));
-      } else {
-        float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + e0);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) o[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+        for (int j = 0; j < 4; ++j)
+          pk[j] = pack_bf16x2(col[((w >> (8 * j)) & 15u) * 256], col[((w >> (8 * j + 4)) & 15u) * 256]);
+        if (full_blk) {
+          reinterpret_cast<uint4*>(o)[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        } else {
+          const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(pk);
+          for (int j = 0; j < 8; ++j)
+            if (e0 + q * 8 + j < n) o[q * 8 + j] = e[j];
+        }
       }
     } else {
-      for (int j = 0; j < 32; ++j) {
-        if (e0 + j >= n) break;
-        if (OUT == QLRT_BF16) static_cast<__nv_bfloat16*>(out)[e0 + j] = __float2bfloat16_rn(f[j]);
-        else static_cast<float*>(out)[e0 + j] = f[j];
+      LT* o = static_cast<LT*>(out) + e0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t w = ws[q];
+        LT v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = col[((w >> (4 * j)) & 15u) * 256];
+        if (full_blk) {
+          if constexpr (OUT == QLRT_F64) {
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) *reinterpret_cast<double2*>(o + q * 8 + j) = make_double2(v[j], v[j + 1]);
+          } else {
+            reinterpret_cast<float4*>(o + q * 8)[0] = make_float4(v[0], v[1], v[2], v[3]);
+            reinterpret_cast<float4*>(o + q * 8)[1] = make_float4(v[4], v[5], v[6], v[7]);
+          }
+        } else {
+          for (int j = 0; j < 8; ++j)
+            if (e0 + q * 8 + j < n) o[q * 8 + j] = v[j];
+        }
       }
-    }
     }
   }
 }
@@ -602,7 +607,7 @@ qlrt_status qlrt_dequantize4(const uint8_t* codes, int64_t n, int blocksize,
   cudaStream_t s = (cudaStream_t)stream;
   const bool aligned = (((uintptr_t)codes) & 15) == 0 && (((uintptr_t)out) & 15) == 0;
   if (blocksize == 64 && aligned) {
-    const int g = grid_for(cdiv(n, 32), 256, 8);
+    const int g = grid_for(cdiv(n, 64), 256, 8);
 #define QLRT_DQ64(O) dequant64_kernel<O><<<g, 256, 0, s>>>((const uint4*)codes, n, *cb, absmax, dq_codes, c1, mu, \
                                                            blocksize2, spec, out)
     if (out_dtype == QLRT_BF16) QLRT_DQ64(QLRT_BF16);

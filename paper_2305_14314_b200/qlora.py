@@ -256,12 +256,21 @@ def _split_into(v: torch.Tensor, pair: torch.Tensor) -> None:
 _GEMM_WS: dict = {}
 
 
+def _pad2(t: torch.Tensor, r: int, c: int) -> torch.Tensor:
+    if t.shape[0] == r and t.shape[1] == c:
+        return t
+    out = torch.zeros(r, c, dtype=t.dtype, device=t.device)
+    out[: t.shape[0], : t.shape[1]] = t
+    return out
+
+
 def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, alpha: float = 1.0,
               a_t: bool = False, b_t: bool = False, out_dtype=None) -> torch.Tensor:
     """out = alpha * op(a) @ op(b) on the tcgen05 engine (fp32 accumulate).
 
     ``a`` is [M, K] (or [K, M] with ``a_t``), ``b`` is [K, N] (or [N, K] with
-    ``b_t``); operands are bf16 and contiguous.
+    ``b_t``); operands are bf16.  Row pitches must be 16-byte multiples for
+    TMA: unaligned extents are zero-padded (exact) and the result sliced.
     """
     a = a.to(torch.bfloat16).contiguous()
     b = b.to(torch.bfloat16).contiguous()
@@ -271,6 +280,14 @@ def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
         out = torch.empty(m, n, dtype=out_dtype or torch.bfloat16, device=a.device)
     if out.dtype not in (torch.bfloat16, torch.float32):
         raise ValueError("gemm_bf16 writes bf16 or fp32")
+    r8 = lambda v: (v + 7) // 8 * 8  # noqa: E731
+    mp, kp, np_ = r8(m), r8(k), r8(n)
+    if (mp, kp, np_) != (m, k, n) or not out.is_contiguous():
+        a = _pad2(a, kp, mp) if a_t else _pad2(a, mp, kp)
+        b = _pad2(b, np_, kp) if b_t else _pad2(b, kp, np_)
+        tmp = gemm_bf16(a, b, alpha=alpha, a_t=a_t, b_t=b_t, out_dtype=out.dtype)
+        out.copy_(tmp[:m, :n])
+        return out
     dev = a.device
     ws = _GEMM_WS.get(dev)
     need = 16 * m * n * 4 + 4096

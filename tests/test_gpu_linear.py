@@ -177,11 +177,12 @@ def test_fresh_adapter_is_exact_noop(qb, cuda):
 
 @pytest.mark.parametrize("k,n", [(8192, 8192), (4096, 11008)])
 def test_gemv_batch1(k, n, oracle, qb, cuda):
-    """Batch-1 GEMV vs the fp64 oracle over the reference's float32 weight."""
+    """Batch-1 GEMV (same engine, W decoded to bf16 in-kernel) vs the fp64
+    oracle over W = bf16(f32(dequantize(q))) -- the GEMM parity definition."""
     rng = np.random.default_rng(k + n)
     w = (0.02 * rng.standard_normal((k, n))).astype(np.float32)
     q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)
-    wd = qb.dequantize(q, torch.float64).cpu().numpy()
+    wd = bf16_round(qb.dequantize(q, torch.float32).cpu().numpy()).astype(np.float64)
     x = bf16_round(rng.standard_normal((1, k)))
     r = 64
     l1 = bf16_round(rng.standard_normal((k, r)) / 8)

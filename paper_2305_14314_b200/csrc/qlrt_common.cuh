@@ -61,11 +61,26 @@ __device__ __forceinline__ unsigned fp8_encode(double q, int E, int M, int B, do
   return (q < 0.0 ? 0x80u : 0u) | mag;
 }
 
+// exact decode by assembling the fp64 bit pattern (no ldexp)
+__device__ __forceinline__ double fp8_decode_fast(unsigned b, const qlrt_fp8spec& sp) {
+  const unsigned M = sp.mant_bits;
+  const unsigned e = (b >> M) & ((1u << sp.exp_bits) - 1u);
+  const unsigned m = b & ((1u << M) - 1u);
+  double mag;
+  if (e == 0) {  // m * 2^(1-B-M): exact product with a power of two
+    mag = (double)m * __longlong_as_double((long long)((unsigned long long)(1023 + 1 - sp.bias - (int)M) << 52));
+  } else {
+    mag = __longlong_as_double((long long)(((unsigned long long)(e - sp.bias + 1023) << 52) |
+                                           ((unsigned long long)m << (52 - M))));
+  }
+  return (b >> 7) ? -mag : mag;
+}
+
 // reconstruct one first-level constant (doublequant.py:190-195): two
 // separate fp64 roundings (no FMA contraction), clamp at 0, round to f32.
 __device__ __forceinline__ float dq_constant(unsigned code, float c1, float mu,
                                              const qlrt_fp8spec& sp) {
-  double d = fp8_decode(code, sp.exp_bits, sp.mant_bits, sp.bias);
+  double d = fp8_decode_fast(code, sp);
   double r = __dadd_rn(__dmul_rn(d, (double)c1), (double)mu);
   r = r > 0.0 ? r : 0.0;
   return __double2float_rn(r);

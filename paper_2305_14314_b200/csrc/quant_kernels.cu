@@ -103,33 +103,80 @@ __device__ __forceinline__ bool finite_v(double a) { return fabs(a) <= 1.7976931
 __device__ __forceinline__ float to_f32_const(float m) { return m; }
 __device__ __forceinline__ float to_f32_const(double m) { return __double2float_rn(m); }
 
+// Bin table for the code search.  q in [-1, 1] is cut into NBIN equal bins;
+// every bin overlaps at most one midpoint bracket (the host checks the
+// spacing), so  j = base[bin] + (q > lo[base])  and the result is certain
+// iff  lower[j] <= q <= upper[j]  with lower[j] = hi[j-1], upper[j] = lo[j];
+// otherwise (inside a bracket, or a bin-edge rounding case) the code is
+// re-decided exactly in fp64.
+constexpr int NBIN = 1024;
+struct BinTables {
+  float2 bin[NBIN];      // (base code as float bits, lo[base])
+  float2 bound[16];      // (hi[j-1] or -inf, lo[j] or +inf)
+  double mids[15];
+  int n_mids;
+};
+
+__device__ void build_bin_tables(BinTables& T, const qlrt_codebook4& cb) {
+  const int n = cb.n_mids;
+  for (int b = threadIdx.x; b < NBIN; b += blockDim.x) {
+    const float qb = -1.0f + 2.0f * (float)b / (float)NBIN;  // bin start (exact)
+    int base = 0;
+    while (base < n && cb.hi[base] <= qb) ++base;
+    T.bin[b] = make_float2(__int_as_float(base), base < n ? cb.lo[base] : __int_as_float(0x7f800000));
+  }
+  if (threadIdx.x < 16) {
+    const int j = threadIdx.x;
+    T.bound[j] = make_float2(j == 0 ? __int_as_float(0xff800000) : (j <= n ? cb.hi[j - 1] : __int_as_float(0x7f800000)),
+                             j < n ? cb.lo[j] : __int_as_float(0x7f800000));
+    if (j < 15) T.mids[j] = cb.mids[j];
+  }
+  if (threadIdx.x == 0) T.n_mids = n;
+}
+
+__device__ __forceinline__ unsigned exact_code_t(double x, float c, const BinTables& t) {
+  double q = __ddiv_rn(x, (double)c);
+  unsigned k = 0;
+  if (q >= 0.0) {
+    for (int i = 0; i < t.n_mids; ++i) k += (t.mids[i] <= q) ? 1u : 0u;
+  } else {
+    for (int i = 0; i < t.n_mids; ++i) k += (t.mids[i] < q) ? 1u : 0u;
+  }
+  return k;
+}
+
+template <typename V>
+__device__ __forceinline__ unsigned bin_code(V x, float r, float c, const BinTables& t) {
+  const float q = (float)x * r;
+  int b = __float2int_rd(fmaf(q, 0.5f * NBIN, 0.5f * NBIN));
+  b = min(max(b, 0), NBIN - 1);
+  const float2 e = t.bin[b];
+  const unsigned j = (unsigned)__float_as_int(e.x) + (q > e.y ? 1u : 0u);
+  const float2 bd = t.bound[j];
+  if (!(q >= bd.x && q <= bd.y)) return exact_code_t((double)x, c, t);
+  return j;
+}
+
 // Phase A, blocksize 64: 8 consecutive lanes own one 64-block, 8 elements
-// each (two 16B loads for fp32, one for bf16); absmax by 3 xor-shuffles;
-// 8 codes -> one 32-bit packed store.
+// each (two 16B loads for fp32, one for bf16, four for fp64); absmax by 3
+// xor-shuffles; 8 codes -> one 32-bit packed store.
 template <typename T>
-__global__ void __launch_bounds__(256) quantize64_kernel(const T* __restrict__ x, int64_t n,
-                                                         int64_t n_groups, qlrt_codebook4 cb,
-                                                         uint32_t* __restrict__ codes,
+__global__ void __launch_bounds__(256) quantize64_kernel(const T* __restrict__ x, int64_t n, int64_t n_groups,
+                                                         qlrt_codebook4 cb, uint32_t* __restrict__ codes,
                                                          float* __restrict__ absmax,
                                                          unsigned long long* __restrict__ first_bad) {
-  __shared__ CodeTables t;
-  if (threadIdx.x < 16) {
-    t.lo[threadIdx.x] = cb.lo[threadIdx.x];
-    t.hi[threadIdx.x] = cb.hi[threadIdx.x];
-    if (threadIdx.x < 15) t.mids[threadIdx.x] = cb.mids[threadIdx.x];
-  }
-  if (threadIdx.x == 0) t.n_mids = cb.n_mids;
+  __shared__ BinTables t;
+  build_bin_tables(t, cb);
   __syncthreads();
   const unsigned pad = (unsigned)cb.pad_code;
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  using V = typename AccT<T>::type;
   // warp-uniform trip count: every lane reaches the shuffles
-  for (int64_t gb = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); gb < n_groups;
-       gb += stride) {
+  for (int64_t gb = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); gb < n_groups; gb += stride) {
     const int64_t g = gb + lane;
     const bool act = g < n_groups;  // n_groups % 8 == 0: 8-lane groups are all-in or all-out
     const int64_t i0 = g * 8;
-    using V = typename AccT<T>::type;
     V v[8];
     if (act) {
       load8<T>(x, i0, n, v);
@@ -139,10 +186,20 @@ __global__ void __launch_bounds__(256) quantize64_kernel(const T* __restrict__ x
     }
     V m = (V)0;
     bool finite = true;
+    if constexpr (sizeof(V) == 4) {
+      // integer max of the magnitude bits: equals the float max for finite
+      // values and flags inf/NaN (exponent all ones) in one compare
+      unsigned mb = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      finite &= finite_v(v[j]);  // false for inf and NaN
-      m = fmax(m, fabs(v[j]));
+      for (int j = 0; j < 8; ++j) mb = max(mb, __float_as_uint(v[j]) & 0x7FFFFFFFu);
+      finite = mb < 0x7F800000u;
+      m = __uint_as_float(mb);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        finite &= finite_v(v[j]);
+        m = fmax(m, fabs(v[j]));
+      }
     }
     if (!finite) {
       unsigned long long bad = ~0ull;
@@ -160,11 +217,16 @@ __global__ void __launch_bounds__(256) quantize64_kernel(const T* __restrict__ x
     if (c > 0.0f) {
       const float r = __frcp_rn(c);
       const bool fast_ok = r <= 3.402823466e38f;  // subnormal c: 1/c overflows
+      if (fast_ok && i0 + 8 <= n) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        unsigned k = pad;
-        if (i0 + j < n) k = fast_ok ? fast_code((double)v[j], r, c, t) : exact_code((double)v[j], c, t);
-        word |= k << (4 * j);
+        for (int j = 0; j < 8; ++j) word |= bin_code(v[j], r, c, t) << (4 * j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          unsigned k = pad;
+          if (i0 + j < n) k = fast_ok ? bin_code(v[j], r, c, t) : exact_code_t((double)v[j], c, t);
+          word |= k << (4 * j);
+        }
       }
     } else {
       word = pad * 0x11111111u;
@@ -385,77 +447,94 @@ __global__ void dq_decompress_kernel(const uint8_t* __restrict__ codes,
 
 // ---------------------------------------------------------------------------
 // dequantize (blockquant.py:198-213): out = f32(values[code] * f64(c)).
-// blocksize 64 fast path: one thread = one 64-block (32 code bytes in two
-// 16B loads, its DQ byte and c1 in flight together).  The block's 16 exact
-// products f64(v_i) * f64(c) are computed once (16 DMUL) into a per-thread
-// column of a [code][thread] shared table (conflict-free), then each element
-// is one table read.
+// blocksize 64 fast path: a warp owns 32 consecutive 64-blocks, one per lane.
+// Each lane loads its 32 code bytes (two 16B loads) with its DQ byte and c1,
+// computes the block's 16 exact products f64(v_i) * f64(c) once (16 DMUL) into
+// its column of a [code][thread] shared table (conflict-free reads), decodes
+// its block into a 128B-swizzled row of a per-warp staging buffer, and the
+// warp then writes the 32 rows out with fully coalesced 16B stores.
 // ---------------------------------------------------------------------------
+constexpr int DQ_TPB = 128;  // threads per CTA of the dequant kernel
+
 template <int OUT>
-__global__ void __launch_bounds__(256) dequant64_kernel(const uint4* __restrict__ codes, int64_t n, qlrt_codebook4 cb,
+__global__ void __launch_bounds__(DQ_TPB) dequant64_kernel(const uint4* __restrict__ codes, int64_t n, qlrt_codebook4 cb,
                                                         const float* __restrict__ absmax,
                                                         const uint8_t* __restrict__ dq_codes,
                                                         const float* __restrict__ c1, const float* __restrict__ mu,
                                                         int bs2, qlrt_fp8spec sp, void* __restrict__ out) {
   using LT = typename std::conditional<OUT == QLRT_F64, double, float>::type;
-  __shared__ LT lut[16 * 256];
+  using OT = typename std::conditional<OUT == QLRT_F64, double,
+                                       typename std::conditional<OUT == QLRT_F32, float, __nv_bfloat16>::type>::type;
+  constexpr int EPP = 128 / sizeof(OT);     // elements per lane per pass (one 128B row)
+  constexpr int PASSES = 64 / EPP;          // 1 (bf16), 2 (f32), 4 (f64)
+  __shared__ LT lut[16 * DQ_TPB];
+  __shared__ __align__(16) uint8_t stage[DQ_TPB / 32][32 * 128];
   const float mu_v = dq_codes ? *mu : 0.0f;
   const int64_t nb = cdiv(n, 64);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   LT* col = lut + threadIdx.x;
-  for (int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; blk < nb;
-       blk += (int64_t)gridDim.x * blockDim.x) {
-    const uint4 w0 = __ldg(codes + 2 * blk);
-    const uint4 w1 = __ldg(codes + 2 * blk + 1);
-    const float c = dq_codes ? dq_constant(__ldg(dq_codes + blk), __ldg(c1 + blk / bs2), mu_v, sp)
-                             : __ldg(absmax + blk);
+  uint8_t* st = stage[wid];
+  const int64_t n_warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t wb = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wid) * 32; wb < nb; wb += n_warps_total * 32) {
+    const int64_t blk = wb + lane;
+    const bool live = blk < nb;
+    uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0;
+    float c = 0.0f;
+    if (live) {
+      w0 = __ldg(codes + 2 * blk);
+      w1 = __ldg(codes + 2 * blk + 1);
+      c = dq_codes ? dq_constant(__ldg(dq_codes + blk), __ldg(c1 + blk / bs2), mu_v, sp) : __ldg(absmax + blk);
+    }
     const double cd = (double)c;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const double d = __dmul_rn(cb.values[i], cd);
-      if constexpr (OUT == QLRT_F64) col[i * 256] = d;
-      else col[i * 256] = __double2float_rn(d);
+      if constexpr (OUT == QLRT_F64) col[i * DQ_TPB] = d;
+      else col[i * DQ_TPB] = __double2float_rn(d);
     }
     const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-    const int64_t e0 = blk * 64;
-    const bool full_blk = e0 + 64 <= n;
-    if constexpr (OUT == QLRT_BF16) {
-      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + e0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const uint32_t w = ws[q];
+    for (int pass = 0; pass < PASSES; ++pass) {
+      // this lane's row: elements [pass*EPP, (pass+1)*EPP) of its block, 8 x 16B chunks
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        constexpr int EPC = 16 / sizeof(OT);  // elements per 16B chunk
         uint32_t pk[4];
+        if constexpr (OUT == QLRT_BF16) {
+          const uint32_t w = ws[pass * 8 + ch];  // 8 codes
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          pk[j] = pack_bf16x2(col[((w >> (8 * j)) & 15u) * 256], col[((w >> (8 * j + 4)) & 15u) * 256]);
-        if (full_blk) {
-          reinterpret_cast<uint4*>(o)[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          for (int j = 0; j < 4; ++j)
+            pk[j] = pack_bf16x2(col[((w >> (8 * j)) & 15u) * DQ_TPB], col[((w >> (8 * j + 4)) & 15u) * DQ_TPB]);
         } else {
-          const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(pk);
-          for (int j = 0; j < 8; ++j)
-            if (e0 + q * 8 + j < n) o[q * 8 + j] = e[j];
+          const int e = pass * EPP + ch * EPC;  // first element of the chunk
+          const uint32_t w = ws[e >> 3] >> (4 * (e & 7));
+          LT v[EPC];
+#pragma unroll
+          for (int j = 0; j < EPC; ++j) v[j] = col[((w >> (4 * j)) & 15u) * DQ_TPB];
+          const uint4 u = *reinterpret_cast<const uint4*>(v);
+          pk[0] = u.x; pk[1] = u.y; pk[2] = u.z; pk[3] = u.w;
         }
+        *reinterpret_cast<uint4*>(st + lane * 128 + ((ch ^ (lane & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
-    } else {
-      LT* o = static_cast<LT*>(out) + e0;
+      __syncwarp();
+      // coalesced copy-out: 4 rows (blocks) x 128B per instruction
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const uint32_t w = ws[q];
-        LT v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = col[((w >> (4 * j)) & 15u) * 256];
-        if (full_blk) {
-          if constexpr (OUT == QLRT_F64) {
-#pragma unroll
-            for (int j = 0; j < 8; j += 2) *reinterpret_cast<double2*>(o + q * 8 + j) = make_double2(v[j], v[j + 1]);
+      for (int it = 0; it < 8; ++it) {
+        const int row = it * 4 + (lane >> 3), ch = lane & 7;
+        const uint4 u = *reinterpret_cast<const uint4*>(st + row * 128 + ((ch ^ (row & 7)) << 4));
+        const int64_t b = wb + row;
+        const int64_t e0 = b * 64 + pass * EPP + ch * (16 / (int)sizeof(OT));
+        if (b < nb) {
+          OT* o = static_cast<OT*>(out) + e0;
+          if (e0 + 16 / (int)sizeof(OT) <= n) {
+            *reinterpret_cast<uint4*>(o) = u;
           } else {
-            reinterpret_cast<float4*>(o + q * 8)[0] = make_float4(v[0], v[1], v[2], v[3]);
-            reinterpret_cast<float4*>(o + q * 8)[1] = make_float4(v[4], v[5], v[6], v[7]);
+            const OT* e = reinterpret_cast<const OT*>(&u);
+            for (int j = 0; j < 16 / (int)sizeof(OT) && e0 + j < n; ++j) o[j] = e[j];
           }
-        } else {
-          for (int j = 0; j < 8; ++j)
-            if (e0 + q * 8 + j < n) o[q * 8 + j] = v[j];
         }
       }
+      __syncwarp();
     }
   }
 }
@@ -607,8 +686,8 @@ qlrt_status qlrt_dequantize4(const uint8_t* codes, int64_t n, int blocksize,
   cudaStream_t s = (cudaStream_t)stream;
   const bool aligned = (((uintptr_t)codes) & 15) == 0 && (((uintptr_t)out) & 15) == 0;
   if (blocksize == 64 && aligned) {
-    const int g = grid_for(cdiv(n, 64), 256, 8);
-#define QLRT_DQ64(O) dequant64_kernel<O><<<g, 256, 0, s>>>((const uint4*)codes, n, *cb, absmax, dq_codes, c1, mu, \
+    const int g = grid_for(cdiv(n, 64), DQ_TPB, 16);
+#define QLRT_DQ64(O) dequant64_kernel<O><<<g, DQ_TPB, 0, s>>>((const uint4*)codes, n, *cb, absmax, dq_codes, c1, mu, \
                                                            blocksize2, spec, out)
     if (out_dtype == QLRT_BF16) QLRT_DQ64(QLRT_BF16);
     else if (out_dtype == QLRT_F32) QLRT_DQ64(QLRT_F32);

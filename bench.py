@@ -404,6 +404,17 @@ def secondary(qb, torch, dev, flush, stream, hbm):
     out["c1_quantize_dq_f32"] = {"gbs": q_bytes / (t / 1e3) / 1e9, "ms": t, "bytes": q_bytes,
                                  "frac_hbm": q_bytes / (t / 1e3) / 1e9 / hbm,
                                  "note": "quantize + DQ kernels (3 launches); the non-finite check's host read excluded"}
+    # the same tcgen05 engine without the dequant producer: bf16 X W with W
+    # already dense (TMA-fed A and B), C2 shape -- separates MMA/pipeline
+    # limits from the NF4 decode cost, and is the unfused alternative
+    wq = torch.randn(4096, 11008, device=dev, generator=torch.Generator(device=dev).manual_seed(3)) * 0.02
+    wb = wq.bfloat16()
+    xb = torch.randn(2048, 4096, device=dev).bfloat16()
+    ob = torch.empty(2048, 11008, device=dev, dtype=torch.bfloat16)
+    t = timed(lambda: qb.gemm_bf16(xb, wb, out=ob))
+    fl = 2 * 2048 * 4096 * 11008
+    out["engine_bf16_gemm_2048x4096x11008"] = {"tflops": fl / (t / 1e3) / 1e12, "ms": t}
+    del wq, wb, xb, ob
     w = torch.randn(8192, 22016, device=dev) * 0.02
     qw = qb.quantize(w, cb, 64, double_quant=True)
     del w

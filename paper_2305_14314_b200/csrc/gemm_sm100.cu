@@ -27,6 +27,8 @@ constexpr int BK = 64;              // one 128B swizzle row of bf16
 constexpr int A_STAGE = BM * BK * 2;  // 16 KB
 constexpr int kTmaWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2, kNumEpiWarps = 4, kXfWarp0 = 6;
 constexpr int kNumXfWarps = 8;
+constexpr int kCstWarp = kXfWarp0 + kNumXfWarps;  // NF4: codes (TMA) + block-constant producer
+constexpr int kNF4Threads = (kCstWarp + 1) * 32;  // 480
 
 struct Args {
   int M, N;             // output extent (UMMA M rows, N cols)
@@ -61,18 +63,20 @@ struct Args {
 template <int BN, bool NF4>
 struct Smem {
   static constexpr int B_STAGE = BN * BK * 2;
-  static constexpr int C_STAGE = NF4 ? 4096 : 0;  // packed NF4 codes of one A stage (128 x 64 nibbles)
-  static constexpr int STAGE = A_STAGE + B_STAGE + C_STAGE;
   static constexpr int EPI_BYTES = kNumEpiWarps * 32 * 32 * 2;  // 32x32 bf16 transpose tile per warp
-  // as many stages as fit in ~220 KB, at most 8, even (a stage is always
-  // refilled by the same dequant group)
-  static constexpr int FIT = (220 * 1024 - EPI_BYTES) / STAGE;
+  // NF4: a separate, decoupled ring of packed codes (4 KB = 128 x 64 nibbles)
+  // plus the 128 fp32 block constants of each A stage
+  static constexpr int CODE_BYTES = 4096, CONST_BYTES = 512;
+  static constexpr int CST = NF4 ? (BN >= 128 ? 4 : 8) : 0;
+  static constexpr int CRING = CST * (CODE_BYTES + CONST_BYTES);
+  // as many A/B stages as fit in ~220 KB, at most 8, even
+  static constexpr int FIT = (220 * 1024 - EPI_BYTES - CRING) / (A_STAGE + B_STAGE);
   static constexpr int STAGES = (FIT > 8 ? 8 : FIT) & ~1;
   static constexpr int C_OFF = STAGES * (A_STAGE + B_STAGE);
-  static constexpr int EPI_OFF = STAGES * STAGE;
+  static constexpr int EPI_OFF = C_OFF + CRING;
   static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
-  // full[S], afull[S], empty[S], tmem_full[2], tmem_empty[2], tmem_ptr
-  static constexpr int BYTES = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
+  // full[S], afull[S], empty[S], cfull[CST], cempty[CST], tmem_full[2], tmem_empty[2], tmem_ptr
+  static constexpr int BYTES = BAR_OFF + (3 * STAGES + 2 * CST + 4) * 8 + 16 + 1024;  // + align slack
   static_assert(STAGES >= 2 && BYTES <= 232448, "shared memory budget");
 };
 
@@ -195,23 +199,27 @@ __device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[E
 // the kernel
 // ---------------------------------------------------------------------------
 template <int BN, bool NF4>
-__global__ void __launch_bounds__(NF4 ? 448 : 192, 1)
+__global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ Args p) {
   using L = Smem<BN, NF4>;
   constexpr int STAGES = L::STAGES;
+  constexpr int CST = L::CST > 0 ? L::CST : 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE;
-  uint8_t* sC = smem + L::C_OFF;                       // packed codes per stage (NF4)
+  uint8_t* sC = smem + L::C_OFF;                       // NF4 codes ring: [CST][4 KB]
+  float* sK = reinterpret_cast<float*>(smem + L::C_OFF + L::CST * L::CODE_BYTES);  // [CST][128] constants
   __nv_bfloat16* sE = reinterpret_cast<__nv_bfloat16*>(smem + L::EPI_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* full = bars;
   uint64_t* afull = bars + STAGES;
   uint64_t* empty = bars + 2 * STAGES;
-  uint64_t* tfull = bars + 3 * STAGES;
+  uint64_t* cfull = bars + 3 * STAGES;
+  uint64_t* cempty = cfull + L::CST;
+  uint64_t* tfull = cempty + L::CST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -232,6 +240,10 @@ __global__ void __launch_bounds__(NF4 ? 448 : 192, 1)
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&afull[s], NF4 ? 128 : 1);
       ptx::mbar_init(&empty[s], 1);
+    }
+    for (int c = 0; c < L::CST; ++c) {
+      ptx::mbar_init(&cfull[c], 2);      // TMA expect_tx arrival + constants-written arrival
+      ptx::mbar_init(&cempty[c], 128);   // every thread of the consuming dequant group
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -266,15 +278,9 @@ __global__ void __launch_bounds__(NF4 ? 448 : 192, 1)
           const int bmn = aug ? p.b2_mn : p.b_mn;
           const int k0 = (aug ? (i - nk) : (kb + i)) * BK;
           const bool a_tma = aug || !NF4;
-          ptx::mbar_arrive_expect_tx(&full[s], L::B_STAGE + (a_tma ? A_STAGE : L::C_STAGE));
+          ptx::mbar_arrive_expect_tx(&full[s], L::B_STAGE + (a_tma ? A_STAGE : 0));
           uint8_t* a_dst = sA + s * A_STAGE;
           uint8_t* b_dst = sB + s * L::B_STAGE;
-          if (!a_tma) {
-            // packed NF4 codes of the A tile: fwd  W[k0:k0+64, m0:m0+128] -> 64 rows x 64 B
-            //                                 bwd  W[m0:m0+128, k0:k0+64] -> 128 rows x 32 B
-            if (p.nf4_mode == 1) ptx::tma_load_2d(&tmC, &full[s], sC + s * L::C_STAGE, mt * BM / 2, k0);
-            else ptx::tma_load_2d(&tmC, &full[s], sC + s * L::C_STAGE, k0 / 2, mt * BM);
-          }
           if (a_tma) {
             if (amn) {
               ptx::tma_load_2d(ma, &full[s], a_dst, mt * BM, k0);
@@ -383,6 +389,60 @@ __global__ void __launch_bounds__(NF4 ? 448 : 192, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
     }
+  } else if (NF4 && warp == kCstWarp) {
+    // ======================= codes + block-constant producer =======================
+    // Runs ahead of the dequant warps through its own ring: lane 0 TMA-loads
+    // the packed codes of the next A tile (fwd: W[k0:k0+64, m0:m0+128] as
+    // 64 rows x 64 B; bwd: W[m0:m0+128, k0:k0+64] as 128 rows x 32 B) and all
+    // lanes rebuild the 128 block constants from their DQ bytes (exact fp64,
+    // doublequant.py:190-195), so the dequant warps never wait on global memory.
+    const float mu = p.dq_codes ? *p.mu : 0.0f;
+    uint32_t cit = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+      int mt, nt, z;
+      tile_coords(t, m_tiles, n_tiles, mt, nt, z);
+      const int kb = z * kc;
+      const int nk = min(kc, p.k_iters - kb);
+      for (int i = 0; i < nk; ++i, ++cit) {
+        const int c = cit % CST;
+        const uint32_t cph = (cit / CST) & 1;
+        const int k0 = (kb + i) * BK;
+        // issue the constant loads before waiting for the slot
+        float cv[4];
+        uint32_t dqb[4];
+        bool live[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int item = q * 32 + lane;
+          const int h = item & 1, rr = item >> 1;
+          const int64_t wr = p.nf4_mode == 1 ? (int64_t)k0 + rr : (int64_t)mt * BM + item;
+          const int64_t wc = p.nf4_mode == 1 ? (int64_t)mt * BM + h * 64 : (int64_t)k0;
+          live[q] = wr < p.w_rows && wc < p.w_cols;
+          const int64_t blk = live[q] ? (wr * p.w_cols + wc) >> 6 : 0;
+          if (p.dq_codes) {
+            dqb[q] = __ldg(p.dq_codes + blk);
+            cv[q] = __ldg(p.c1 + (p.bs2_shift >= 0 ? (blk >> p.bs2_shift) : blk / p.bs2));
+          } else {
+            dqb[q] = 0;
+            cv[q] = __ldg(p.absmax + blk);
+          }
+        }
+        ptx::mbar_wait(&cempty[c], cph ^ 1);
+        if (lane == 0) {
+          ptx::mbar_arrive_expect_tx(&cfull[c], L::CODE_BYTES);
+          if (p.nf4_mode == 1) ptx::tma_load_2d(&tmC, &cfull[c], sC + c * L::CODE_BYTES, mt * BM / 2, k0);
+          else ptx::tma_load_2d(&tmC, &cfull[c], sC + c * L::CODE_BYTES, k0 / 2, mt * BM);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float cc = cv[q];
+          if (p.dq_codes) cc = dq_constant(dqb[q], cv[q], mu, p.spec);
+          sK[c * 128 + q * 32 + lane] = live[q] ? cc : 0.0f;
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&cfull[c]);
+      }
+    }
   } else if (NF4 && warp >= kXfWarp0 && warp < kXfWarp0 + kNumXfWarps) {
     // ======================= NF4 dequant producer =======================
     const int xw = warp - kXfWarp0;
@@ -391,103 +451,55 @@ __global__ void __launch_bounds__(NF4 ? 448 : 192, 1)
     float vals[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) vals[i] = (float)p.values[i];
-    const float mu = p.dq_codes ? *p.mu : 0.0f;
-    const double sub_scale = ldexp(1.0, 1 - p.spec.bias - p.spec.mant_bits);
     // fwd: item -> (h = item & 1, r = item >> 1): A image at h*8192 + r*128,
     //      codes at r*64 + h*32 (W row k0+r, cols m0+64h..+64)
     // bwd: item -> W row m0+item, cols k0..k0+64: A image item*128, codes item*32
     const int h = item & 1, rr = item >> 1;
     const uint32_t soff = p.nf4_mode == 1 ? (uint32_t)(h * 8192 + rr * 128) : (uint32_t)(item * 128);
-    const uint32_t coff = (uint32_t)item * 32;
     const uint32_t swz = (soff >> 7) & 7;
-    // cursor over (tile, k-iteration); this group handles global iterations it with it % 2 == grp
-    int t = blockIdx.x, i = 0, total = 0, nk = 0, mt = 0, kb = 0;
-    auto enter = [&](int tt) {
-      int nt_, z_;
-      tile_coords(tt, m_tiles, n_tiles, mt, nt_, z_);
-      kb = z_ * kc;
-      nk = min(kc, p.k_iters - kb);
-      total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
-    };
-    // block constant of this thread's item in iteration (mt, kb + i): loads only
-    auto fetch = [&](int mt_, int kk, uint32_t& dqb, float& c1v, bool& live) {
-      const int64_t kg = (int64_t)kk * BK;
-      const int64_t wr = p.nf4_mode == 1 ? kg + rr : (int64_t)mt_ * BM + item;
-      const int64_t wc = p.nf4_mode == 1 ? (int64_t)mt_ * BM + h * 64 : kg;
-      live = wr < p.w_rows && wc < p.w_cols;
-      dqb = 0;
-      c1v = 0.0f;
-      if (live) {
-        const int64_t blk = (wr * p.w_cols + wc) >> 6;
-        if (p.dq_codes) {
-          dqb = __ldg(p.dq_codes + blk);
-          c1v = __ldg(p.c1 + (p.bs2_shift >= 0 ? (blk >> p.bs2_shift) : blk / p.bs2));
-        } else {
-          c1v = __ldg(p.absmax + blk);
+    const uint32_t codes_s = ptx::smem_u32(sC) + (uint32_t)item * 32;
+    const uint32_t consts_s = ptx::smem_u32(sK) + (uint32_t)item * 4;
+    const uint32_t a_s = ptx::smem_u32(sA) + soff;
+    uint32_t it = 0, cit = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+      int mt, nt, z;
+      tile_coords(t, m_tiles, n_tiles, mt, nt, z);
+      const int kb = z * kc;
+      const int nk = min(kc, p.k_iters - kb);
+      const int total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
+      for (int i = (int)((it & 1) != (uint32_t)grp); i < total; i += 2) {
+        const uint32_t my = it + i;
+        const int s = my % STAGES;
+        const uint32_t ph = (my / STAGES) & 1;
+        if (i >= nk) {  // augmented (TMA-fed) stage: keep afull's phase in step
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          ptx::mbar_arrive(&afull[s]);
+          continue;
         }
-      }
-    };
-    if (t < n_tiles_total) enter(t);
-    uint32_t it = 0;
-    // advance to the first handled iteration
-    auto step = [&]() {
-      ++it;
-      if (++i >= total) {
-        i = 0;
-        t += gridDim.x;
-        if (t < n_tiles_total) enter(t);
-      }
-    };
-    if ((int)(it & 1) != grp && t < n_tiles_total) step();
-    uint32_t dqb = 0;
-    float c1v = 0.0f;
-    bool live = false;
-    if (t < n_tiles_total && i < nk) fetch(mt, kb + i, dqb, c1v, live);
-    while (t < n_tiles_total) {
-      const int s = it % STAGES;
-      const uint32_t ph = (it / STAGES) & 1;
-      const bool main_it = i < nk;
-      const int cur_mt = mt;
-      (void)cur_mt;
-      const uint32_t cur_dqb = dqb;
-      const float cur_c1 = c1v;
-      const bool cur_live = live;
-      // move the cursor two iterations ahead and prefetch that item's constant
-      step();
-      if (t < n_tiles_total) step();
-      if (t < n_tiles_total && i < nk) fetch(mt, kb + i, dqb, c1v, live);
-      if (!main_it) {  // augmented (TMA-fed) stage: keep afull's phase in step
+        const uint32_t ci = cit + i;
+        const int c = ci % CST;
+        ptx::mbar_wait(&cfull[c], (ci / CST) & 1);
+        const uint4 w0 = ptx::ld_shared_v4(codes_s + c * L::CODE_BYTES);
+        const uint4 w1 = ptx::ld_shared_v4(codes_s + c * L::CODE_BYTES + 16);
+        const float cst = ptx::ld_shared_f32(consts_s + c * L::CONST_BYTES);
+        ptx::mbar_arrive(&cempty[c]);
+        uint32_t Lp[4], Hp[4];
+        build_planes(vals, cst, Lp, Hp);
         ptx::mbar_wait(&empty[s], ph ^ 1);
-        ptx::mbar_arrive(&afull[s]);
-        continue;
-      }
-      float c = 0.0f;
-      if (cur_live) {
-        if (p.dq_codes) {
-          double d = fp8_decode_bits(cur_dqb, p.spec, sub_scale);
-          double rcon = __dadd_rn(__dmul_rn(d, (double)cur_c1), (double)mu);
-          c = __double2float_rn(rcon > 0.0 ? rcon : 0.0);
-        } else {
-          c = cur_c1;
-        }
-      }
-      uint32_t Lp[4], Hp[4];
-      build_planes(vals, c, Lp, Hp);
-      ptx::mbar_wait(&full[s], ph);  // codes (and B) landed; implies the A slot is free
-      const uint8_t* cs = sC + s * L::C_STAGE + coff;
-      const uint4 w0 = *reinterpret_cast<const uint4*>(cs);
-      const uint4 w1 = *reinterpret_cast<const uint4*>(cs + 16);
-      const uint32_t base = ptx::smem_u32(sA + s * A_STAGE) + soff;
-      const uint32_t words[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        const uint32_t base = a_s + s * A_STAGE;
+        const uint32_t words[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        uint32_t o0, o1, o2, o3;
-        lookup4(words[ch], Lp, Hp, o0, o1);
-        lookup4(words[ch] >> 16, Lp, Hp, o2, o3);
-        ptx::st_shared_v4(base + ((ch ^ swz) << 4), o0, o1, o2, o3);
+        for (int ch = 0; ch < 8; ++ch) {
+          uint32_t o0, o1, o2, o3;
+          lookup4(words[ch], Lp, Hp, o0, o1);
+          lookup4(words[ch] >> 16, Lp, Hp, o2, o3);
+          ptx::st_shared_v4(base + ((ch ^ swz) << 4), o0, o1, o2, o3);
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&afull[s]);
       }
-      ptx::fence_proxy_async_smem();
-      ptx::mbar_arrive(&afull[s]);
+      it += total;
+      cit += nk;
     }
   }
 
@@ -625,7 +637,7 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
   const int m_tiles = (args.M + BM - 1) / BM, n_tiles = (args.N + BN - 1) / BN;
   const int tiles = m_tiles * n_tiles * args.splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, NF4 ? 448 : 192, L::BYTES, s>>>(a, b, a2, b2, c, args);
+  kern<<<grid, NF4 ? kNF4Threads : 192, L::BYTES, s>>>(a, b, a2, b2, c, args);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }

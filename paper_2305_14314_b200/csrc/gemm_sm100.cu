@@ -44,6 +44,8 @@ struct Args {
   const float* c1;
   const float* mu;
   const float* absmax;  // plain constants if dq_codes == nullptr
+  const float* consts;  // fp32 block constants [w_rows][kpitch] (prepass; TMA-fed)
+  int64_t kpitch;
   int64_t w_rows, w_cols;
   int bs2;
   int bs2_shift;        // log2(bs2) when bs2 is a power of two, else -1
@@ -66,11 +68,11 @@ struct Smem {
   static constexpr int EPI_BYTES = kNumEpiWarps * 32 * 32 * 2;  // 32x32 bf16 transpose tile per warp
   // NF4: a separate, decoupled ring of packed codes (4 KB = 128 x 64 nibbles)
   // plus the 128 fp32 block constants of each A stage
-  static constexpr int CODE_BYTES = 4096, CONST_BYTES = 512;
+  static constexpr int CODE_BYTES = 4096, CONST_BYTES = 2048;
   static constexpr int CST = NF4 ? (BN >= 128 ? 4 : 8) : 0;
   static constexpr int CRING = CST * (CODE_BYTES + CONST_BYTES);
-  // as many A/B stages as fit in ~220 KB, at most 8, even
-  static constexpr int FIT = (220 * 1024 - EPI_BYTES - CRING) / (A_STAGE + B_STAGE);
+  // as many A/B stages as fit in ~226 KB, at most 8, even
+  static constexpr int FIT = (226 * 1024 - EPI_BYTES - CRING) / (A_STAGE + B_STAGE);
   static constexpr int STAGES = (FIT > 8 ? 8 : FIT) & ~1;
   static constexpr int C_OFF = STAGES * (A_STAGE + B_STAGE);
   static constexpr int EPI_OFF = C_OFF + CRING;
@@ -202,7 +204,8 @@ template <int BN, bool NF4>
 __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
-                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ Args p) {
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmK,
+                const __grid_constant__ Args p) {
   using L = Smem<BN, NF4>;
   constexpr int STAGES = L::STAGES;
   constexpr int CST = L::CST > 0 ? L::CST : 1;
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
   if (warp == kTmaWarp && lane == 0) {
     ptx::prefetch_tmap(&tmB);
     if (!NF4) ptx::prefetch_tmap(&tmA);
-    if (NF4) ptx::prefetch_tmap(&tmC);
+    if (NF4) { ptx::prefetch_tmap(&tmC); ptx::prefetch_tmap(&tmK); }
     if (p.k_iters_aug) { ptx::prefetch_tmap(&tmA2); ptx::prefetch_tmap(&tmB2); }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
       ptx::mbar_init(&empty[s], 1);
     }
     for (int c = 0; c < L::CST; ++c) {
-      ptx::mbar_init(&cfull[c], 2);      // TMA expect_tx arrival + constants-written arrival
+      ptx::mbar_init(&cfull[c], 1);      // TMA expect_tx arrival (codes + constants bytes)
       ptx::mbar_init(&cempty[c], 128);   // every thread of the consuming dequant group
     }
     for (int a = 0; a < 2; ++a) {
@@ -391,56 +394,33 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     }
   } else if (NF4 && warp == kCstWarp) {
     // ======================= codes + block-constant producer =======================
-    // Runs ahead of the dequant warps through its own ring: lane 0 TMA-loads
-    // the packed codes of the next A tile (fwd: W[k0:k0+64, m0:m0+128] as
-    // 64 rows x 64 B; bwd: W[m0:m0+128, k0:k0+64] as 128 rows x 32 B) and all
-    // lanes rebuild the 128 block constants from their DQ bytes (exact fp64,
-    // doublequant.py:190-195), so the dequant warps never wait on global memory.
-    const float mu = p.dq_codes ? *p.mu : 0.0f;
-    uint32_t cit = 0;
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
-      int mt, nt, z;
-      tile_coords(t, m_tiles, n_tiles, mt, nt, z);
-      const int kb = z * kc;
-      const int nk = min(kc, p.k_iters - kb);
-      for (int i = 0; i < nk; ++i, ++cit) {
-        const int c = cit % CST;
-        const uint32_t cph = (cit / CST) & 1;
-        const int k0 = (kb + i) * BK;
-        // issue the constant loads before waiting for the slot
-        float cv[4];
-        uint32_t dqb[4];
-        bool live[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int item = q * 32 + lane;
-          const int h = item & 1, rr = item >> 1;
-          const int64_t wr = p.nf4_mode == 1 ? (int64_t)k0 + rr : (int64_t)mt * BM + item;
-          const int64_t wc = p.nf4_mode == 1 ? (int64_t)mt * BM + h * 64 : (int64_t)k0;
-          live[q] = wr < p.w_rows && wc < p.w_cols;
-          const int64_t blk = live[q] ? (wr * p.w_cols + wc) >> 6 : 0;
-          if (p.dq_codes) {
-            dqb[q] = __ldg(p.dq_codes + blk);
-            cv[q] = __ldg(p.c1 + (p.bs2_shift >= 0 ? (blk >> p.bs2_shift) : blk / p.bs2));
+    // Runs ahead of the dequant warps through its own ring, TMA-loading the
+    // packed codes of the next A tile (fwd: W[k0:k0+64, m0:m0+128] as 64 rows
+    // x 64 B; bwd: W[m0:m0+128, k0:k0+64] as 128 rows x 32 B) and the matching
+    // fp32 block constants (fwd: 64 rows x 4; bwd: 128 rows x 4, box-padded).
+    if (lane == 0) {
+      uint32_t cit = 0;
+      const uint32_t kbytes = p.nf4_mode == 1 ? 64 * 16 : 128 * 16;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+        int mt, nt, z;
+        tile_coords(t, m_tiles, n_tiles, mt, nt, z);
+        const int kb = z * kc;
+        const int nk = min(kc, p.k_iters - kb);
+        for (int i = 0; i < nk; ++i, ++cit) {
+          const int c = cit % CST;
+          const int k0 = (kb + i) * BK;
+          ptx::mbar_wait(&cempty[c], ((cit / CST) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&cfull[c], L::CODE_BYTES + kbytes);
+          uint8_t* cdst = sC + c * L::CODE_BYTES;
+          float* kdst = sK + c * (L::CONST_BYTES / 4);
+          if (p.nf4_mode == 1) {
+            ptx::tma_load_2d(&tmC, &cfull[c], cdst, mt * BM / 2, k0);
+            ptx::tma_load_2d(&tmK, &cfull[c], kdst, mt * 2, k0);
           } else {
-            dqb[q] = 0;
-            cv[q] = __ldg(p.absmax + blk);
+            ptx::tma_load_2d(&tmC, &cfull[c], cdst, k0 / 2, mt * BM);
+            ptx::tma_load_2d(&tmK, &cfull[c], kdst, k0 / 64, mt * BM);
           }
         }
-        ptx::mbar_wait(&cempty[c], cph ^ 1);
-        if (lane == 0) {
-          ptx::mbar_arrive_expect_tx(&cfull[c], L::CODE_BYTES);
-          if (p.nf4_mode == 1) ptx::tma_load_2d(&tmC, &cfull[c], sC + c * L::CODE_BYTES, mt * BM / 2, k0);
-          else ptx::tma_load_2d(&tmC, &cfull[c], sC + c * L::CODE_BYTES, k0 / 2, mt * BM);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float cc = cv[q];
-          if (p.dq_codes) cc = dq_constant(dqb[q], cv[q], mu, p.spec);
-          sK[c * 128 + q * 32 + lane] = live[q] ? cc : 0.0f;
-        }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&cfull[c]);
       }
     }
   } else if (NF4 && warp >= kXfWarp0 && warp < kXfWarp0 + kNumXfWarps) {
@@ -458,7 +438,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     const uint32_t soff = p.nf4_mode == 1 ? (uint32_t)(h * 8192 + rr * 128) : (uint32_t)(item * 128);
     const uint32_t swz = (soff >> 7) & 7;
     const uint32_t codes_s = ptx::smem_u32(sC) + (uint32_t)item * 32;
-    const uint32_t consts_s = ptx::smem_u32(sK) + (uint32_t)item * 4;
+    // constants tile: fwd [64 rows][4] -> (r, h); bwd [128 rows][4] -> (item, 0)
+    const uint32_t consts_s = ptx::smem_u32(sK) + (p.nf4_mode == 1 ? (uint32_t)(rr * 16 + h * 4) : (uint32_t)item * 16);
     const uint32_t a_s = ptx::smem_u32(sA) + soff;
     uint32_t it = 0, cit = 0;
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
@@ -541,6 +522,25 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
   }
 }
 
+// double-dequantized block constants of a weight as an fp32 matrix
+// [w_rows][kpitch] (kpitch = n_out/64 rounded up to 4 for TMA): the same
+// arithmetic as dq_decompress (doublequant.py:190-195), once per GEMM call.
+__global__ void dq_constants_kernel(const uint8_t* __restrict__ dq_codes, const float* __restrict__ c1,
+                                    const float* __restrict__ mu, int64_t rows, int64_t nbr, int64_t kpitch,
+                                    int bs2, qlrt_fp8spec sp, float* __restrict__ out) {
+  const float m = *mu;
+  const int64_t total = rows * kpitch;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / kpitch, j = i - r * kpitch;
+    float c = 0.0f;
+    if (j < nbr) {
+      const int64_t blk = r * nbr + j;
+      c = dq_constant(dq_codes[blk], c1[blk / bs2], m, sp);
+    }
+    out[i] = c;
+  }
+}
+
 // GEMV finish: y[n] = bf16( sum_z ws[z][n] + s * sum_j t[j] l2[j][n] )
 __global__ void gemv_finish_kernel(const float* __restrict__ ws, int splits, int N,
                                    const float* __restrict__ t, const __nv_bfloat16* __restrict__ l2, int rank,
@@ -606,6 +606,20 @@ static bool make_tmap_u8(CUtensorMap* m, const void* base, int64_t inner_bytes, 
   return r == CUDA_SUCCESS;
 }
 
+// fp32 matrix [rows][inner] (inner padded to a 16 B multiple), no swizzle
+static bool make_tmap_f32(CUtensorMap* m, const void* base, int64_t inner, int64_t rows, int box_inner, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || (((uintptr_t)base) & 15) || ((inner * 4) & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(inner * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // One GEMM operand.  K-major: stored [rows][K] (pitch ld); MN-major: stored [K][rows].
 struct Operand {
   const void* ptr = nullptr;
@@ -625,7 +639,7 @@ static int num_sms() {
 
 template <int BN, bool NF4>
 static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2, const CUtensorMap& b2,
-                            const CUtensorMap& c, const Args& args, cudaStream_t s) {
+                            const CUtensorMap& c, const CUtensorMap& k, const Args& args, cudaStream_t s) {
   using L = Smem<BN, NF4>;
   auto kern = gemm_kernel<BN, NF4>;
   static bool attr = false;
@@ -637,7 +651,7 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
   const int m_tiles = (args.M + BM - 1) / BM, n_tiles = (args.N + BN - 1) / BN;
   const int tiles = m_tiles * n_tiles * args.splits;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, NF4 ? kNF4Threads : 192, L::BYTES, s>>>(a, b, a2, b2, c, args);
+  kern<<<grid, NF4 ? kNF4Threads : 192, L::BYTES, s>>>(a, b, a2, b2, c, k, args);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }
@@ -652,16 +666,18 @@ static int effective_splits(int splits, int k_iters) {
 // args.nf4_mode != 0 makes A the quantized weight (A operand ignored).
 static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand* A2, const Operand* B2, int64_t K,
                        int64_t K2, Args args, cudaStream_t s) {
-  CUtensorMap ta{}, tb{}, ta2{}, tb2{}, tc{};
+  CUtensorMap ta{}, tb{}, ta2{}, tb2{}, tc{}, tk{};
   const bool nf4 = args.nf4_mode != 0;
   if (nf4) {
-    // packed codes as a uint8 matrix [w_rows][w_cols/2]
+    // packed codes as a uint8 matrix [w_rows][w_cols/2]; constants fp32 [w_rows][kpitch]
     const bool ok = args.nf4_mode == 1 ? make_tmap_u8(&tc, args.codes, args.w_cols / 2, args.w_rows, 64, 64)
                                        : make_tmap_u8(&tc, args.codes, args.w_cols / 2, args.w_rows, 32, 128);
-    if (!ok) return QLRT_ERR_UNSUPPORTED;
+    if (!ok || !make_tmap_f32(&tk, args.consts, args.kpitch, args.w_rows, 4, args.nf4_mode == 1 ? 64 : 128))
+      return QLRT_ERR_UNSUPPORTED;
     args.bs2_shift = (args.bs2 > 0 && (args.bs2 & (args.bs2 - 1)) == 0) ? __builtin_ctz((unsigned)args.bs2) : -1;
   } else {
     tc = tb;
+    tk = tb;
   }
   const int64_t M = args.M, N = args.N;
   if (bn < 64 && (B.mn || (B2 && B2->mn))) return QLRT_ERR_UNSUPPORTED;
@@ -687,10 +703,10 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   args.splits = effective_splits(args.splits, args.k_iters);
   if (args.splits > 1 && K2) return QLRT_ERR_UNSUPPORTED;
   switch (bn) {
-    case 256: return nf4 ? launch_t<256, true>(ta, tb, ta2, tb2, tc, args, s) : launch_t<256, false>(ta, tb, ta2, tb2, tc, args, s);
-    case 128: return nf4 ? launch_t<128, true>(ta, tb, ta2, tb2, tc, args, s) : launch_t<128, false>(ta, tb, ta2, tb2, tc, args, s);
-    case 64: return nf4 ? launch_t<64, true>(ta, tb, ta2, tb2, tc, args, s) : launch_t<64, false>(ta, tb, ta2, tb2, tc, args, s);
-    case 16: return nf4 ? launch_t<16, true>(ta, tb, ta2, tb2, tc, args, s) : launch_t<16, false>(ta, tb, ta2, tb2, tc, args, s);
+    case 256: return nf4 ? launch_t<256, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<256, false>(ta, tb, ta2, tb2, tc, tk, args, s);
+    case 128: return nf4 ? launch_t<128, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<128, false>(ta, tb, ta2, tb2, tc, tk, args, s);
+    case 64: return nf4 ? launch_t<64, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<64, false>(ta, tb, ta2, tb2, tc, tk, args, s);
+    case 16: return nf4 ? launch_t<16, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<16, false>(ta, tb, ta2, tb2, tc, tk, args, s);
   }
   return QLRT_ERR_UNSUPPORTED;
 }
@@ -742,7 +758,13 @@ static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, 
   return reduce(a, s);
 }
 
-static void fill_nf4(Args& a, const qlrt_nf4_weight* w, int mode) {
+static int64_t kpitch_of(const qlrt_nf4_weight* w) { return ((w->n_out / 64) + 3) / 4 * 4; }
+static size_t consts_bytes(int64_t k_in, int64_t n_out) {
+  return (size_t)k_in * (size_t)(((n_out / 64) + 3) / 4 * 4) * 4;
+}
+
+// NF4 operand description + the per-call constants prepass into `consts`
+static qlrt_status fill_nf4(Args& a, const qlrt_nf4_weight* w, int mode, float* consts, cudaStream_t st) {
   a.nf4_mode = mode;
   a.codes = w->codes;
   a.dq_codes = w->dq_codes;
@@ -754,6 +776,15 @@ static void fill_nf4(Args& a, const qlrt_nf4_weight* w, int mode) {
   a.bs2 = w->blocksize2;
   a.spec = w->spec;
   for (int i = 0; i < 16; ++i) a.values[i] = w->values[i];
+  a.consts = consts;
+  a.kpitch = kpitch_of(w);
+  const int64_t total = w->k_in * a.kpitch;
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  dq_constants_kernel<<<(int)g, 256, 0, st>>>(w->dq_codes, w->c1, w->mu, w->k_in, w->n_out / 64, a.kpitch,
+                                             w->blocksize2, w->spec, consts);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
 }
 
 static bool weight_ok(const qlrt_nf4_weight* w) {
@@ -768,7 +799,7 @@ static size_t dbl_bytes(int64_t k_in, int64_t n_out, int rank) {
   const int64_t mx = k_in > n_out ? k_in : n_out;
   return align256((size_t)mx * 2 * rank * 2);
 }
-// the doubled-operand region sits at the end of the linear workspace
+// layout of the linear workspace: [split-K partials][constants][doubled adapter]
 static void* dbl_region(void* ws, size_t ws_bytes, int64_t k_in, int64_t n_out, int rank) {
   return (uint8_t*)ws + (ws_bytes - dbl_bytes(k_in, n_out, rank));
 }
@@ -789,7 +820,8 @@ size_t qlrt_linear_workspace_bytes(int64_t m, int64_t k_in, int64_t n_out, int r
   mx = mx > c ? mx : c;
   int64_t gemv = 32 * (n_out > k_in ? n_out : k_in) + 64 * ((r + 63) / 64) + 16 * r + 256;
   mx = mx > gemv ? mx : gemv;
-  return gemm::align256((size_t)mx * 4) + 4096 + gemm::dbl_bytes(k_in, n_out, rank > 0 ? rank : 0);
+  return gemm::align256((size_t)mx * 4) + 4096 + gemm::align256(gemm::consts_bytes(k_in, n_out)) +
+         gemm::dbl_bytes(k_in, n_out, rank > 0 ? rank : 0);
 }
 
 qlrt_status qlrt_gemm_bf16(const void* a, const void* b, void* d, int64_t m, int64_t n, int64_t k, int a_mn, int b_mn,
@@ -811,7 +843,8 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t K = w->k_in, N = w->n_out;
   const size_t ws_bytes = qlrt_linear_workspace_bytes(m, K, N, rank);
-  const size_t part_bytes = ws_bytes - gemm::dbl_bytes(K, N, rank);
+  const size_t part_bytes = ws_bytes - gemm::dbl_bytes(K, N, rank) - gemm::align256(gemm::consts_bytes(K, N));
+  float* consts = (float*)((uint8_t*)workspace + part_bytes);
   qlrt_status rc;
   if (rank > 0) {
     // Ts[m, 0:r] + Ts[m, r:2r] = s * Xa l1 as a bf16 hi/lo pair:
@@ -830,7 +863,7 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   a.out_f32 = 0;
   a.out_t = 1;
   a.alpha = 1.0f;
-  gemm::fill_nf4(a, w, 1);
+  if ((rc = gemm::fill_nf4(a, w, 1, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{x, K, 0};
   // augmented segment K2 = 2r: [l2 ; l2]^T [Ts_hi | Ts_lo]^T, i.e. the pair at ~16-bit precision
   __nv_bfloat16* l2d = (__nv_bfloat16*)gemm::dbl_region(workspace, ws_bytes, K, N, rank);
@@ -851,7 +884,8 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t K = w->k_in, N = w->n_out;
   const size_t ws_bytes = qlrt_linear_workspace_bytes(m, K, N, rank);
-  const size_t part_bytes = ws_bytes - gemm::dbl_bytes(K, N, rank);
+  const size_t part_bytes = ws_bytes - gemm::dbl_bytes(K, N, rank) - gemm::align256(gemm::consts_bytes(K, N));
+  float* consts = (float*)((uint8_t*)workspace + part_bytes);
   qlrt_status rc;
   if (rank > 0) {
     // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):
@@ -870,7 +904,7 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   a.out_f32 = 0;
   a.out_t = 1;
   a.alpha = 1.0f;
-  gemm::fill_nf4(a, w, 2);
+  if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{dy, N, 0};
   // augmented segment K2 = 2r: [l1 | l1] [dT_hi | dT_lo]^T
   __nv_bfloat16* l1d = (__nv_bfloat16*)gemm::dbl_region(workspace, ws_bytes, K, N, rank);
@@ -925,11 +959,15 @@ qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* l
   a.ws = ws;
   a.out_f32 = 1;
   a.alpha = 1.0f;
-  gemm::fill_nf4(a, w, 1);
-  Operand none{}, B{x, K, 0};
-  qlrt_status rc = gemm::run(16, none, B, nullptr, nullptr, K, 0, a, st);
-  if (rc != QLRT_OK) return rc;
+  // workspace: [partials 32*max(N,K)][t, t-partials][constants]
   float* t = ws + (size_t)32 * (N > K ? N : K);
+  float* consts = (float*)((uint8_t*)workspace +
+                           gemm::align256(((size_t)32 * (N > K ? N : K) + 64 * ((rank + 63) / 64) + 16 * rank + 256) * 4));
+  qlrt_status rc = gemm::fill_nf4(a, w, 1, consts, st);
+  if (rc != QLRT_OK) return rc;
+  Operand none{}, B{x, K, 0};
+  rc = gemm::run(16, none, B, nullptr, nullptr, K, 0, a, st);
+  if (rc != QLRT_OK) return rc;
   float* tws = t + 64 * ((rank + 63) / 64);
   if (rank > 0) {
     // t^T[r, 1] = l1^T x^T: A = l1 (MN-major [K][r]), B = x (K-major [1][K]), fp32, scaled later

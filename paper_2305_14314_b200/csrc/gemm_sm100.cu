@@ -415,10 +415,10 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           float* kdst = sK + c * (L::CONST_BYTES / 4);
           if (p.nf4_mode == 1) {
             ptx::tma_load_2d(&tmC, &cfull[c], cdst, mt * BM / 2, k0);
-            ptx::tma_load_2d(&tmK, &cfull[c], kdst, mt * 2, k0);
+            ptx::tma_load_2d(&tmK, &cfull[c], kdst, ((mt * 2) & ~3) * 4, k0);  // 16 B aligned start
           } else {
             ptx::tma_load_2d(&tmC, &cfull[c], cdst, k0 / 2, mt * BM);
-            ptx::tma_load_2d(&tmK, &cfull[c], kdst, k0 / 64, mt * BM);
+            ptx::tma_load_2d(&tmK, &cfull[c], kdst, ((k0 / 64) & ~3) * 4, mt * BM);
           }
         }
       }
@@ -459,11 +459,12 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
         }
         const uint32_t ci = cit + i;
         const int c = ci % CST;
+        // the constants box starts at a 16 B aligned column: index within it
+        const uint32_t kcol = (uint32_t)((p.nf4_mode == 1 ? mt * 2 : kb + i) & 3) * 4;
         ptx::mbar_wait(&cfull[c], (ci / CST) & 1);
         const uint4 w0 = ptx::ld_shared_v4(codes_s + c * L::CODE_BYTES);
         const uint4 w1 = ptx::ld_shared_v4(codes_s + c * L::CODE_BYTES + 16);
-        const float cst = ptx::ld_shared_f32(consts_s + c * L::CONST_BYTES);
-        ptx::mbar_arrive(&cempty[c]);
+        const float cst = ptx::ld_shared_f32(consts_s + c * L::CONST_BYTES + kcol);
         uint32_t Lp[4], Hp[4];
         build_planes(vals, cst, Lp, Hp);
         ptx::mbar_wait(&empty[s], ph ^ 1);
@@ -478,6 +479,10 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&afull[s]);
+        // release the codes slot only now: every loaded word has been consumed
+        // (an arrive right after the loads can overtake them, and the next TMA
+        // would overwrite the slot under an in-flight ld.shared)
+        ptx::mbar_arrive(&cempty[c]);
       }
       it += total;
       cit += nk;
@@ -606,20 +611,6 @@ static bool make_tmap_u8(CUtensorMap* m, const void* base, int64_t inner_bytes, 
   return r == CUDA_SUCCESS;
 }
 
-// fp32 matrix [rows][inner] (inner padded to a 16 B multiple), no swizzle
-static bool make_tmap_f32(CUtensorMap* m, const void* base, int64_t inner, int64_t rows, int box_inner, int box_rows) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn || (((uintptr_t)base) & 15) || ((inner * 4) & 15)) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(inner * 4)};
-  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 // One GEMM operand.  K-major: stored [rows][K] (pitch ld); MN-major: stored [K][rows].
 struct Operand {
   const void* ptr = nullptr;
@@ -672,7 +663,8 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
     // packed codes as a uint8 matrix [w_rows][w_cols/2]; constants fp32 [w_rows][kpitch]
     const bool ok = args.nf4_mode == 1 ? make_tmap_u8(&tc, args.codes, args.w_cols / 2, args.w_rows, 64, 64)
                                        : make_tmap_u8(&tc, args.codes, args.w_cols / 2, args.w_rows, 32, 128);
-    if (!ok || !make_tmap_f32(&tk, args.consts, args.kpitch, args.w_rows, 4, args.nf4_mode == 1 ? 64 : 128))
+    // the fp32 constants are moved as raw bytes (16 B = 4 floats per row)
+    if (!ok || !make_tmap_u8(&tk, args.consts, args.kpitch * 4, args.w_rows, 16, args.nf4_mode == 1 ? 64 : 128))
       return QLRT_ERR_UNSUPPORTED;
     args.bs2_shift = (args.bs2 > 0 && (args.bs2 & (args.bs2 - 1)) == 0) ? __builtin_ctz((unsigned)args.bs2) : -1;
   } else {

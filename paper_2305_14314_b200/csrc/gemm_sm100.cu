@@ -60,16 +60,18 @@ struct Args {
   int to_ws;            // force fp32 partials to ws (finished by the reduce kernel)
   int out_split;        // bf16 out: also store lo = bf16(v - hi) at column offset out_split
   int fold;             // reduce: out[:, n] = D[:, n] + D[:, n + fold] for n < fold
+  int pair;             // 2-CTA (cta_group::2) 256 x BN tiles
 };
 
-template <int BN, bool NF4>
+template <int BN, bool NF4, bool PAIR = false>
 struct Smem {
-  static constexpr int B_STAGE = BN * BK * 2;
+  static constexpr int BNC = PAIR ? BN / 2 : BN;       // B rows (tokens) held by this CTA
+  static constexpr int B_STAGE = BNC * BK * 2;
   static constexpr int EPI_BYTES = kNumEpiWarps * 32 * 32 * 2;  // 32x32 bf16 transpose tile per warp
   // NF4: a separate, decoupled ring of packed codes (4 KB = 128 x 64 nibbles)
-  // plus the 128 fp32 block constants of each A stage
+  // plus the fp32 block constants of each A stage
   static constexpr int CODE_BYTES = 4096, CONST_BYTES = 2048;
-  static constexpr int CST = NF4 ? (BN >= 128 ? 4 : 8) : 0;
+  static constexpr int CST = NF4 ? (BNC >= 128 ? 4 : 8) : 0;
   static constexpr int CRING = CST * (CODE_BYTES + CONST_BYTES);
   // as many A/B stages as fit in ~226 KB, at most 8, even
   static constexpr int FIT = (226 * 1024 - EPI_BYTES - CRING) / (A_STAGE + B_STAGE);
@@ -199,22 +201,29 @@ __device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[E
 
 // ---------------------------------------------------------------------------
 // the kernel
+// PAIR: a 2-CTA cluster computes a 256 x BN tile with tcgen05.mma.cta_group::2;
+// each CTA owns 128 rows of A (its half of M, dequantized or TMA-loaded into
+// its own smem) and BN/2 rows of B; the leader (rank 0) issues the MMAs, the
+// byte counts and producer arrivals of both CTAs land on the leader's
+// barriers, and its commits are multicast to both CTAs.
 // ---------------------------------------------------------------------------
-template <int BN, bool NF4>
+template <int BN, bool NF4, bool PAIR>
 __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ Args p) {
-  using L = Smem<BN, NF4>;
+  using L = Smem<BN, NF4, PAIR>;
   constexpr int STAGES = L::STAGES;
   constexpr int CST = L::CST > 0 ? L::CST : 1;
+  constexpr int BMP = PAIR ? 2 * BM : BM;   // M rows per (pair) tile
+  constexpr int BNC = L::BNC;               // B rows per CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE;
   uint8_t* sC = smem + L::C_OFF;                       // NF4 codes ring: [CST][4 KB]
-  float* sK = reinterpret_cast<float*>(smem + L::C_OFF + L::CST * L::CODE_BYTES);  // [CST][128] constants
+  float* sK = reinterpret_cast<float*>(smem + L::C_OFF + L::CST * L::CODE_BYTES);  // constants ring
   __nv_bfloat16* sE = reinterpret_cast<__nv_bfloat16*>(smem + L::EPI_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* full = bars;
@@ -228,11 +237,17 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  // work unit = one (pair) tile; a cluster walks the tile list
+  const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int n_units = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
-  const int m_tiles = (p.M + BM - 1) / BM;
+  const int m_tiles = (p.M + BMP - 1) / BMP;
   const int n_tiles = (p.N + BN - 1) / BN;
   const int n_tiles_total = m_tiles * n_tiles * p.splits;
   const int kc = (p.k_iters + p.splits - 1) / p.splits;
+  constexpr uint32_t kNTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
 
   if (warp == kTmaWarp && lane == 0) {
     ptx::prefetch_tmap(&tmB);
@@ -241,7 +256,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     if (p.k_iters_aug) { ptx::prefetch_tmap(&tmA2); ptx::prefetch_tmap(&tmB2); }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&afull[s], NF4 ? 128 : 1);
+      ptx::mbar_init(&afull[s], NF4 ? (PAIR ? 256 : 128) : 1);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int c = 0; c < L::CST; ++c) {
@@ -250,26 +265,49 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], kNumEpiWarps * 32);
+      ptx::mbar_init(&tempty[a], (PAIR ? 2 : 1) * kNumEpiWarps * 32);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == kMmaWarp) ptx::tmem_alloc(tmem_slot, 2 * BN < 32 ? 32 : 2 * BN);
+  if (warp == kMmaWarp) {
+    if (PAIR) ptx::tmem_alloc_pair(tmem_slot, kNTmemCols);
+    else ptx::tmem_alloc(tmem_slot, kNTmemCols);
+  }
   ptx::tc_fence_before();
   __syncthreads();
+  if (PAIR) ptx::cluster_sync();  // peer barriers initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // leader-side barrier addresses (shared::cluster) for remote arrivals / TMA bytes
+  auto leader_addr = [&](uint64_t* bar) -> uint32_t {
+    return PAIR ? ptx::mapa_shared(ptx::smem_u32(bar), 0) : ptx::smem_u32(bar);
+  };
+  auto arrive_leader = [&](uint64_t* bar) {
+    if (PAIR) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(bar), 0));
+    else ptx::mbar_arrive(bar);
+  };
+  auto wait_x = [&](uint64_t* bar, uint32_t ph) {
+    if (PAIR) ptx::mbar_wait_cluster(bar, ph);
+    else ptx::mbar_wait(bar, ph);
+  };
+  auto tma = [&](const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1) {
+    if (PAIR) ptx::tma_load_2d_pair(m, leader_addr(bar), dst, c0, c1);
+    else ptx::tma_load_2d(m, bar, dst, c0, c1);
+  };
+
   if (warp == kTmaWarp) {
-    // ======================= TMA producer =======================
+    // ======================= TMA producer (every CTA loads its own halves) =======================
     if (lane == 0) {
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+      for (int t = unit0; t < n_tiles_total; t += n_units) {
         int mt, nt, z;
         tile_coords(t, m_tiles, n_tiles, mt, nt, z);
         const int kb = z * kc;
         const int nk = min(kc, p.k_iters - kb);
         const int total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
+        const int m_cta = mt * BMP + (int)rank * BM;
+        const int n_cta = nt * BN + (int)rank * BNC;
         for (int i = 0; i < total; ++i, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -281,81 +319,89 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           const int bmn = aug ? p.b2_mn : p.b_mn;
           const int k0 = (aug ? (i - nk) : (kb + i)) * BK;
           const bool a_tma = aug || !NF4;
-          ptx::mbar_arrive_expect_tx(&full[s], L::B_STAGE + (a_tma ? A_STAGE : 0));
+          if (leader)  // one arrival per phase; both CTAs' bytes
+            ptx::mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * (L::B_STAGE + (a_tma ? A_STAGE : 0)));
           uint8_t* a_dst = sA + s * A_STAGE;
           uint8_t* b_dst = sB + s * L::B_STAGE;
           if (a_tma) {
             if (amn) {
-              ptx::tma_load_2d(ma, &full[s], a_dst, mt * BM, k0);
-              ptx::tma_load_2d(ma, &full[s], a_dst + 8192, mt * BM + 64, k0);
+              tma(ma, &full[s], a_dst, m_cta, k0);
+              tma(ma, &full[s], a_dst + 8192, m_cta + 64, k0);
             } else {
-              ptx::tma_load_2d(ma, &full[s], a_dst, k0, mt * BM);
+              tma(ma, &full[s], a_dst, k0, m_cta);
             }
           }
           if (bmn) {
 #pragma unroll
-            for (int j = 0; j < (BN + 63) / 64; ++j)
-              ptx::tma_load_2d(mb, &full[s], b_dst + j * 8192, nt * BN + j * 64, k0);
+            for (int j = 0; j < (BNC + 63) / 64; ++j) tma(mb, &full[s], b_dst + j * 8192, n_cta + j * 64, k0);
           } else {
-            ptx::tma_load_2d(mb, &full[s], b_dst, k0, nt * BN);
+            tma(mb, &full[s], b_dst, k0, n_cta);
           }
         }
       }
     }
   } else if (warp == kMmaWarp) {
-    // ======================= MMA issuer =======================
-    uint32_t it = 0, local = 0;
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++local) {
-      int mt, nt, z;
-      tile_coords(t, m_tiles, n_tiles, mt, nt, z);
-      const int kb = z * kc;
-      const int nk = min(kc, p.k_iters - kb);
-      const int total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
-      const uint32_t acc = local & 1;
-      ptx::mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
-      ptx::tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int i = 0; i < total; ++i, ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        const bool aug = i >= nk;
-        ptx::mbar_wait(&full[s], ph);
-        if (NF4) ptx::mbar_wait(&afull[s], ph);
+    // ======================= MMA issuer (leader only) =======================
+    if (leader) {
+      uint32_t it = 0, local = 0;
+      for (int t = unit0; t < n_tiles_total; t += n_units, ++local) {
+        int mt, nt, z;
+        tile_coords(t, m_tiles, n_tiles, mt, nt, z);
+        const int kb = z * kc;
+        const int nk = min(kc, p.k_iters - kb);
+        const int total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
+        const uint32_t acc = local & 1;
+        wait_x(&tempty[acc], ((local >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
-        const int amn = aug ? p.a2_mn : (NF4 ? (p.nf4_mode == 1) : p.a_mn);
-        const int bmn = aug ? p.b2_mn : p.b_mn;
-        const uint32_t idesc = ptx::idesc_bf16(BM, BN, amn, bmn);
-        const uint32_t a_addr = ptx::smem_u32(sA + s * A_STAGE);
-        const uint32_t b_addr = ptx::smem_u32(sB + s * L::B_STAGE);
-        if (lane == 0) {
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int i = 0; i < total; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          const bool aug = i >= nk;
+          wait_x(&full[s], ph);
+          if (NF4) wait_x(&afull[s], ph);
+          ptx::tc_fence_after();
+          const int amn = aug ? p.a2_mn : (NF4 ? (p.nf4_mode == 1) : p.a_mn);
+          const int bmn = aug ? p.b2_mn : p.b_mn;
+          const uint32_t idesc = ptx::idesc_bf16(BMP, BN, amn, bmn);
+          const uint32_t a_addr = ptx::smem_u32(sA + s * A_STAGE);
+          const uint32_t b_addr = ptx::smem_u32(sB + s * L::B_STAGE);
+          if (lane == 0) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = amn ? ptx::sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
-                                    : ptx::sdesc_sw128(a_addr + kk * 32, 16, 1024);
-            const uint64_t bd = bmn ? ptx::sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
-                                    : ptx::sdesc_sw128(b_addr + kk * 32, 16, 1024);
-            ptx::umma_bf16(d_tmem, ad, bd, idesc, (i | kk) != 0);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t ad = amn ? ptx::sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
+                                      : ptx::sdesc_sw128(a_addr + kk * 32, 16, 1024);
+              const uint64_t bd = bmn ? ptx::sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
+                                      : ptx::sdesc_sw128(b_addr + kk * 32, 16, 1024);
+              if (PAIR) ptx::umma_bf16_pair(d_tmem, ad, bd, idesc, (i | kk) != 0);
+              else ptx::umma_bf16(d_tmem, ad, bd, idesc, (i | kk) != 0);
+            }
+            if (PAIR) ptx::umma_commit_pair_mc(&empty[s], 0x3);
+            else ptx::umma_commit(&empty[s]);
           }
-          ptx::umma_commit(&empty[s]);
+          __syncwarp();
+        }
+        if (lane == 0) {
+          if (PAIR) ptx::umma_commit_pair_mc(&tfull[acc], 0x3);
+          else ptx::umma_commit(&tfull[acc]);
         }
         __syncwarp();
       }
-      if (lane == 0) ptx::umma_commit(&tfull[acc]);
-      __syncwarp();
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpiWarps) {
-    // ======================= epilogue =======================
+    // ======================= epilogue (each CTA drains its own TMEM rows) =======================
     constexpr int EC = BN < 32 ? BN : 32;   // columns per tcgen05.ld
     const int quarter = warp & 3;           // TMEM lane quarter this warp may access
-    const int row = quarter * 32 + lane;    // accumulator row (M index within tile)
+    const int row = quarter * 32 + lane;    // accumulator row (M index within this CTA's half)
     uint32_t local = 0;
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++local) {
+    for (int t = unit0; t < n_tiles_total; t += n_units, ++local) {
       int mt, nt, z;
       tile_coords(t, m_tiles, n_tiles, mt, nt, z);
       const uint32_t acc = local & 1;
       ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
-      const int64_t m = (int64_t)mt * BM + row;
+      const int64_t m_base = (int64_t)mt * BMP + (int64_t)rank * BM;
+      const int64_t m = m_base + row;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += EC) {
         uint32_t r[EC];
@@ -368,7 +414,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
 #pragma unroll
           for (int j = 0; j < EC; ++j) st[j * 32 + lane] = __float2bfloat16_rn(__uint_as_float(r[j]) * p.alpha);
           __syncwarp();
-          const int64_t mcol = (int64_t)mt * BM + quarter * 32 + (lane & 3) * 8;
+          const int64_t mcol = m_base + quarter * 32 + (lane & 3) * 8;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int rr = q * 8 + (lane >> 2);
@@ -390,22 +436,23 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
         }
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[acc]);
+      arrive_leader(&tempty[acc]);
     }
   } else if (NF4 && warp == kCstWarp) {
     // ======================= codes + block-constant producer =======================
     // Runs ahead of the dequant warps through its own ring, TMA-loading the
-    // packed codes of the next A tile (fwd: W[k0:k0+64, m0:m0+128] as 64 rows
-    // x 64 B; bwd: W[m0:m0+128, k0:k0+64] as 128 rows x 32 B) and the matching
-    // fp32 block constants (fwd: 64 rows x 4; bwd: 128 rows x 4, box-padded).
+    // packed codes of this CTA's next A half-tile (fwd: W[k0:k0+64, m:m+128]
+    // as 64 rows x 64 B; bwd: W[m:m+128, k0:k0+64] as 128 rows x 32 B) and the
+    // matching fp32 block constants (fwd: 64 rows x 4; bwd: 128 rows x 4).
     if (lane == 0) {
       uint32_t cit = 0;
       const uint32_t kbytes = p.nf4_mode == 1 ? 64 * 16 : 128 * 16;
-      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+      for (int t = unit0; t < n_tiles_total; t += n_units) {
         int mt, nt, z;
         tile_coords(t, m_tiles, n_tiles, mt, nt, z);
         const int kb = z * kc;
         const int nk = min(kc, p.k_iters - kb);
+        const int m_cta = mt * BMP + (int)rank * BM;
         for (int i = 0; i < nk; ++i, ++cit) {
           const int c = cit % CST;
           const int k0 = (kb + i) * BK;
@@ -414,11 +461,11 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           uint8_t* cdst = sC + c * L::CODE_BYTES;
           float* kdst = sK + c * (L::CONST_BYTES / 4);
           if (p.nf4_mode == 1) {
-            ptx::tma_load_2d(&tmC, &cfull[c], cdst, mt * BM / 2, k0);
-            ptx::tma_load_2d(&tmK, &cfull[c], kdst, ((mt * 2) & ~3) * 4, k0);  // 16 B aligned start
+            ptx::tma_load_2d(&tmC, &cfull[c], cdst, m_cta / 2, k0);
+            ptx::tma_load_2d(&tmK, &cfull[c], kdst, ((m_cta / 64) & ~3) * 4, k0);  // 16 B aligned start
           } else {
-            ptx::tma_load_2d(&tmC, &cfull[c], cdst, k0 / 2, mt * BM);
-            ptx::tma_load_2d(&tmK, &cfull[c], kdst, ((k0 / 64) & ~3) * 4, mt * BM);
+            ptx::tma_load_2d(&tmC, &cfull[c], cdst, k0 / 2, m_cta);
+            ptx::tma_load_2d(&tmK, &cfull[c], kdst, ((k0 / 64) & ~3) * 4, m_cta);
           }
         }
       }
@@ -432,8 +479,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
 #pragma unroll
     for (int i = 0; i < 16; ++i) vals[i] = (float)p.values[i];
     // fwd: item -> (h = item & 1, r = item >> 1): A image at h*8192 + r*128,
-    //      codes at r*64 + h*32 (W row k0+r, cols m0+64h..+64)
-    // bwd: item -> W row m0+item, cols k0..k0+64: A image item*128, codes item*32
+    //      codes at r*64 + h*32 (W row k0+r, cols m+64h..+64)
+    // bwd: item -> W row m+item, cols k0..k0+64: A image item*128, codes item*32
     const int h = item & 1, rr = item >> 1;
     const uint32_t soff = p.nf4_mode == 1 ? (uint32_t)(h * 8192 + rr * 128) : (uint32_t)(item * 128);
     const uint32_t swz = (soff >> 7) & 7;
@@ -442,25 +489,26 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     const uint32_t consts_s = ptx::smem_u32(sK) + (p.nf4_mode == 1 ? (uint32_t)(rr * 16 + h * 4) : (uint32_t)item * 16);
     const uint32_t a_s = ptx::smem_u32(sA) + soff;
     uint32_t it = 0, cit = 0;
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+    for (int t = unit0; t < n_tiles_total; t += n_units) {
       int mt, nt, z;
       tile_coords(t, m_tiles, n_tiles, mt, nt, z);
       const int kb = z * kc;
       const int nk = min(kc, p.k_iters - kb);
       const int total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
+      const int m_cta = mt * BMP + (int)rank * BM;
       for (int i = (int)((it & 1) != (uint32_t)grp); i < total; i += 2) {
         const uint32_t my = it + i;
         const int s = my % STAGES;
         const uint32_t ph = (my / STAGES) & 1;
         if (i >= nk) {  // augmented (TMA-fed) stage: keep afull's phase in step
           ptx::mbar_wait(&empty[s], ph ^ 1);
-          ptx::mbar_arrive(&afull[s]);
+          arrive_leader(&afull[s]);
           continue;
         }
         const uint32_t ci = cit + i;
         const int c = ci % CST;
         // the constants box starts at a 16 B aligned column: index within it
-        const uint32_t kcol = (uint32_t)((p.nf4_mode == 1 ? mt * 2 : kb + i) & 3) * 4;
+        const uint32_t kcol = (uint32_t)((p.nf4_mode == 1 ? m_cta / 64 : kb + i) & 3) * 4;
         ptx::mbar_wait(&cfull[c], (ci / CST) & 1);
         const uint4 w0 = ptx::ld_shared_v4(codes_s + c * L::CODE_BYTES);
         const uint4 w1 = ptx::ld_shared_v4(codes_s + c * L::CODE_BYTES + 16);
@@ -478,7 +526,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           ptx::st_shared_v4(base + ((ch ^ swz) << 4), o0, o1, o2, o3);
         }
         ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&afull[s]);
+        arrive_leader(&afull[s]);
         // release the codes slot only now: every loaded word has been consumed
         // (an arrive right after the loads can overtake them, and the next TMA
         // would overwrite the slot under an in-flight ld.shared)
@@ -491,12 +539,13 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (PAIR) ptx::cluster_sync();
   if (warp == kMmaWarp) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, 2 * BN < 32 ? 32 : 2 * BN);
+    if (PAIR) ptx::tmem_dealloc_pair(tmem_base, kNTmemCols);
+    else ptx::tmem_dealloc(tmem_base, kNTmemCols);
   }
 }
-
 
 // split-K reduction: out = alpha * sum_z ws[z]  (fixed order -> deterministic);
 // fold > 0 also adds column n + fold into column n (hi/lo operand pairs);
@@ -628,21 +677,37 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, bool NF4>
+template <int BN, bool NF4, bool PAIR = false>
 static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2, const CUtensorMap& b2,
                             const CUtensorMap& c, const CUtensorMap& k, const Args& args, cudaStream_t s) {
-  using L = Smem<BN, NF4>;
-  auto kern = gemm_kernel<BN, NF4>;
+  using L = Smem<BN, NF4, PAIR>;
+  auto kern = gemm_kernel<BN, NF4, PAIR>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES) != cudaSuccess)
       return QLRT_ERR_CUDA;
     attr = true;
   }
-  const int m_tiles = (args.M + BM - 1) / BM, n_tiles = (args.N + BN - 1) / BN;
+  const int bmp = PAIR ? 2 * BM : BM;
+  const int m_tiles = (args.M + bmp - 1) / bmp, n_tiles = (args.N + BN - 1) / BN;
   const int tiles = m_tiles * n_tiles * args.splits;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, NF4 ? kNF4Threads : 192, L::BYTES, s>>>(a, b, a2, b2, c, k, args);
+  const int units_max = PAIR ? num_sms() / 2 : num_sms();
+  const int units = tiles < units_max ? tiles : units_max;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(units * (PAIR ? 2 : 1));
+  cfg.blockDim = dim3(NF4 ? kNF4Threads : 192);
+  cfg.dynamicSmemBytes = L::BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[1];
+  if (PAIR) {
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+  }
+  if (cudaLaunchKernelEx(&cfg, kern, a, b, a2, b2, c, k, args) != cudaSuccess) return QLRT_ERR_CUDA;
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }
@@ -675,12 +740,14 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   if (bn < 64 && (B.mn || (B2 && B2->mn))) return QLRT_ERR_UNSUPPORTED;
   if (!nf4 && !(A.mn ? make_tmap(&ta, A.ptr, M, K, A.ld, 64) : make_tmap(&ta, A.ptr, K, M, A.ld, BM)))
     return QLRT_ERR_UNSUPPORTED;
-  if (!(B.mn ? make_tmap(&tb, B.ptr, N, K, B.ld, 64) : make_tmap(&tb, B.ptr, K, N, B.ld, bn)))
+  if (args.pair && (bn != 256 || (B2 && B2->mn && bn / 2 < 64))) return QLRT_ERR_UNSUPPORTED;
+  const int bbox = args.pair ? bn / 2 : bn;  // B rows each CTA loads
+  if (!(B.mn ? make_tmap(&tb, B.ptr, N, K, B.ld, 64) : make_tmap(&tb, B.ptr, K, N, B.ld, bbox)))
     return QLRT_ERR_UNSUPPORTED;
   if (K2) {
     if (!(A2->mn ? make_tmap(&ta2, A2->ptr, M, K2, A2->ld, 64) : make_tmap(&ta2, A2->ptr, K2, M, A2->ld, BM)))
       return QLRT_ERR_UNSUPPORTED;
-    if (!(B2->mn ? make_tmap(&tb2, B2->ptr, N, K2, B2->ld, 64) : make_tmap(&tb2, B2->ptr, K2, N, B2->ld, bn)))
+    if (!(B2->mn ? make_tmap(&tb2, B2->ptr, N, K2, B2->ld, 64) : make_tmap(&tb2, B2->ptr, K2, N, B2->ld, bbox)))
       return QLRT_ERR_UNSUPPORTED;
   } else {
     ta2 = nf4 ? tb : ta;
@@ -695,7 +762,10 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   args.splits = effective_splits(args.splits, args.k_iters);
   if (args.splits > 1 && K2) return QLRT_ERR_UNSUPPORTED;
   switch (bn) {
-    case 256: return nf4 ? launch_t<256, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<256, false>(ta, tb, ta2, tb2, tc, tk, args, s);
+    case 256:
+      if (args.pair) return nf4 ? launch_t<256, true, true>(ta, tb, ta2, tb2, tc, tk, args, s)
+                                : launch_t<256, false, true>(ta, tb, ta2, tb2, tc, tk, args, s);
+      return nf4 ? launch_t<256, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<256, false>(ta, tb, ta2, tb2, tc, tk, args, s);
     case 128: return nf4 ? launch_t<128, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<128, false>(ta, tb, ta2, tb2, tc, tk, args, s);
     case 64: return nf4 ? launch_t<64, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<64, false>(ta, tb, ta2, tb2, tc, tk, args, s);
     case 16: return nf4 ? launch_t<16, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<16, false>(ta, tb, ta2, tb2, tc, tk, args, s);
@@ -740,6 +810,7 @@ static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, 
   a.bs2 = 1;
   a.fold = fold;
   a.out_split = out_split;
+  a.pair = bn == 256 && !B.mn;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
   const int64_t kit = (K + BK - 1) / BK;
   a.splits = effective_splits(ws ? pick_splits(tiles, kit, M * N * 4, ws_bytes) : 1, (int)kit);
@@ -855,6 +926,7 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   a.out_f32 = 0;
   a.out_t = 1;
   a.alpha = 1.0f;
+  a.pair = 1;
   if ((rc = gemm::fill_nf4(a, w, 1, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{x, K, 0};
   // augmented segment K2 = 2r: [l2 ; l2]^T [Ts_hi | Ts_lo]^T, i.e. the pair at ~16-bit precision
@@ -896,6 +968,7 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   a.out_f32 = 0;
   a.out_t = 1;
   a.alpha = 1.0f;
+  a.pair = 1;
   if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{dy, N, 0};
   // augmented segment K2 = 2r: [l1 | l1] [dT_hi | dT_lo]^T

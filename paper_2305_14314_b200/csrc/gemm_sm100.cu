@@ -16,6 +16,8 @@
 //               128B-swizzled UMMA tile in shared memory
 // The W tile is always the A operand (M = 128 W rows/cols), so each
 // dequantized weight feeds BN = 256 token columns of MMA.
+#include <cstdlib>
+
 #include "qlrt_common.cuh"
 #include "sm100_ptx.cuh"
 
@@ -256,16 +258,16 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     if (p.k_iters_aug) { ptx::prefetch_tmap(&tmA2); ptx::prefetch_tmap(&tmB2); }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&afull[s], NF4 ? (PAIR ? 256 : 128) : 1);
+      ptx::mbar_init(&afull[s], NF4 ? (PAIR ? 8 : 4) : 1);  // one elected lane per dequant warp
       ptx::mbar_init(&empty[s], 1);
     }
     for (int c = 0; c < L::CST; ++c) {
       ptx::mbar_init(&cfull[c], 1);      // TMA expect_tx arrival (codes + constants bytes)
-      ptx::mbar_init(&cempty[c], 128);   // every thread of the consuming dequant group
+      ptx::mbar_init(&cempty[c], 4);     // one elected lane per warp of the consuming dequant group
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], (PAIR ? 2 : 1) * kNumEpiWarps * 32);
+      ptx::mbar_init(&tempty[a], (PAIR ? 2 : 1) * kNumEpiWarps);  // one lane per epilogue warp
     }
     ptx::fence_mbar_init();
   }
@@ -436,7 +438,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
         }
       }
       ptx::tc_fence_before();
-      arrive_leader(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) arrive_leader(&tempty[acc]);
     }
   } else if (NF4 && warp == kCstWarp) {
     // ======================= codes + block-constant producer =======================
@@ -502,7 +505,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
         const uint32_t ph = (my / STAGES) & 1;
         if (i >= nk) {  // augmented (TMA-fed) stage: keep afull's phase in step
           ptx::mbar_wait(&empty[s], ph ^ 1);
-          arrive_leader(&afull[s]);
+          __syncwarp();
+          if (lane == 0) arrive_leader(&afull[s]);
           continue;
         }
         const uint32_t ci = cit + i;
@@ -526,11 +530,14 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           ptx::st_shared_v4(base + ((ch ^ swz) << 4), o0, o1, o2, o3);
         }
         ptx::fence_proxy_async_smem();
-        arrive_leader(&afull[s]);
-        // release the codes slot only now: every loaded word has been consumed
-        // (an arrive right after the loads can overtake them, and the next TMA
-        // would overwrite the slot under an in-flight ld.shared)
-        ptx::mbar_arrive(&cempty[c]);
+        __syncwarp();  // orders the warp's smem writes before the elected release
+        if (lane == 0) {
+          arrive_leader(&afull[s]);
+          // release the codes slot only now: every loaded word has been consumed
+          // (an arrive right after the loads can overtake them, and the next TMA
+          // would overwrite the slot under an in-flight ld.shared)
+          ptx::mbar_arrive(&cempty[c]);
+        }
       }
       it += total;
       cit += nk;
@@ -666,6 +673,16 @@ struct Operand {
   int64_t ld = 0;
   int mn = 0;
 };
+
+// 2-CTA pairing policy: QLRT_PAIR=0 off, 1 on, unset -> the per-GEMM default
+static int pair_policy(int dflt) {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("QLRT_PAIR");
+    v = e ? atoi(e) : -1;
+  }
+  return v < 0 ? dflt : v;
+}
 
 static int num_sms() {
   static int n = 0;
@@ -810,7 +827,7 @@ static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, 
   a.bs2 = 1;
   a.fold = fold;
   a.out_split = out_split;
-  a.pair = bn == 256 && !B.mn;
+  a.pair = (bn == 256 && !B.mn) ? pair_policy(1) : 0;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
   const int64_t kit = (K + BK - 1) / BK;
   a.splits = effective_splits(ws ? pick_splits(tiles, kit, M * N * 4, ws_bytes) : 1, (int)kit);
@@ -926,7 +943,7 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   a.out_f32 = 0;
   a.out_t = 1;
   a.alpha = 1.0f;
-  a.pair = 1;
+  a.pair = gemm::pair_policy(0);
   if ((rc = gemm::fill_nf4(a, w, 1, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{x, K, 0};
   // augmented segment K2 = 2r: [l2 ; l2]^T [Ts_hi | Ts_lo]^T, i.e. the pair at ~16-bit precision
@@ -968,7 +985,7 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   a.out_f32 = 0;
   a.out_t = 1;
   a.alpha = 1.0f;
-  a.pair = 1;
+  a.pair = gemm::pair_policy(0);
   if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{dy, N, 0};
   // augmented segment K2 = 2r: [l1 | l1] [dT_hi | dT_lo]^T

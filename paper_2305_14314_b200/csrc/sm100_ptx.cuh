@@ -53,8 +53,12 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
+// remote arrive (the 2-SM producer -> leader signal).  Default semantics, as
+// CUTLASS's umma_arrive_2x1SM_sm0: ".release.cluster" would emit a GPU-scope
+// MEMBAR + ERRBAR drain per arrive; the smem data the leader's tensor core
+// reads is ordered by the writer's fence.proxy.async before this arrive.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(

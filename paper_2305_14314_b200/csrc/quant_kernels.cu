@@ -456,6 +456,19 @@ __global__ void dq_decompress_kernel(const uint8_t* __restrict__ codes,
 // ---------------------------------------------------------------------------
 constexpr int DQ_TPB = 128;  // threads per CTA of the dequant kernel
 
+// 4 codes (nibbles of the low 16 bits of w) -> 4 bf16 from a 16-entry table
+// held as lo/hi byte planes: 3 byte-permutes per plane (codes 0-7 / 8-15 and
+// a select on bit 3), 2 to interleave -- no shared-memory table reads.
+__device__ __forceinline__ void lookup4_bf16(uint32_t w, const uint32_t (&L)[4], const uint32_t (&H)[4],
+                                             uint32_t& o0, uint32_t& o1) {
+  const uint32_t sel = w & 0x7777u;
+  const uint32_t bsel = ((w >> 1) & 0x4444u) | 0x3210u;
+  const uint32_t lo = __byte_perm(__byte_perm(L[0], L[1], sel), __byte_perm(L[2], L[3], sel), bsel);
+  const uint32_t hi = __byte_perm(__byte_perm(H[0], H[1], sel), __byte_perm(H[2], H[3], sel), bsel);
+  o0 = __byte_perm(lo, hi, 0x5140);
+  o1 = __byte_perm(lo, hi, 0x7362);
+}
+
 template <int OUT>
 __global__ void __launch_bounds__(DQ_TPB) dequant64_kernel(const uint4* __restrict__ codes, int64_t n, qlrt_codebook4 cb,
                                                         const float* __restrict__ absmax,
@@ -486,11 +499,25 @@ __global__ void __launch_bounds__(DQ_TPB) dequant64_kernel(const uint4* __restri
       c = dq_codes ? dq_constant(__ldg(dq_codes + blk), __ldg(c1 + blk / bs2), mu_v, sp) : __ldg(absmax + blk);
     }
     const double cd = (double)c;
+    uint32_t Lp[4], Hp[4];  // bf16 path: exact table bf16(f32(v64*c64)) as lo/hi byte planes
+    if constexpr (OUT == QLRT_BF16) {
+      uint32_t P[8];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const double d = __dmul_rn(cb.values[i], cd);
-      if constexpr (OUT == QLRT_F64) col[i * DQ_TPB] = d;
-      else col[i * DQ_TPB] = __double2float_rn(d);
+      for (int j = 0; j < 8; ++j)
+        P[j] = pack_bf16x2(__double2float_rn(__dmul_rn(cb.values[2 * j], cd)),
+                           __double2float_rn(__dmul_rn(cb.values[2 * j + 1], cd)));
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        Lp[q] = __byte_perm(P[2 * q], P[2 * q + 1], 0x6420);
+        Hp[q] = __byte_perm(P[2 * q], P[2 * q + 1], 0x7531);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const double d = __dmul_rn(cb.values[i], cd);
+        if constexpr (OUT == QLRT_F64) col[i * DQ_TPB] = d;
+        else col[i * DQ_TPB] = __double2float_rn(d);
+      }
     }
     const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
@@ -501,10 +528,9 @@ __global__ void __launch_bounds__(DQ_TPB) dequant64_kernel(const uint4* __restri
         constexpr int EPC = 16 / sizeof(OT);  // elements per 16B chunk
         uint32_t pk[4];
         if constexpr (OUT == QLRT_BF16) {
-          const uint32_t w = ws[pass * 8 + ch];  // 8 codes
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            pk[j] = pack_bf16x2(col[((w >> (8 * j)) & 15u) * DQ_TPB], col[((w >> (8 * j + 4)) & 15u) * DQ_TPB]);
+          const uint32_t w = ws[pass * 8 + ch];  // 8 codes -> 8 bf16 by register byte-permutes
+          lookup4_bf16(w, Lp, Hp, pk[0], pk[1]);
+          lookup4_bf16(w >> 16, Lp, Hp, pk[2], pk[3]);
         } else {
           const int e = pass * EPP + ch * EPC;  // first element of the chunk
           const uint32_t w = ws[e >> 3] >> (4 * (e & 7));

@@ -105,7 +105,18 @@ typedef struct {
   int blocksize2;
   qlrt_fp8spec spec;
   double values[16];       /* codebook decode table                      */
+  float* consts;           /* optional fp32 block-constant cache [k_in][round4(n_out/64)]:
+                              NULL -> rebuilt in the workspace every call;
+                              non-NULL -> (re)built by qlrt_nf4_constants,
+                              read by fwd/bwd/gemv (the reference caches the
+                              dequantized W from forward to backward,
+                              qlora.py:146-147,179) */
 } qlrt_nf4_weight;
+
+/* Bytes of the constant cache of a weight and the call that fills it
+ * (doublequant.py:190-195 arithmetic, laid out for the fused GEMM). */
+size_t qlrt_nf4_constants_bytes(int64_t k_in, int64_t n_out);
+qlrt_status qlrt_nf4_constants(const qlrt_nf4_weight* w, float* out, void* stream);
 
 /* Workspace bytes for the linear entry points (split-K partial sums). */
 size_t qlrt_linear_workspace_bytes(int64_t m, int64_t k_in, int64_t n_out, int rank);

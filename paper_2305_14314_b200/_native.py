@@ -34,7 +34,7 @@ class Fp8SpecC(ctypes.Structure):
 class NF4Weight(ctypes.Structure):
     _fields_ = [("codes", c_void_p), ("dq_codes", c_void_p), ("c1", c_void_p), ("mu", c_void_p),
                 ("k_in", c_int64), ("n_out", c_int64), ("blocksize2", c_int),
-                ("spec", Fp8SpecC), ("values", c_double * 16)]
+                ("spec", Fp8SpecC), ("values", c_double * 16), ("consts", c_void_p)]
 
 
 _SIGS = {
@@ -49,6 +49,8 @@ _SIGS = {
     "qlrt_pack4": [c_void_p, c_int64, c_void_p, c_void_p],
     "qlrt_unpack4": [c_void_p, c_int64, c_void_p, c_void_p],
     "qlrt_linear_workspace_bytes": [c_int64, c_int64, c_int64, c_int],
+    "qlrt_nf4_constants_bytes": [c_int64, c_int64],
+    "qlrt_nf4_constants": [POINTER(NF4Weight), c_void_p, c_void_p],
     "qlrt_nf4_linear_fwd": [POINTER(NF4Weight), c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int, c_float,
                             c_void_p, c_void_p, c_void_p, c_void_p],
     "qlrt_nf4_linear_bwd": [POINTER(NF4Weight), c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
@@ -63,6 +65,7 @@ _SIGS = {
     "qlrt_build_info": [],
 }
 _RESTYPE = {"qlrt_dq_workspace_bytes": c_size_t, "qlrt_linear_workspace_bytes": c_size_t,
+            "qlrt_nf4_constants_bytes": c_size_t,
             "qlrt_build_info": ctypes.c_char_p}
 
 EXPORTS = tuple(_SIGS)

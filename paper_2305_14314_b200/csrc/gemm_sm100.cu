@@ -856,8 +856,12 @@ static qlrt_status fill_nf4(Args& a, const qlrt_nf4_weight* w, int mode, float* 
   a.bs2 = w->blocksize2;
   a.spec = w->spec;
   for (int i = 0; i < 16; ++i) a.values[i] = w->values[i];
-  a.consts = consts;
   a.kpitch = kpitch_of(w);
+  if (w->consts) {  // caller-provided cache, already filled by qlrt_nf4_constants
+    a.consts = w->consts;
+    return QLRT_OK;
+  }
+  a.consts = consts;
   const int64_t total = w->k_in * a.kpitch;
   int64_t g = (total + 255) / 256;
   if (g > 148 * 8) g = 148 * 8;
@@ -891,6 +895,16 @@ using namespace qlrt;
 using gemm::Operand;
 
 extern "C" {
+
+size_t qlrt_nf4_constants_bytes(int64_t k_in, int64_t n_out) { return gemm::consts_bytes(k_in, n_out); }
+
+qlrt_status qlrt_nf4_constants(const qlrt_nf4_weight* w, float* out, void* stream) {
+  if (!w || !w->dq_codes || !w->c1 || !w->mu || !out || w->n_out % 64) return QLRT_ERR_ARG;
+  qlrt_nf4_weight tmp = *w;
+  tmp.consts = nullptr;
+  gemm::Args a{};
+  return gemm::fill_nf4(a, &tmp, 1, out, (cudaStream_t)stream);
+}
 
 size_t qlrt_linear_workspace_bytes(int64_t m, int64_t k_in, int64_t n_out, int rank) {
   // split-K partials of the skinny adapter GEMMs (<= 16 splits each) + GEMV scratch

@@ -544,6 +544,17 @@ __global__ void __launch_bounds__(DQ_TPB) dequant64_kernel(const uint4* __restri
       }
       __syncwarp();
       // coalesced copy-out: 4 rows (blocks) x 128B per instruction
+      if (wb + 32 <= nb && (wb + 32) * 64 <= n) {  // whole warp in range: no per-store checks
+        uint8_t* ob = reinterpret_cast<uint8_t*>(static_cast<OT*>(out) + wb * 64 + pass * EPP);
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int row = it * 4 + (lane >> 3), ch = lane & 7;
+          const uint4 u = *reinterpret_cast<const uint4*>(st + row * 128 + ((ch ^ (row & 7)) << 4));
+          *reinterpret_cast<uint4*>(ob + row * (64 * (int)sizeof(OT)) + ch * 16) = u;
+        }
+        __syncwarp();
+        continue;
+      }
 #pragma unroll
       for (int it = 0; it < 8; ++it) {
         const int row = it * 4 + (lane >> 3), ch = lane & 7;

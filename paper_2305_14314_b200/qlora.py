@@ -118,7 +118,9 @@ class QLinear:
         return (isinstance(b, BlockQuantized) and b.dq is not None and b.blocksize == 64
                 and b.codebook.bits == 4 and self.out_dim % 64 == 0 and self.in_dim % 8 == 0)
 
-    def weight_desc(self) -> _native.NF4Weight:
+    def weight_desc(self, consts: torch.Tensor | None = None) -> _native.NF4Weight:
+        """C descriptor of the base; ``consts`` = the per-forward fp32
+        block-constant cache shared with the matching backward."""
         if self._wdesc is None:
             b = self.base
             w = _native.NF4Weight()
@@ -128,7 +130,17 @@ class QLinear:
             for i in range(16):
                 w.values[i] = float(b.codebook.values[i])
             self._wdesc = w
+        self._wdesc.consts = ptr(consts)
         return self._wdesc
+
+    def _constants(self) -> torch.Tensor:
+        """Double-dequantize the block constants once per forward (kept in the
+        cache for backward, like the reference keeps cache['w'])."""
+        L = lib()
+        out = torch.empty(int(L.qlrt_nf4_constants_bytes(self.in_dim, self.out_dim)) // 4, dtype=torch.float32,
+                          device="cuda")
+        check(L.qlrt_nf4_constants(self.weight_desc(None), ptr(out), stream_ptr()), "QLinear constants")
+        return out
 
     def dequant_weight(self) -> torch.Tensor:
         """Base weight at compute precision (qlora.py:117-122); only the
@@ -166,16 +178,17 @@ class QLinear:
         y = torch.empty(m, self.out_dim, dtype=self.dtype, device=x2.device)
         rp = _pad8(ad.rank) if ad else 0
         ts = torch.empty(m, 2 * rp, dtype=self.dtype, device=x2.device) if ad else None  # bf16 hi | lo
+        consts = self._constants() if self.fused() else None
         if self.fused() and m > 1:
             l1b, l2b = ad.bf16_operands() if ad else (None, None)
-            check(lib().qlrt_nf4_linear_fwd(self.weight_desc(), ptr(x2), ptr(xa) if mask is not None else None, m,
+            check(lib().qlrt_nf4_linear_fwd(self.weight_desc(consts), ptr(x2), ptr(xa) if mask is not None else None, m,
                                             ptr(l1b), ptr(l2b), rp, float(ad.scaling) if ad else 0.0, ptr(ts),
                                             ptr(y), ptr(self._workspace(m)), stream_ptr()), "QLinear.forward")
         elif self.fused() and m == 1:
             l1b, l2b = ad.bf16_operands() if ad else (None, None)
             if ad is not None:
                 _split_into(gemm_bf16(xa, l1b, alpha=ad.scaling, out_dtype=torch.float32), ts)
-            check(lib().qlrt_nf4_gemv(self.weight_desc(), ptr(x2), ptr(l1b), ptr(l2b), rp,
+            check(lib().qlrt_nf4_gemv(self.weight_desc(consts), ptr(x2), ptr(l1b), ptr(l2b), rp,
                                       float(ad.scaling) if ad else 0.0, ptr(y), ptr(self._workspace(m)),
                                       stream_ptr()), "QLinear.forward(gemv)")
         else:
@@ -186,7 +199,7 @@ class QLinear:
                 _split_into(gemm_bf16(xa, l1b, alpha=ad.scaling, out_dtype=torch.float32), ts)
                 y.copy_((y.float() + gemm_bf16(ts[:, :rp], l2b, out_dtype=torch.float32)
                          + gemm_bf16(ts[:, rp:], l2b, out_dtype=torch.float32)).to(self.dtype))
-        cache = {"x": x2, "xa": xa, "ts": ts, "mask": mask, "lead": lead}
+        cache = {"x": x2, "xa": xa, "ts": ts, "mask": mask, "lead": lead, "consts": consts}
         return y.reshape(*lead, self.out_dim), cache
 
     def backward(self, d_y, cache: dict[str, Any]) -> tuple[torch.Tensor, dict[str, torch.Tensor]]:
@@ -204,17 +217,17 @@ class QLinear:
             dl2 = torch.empty(rp, self.out_dim, dtype=torch.float32, device=d_y.device)
         if self.fused() and mask is None:
             if ad is None:
-                check(lib().qlrt_nf4_linear_bwd(self.weight_desc(), ptr(d_y), m, None, None, None, None, 0, 0.0,
+                check(lib().qlrt_nf4_linear_bwd(self.weight_desc(cache.get("consts")), ptr(d_y), m, None, None, None, None, 0, 0.0,
                                                 None, ptr(d_x), None, None, ptr(self._workspace(m)), stream_ptr()),
                       "QLinear.backward")
             else:
-                check(lib().qlrt_nf4_linear_bwd(self.weight_desc(), ptr(d_y), m, ptr(cache["xa"]), ptr(cache["ts"]),
+                check(lib().qlrt_nf4_linear_bwd(self.weight_desc(cache.get("consts")), ptr(d_y), m, ptr(cache["xa"]), ptr(cache["ts"]),
                                                 ptr(l1b), ptr(l2b), rp, float(ad.scaling), ptr(dt), ptr(d_x),
                                                 ptr(dl1), ptr(dl2), ptr(self._workspace(m)), stream_ptr()),
                       "QLinear.backward")
         else:
             if self.fused():
-                check(lib().qlrt_nf4_linear_bwd(self.weight_desc(), ptr(d_y), m, None, None, None, None, 0, 0.0,
+                check(lib().qlrt_nf4_linear_bwd(self.weight_desc(cache.get("consts")), ptr(d_y), m, None, None, None, None, 0, 0.0,
                                                 None, ptr(d_x), None, None, ptr(self._workspace(m)), stream_ptr()),
                       "QLinear.backward")
             else:

@@ -146,10 +146,17 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
                                 float* dl1, float* dl2, void* workspace, void* stream);
 
 /* batch-1 GEMV variant of forward (M = 1), HBM-bound on the packed codes:
- *   y[N] = x[K] W + s (x l1) l2          fp32 accumulate, bf16 out. */
+ *   y[N] = x[K] W + s (x l1) l2          fp32 accumulate, bf16 out.
+ * W decodes as bf16(f32(v) * c) (as the fused GEMM); split-K partials are
+ * summed in a fixed order (deterministic).  Needs N % 64 == 0, a
+ * power-of-two blocksize2, 32-byte aligned codes; rank <= 512. */
 qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* l1,
                           const void* l2, int rank, float s, void* y, void* workspace,
                           void* stream);
+
+/* Workspace bytes of qlrt_nf4_gemv (split-K partials, LoRA partials, strip
+ * tickets); qlrt_linear_workspace_bytes(m = 1, ...) already covers it. */
+size_t qlrt_gemv_workspace_bytes(int64_t k_in, int64_t n_out, int rank);
 
 /* Plain bf16 GEMM on the same tcgen05 engine (test + building block):
  * D[M,N] = alpha * A[M,K] B[K,N]; a_mn/b_mn select MN-major storage

@@ -56,6 +56,7 @@ _SIGS = {
     "qlrt_nf4_linear_bwd": [POINTER(NF4Weight), c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
                             c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "qlrt_nf4_gemv": [POINTER(NF4Weight), c_void_p, c_void_p, c_void_p, c_int, c_float, c_void_p, c_void_p, c_void_p],
+    "qlrt_gemv_workspace_bytes": [c_int64, c_int64, c_int],
     "qlrt_gemm_bf16": [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_int, c_float, c_int, c_int,
                        c_void_p, c_size_t, c_void_p],
     "qlrt_adam_step": [c_void_p, c_void_p, c_void_p, c_void_p, c_int64] + [c_float] * 8 + [c_void_p, c_void_p],
@@ -65,6 +66,7 @@ _SIGS = {
     "qlrt_build_info": [],
 }
 _RESTYPE = {"qlrt_dq_workspace_bytes": c_size_t, "qlrt_linear_workspace_bytes": c_size_t,
+            "qlrt_gemv_workspace_bytes": c_size_t,
             "qlrt_nf4_constants_bytes": c_size_t,
             "qlrt_build_info": ctypes.c_char_p}
 

@@ -602,22 +602,6 @@ __global__ void dq_constants_kernel(const uint8_t* __restrict__ dq_codes, const 
   }
 }
 
-// GEMV finish: y[n] = bf16( sum_z ws[z][n] + s * sum_j t[j] l2[j][n] )
-__global__ void gemv_finish_kernel(const float* __restrict__ ws, int splits, int N,
-                                   const float* __restrict__ t, const __nv_bfloat16* __restrict__ l2, int rank,
-                                   float s, __nv_bfloat16* __restrict__ y) {
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-    float acc = 0.0f;
-    for (int z = 0; z < splits; ++z) acc += ws[(int64_t)z * N + n];
-    if (rank > 0) {
-      float lr = 0.0f;
-      for (int j = 0; j < rank; ++j) lr = fmaf(t[j], __bfloat162float(l2[(int64_t)j * N + n]), lr);
-      acc += s * lr;
-    }
-    y[n] = __float2bfloat16_rn(acc);
-  }
-}
-
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -912,10 +896,10 @@ size_t qlrt_linear_workspace_bytes(int64_t m, int64_t k_in, int64_t n_out, int r
   int64_t a = 16 * m * 2 * r, b = 16 * k_in * 2 * r, c = 16 * 2 * r * n_out;
   int64_t mx = a > b ? a : b;
   mx = mx > c ? mx : c;
-  int64_t gemv = 32 * (n_out > k_in ? n_out : k_in) + 64 * ((r + 63) / 64) + 16 * r + 256;
-  mx = mx > gemv ? mx : gemv;
-  return gemm::align256((size_t)mx * 4) + 4096 + gemm::align256(gemm::consts_bytes(k_in, n_out)) +
-         gemm::dbl_bytes(k_in, n_out, rank > 0 ? rank : 0);
+  size_t total = gemm::align256((size_t)mx * 4) + 4096 + gemm::align256(gemm::consts_bytes(k_in, n_out)) +
+                 gemm::dbl_bytes(k_in, n_out, rank > 0 ? rank : 0);
+  const size_t gv = qlrt_gemv_workspace_bytes(k_in, n_out, rank > 0 ? rank : 0);  // M = 1 path
+  return total > gv ? total : gv;
 }
 
 qlrt_status qlrt_gemm_bf16(const void* a, const void* b, void* d, int64_t m, int64_t n, int64_t k, int a_mn, int b_mn,
@@ -1028,65 +1012,6 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
                      part_bytes, st, rank);
   }
   return rc;
-}
-
-qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* l1, const void* l2, int rank, float s,
-                          void* y, void* workspace, void* stream) {
-  if (!gemm::weight_ok(w) || !x || !y || rank < 0 || !workspace) return QLRT_ERR_ARG;
-  if (rank > 0 && (!l1 || !l2 || (rank % 8))) return QLRT_ERR_ARG;
-  cudaStream_t st = (cudaStream_t)stream;
-  const int64_t K = w->k_in, N = w->n_out;
-  float* ws = (float*)workspace;
-  // y^T[N, 1] = W^T x^T with split-K over K_in (BN = 16: one live column)
-  const int m_tiles = (int)((N + 127) / 128);
-  const int kit = (int)((K + 63) / 64);
-  int best = 1;
-  double best_eff = 0.0;
-  for (int sp = 1; sp <= 32 && sp <= kit / 2; ++sp) {  // fill whole waves of 148 SMs
-    int tiles = m_tiles * sp;
-    double eff = (double)tiles / (double)(((tiles + 147) / 148) * 148);
-    if (tiles >= 148 && eff > best_eff + 1e-9) { best = sp; best_eff = eff; }
-    if (tiles < 148) { best = sp; best_eff = eff; }
-  }
-  gemm::Args a{};
-  a.M = (int)N;
-  a.N = 1;
-  a.splits = gemm::effective_splits(best, kit);
-  a.ws = ws;
-  a.out_f32 = 1;
-  a.alpha = 1.0f;
-  // workspace: [partials 32*max(N,K)][t, t-partials][constants]
-  float* t = ws + (size_t)32 * (N > K ? N : K);
-  float* consts = (float*)((uint8_t*)workspace +
-                           gemm::align256(((size_t)32 * (N > K ? N : K) + 64 * ((rank + 63) / 64) + 16 * rank + 256) * 4));
-  qlrt_status rc = gemm::fill_nf4(a, w, 1, consts, st);
-  if (rc != QLRT_OK) return rc;
-  Operand none{}, B{x, K, 0};
-  rc = gemm::run(16, none, B, nullptr, nullptr, K, 0, a, st);
-  if (rc != QLRT_OK) return rc;
-  float* tws = t + 64 * ((rank + 63) / 64);
-  if (rank > 0) {
-    // t^T[r, 1] = l1^T x^T: A = l1 (MN-major [K][r]), B = x (K-major [1][K]), fp32, scaled later
-    Operand A{l1, rank, 1}, B2{x, K, 0};
-    gemm::Args b{};
-    b.M = rank;
-    b.N = 1;
-    b.out = t;
-    b.ldo = 1;
-    b.out_f32 = 1;
-    b.alpha = 1.0f;
-    b.ws = tws;
-    b.bs2 = 1;
-    b.splits = gemm::effective_splits(kit >= 64 ? 16 : 1, kit);
-    rc = gemm::run(16, A, B2, nullptr, nullptr, K, 0, b, st);
-    if (rc != QLRT_OK) return rc;
-    if (b.splits > 1 && (rc = gemm::reduce(b, st)) != QLRT_OK) return rc;
-  }
-  gemm::gemv_finish_kernel<<<(int)((N + 255) / 256), 256, 0, st>>>(ws, a.splits, (int)N, t,
-                                                                 (const __nv_bfloat16*)l2, rank, s,
-                                                                 (__nv_bfloat16*)y);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
 }
 
 }  // extern "C"

@@ -576,6 +576,135 @@ __global__ void __launch_bounds__(DQ_TPB) dequant64_kernel(const uint4* __restri
   }
 }
 
+// ---------------------------------------------------------------------------
+// bf16 output, blocksize 64, no shared-memory staging: one lane per 64-block.
+// A lane loads its block's 32 code bytes with one 256-bit load (a warp reads
+// 1 KB contiguous), builds the block's 16-entry table bf16(f32(f64(v_i) *
+// f64(c))) exactly (16 DMUL with the codebook as constant-bank operands), split
+// into lo/hi byte planes, decodes 8 codes per 21 integer ops (lookup8_bf16) and
+// writes its 128 output bytes with four 256-bit stores.  The DQ constant comes
+// from a 256-entry fp64 decode table of the 8-bit float in shared memory.
+// Each warp owns a balanced contiguous range of 32-block steps and prefetches
+// step i+1's codes and constants before decoding step i.
+// ---------------------------------------------------------------------------
+constexpr int DQB_TPB = 256;
+
+__device__ __forceinline__ void st_global_v8(void* p, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                             uint32_t a4, uint32_t a5, uint32_t a6, uint32_t a7) {
+  asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a0), "r"(a1),
+               "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
+               : "memory");
+}
+
+__device__ __forceinline__ void ld_stream_v8(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+
+// 8 codes (nibbles of w, element order) -> 8 bf16 in o[0..3]
+__device__ __forceinline__ void lookup8_bf16(uint32_t w, const uint32_t (&L)[4], const uint32_t (&H)[4],
+                                             uint32_t& o0, uint32_t& o1, uint32_t& o2, uint32_t& o3) {
+  const uint32_t sel = w & 0x77777777u;
+  const uint32_t bs = ((w >> 1) & 0x44444444u) | 0x32103210u;
+  const uint32_t selh = sel >> 16, bsh = bs >> 16;
+  const uint32_t la = __byte_perm(__byte_perm(L[0], L[1], sel), __byte_perm(L[2], L[3], sel), bs);
+  const uint32_t ha = __byte_perm(__byte_perm(H[0], H[1], sel), __byte_perm(H[2], H[3], sel), bs);
+  const uint32_t lb = __byte_perm(__byte_perm(L[0], L[1], selh), __byte_perm(L[2], L[3], selh), bsh);
+  const uint32_t hb = __byte_perm(__byte_perm(H[0], H[1], selh), __byte_perm(H[2], H[3], selh), bsh);
+  o0 = __byte_perm(la, ha, 0x5140);
+  o1 = __byte_perm(la, ha, 0x7362);
+  o2 = __byte_perm(lb, hb, 0x5140);
+  o3 = __byte_perm(lb, hb, 0x7362);
+}
+
+template <bool DQ>
+__global__ void __launch_bounds__(DQB_TPB, 3) dequant64_bf16_kernel(const uint8_t* __restrict__ codes, int64_t n,
+                                                                    qlrt_codebook4 cb,
+                                                                    const float* __restrict__ absmax,
+                                                                    const uint8_t* __restrict__ dq_codes,
+                                                                    const float* __restrict__ c1,
+                                                                    const float* __restrict__ mu, int bs2_shift,
+                                                                    qlrt_fp8spec sp, __nv_bfloat16* __restrict__ out) {
+  __shared__ double fp8_lut[256];
+  const int lane = threadIdx.x & 31;
+  const int64_t nb = cdiv(n, 64), n_steps = cdiv(nb, 32);
+  const int64_t n_warps = (int64_t)gridDim.x * (DQB_TPB / 32);
+  const int64_t w = (int64_t)blockIdx.x * (DQB_TPB / 32) + (threadIdx.x >> 5);
+  const int64_t s_beg = n_steps * w / n_warps, s_end = n_steps * (w + 1) / n_warps;
+
+  uint32_t cw[8];
+  float craw = 0.0f;   // absmax, or c1 of the block (DQ)
+  uint32_t dqb = 0;    // DQ code byte
+  auto fetch = [&](int64_t s) {
+    const int64_t blk = s * 32 + lane;
+    if (blk < nb) {
+      ld_stream_v8(codes + blk * 32, cw);
+      if (DQ) {
+        dqb = __ldg(dq_codes + blk);
+        craw = __ldg(c1 + (blk >> bs2_shift));
+      } else {
+        craw = __ldg(absmax + blk);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cw[i] = 0u;
+    }
+  };
+  if (s_beg < s_end) fetch(s_beg);  // first loads in flight before the table build
+  if (DQ) {
+    fp8_lut[threadIdx.x] = fp8_decode_fast(threadIdx.x, sp);
+    __syncthreads();
+  }
+  const double mu_d = DQ ? (double)__ldg(mu) : 0.0;
+  for (int64_t s = s_beg; s < s_end; ++s) {
+    uint32_t cur[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cur[i] = cw[i];
+    float c;
+    if (DQ) {
+      const double r = __dadd_rn(__dmul_rn(fp8_lut[dqb], (double)craw), mu_d);
+      c = __double2float_rn(r > 0.0 ? r : 0.0);
+    } else {
+      c = craw;
+    }
+    if (s + 1 < s_end) fetch(s + 1);
+    const double cd = (double)c;
+    uint32_t L[4], H[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t p0 = pack_bf16x2(__double2float_rn(__dmul_rn(cb.values[4 * q], cd)),
+                                      __double2float_rn(__dmul_rn(cb.values[4 * q + 1], cd)));
+      const uint32_t p1 = pack_bf16x2(__double2float_rn(__dmul_rn(cb.values[4 * q + 2], cd)),
+                                      __double2float_rn(__dmul_rn(cb.values[4 * q + 3], cd)));
+      L[q] = __byte_perm(p0, p1, 0x6420);
+      H[q] = __byte_perm(p0, p1, 0x7531);
+    }
+    const int64_t blk = s * 32 + lane;
+    __nv_bfloat16* dst = out + blk * 64;
+    if (blk * 64 + 64 <= n) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t o[8];
+        lookup8_bf16(cur[2 * j], L, H, o[0], o[1], o[2], o[3]);
+        lookup8_bf16(cur[2 * j + 1], L, H, o[4], o[5], o[6], o[7]);
+        st_global_v8(dst + 16 * j, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
+      }
+    } else if (blk < nb) {  // ragged last block: element-wise, registers only
+      unsigned short* d16 = reinterpret_cast<unsigned short*>(dst);
+      const int rem = (int)(n - blk * 64);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        uint32_t o[4];
+        lookup8_bf16(cur[j], L, H, o[0], o[1], o[2], o[3]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (8 * j + e < rem) d16[8 * j + e] = (unsigned short)((e & 1) ? (o[e >> 1] >> 16) : (o[e >> 1] & 0xFFFFu));
+      }
+    }
+  }
+}
+
 // generic blocksize: one thread per element
 template <int OUT>
 __global__ void dequant_generic_kernel(const uint8_t* __restrict__ codes, int64_t n, int bs,
@@ -722,7 +851,20 @@ qlrt_status qlrt_dequantize4(const uint8_t* codes, int64_t n, int blocksize,
   if (out_dtype != QLRT_F32 && out_dtype != QLRT_BF16 && out_dtype != QLRT_F64) return QLRT_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const bool aligned = (((uintptr_t)codes) & 15) == 0 && (((uintptr_t)out) & 15) == 0;
-  if (blocksize == 64 && aligned) {
+  const bool pow2_bs2 = blocksize2 > 0 && (blocksize2 & (blocksize2 - 1)) == 0;
+  if (blocksize == 64 && out_dtype == QLRT_BF16 && (((uintptr_t)codes) & 31) == 0 &&
+      (((uintptr_t)out) & 31) == 0 && (!dq_codes || (pow2_bs2 && (((uintptr_t)dq_codes) & 15) == 0))) {
+    // persistent: 3 CTAs x 8 warps per SM, balanced 32-block steps per warp
+    const int64_t ctas = cdiv(cdiv(cdiv(n, 64), 32), DQB_TPB / 32);
+    const int g = (int)(ctas < (int64_t)kNumSMs * 3 ? ctas : (int64_t)kNumSMs * 3);
+    const int sh = pow2_bs2 ? __builtin_ctz((unsigned)blocksize2) : 0;
+    if (dq_codes)
+      dequant64_bf16_kernel<true><<<g, DQB_TPB, 0, s>>>(codes, n, *cb, absmax, dq_codes, c1, mu, sh, spec,
+                                                        (__nv_bfloat16*)out);
+    else
+      dequant64_bf16_kernel<false><<<g, DQB_TPB, 0, s>>>(codes, n, *cb, absmax, dq_codes, c1, mu, sh, spec,
+                                                         (__nv_bfloat16*)out);
+  } else if (blocksize == 64 && aligned) {
     const int g = grid_for(cdiv(n, 64), DQ_TPB, 16);
 #define QLRT_DQ64(O) dequant64_kernel<O><<<g, DQ_TPB, 0, s>>>((const uint4*)codes, n, *cb, absmax, dq_codes, c1, mu, \
                                                            blocksize2, spec, out)

@@ -178,7 +178,9 @@ class QLinear:
         y = torch.empty(m, self.out_dim, dtype=self.dtype, device=x2.device)
         rp = _pad8(ad.rank) if ad else 0
         ts = torch.empty(m, 2 * rp, dtype=self.dtype, device=x2.device) if ad else None  # bf16 hi | lo
-        consts = self._constants() if self.fused() else None
+        # the GEMV decodes the DQ constants itself; at m > 1 the fp32 constants are
+        # built once here and shared with backward (None -> backward rebuilds them)
+        consts = self._constants() if self.fused() and m > 1 else None
         if self.fused() and m > 1:
             l1b, l2b = ad.bf16_operands() if ad else (None, None)
             check(lib().qlrt_nf4_linear_fwd(self.weight_desc(consts), ptr(x2), ptr(xa) if mask is not None else None, m,
@@ -188,7 +190,7 @@ class QLinear:
             l1b, l2b = ad.bf16_operands() if ad else (None, None)
             if ad is not None:
                 _split_into(gemm_bf16(xa, l1b, alpha=ad.scaling, out_dtype=torch.float32), ts)
-            check(lib().qlrt_nf4_gemv(self.weight_desc(consts), ptr(x2), ptr(l1b), ptr(l2b), rp,
+            check(lib().qlrt_nf4_gemv(self.weight_desc(None), ptr(x2), ptr(l1b), ptr(l2b), rp,
                                       float(ad.scaling) if ad else 0.0, ptr(y), ptr(self._workspace(m)),
                                       stream_ptr()), "QLinear.forward(gemv)")
         else:

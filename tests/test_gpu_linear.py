@@ -175,7 +175,7 @@ def test_fresh_adapter_is_exact_noop(qb, cuda):
     assert torch.equal(plain.forward(x)[0], adapted.forward(x)[0])
 
 
-@pytest.mark.parametrize("k,n", [(8192, 8192), (4096, 11008)])
+@pytest.mark.parametrize("k,n", [(8192, 8192), (4096, 11008), (1000, 22016), (64, 192), (8, 64)])
 def test_gemv_batch1(k, n, oracle, qb, cuda):
     """Batch-1 GEMV (same engine, W decoded to bf16 in-kernel) vs the fp64
     oracle over W = bf16(f32(dequantize(q))) -- the GEMM parity definition."""
@@ -191,6 +191,11 @@ def test_gemv_batch1(k, n, oracle, qb, cuda):
     y, _ = lin.forward(torch.from_numpy(x))
     ref = x.astype(np.float64) @ wd + 0.25 * (x.astype(np.float64) @ l1) @ l2
     assert_tol(y.float().cpu().numpy(), bf16_round(ref), "gemv")
+    # no adapter, and determinism (split-K partials summed in a fixed order)
+    plain = qb.QLinear(q, [])
+    y0 = plain.forward(torch.from_numpy(x))[0]
+    assert_tol(y0.float().cpu().numpy(), bf16_round(x.astype(np.float64) @ wd), "gemv r=0")
+    assert torch.equal(y0, plain.forward(torch.from_numpy(x))[0])
 
 
 def test_unfused_shape_path(oracle, qb, cuda):

@@ -187,3 +187,32 @@ def test_pack_unpack(qb, cuda):
         qb.pack_codes(np.array([16]), 4)
     with pytest.raises(ValueError, match="shorter"):
         qb.unpack_codes(np.array([0x21], dtype=np.uint8), 4, 3)
+
+
+@pytest.mark.parametrize("dq", [False, True])
+def test_dequant_bf16_ragged_and_misaligned(dq, oracle, qb, cuda):
+    """bf16 dequant (the two-lanes-per-block STG.256 kernel, and the staged
+    kernel it falls back to for a 16B- but not 32B-aligned output) equals
+    bf16(f32(dequantize)) of the oracle at ragged sizes."""
+    from paper_2305_14314_b200 import _native
+    cb = qb.get_codebook("nf4")
+    rng = np.random.default_rng(7)
+    for n in (1, 31, 63, 64, 65, 1000, 64 * 17 + 5, 64 * 1000 + 33, 64 * 4099):
+        x = (rng.standard_normal(n) * rng.uniform(0.01, 3)).astype(np.float32)
+        q = qb.quantize(torch.from_numpy(x).cuda(), cb, 64, double_quant=dq)
+        ref = oracle.dequantize(oracle.quantize(x, oracle.get_codebook("nf4"), 64, double_quant=dq))
+        want = torch.from_numpy(ref.astype(np.float32)).to(torch.bfloat16)
+        assert torch.equal(qb.dequantize(q, torch.bfloat16).cpu(), want), n
+        # misaligned destination (offset 8 elements = 16 B): staged kernel
+        buf = torch.empty(n + 8, dtype=torch.bfloat16, device="cuda")
+        dst = buf[8:]
+        d = q.dq
+        spec = (d.spec if dq else qb.Fp8Spec()).to_c()
+        rc = _native.lib().qlrt_dequantize4(
+            _native.ptr(q.codes), n, 64, q.codebook.to_c(),
+            None if dq else _native.ptr(q.constants),
+            _native.ptr(d.codes) if dq else None, _native.ptr(d.c1) if dq else None,
+            _native.ptr(d.mu) if dq else None, 256, spec, _native.ptr(dst), _native.BF16, _native.stream_ptr())
+        assert rc == 0
+        torch.cuda.synchronize()
+        assert torch.equal(dst.cpu(), want), ("misaligned", n)

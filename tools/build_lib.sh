@@ -8,11 +8,13 @@ mkdir -p "$OUT"
 NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$ROOT/include -I$SRC ${QLRT_NVCC_EXTRA:-}"
 objs=()
-for f in quant_kernels gemm_sm100 optim_kernels; do
+pids=()
+for f in quant_kernels gemm_sm100 gemv_nf4 optim_kernels; do
   "$NVCC" $FLAGS -c "$SRC/$f.cu" -o "$OUT/$f.o" &
+  pids+=($!)
   objs+=("$OUT/$f.o")
 done
-wait
+for p in "${pids[@]}"; do wait "$p"; done  # a failed compile fails the build
 "$NVCC" -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT/libqlrt_b200.so" "${objs[@]}" -lcudart
 rm -f "${objs[@]}"
 echo "built $OUT/libqlrt_b200.so"

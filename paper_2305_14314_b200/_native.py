@@ -15,7 +15,7 @@ from ctypes import POINTER, c_double, c_float, c_int, c_int64, c_size_t, c_uint8
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libqlrt_b200.so")
+LIB_PATH = os.environ.get("QLRT_LIB_PATH") or os.path.join(_HERE, "_lib", "libqlrt_b200.so")
 
 QLRT_OK, QLRT_ERR_ARG, QLRT_ERR_CUDA, QLRT_ERR_UNSUPPORTED = 0, 1, 2, 3
 F32, BF16, F64 = 0, 1, 2

@@ -63,6 +63,13 @@ struct Args {
   int out_split;        // bf16 out: also store lo = bf16(v - hi) at column offset out_split
   int fold;             // reduce: out[:, n] = D[:, n] + D[:, n + fold] for n < fold
   int pair;             // 2-CTA (cta_group::2) 256 x BN tiles
+  // stream-K: the (tile, k-iteration) space is cut into equal contiguous ranges,
+  // one per unit (CTA or pair); a tile split across units is finished by the
+  // unit holding its k = 0 segment (the "owner"), which adds the fp32
+  // partials of the later units in unit order (deterministic)
+  int streamk;
+  float* sk_ws;         // [gridDim.x][BM][BN] fp32 partials (one per CTA)
+  int* sk_flags;        // [gridDim.x], zeroed before the launch; 1 = partial ready
 };
 
 template <int BN, bool NF4, bool PAIR = false>
@@ -93,6 +100,39 @@ __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int
   mt = r / n_tiles;
   nt = r - mt * n_tiles;
 }
+
+// Walks the segments (tile, [i0, i1)) of one unit: round-robin whole tiles, or
+// (stream-K) the unit's contiguous share of tiles x T iterations.
+struct Sched {
+  long long g, g1, T;
+  int t, n_tiles_total, n_units, streamk;
+  __device__ Sched(int unit, int n_units_, int n_tiles_total_, int T_, int streamk_)
+      : T(T_), t(unit), n_tiles_total(n_tiles_total_), n_units(n_units_), streamk(streamk_) {
+    const long long G = (long long)n_tiles_total_ * T_;
+    g = G * unit / n_units_;
+    g1 = G * (unit + 1) / n_units_;
+  }
+  // full-tile mode: i1 = T (the caller clips split-K tiles to their own extent)
+  __device__ bool next(int& tile, int& i0, int& i1) {
+    if (!streamk) {
+      if (t >= n_tiles_total) return false;
+      tile = t;
+      i0 = 0;
+      i1 = (int)T;
+      t += n_units;
+      return true;
+    }
+    if (g >= g1) return false;
+    tile = (int)(g / T);
+    i0 = (int)(g - (long long)tile * T);
+    const long long e = (long long)tile * T + T < g1 ? (long long)tile * T + T : g1;
+    i1 = (int)(e - (long long)tile * T);
+    g = e;
+    return true;
+  }
+  // first unit whose range starts at or after global iteration x
+  __device__ static long long range_begin(long long G, int unit, int n_units_) { return G * unit / n_units_; }
+};
 
 // exact decode of the DQ 8-bit float by assembling the fp64 bit pattern
 __device__ __forceinline__ double fp8_decode_bits(unsigned b, const qlrt_fp8spec& sp, double sub_scale) {
@@ -125,15 +165,22 @@ __device__ __forceinline__ void build_planes(const float (&v)[16], float c, uint
   }
 }
 
-// 4 codes (nibbles of the low 16 bits of w) -> 4 bf16 packed in 2 words
-__device__ __forceinline__ void lookup4(uint32_t w, const uint32_t (&L)[4], const uint32_t (&H)[4],
-                                        uint32_t& o0, uint32_t& o1) {
-  const uint32_t sel = w & 0x7777u;
-  const uint32_t bsel = ((w >> 1) & 0x4444u) | 0x3210u;
-  const uint32_t lo = ptx::prmt(ptx::prmt(L[0], L[1], sel), ptx::prmt(L[2], L[3], sel), bsel);
-  const uint32_t hi = ptx::prmt(ptx::prmt(H[0], H[1], sel), ptx::prmt(H[2], H[3], sel), bsel);
-  o0 = ptx::prmt(lo, hi, 0x5140);
-  o1 = ptx::prmt(lo, hi, 0x7362);
+// 8 codes (the nibbles of w, element order) -> 8 bf16 packed in 4 words.
+// Selector bookkeeping runs on the FMA pipe (mul.hi for the right shifts) so
+// the ALU pipe -- the co-limiter of the fused GEMM -- sees 2 LOP3 + 16 PRMT.
+__device__ __forceinline__ void lookup8(uint32_t w, const uint32_t (&L)[4], const uint32_t (&H)[4], uint32_t k3210,
+                                        uint32_t& o0, uint32_t& o1, uint32_t& o2, uint32_t& o3) {
+  const uint32_t sel = w & 0x77777777u;
+  const uint32_t bs = (__umulhi(w, 0x80000000u) & 0x44444444u) | k3210;  // bit 3 of each code -> byte select
+  const uint32_t selh = __umulhi(sel, 0x10000u), bsh = __umulhi(bs, 0x10000u);
+  const uint32_t la = ptx::prmt(ptx::prmt(L[0], L[1], sel), ptx::prmt(L[2], L[3], sel), bs);
+  const uint32_t ha = ptx::prmt(ptx::prmt(H[0], H[1], sel), ptx::prmt(H[2], H[3], sel), bs);
+  const uint32_t lb = ptx::prmt(ptx::prmt(L[0], L[1], selh), ptx::prmt(L[2], L[3], selh), bsh);
+  const uint32_t hb = ptx::prmt(ptx::prmt(H[0], H[1], selh), ptx::prmt(H[2], H[3], selh), bsh);
+  o0 = ptx::prmt(la, ha, 0x5140);
+  o1 = ptx::prmt(la, ha, 0x7362);
+  o2 = ptx::prmt(lb, hb, 0x5140);
+  o3 = ptx::prmt(lb, hb, 0x7362);
 }
 
 // one accumulator row segment of EC fp32 values -> global
@@ -250,6 +297,14 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
   const int n_tiles_total = m_tiles * n_tiles * p.splits;
   const int kc = (p.k_iters + p.splits - 1) / p.splits;
   constexpr uint32_t kNTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+  // iterations of a whole tile (stream-K needs splits == 1)
+  const int T_tile = p.streamk ? p.k_iters + p.k_iters_aug : (1 << 30);
+  auto seg_extent = [&](int tile, int& mt, int& nt, int& z, int& kb, int& nk, int& total) {
+    tile_coords(tile, m_tiles, n_tiles, mt, nt, z);
+    kb = z * kc;
+    nk = min(kc, p.k_iters - kb);
+    total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
+  };
 
   if (warp == kTmaWarp && lane == 0) {
     ptx::prefetch_tmap(&tmB);
@@ -302,15 +357,15 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     // ======================= TMA producer (every CTA loads its own halves) =======================
     if (lane == 0) {
       uint32_t it = 0;
-      for (int t = unit0; t < n_tiles_total; t += n_units) {
-        int mt, nt, z;
-        tile_coords(t, m_tiles, n_tiles, mt, nt, z);
-        const int kb = z * kc;
-        const int nk = min(kc, p.k_iters - kb);
-        const int total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
+      Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
+      int tile, i0, i1;
+      while (sc.next(tile, i0, i1)) {
+        int mt, nt, z, kb, nk, total;
+        seg_extent(tile, mt, nt, z, kb, nk, total);
+        i1 = min(i1, total);
         const int m_cta = mt * BMP + (int)rank * BM;
         const int n_cta = nt * BN + (int)rank * BNC;
-        for (int i = 0; i < total; ++i, ++it) {
+        for (int i = i0; i < i1; ++i, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           ptx::mbar_wait(&empty[s], ph ^ 1);
@@ -346,17 +401,17 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     // ======================= MMA issuer (leader only) =======================
     if (leader) {
       uint32_t it = 0, local = 0;
-      for (int t = unit0; t < n_tiles_total; t += n_units, ++local) {
-        int mt, nt, z;
-        tile_coords(t, m_tiles, n_tiles, mt, nt, z);
-        const int kb = z * kc;
-        const int nk = min(kc, p.k_iters - kb);
-        const int total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
+      Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
+      int tile, i0, i1;
+      for (; sc.next(tile, i0, i1); ++local) {
+        int mt, nt, z, kb, nk, total;
+        seg_extent(tile, mt, nt, z, kb, nk, total);
+        i1 = min(i1, total);
         const uint32_t acc = local & 1;
         wait_x(&tempty[acc], ((local >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int i = 0; i < total; ++i, ++it) {
+        for (int i = i0; i < i1; ++i, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           const bool aug = i >= nk;
@@ -375,8 +430,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
                                       : ptx::sdesc_sw128(a_addr + kk * 32, 16, 1024);
               const uint64_t bd = bmn ? ptx::sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
                                       : ptx::sdesc_sw128(b_addr + kk * 32, 16, 1024);
-              if (PAIR) ptx::umma_bf16_pair(d_tmem, ad, bd, idesc, (i | kk) != 0);
-              else ptx::umma_bf16(d_tmem, ad, bd, idesc, (i | kk) != 0);
+              if (PAIR) ptx::umma_bf16_pair(d_tmem, ad, bd, idesc, (i != i0) || kk != 0);
+              else ptx::umma_bf16(d_tmem, ad, bd, idesc, (i != i0) || kk != 0);
             }
             if (PAIR) ptx::umma_commit_pair_mc(&empty[s], 0x3);
             else ptx::umma_commit(&empty[s]);
@@ -396,18 +451,58 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     const int quarter = warp & 3;           // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;    // accumulator row (M index within this CTA's half)
     uint32_t local = 0;
-    for (int t = unit0; t < n_tiles_total; t += n_units, ++local) {
-      int mt, nt, z;
-      tile_coords(t, m_tiles, n_tiles, mt, nt, z);
+    Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
+    const long long G = (long long)n_tiles_total * T_tile;
+    int tile, i0, i1;
+    for (; sc.next(tile, i0, i1); ++local) {
+      int mt, nt, z, kb, nk, total;
+      seg_extent(tile, mt, nt, z, kb, nk, total);
+      i1 = min(i1, total);
+      // stream-K: a segment not starting at k = 0 leaves an fp32 partial; the
+      // k = 0 segment (owner) adds the partials of units unit0+1 .. v_end-1
+      const bool partial = p.streamk && i0 != 0;
+      int v_end = unit0 + 1;
+      if (p.streamk && i0 == 0 && i1 < total)
+        while (v_end < n_units && Sched::range_begin(G, v_end, n_units) < (long long)(tile + 1) * T_tile) ++v_end;
       const uint32_t acc = local & 1;
       ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
+      if (v_end > unit0 + 1) {  // wait for the later units' partials of this tile
+        if (lane == 0)
+          for (int v = unit0 + 1; v < v_end; ++v) {
+            const int* f = p.sk_flags + (PAIR ? 2 * v + (int)rank : v);
+            int ready = 0;
+            while (!ready) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(ready) : "l"(f) : "memory");
+          }
+        __syncwarp();
+      }
       const int64_t m_base = (int64_t)mt * BMP + (int64_t)rank * BM;
       const int64_t m = m_base + row;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += EC) {
         uint32_t r[EC];
         ptx::tmem_ld<EC>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, r);
+        // partial tile layout per CTA: [column group of 4][row][4] -> a warp's
+        // float4 accesses cover 512 contiguous bytes
+        if (partial) {
+          float* dst = p.sk_ws + (size_t)blockIdx.x * BM * BN + (size_t)c0 * BM + row * 4;
+#pragma unroll
+          for (int j = 0; j < EC; j += 4)
+            __stcg(reinterpret_cast<float4*>(dst + j * BM), make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                                       __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+          continue;
+        }
+        for (int v = unit0 + 1; v < v_end; ++v) {
+          const float* src = p.sk_ws + (size_t)(PAIR ? 2 * v + (int)rank : v) * BM * BN + (size_t)c0 * BM + row * 4;
+#pragma unroll
+          for (int j = 0; j < EC; j += 4) {
+            const float4 w4 = __ldcg(reinterpret_cast<const float4*>(src + j * BM));
+            r[j] = __float_as_uint(__uint_as_float(r[j]) + w4.x);
+            r[j + 1] = __float_as_uint(__uint_as_float(r[j + 1]) + w4.y);
+            r[j + 2] = __float_as_uint(__uint_as_float(r[j + 2]) + w4.z);
+            r[j + 3] = __float_as_uint(__uint_as_float(r[j + 3]) + w4.w);
+          }
+        }
         const int64_t n0 = (int64_t)nt * BN + c0;
         if (EC == 32 && p.out_t && !p.out_f32 && p.splits == 1 && !p.to_ws) {
           // D^T tile through shared memory: row j = token n0+j, 32 features per row,
@@ -440,6 +535,13 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) arrive_leader(&tempty[acc]);
+      if (partial) {  // all four epilogue warps wrote their rows: publish
+        asm volatile("bar.sync 1, %0;" ::"n"(kNumEpiWarps * 32) : "memory");
+        if (warp == kEpiWarp0 && lane == 0) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.sk_flags + blockIdx.x), "r"(1) : "memory");
+        }
+      }
     }
   } else if (NF4 && warp == kCstWarp) {
     // ======================= codes + block-constant producer =======================
@@ -450,13 +552,13 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     if (lane == 0) {
       uint32_t cit = 0;
       const uint32_t kbytes = p.nf4_mode == 1 ? 64 * 16 : 128 * 16;
-      for (int t = unit0; t < n_tiles_total; t += n_units) {
-        int mt, nt, z;
-        tile_coords(t, m_tiles, n_tiles, mt, nt, z);
-        const int kb = z * kc;
-        const int nk = min(kc, p.k_iters - kb);
+      Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
+      int tile, i0, i1;
+      while (sc.next(tile, i0, i1)) {
+        int mt, nt, z, kb, nk, total;
+        seg_extent(tile, mt, nt, z, kb, nk, total);
         const int m_cta = mt * BMP + (int)rank * BM;
-        for (int i = 0; i < nk; ++i, ++cit) {
+        for (int i = i0; i < min(i1, nk); ++i, ++cit) {
           const int c = cit % CST;
           const int k0 = (kb + i) * BK;
           ptx::mbar_wait(&cempty[c], ((cit / CST) & 1) ^ 1);
@@ -484,23 +586,31 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     // fwd: item -> (h = item & 1, r = item >> 1): A image at h*8192 + r*128,
     //      codes at r*64 + h*32 (W row k0+r, cols m+64h..+64)
     // bwd: item -> W row m+item, cols k0..k0+64: A image item*128, codes item*32
-    const int h = item & 1, rr = item >> 1;
-    const uint32_t soff = p.nf4_mode == 1 ? (uint32_t)(h * 8192 + rr * 128) : (uint32_t)(item * 128);
-    const uint32_t swz = (soff >> 7) & 7;
-    const uint32_t codes_s = ptx::smem_u32(sC) + (uint32_t)item * 32;
+    // fwd: warp (xw & 3) -> half h = xw & 1 of rows rr = 32 * ((xw & 3) >> 1) + lane: consecutive lanes
+    // write consecutive 128 B rows of the MN-major image (conflict-free 16 B stores)
+    const int h = xw & 1, rr = 32 * ((xw & 3) >> 1) + lane;
+    const bool fwd = p.nf4_mode == 1;
+    const uint32_t soff = fwd ? (uint32_t)(h * 8192 + rr * 128) : (uint32_t)(item * 128);
+    // the two 16 B halves of an item's 32 code bytes are read in lane-alternating
+    // order (fewer bank conflicts); jA = 1 swaps chunk indices 0-3 <-> 4-7
+    const uint32_t jA = fwd ? (uint32_t)((rr >> 1) & 1) : (uint32_t)((item >> 2) & 1);
+    const uint32_t swz = ((soff >> 7) & 7) ^ (jA << 2);
+    const uint32_t codes_s = ptx::smem_u32(sC) + (fwd ? (uint32_t)(rr * 64 + h * 32) : (uint32_t)item * 32);
     // constants tile: fwd [64 rows][4] -> (r, h); bwd [128 rows][4] -> (item, 0)
-    const uint32_t consts_s = ptx::smem_u32(sK) + (p.nf4_mode == 1 ? (uint32_t)(rr * 16 + h * 4) : (uint32_t)item * 16);
+    const uint32_t consts_s = ptx::smem_u32(sK) + (fwd ? (uint32_t)(rr * 16 + h * 4) : (uint32_t)item * 16);
+    const uint32_t k3210 = 0x32103210u;
     const uint32_t a_s = ptx::smem_u32(sA) + soff;
     uint32_t it = 0, cit = 0;
-    for (int t = unit0; t < n_tiles_total; t += n_units) {
-      int mt, nt, z;
-      tile_coords(t, m_tiles, n_tiles, mt, nt, z);
-      const int kb = z * kc;
-      const int nk = min(kc, p.k_iters - kb);
-      const int total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
+    Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
+    int tile, i0, i1;
+    while (sc.next(tile, i0, i1)) {
+      int mt, nt, z, kb, nk, total;
+      seg_extent(tile, mt, nt, z, kb, nk, total);
+      i1 = min(i1, total);
       const int m_cta = mt * BMP + (int)rank * BM;
-      for (int i = (int)((it & 1) != (uint32_t)grp); i < total; i += 2) {
-        const uint32_t my = it + i;
+      // stages alternate between the two groups by the running stage count
+      for (int i = i0 + (int)(((it & 1) != (uint32_t)grp)); i < i1; i += 2) {
+        const uint32_t my = it + (uint32_t)(i - i0);
         const int s = my % STAGES;
         const uint32_t ph = (my / STAGES) & 1;
         if (i >= nk) {  // augmented (TMA-fed) stage: keep afull's phase in step
@@ -509,24 +619,26 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           if (lane == 0) arrive_leader(&afull[s]);
           continue;
         }
-        const uint32_t ci = cit + i;
+        const uint32_t ci = cit + (uint32_t)(i - i0);
         const int c = ci % CST;
         // the constants box starts at a 16 B aligned column: index within it
         const uint32_t kcol = (uint32_t)((p.nf4_mode == 1 ? m_cta / 64 : kb + i) & 3) * 4;
         ptx::mbar_wait(&cfull[c], (ci / CST) & 1);
-        const uint4 w0 = ptx::ld_shared_v4(codes_s + c * L::CODE_BYTES);
-        const uint4 w1 = ptx::ld_shared_v4(codes_s + c * L::CODE_BYTES + 16);
+        const uint4 w0 = ptx::ld_shared_v4(codes_s + c * L::CODE_BYTES + jA * 16);
+        const uint4 w1 = ptx::ld_shared_v4(codes_s + c * L::CODE_BYTES + (jA ^ 1u) * 16);
         const float cst = ptx::ld_shared_f32(consts_s + c * L::CONST_BYTES + kcol);
         uint32_t Lp[4], Hp[4];
         build_planes(vals, cst, Lp, Hp);
         ptx::mbar_wait(&empty[s], ph ^ 1);
         const uint32_t base = a_s + s * A_STAGE;
         const uint32_t words[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#ifndef QLRT_HACK_DECODE
+#define QLRT_HACK_DECODE 8
+#endif
+        uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {
-          uint32_t o0, o1, o2, o3;
-          lookup4(words[ch], Lp, Hp, o0, o1);
-          lookup4(words[ch] >> 16, Lp, Hp, o2, o3);
+          if (ch < QLRT_HACK_DECODE) lookup8(words[ch], Lp, Hp, k3210, o0, o1, o2, o3);
           ptx::st_shared_v4(base + ((ch ^ swz) << 4), o0, o1, o2, o3);
         }
         ptx::fence_proxy_async_smem();
@@ -539,8 +651,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           ptx::mbar_arrive(&cempty[c]);
         }
       }
-      it += total;
-      cit += nk;
+      it += (uint32_t)(i1 - i0);
+      cit += (uint32_t)max(0, min(i1, nk) - i0);
     }
   }
 
@@ -660,12 +772,15 @@ struct Operand {
 
 // 2-CTA pairing policy: QLRT_PAIR=0 off, 1 on, unset -> the per-GEMM default
 static int pair_policy(int dflt) {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("QLRT_PAIR");
-    v = e ? atoi(e) : -1;
-  }
+  const char* e = getenv("QLRT_PAIR");  // read per call: A/B runs toggle it in-process
+  const int v = e ? atoi(e) : -1;
   return v < 0 ? dflt : v;
+}
+
+// stream-K policy: QLRT_STREAMK=0 disables it (whole-tile waves only)
+static int streamk_policy() {
+  const char* e = getenv("QLRT_STREAMK");  // read per call: A/B runs toggle it in-process
+  return e ? atoi(e) : 1;
 }
 
 static int num_sms() {
@@ -693,7 +808,7 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
   const int m_tiles = (args.M + bmp - 1) / bmp, n_tiles = (args.N + BN - 1) / BN;
   const int tiles = m_tiles * n_tiles * args.splits;
   const int units_max = PAIR ? num_sms() / 2 : num_sms();
-  const int units = tiles < units_max ? tiles : units_max;
+  const int units = (tiles < units_max && !args.streamk) ? tiles : units_max;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(units * (PAIR ? 2 : 1));
   cfg.blockDim = dim3(NF4 ? kNF4Threads : 192);
@@ -762,6 +877,21 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   args.b2_mn = B2 ? B2->mn : 0;
   args.splits = effective_splits(args.splits, args.k_iters);
   if (args.splits > 1 && K2) return QLRT_ERR_UNSUPPORTED;
+  if (args.sk_ws && args.splits == 1 && bn >= 64 && num_sms() <= kNumSMs) {
+    // stream-K only for short grids (< 2 waves) that whole-tile waves would
+    // leave > 10% idle: measured, its partial-tile traffic and spread-out
+    // L2 footprint cost ~5% on long grids (tools/ab.py QLRT_STREAMK=0/1)
+    const int bmp = args.pair ? 2 * BM : BM;
+    const int64_t tiles = ((M + bmp - 1) / bmp) * ((N + bn - 1) / bn);
+    const int64_t units = args.pair ? num_sms() / 2 : num_sms();
+    const int64_t waves = (tiles + units - 1) / units;
+    const int64_t T = args.k_iters + args.k_iters_aug;
+    args.streamk = waves <= 2 && (double)tiles / (double)(waves * units) < 0.9 && T * tiles >= 2 * units;
+    if (args.streamk && cudaMemsetAsync(args.sk_flags, 0, sizeof(int) * num_sms(), s) != cudaSuccess)
+      return QLRT_ERR_CUDA;
+  } else {
+    args.streamk = 0;
+  }
   switch (bn) {
     case 256:
       if (args.pair) return nf4 ? launch_t<256, true, true>(ta, tb, ta2, tb2, tc, tk, args, s)
@@ -867,9 +997,16 @@ static size_t dbl_bytes(int64_t k_in, int64_t n_out, int rank) {
   const int64_t mx = k_in > n_out ? k_in : n_out;
   return align256((size_t)mx * 2 * rank * 2);
 }
-// layout of the linear workspace: [split-K partials][constants][doubled adapter]
+// stream-K partials (one BM x 256 fp32 tile per CTA) + flags
+static size_t sk_bytes() { return align256((size_t)kNumSMs * BM * 256 * 4) + align256((size_t)kNumSMs * 4); }
+// layout of the linear workspace: [split-K partials][constants][stream-K][doubled adapter]
 static void* dbl_region(void* ws, size_t ws_bytes, int64_t k_in, int64_t n_out, int rank) {
   return (uint8_t*)ws + (ws_bytes - dbl_bytes(k_in, n_out, rank));
+}
+static void sk_region(void* ws, size_t ws_bytes, int64_t k_in, int64_t n_out, int rank, Args& a) {
+  uint8_t* b = (uint8_t*)ws + (ws_bytes - dbl_bytes(k_in, n_out, rank) - sk_bytes());
+  a.sk_ws = (float*)b;
+  a.sk_flags = (int*)(b + align256((size_t)kNumSMs * BM * 256 * 4));
 }
 
 }  // namespace gemm
@@ -897,7 +1034,7 @@ size_t qlrt_linear_workspace_bytes(int64_t m, int64_t k_in, int64_t n_out, int r
   int64_t mx = a > b ? a : b;
   mx = mx > c ? mx : c;
   size_t total = gemm::align256((size_t)mx * 4) + 4096 + gemm::align256(gemm::consts_bytes(k_in, n_out)) +
-                 gemm::dbl_bytes(k_in, n_out, rank > 0 ? rank : 0);
+                 gemm::sk_bytes() + gemm::dbl_bytes(k_in, n_out, rank > 0 ? rank : 0);
   const size_t gv = qlrt_gemv_workspace_bytes(k_in, n_out, rank > 0 ? rank : 0);  // M = 1 path
   return total > gv ? total : gv;
 }
@@ -921,7 +1058,8 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t K = w->k_in, N = w->n_out;
   const size_t ws_bytes = qlrt_linear_workspace_bytes(m, K, N, rank);
-  const size_t part_bytes = ws_bytes - gemm::dbl_bytes(K, N, rank) - gemm::align256(gemm::consts_bytes(K, N));
+  const size_t part_bytes =
+      ws_bytes - gemm::dbl_bytes(K, N, rank) - gemm::sk_bytes() - gemm::align256(gemm::consts_bytes(K, N));
   float* consts = (float*)((uint8_t*)workspace + part_bytes);
   qlrt_status rc;
   if (rank > 0) {
@@ -942,6 +1080,7 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   a.out_t = 1;
   a.alpha = 1.0f;
   a.pair = gemm::pair_policy(0);
+  if (gemm::streamk_policy()) gemm::sk_region(workspace, ws_bytes, K, N, rank, a);
   if ((rc = gemm::fill_nf4(a, w, 1, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{x, K, 0};
   // augmented segment K2 = 2r: [l2 ; l2]^T [Ts_hi | Ts_lo]^T, i.e. the pair at ~16-bit precision
@@ -963,7 +1102,8 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t K = w->k_in, N = w->n_out;
   const size_t ws_bytes = qlrt_linear_workspace_bytes(m, K, N, rank);
-  const size_t part_bytes = ws_bytes - gemm::dbl_bytes(K, N, rank) - gemm::align256(gemm::consts_bytes(K, N));
+  const size_t part_bytes =
+      ws_bytes - gemm::dbl_bytes(K, N, rank) - gemm::sk_bytes() - gemm::align256(gemm::consts_bytes(K, N));
   float* consts = (float*)((uint8_t*)workspace + part_bytes);
   qlrt_status rc;
   if (rank > 0) {
@@ -984,6 +1124,7 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   a.out_t = 1;
   a.alpha = 1.0f;
   a.pair = gemm::pair_policy(0);
+  if (gemm::streamk_policy()) gemm::sk_region(workspace, ws_bytes, K, N, rank, a);
   if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{dy, N, 0};
   // augmented segment K2 = 2r: [l1 | l1] [dT_hi | dT_lo]^T

@@ -50,6 +50,16 @@ def load_peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+def traffic_of(key):
+    """DRAM bytes per launch of a kernel from the committed ncu capture
+    (profiles/roofline_traffic.json, dram__bytes_read.sum + write.sum)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as fh:
+            return json.load(fh)[key]["dram_bytes"]
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------------
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
@@ -303,15 +313,27 @@ def main() -> None:
     d2h = dxh.numel() * 2 + g1h.numel() * 4 + g2h.numel() * 4
 
     # ---- roofline of the dominant kernel: the fused NF4 dequant-GEMM (forward
-    # main GEMM, no adapter: 2*M*K*N FLOPs per launch), timed alone
+    # main GEMM, 2*M*K*N FLOPs per launch), launched alone through the C ABI
+    # with a pre-built block-constant cache (so the graph holds only that kernel)
     hbm, tf_burst, tf_sus, peak_kind = load_peaks()
+    from paper_2305_14314_b200._native import lib as _lib, ptr as _ptr, stream_ptr as _sp
     lin0 = qb.QLinear(q, [])
+    consts0 = lin0._constants()
+    y0 = torch.empty(M_TOK, N_OUT, dtype=torch.bfloat16, device=dev)
+    ws0 = lin0._workspace(M_TOK)
+    desc0 = lin0.weight_desc(consts0)
+
+    def fused_fwd():
+        rc = _lib().qlrt_nf4_linear_fwd(desc0, _ptr(x), None, M_TOK, None, None, 0, 0.0, None, _ptr(y0), _ptr(ws0),
+                                        _sp())
+        assert rc == 0, rc
+
     for _ in range(3):
-        lin0.forward(x)
+        fused_fwd()
     torch.cuda.synchronize()
     g0 = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g0):
-        lin0.forward(x)
+        fused_fwd()
     g0.replay()
     n_k = 10
     ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -327,9 +349,10 @@ def main() -> None:
     k_flops = 2 * M_TOK * K_IN * N_OUT
     achieved = k_flops / (k_ms / 1e3) / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": tf_burst, "unit": "TFLOP/s",
-                "frac": achieved / tf_burst, "traffic": None,
-                "kernel": "gemm_kernel<256,true> (fused NF4 dequant + tcgen05 GEMM), fwd 2048x4096x11008",
-                "kernel_ms": k_ms, "peak_kind": f"{peak_kind} burst bf16 (cuBLAS 8192^3)"}
+                "frac": achieved / tf_burst, "traffic": traffic_of("fused_fwd_c2"),
+                "kernel": "gemm_kernel<256,NF4> (fused NF4 dequant + tcgen05 GEMM), fwd 2048x4096x11008, alone",
+                "kernel_ms": k_ms, "peak_kind": f"{peak_kind} burst bf16 (cuBLAS)",
+                "algorithmic_flops_per_launch": k_flops}
 
     extras = {}
     if not args.no_extras:
@@ -362,68 +385,79 @@ def main() -> None:
 
 
 def secondary(qb, torch, dev, flush, stream, hbm):
-    """C1 dequant / quantize GB/s and a 65B-shape GEMV, each timed alone."""
+    """HBM-bound kernels (C1 dequant / quantize, 65B-shape dequant and GEMV)
+    and the plain-bf16 engine ceiling, each timed alone: a CUDA graph of the
+    launches replayed after an L2 flush (single = one launch; stream = R
+    launches over R distinct tensors, > L2 in total, per launch)."""
     out = {}
 
-    def timed(fn, n=20, graph=True):
-        """Device time of fn() alone: captured once into a CUDA graph and
-        replayed between L2 flushes (host launch overhead excluded)."""
+    def timed(fns, n=20):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         for _ in range(3):
-            fn()
+            for f in fns:
+                f()
         torch.cuda.synchronize()
-        run = fn
-        if graph:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                fn()
-            run = g.replay
-            run()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for f in fns:
+                f()
+        g.replay()
         tot = 0.0
         for _ in range(n):
             flush.zero_()
             a.record(stream)
-            run()
+            g.replay()
             b.record(stream)
             torch.cuda.synchronize()
             tot += a.elapsed_time(b)
         return tot / n
 
-    x = torch.randn(4096, 4096, device=dev, generator=torch.Generator(device=dev).manual_seed(0))
+    from paper_2305_14314_b200._native import BF16, lib, ptr, stream_ptr
     cb = qb.get_codebook("nf4")
-    q = qb.quantize(x, cb, 64, double_quant=True)
+
+    def deq_launch(q, o):
+        d = q.dq
+        return lambda: lib().qlrt_dequantize4(ptr(q.codes), q.numel, 64, q.codebook.to_c(), None, ptr(d.codes),
+                                              ptr(d.c1), ptr(d.mu), d.blocksize2, d.spec.to_c(), ptr(o), BF16,
+                                              stream_ptr())
+
+    for name, shape, reps in (("c1_dequant_bf16", (4096, 4096), 8), ("c4_dequant_bf16_8192x22016", (8192, 22016), 2)):
+        n = shape[0] * shape[1]
+        qs = [qb.quantize(torch.randn(*shape, device=dev), cb, 64, double_quant=True) for _ in range(reps)]
+        outs = [torch.empty(n, dtype=torch.bfloat16, device=dev) for _ in range(reps)]
+        nb = n // 64
+        by = n // 2 + nb + 4 * (nb // 256) + 4 + 2 * n
+        t1 = timed([deq_launch(qs[0], outs[0])])
+        tr = timed([deq_launch(q, o) for q, o in zip(qs, outs)]) / reps
+        out[name] = {"bytes": by, "single_ms": t1, "single_gbs": by / t1 / 1e6, "stream_ms": tr,
+                     "stream_gbs": by / tr / 1e6, "frac_hbm": by / tr / 1e6 / hbm,
+                     "note": f"stream = {reps} distinct tensors back to back (> L2), per launch"}
+        del qs, outs
+    x = torch.randn(4096, 4096, device=dev, generator=torch.Generator(device=dev).manual_seed(0))
     n = x.numel()
-    nb, n2 = n // 64, n // 64 // 256
-    deq_bytes = n // 2 + nb + 4 * n2 + 4 + 2 * n
-    t = timed(lambda: qb.dequantize(q, torch.bfloat16))
-    out["c1_dequant_bf16"] = {"gbs": deq_bytes / (t / 1e3) / 1e9, "ms": t, "bytes": deq_bytes,
-                              "frac_hbm": deq_bytes / (t / 1e3) / 1e9 / hbm}
-    q_bytes = 4 * n + n // 2 + nb + 4 * n2 + 4
+    nb = n // 64
+    q_bytes = 4 * n + n // 2 + nb + 4 * (nb // 256) + 4
     from paper_2305_14314_b200.blockquant import quantize_async
-    t = timed(lambda: quantize_async(x, cb, 64, double_quant=True))
+    t = timed([lambda: quantize_async(x, cb, 64, double_quant=True)])
     out["c1_quantize_dq_f32"] = {"gbs": q_bytes / (t / 1e3) / 1e9, "ms": t, "bytes": q_bytes,
                                  "frac_hbm": q_bytes / (t / 1e3) / 1e9 / hbm,
-                                 "note": "quantize + DQ kernels (3 launches); the non-finite check's host read excluded"}
-    # the same tcgen05 engine without the dequant producer: bf16 X W with W
-    # already dense (TMA-fed A and B), C2 shape -- separates MMA/pipeline
-    # limits from the NF4 decode cost, and is the unfused alternative
-    wq = torch.randn(4096, 11008, device=dev, generator=torch.Generator(device=dev).manual_seed(3)) * 0.02
-    wb = wq.bfloat16()
+                                 "note": "quantize + DQ kernels; the non-finite check's host read excluded"}
+    # the same tcgen05 engine without the dequant producer (TMA-fed dense bf16 W), C2 shape
+    wb = (torch.randn(4096, 11008, device=dev) * 0.02).bfloat16()
     xb = torch.randn(2048, 4096, device=dev).bfloat16()
     ob = torch.empty(2048, 11008, device=dev, dtype=torch.bfloat16)
-    t = timed(lambda: qb.gemm_bf16(xb, wb, out=ob))
-    fl = 2 * 2048 * 4096 * 11008
-    out["engine_bf16_gemm_2048x4096x11008"] = {"tflops": fl / (t / 1e3) / 1e12, "ms": t}
-    del wq, wb, xb, ob
-    w = torch.randn(8192, 22016, device=dev) * 0.02
-    qw = qb.quantize(w, cb, 64, double_quant=True)
-    del w
-    lin = qb.QLinear(qw, [])
-    xv = torch.randn(1, 8192, device=dev).bfloat16()
-    t = timed(lambda: lin.forward(xv))
-    nw = 8192 * 22016
-    gb = nw // 2 + nw // 64 + 4 * (nw // 64 // 256) + 2 * 8192 + 2 * 22016
-    out["c4_gemv_8192x22016"] = {"gbs": gb / (t / 1e3) / 1e9, "ms": t, "bytes": gb, "frac_hbm": gb / (t / 1e3) / 1e9 / hbm}
+    t = timed([lambda: qb.gemm_bf16(xb, wb, out=ob)])
+    out["engine_bf16_gemm_2048x4096x11008"] = {"tflops": 2 * 2048 * 4096 * 11008 / (t / 1e3) / 1e12, "ms": t}
+    del wb, xb, ob
+    for k, nn in ((8192, 8192), (8192, 22016), (22016, 8192)):
+        lin = qb.QLinear(qb.quantize(torch.randn(k, nn, device=dev) * 0.02, cb, 64, double_quant=True), [])
+        xv = torch.randn(1, k, device=dev).bfloat16()
+        t = timed([lambda: lin.forward(xv)])
+        nw = k * nn
+        gb = nw // 2 + nw // 64 + 4 * (nw // 64 // 256) + 2 * k + 2 * nn
+        out[f"c4_gemv_{k}x{nn}"] = {"gbs": gb / (t / 1e3) / 1e9, "ms": t, "bytes": gb,
+                                    "frac_hbm": gb / (t / 1e3) / 1e9 / hbm}
+        del lin
     return out
 
 

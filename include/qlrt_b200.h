@@ -119,6 +119,9 @@ size_t qlrt_nf4_constants_bytes(int64_t k_in, int64_t n_out);
 qlrt_status qlrt_nf4_constants(const qlrt_nf4_weight* w, float* out, void* stream);
 
 /* Workspace bytes for the linear entry points (split-K partial sums). */
+/* (The workspace also holds the stream-K partial tiles and flags: the caller
+ * zero-fills a new workspace once -- the flags must start at 0, and every
+ * launch leaves them 0 again.) */
 size_t qlrt_linear_workspace_bytes(int64_t m, int64_t k_in, int64_t n_out, int rank);
 
 /* forward (qlora.py:124-148):
@@ -161,7 +164,8 @@ size_t qlrt_gemv_workspace_bytes(int64_t k_in, int64_t n_out, int rank);
 /* Plain bf16 GEMM on the same tcgen05 engine (test + building block):
  * D[M,N] = alpha * A[M,K] B[K,N]; a_mn/b_mn select MN-major storage
  * (A stored [K,M] / B stored [K,N]) vs K-major (A [M,K] / B [N,K]).
- * out_f32 selects fp32 vs bf16 output, out_t stores D^T ([N,M]). */
+ * out_f32 selects fp32 vs bf16 output, out_t stores D^T ([N,M]).  A workspace
+ * of >= ~19.5 MB reserves its tail for stream-K (zero-filled once, as above). */
 qlrt_status qlrt_gemm_bf16(const void* a, const void* b, void* d, int64_t m, int64_t n,
                            int64_t k, int a_mn, int b_mn, float alpha, int out_f32,
                            int out_t, void* workspace, size_t workspace_bytes,

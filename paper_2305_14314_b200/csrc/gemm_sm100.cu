@@ -69,7 +69,7 @@ struct Args {
   // partials of the later units in unit order (deterministic)
   int streamk;
   float* sk_ws;         // [gridDim.x][BM][BN] fp32 partials (one per CTA)
-  int* sk_flags;        // [gridDim.x], zeroed before the launch; 1 = partial ready
+  int* sk_flags;        // [gridDim.x]; 0 between launches (owners re-arm what they consume), 1 = partial ready
 };
 
 template <int BN, bool NF4, bool PAIR = false>
@@ -100,6 +100,8 @@ __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int
   mt = r / n_tiles;
   nt = r - mt * n_tiles;
 }
+
+constexpr int kSkMaxSplit = 4;
 
 // Walks the segments (tile, [i0, i1)) of one unit: round-robin whole tiles, or
 // (stream-K) the unit's contiguous share of tiles x T iterations.
@@ -199,34 +201,37 @@ __device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[E
     }
     return;
   }
+  // direct output: with fold the logical width is fold (columns n and n + fold summed by the caller)
+  const int64_t NL = p.fold ? p.fold : p.N;
+  const bool full_out = n0 + EC <= NL;
   const float a = p.alpha;
   if (p.out_t) {  // D^T: out[n][m]; lanes are consecutive m -> coalesced per column
     if (p.out_f32) {
       float* o = static_cast<float*>(p.out);
 #pragma unroll
       for (int j = 0; j < EC; ++j)
-        if (n0 + j < p.N) o[(n0 + j) * p.ldo + m] = __uint_as_float(r[j]) * a;
+        if (n0 + j < NL) o[(n0 + j) * p.ldo + m] = __uint_as_float(r[j]) * a;
     } else {
       __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out);
 #pragma unroll
       for (int j = 0; j < EC; ++j)
-        if (n0 + j < p.N) o[(n0 + j) * p.ldo + m] = __float2bfloat16_rn(__uint_as_float(r[j]) * a);
+        if (n0 + j < NL) o[(n0 + j) * p.ldo + m] = __float2bfloat16_rn(__uint_as_float(r[j]) * a);
     }
     return;
   }
   if (p.out_f32) {
     float* o = static_cast<float*>(p.out) + m * p.ldo + n0;
-    if (full_chunk && (p.ldo & 3) == 0) {
+    if (full_out && (p.ldo & 3) == 0) {
 #pragma unroll
       for (int j = 0; j < EC; j += 4)
         *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(r[j]) * a, __uint_as_float(r[j + 1]) * a,
                                                         __uint_as_float(r[j + 2]) * a, __uint_as_float(r[j + 3]) * a);
     } else {
-      for (int j = 0; j < EC && n0 + j < p.N; ++j) o[j] = __uint_as_float(r[j]) * a;
+      for (int j = 0; j < EC && n0 + j < NL; ++j) o[j] = __uint_as_float(r[j]) * a;
     }
   } else if (p.out_split) {  // bf16 hi/lo pair: v ~= hi + lo to ~16 mantissa bits
     __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + m * p.ldo + n0;
-    for (int j = 0; j < EC && n0 + j < p.N; ++j) {
+    for (int j = 0; j < EC && n0 + j < NL; ++j) {
       const float v = __uint_as_float(r[j]) * a;
       const __nv_bfloat16 hi = __float2bfloat16_rn(v);
       o[j] = hi;
@@ -234,7 +239,7 @@ __device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[E
     }
   } else {
     __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + m * p.ldo + n0;
-    if (full_chunk && (p.ldo & 7) == 0) {
+    if (full_out && (p.ldo & 7) == 0) {
 #pragma unroll
       for (int j = 0; j < EC; j += 8)
         *reinterpret_cast<uint4*>(o + j) =
@@ -243,7 +248,7 @@ __device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[E
                        pack_bf16x2(__uint_as_float(r[j + 4]) * a, __uint_as_float(r[j + 5]) * a),
                        pack_bf16x2(__uint_as_float(r[j + 6]) * a, __uint_as_float(r[j + 7]) * a));
     } else {
-      for (int j = 0; j < EC && n0 + j < p.N; ++j) o[j] = __float2bfloat16_rn(__uint_as_float(r[j]) * a);
+      for (int j = 0; j < EC && n0 + j < NL; ++j) o[j] = __float2bfloat16_rn(__uint_as_float(r[j]) * a);
     }
   }
 }
@@ -467,41 +472,80 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
       const uint32_t acc = local & 1;
       ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
-      if (v_end > unit0 + 1) {  // wait for the later units' partials of this tile
-        if (lane == 0)
-          for (int v = unit0 + 1; v < v_end; ++v) {
-            const int* f = p.sk_flags + (PAIR ? 2 * v + (int)rank : v);
-            int ready = 0;
-            while (!ready) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(ready) : "l"(f) : "memory");
-          }
-        __syncwarp();
+      if (v_end > unit0 + 1) {  // wait for the later units' partials of this tile (one flag per lane)
+        for (int v0 = unit0 + 1; v0 < v_end; v0 += 32) {
+          const int v = v0 + lane;
+          int ready = v < v_end ? 0 : 1;
+          const int* f = p.sk_flags + (PAIR ? 2 * v + (int)rank : v);
+          while (!__all_sync(0xffffffffu, ready))
+            if (!ready) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(ready) : "l"(f) : "memory");
+        }
       }
       const int64_t m_base = (int64_t)mt * BMP + (int64_t)rank * BM;
       const int64_t m = m_base + row;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += EC) {
-        uint32_t r[EC];
-        ptx::tmem_ld<EC>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, r);
-        // partial tile layout per CTA: [column group of 4][row][4] -> a warp's
-        // float4 accesses cover 512 contiguous bytes
-        if (partial) {
-          float* dst = p.sk_ws + (size_t)blockIdx.x * BM * BN + (size_t)c0 * BM + row * 4;
+      // chunk c of the accumulator (+ the stream-K contributors' partials); the
+      // partial tile layout per CTA is [column group of 4][row][4]: a warp's
+      // float4 accesses cover 512 contiguous bytes
+      auto load_acc = [&](int c, uint32_t (&r)[EC]) {
+        ptx::tmem_ld<EC>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
+        // contributors four at a time, 16 columns at a time: 16 independent L2
+        // loads in flight, then the adds in unit order (deterministic)
+        for (int v0 = unit0 + 1; v0 < v_end; v0 += 4) {
 #pragma unroll
-          for (int j = 0; j < EC; j += 4)
-            __stcg(reinterpret_cast<float4*>(dst + j * BM), make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                                       __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+          for (int h = 0; h < EC; h += 16) {
+            float4 w[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int v = v0 + q < v_end ? v0 + q : v0;
+              const float* src =
+                  p.sk_ws + (size_t)(PAIR ? 2 * v + (int)rank : v) * BM * BN + (size_t)c * BM + row * 4;
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) w[q][jj] = __ldcg(reinterpret_cast<const float4*>(src + (h + 4 * jj) * BM));
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (v0 + q >= v_end) break;
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const int j = h + 4 * jj;
+                r[j] = __float_as_uint(__uint_as_float(r[j]) + w[q][jj].x);
+                r[j + 1] = __float_as_uint(__uint_as_float(r[j + 1]) + w[q][jj].y);
+                r[j + 2] = __float_as_uint(__uint_as_float(r[j + 2]) + w[q][jj].z);
+                r[j + 3] = __float_as_uint(__uint_as_float(r[j + 3]) + w[q][jj].w);
+              }
+            }
+          }
+        }
+      };
+      auto store_partial = [&](int c, const uint32_t (&r)[EC]) {
+        float* dst = p.sk_ws + (size_t)blockIdx.x * BM * BN + (size_t)c * BM + row * 4;
+#pragma unroll
+        for (int j = 0; j < EC; j += 4)
+          __stcg(reinterpret_cast<float4*>(dst + j * BM), make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                                     __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+      };
+      // fold (hi/lo operand pairs, fold <= BN / 2, one column tile): out column
+      // n = D[:, n] + D[:, n + fold]
+      const bool direct_fold = p.fold && !(p.splits > 1 || p.to_ws);  // else the reduce kernel folds
+      const int cend = direct_fold ? p.fold : BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < cend; c0 += EC) {
+        uint32_t r[EC];
+        if (partial) {
+          ptx::tmem_ld<EC>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, r);
+          store_partial(c0, r);
+          if (direct_fold) {
+            ptx::tmem_ld<EC>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0 + p.fold, r);
+            store_partial(c0 + p.fold, r);
+          }
           continue;
         }
-        for (int v = unit0 + 1; v < v_end; ++v) {
-          const float* src = p.sk_ws + (size_t)(PAIR ? 2 * v + (int)rank : v) * BM * BN + (size_t)c0 * BM + row * 4;
+        load_acc(c0, r);
+        if (direct_fold) {
+          uint32_t r2[EC];
+          load_acc(c0 + p.fold, r2);
 #pragma unroll
-          for (int j = 0; j < EC; j += 4) {
-            const float4 w4 = __ldcg(reinterpret_cast<const float4*>(src + j * BM));
-            r[j] = __float_as_uint(__uint_as_float(r[j]) + w4.x);
-            r[j + 1] = __float_as_uint(__uint_as_float(r[j + 1]) + w4.y);
-            r[j + 2] = __float_as_uint(__uint_as_float(r[j + 2]) + w4.z);
-            r[j + 3] = __float_as_uint(__uint_as_float(r[j + 3]) + w4.w);
-          }
+          for (int j = 0; j < EC; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
         }
         const int64_t n0 = (int64_t)nt * BN + c0;
         if (EC == 32 && p.out_t && !p.out_f32 && p.splits == 1 && !p.to_ws) {
@@ -535,6 +579,11 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) arrive_leader(&tempty[acc]);
+      if (v_end > unit0 + 1) {  // every epilogue warp consumed the partials: re-arm the flags
+        asm volatile("bar.sync 1, %0;" ::"n"(kNumEpiWarps * 32) : "memory");
+        if (warp == kEpiWarp0)
+          for (int v = unit0 + 1 + lane; v < v_end; v += 32) p.sk_flags[PAIR ? 2 * v + (int)rank : v] = 0;
+      }
       if (partial) {  // all four epilogue warps wrote their rows: publish
         asm volatile("bar.sync 1, %0;" ::"n"(kNumEpiWarps * 32) : "memory");
         if (warp == kEpiWarp0 && lane == 0) {
@@ -808,7 +857,10 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
   const int m_tiles = (args.M + bmp - 1) / bmp, n_tiles = (args.N + BN - 1) / BN;
   const int tiles = m_tiles * n_tiles * args.splits;
   const int units_max = PAIR ? num_sms() / 2 : num_sms();
-  const int units = (tiles < units_max && !args.streamk) ? tiles : units_max;
+  // stream-K: at most kSkMaxSplit units share a tile (the owner reads the
+  // others' partials from L2; more contributors cost more round trips)
+  int units = (tiles < units_max && !args.streamk) ? tiles : units_max;
+  if (args.streamk && (int64_t)tiles * kSkMaxSplit < units) units = tiles * kSkMaxSplit;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(units * (PAIR ? 2 : 1));
   cfg.blockDim = dim3(NF4 ? kNF4Threads : 192);
@@ -887,8 +939,8 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
     const int64_t waves = (tiles + units - 1) / units;
     const int64_t T = args.k_iters + args.k_iters_aug;
     args.streamk = waves <= 2 && (double)tiles / (double)(waves * units) < 0.9 && T * tiles >= 2 * units;
-    if (args.streamk && cudaMemsetAsync(args.sk_flags, 0, sizeof(int) * num_sms(), s) != cudaSuccess)
-      return QLRT_ERR_CUDA;
+    // the flags are zero between launches: every owner re-arms the flags it
+    // consumed; the caller zero-fills the region once (qlrt_streamk_init)
   } else {
     args.streamk = 0;
   }
@@ -928,7 +980,7 @@ static int pick_splits(int64_t tiles, int64_t k_iters, int64_t per_split_bytes, 
 // reduce kernel (forces the fp32 workspace route); out_split: bf16 hi/lo.
 static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, int64_t N, int64_t K, float alpha,
                          void* out, int64_t ldo, int out_f32, int out_t, float* ws, size_t ws_bytes, cudaStream_t s,
-                         int fold = 0, int out_split = 0) {
+                         int fold = 0, int out_split = 0, const Args* sk = nullptr) {
   Args a{};
   a.M = (int)M;
   a.N = (int)N;
@@ -944,6 +996,19 @@ static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, 
   a.pair = (bn == 256 && !B.mn) ? pair_policy(1) : 0;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
   const int64_t kit = (K + BK - 1) / BK;
+  // (off by default: measured slower than split-K + reduce on the C2 LoRA shapes,
+  //  tools/ab_skinny.py; QLRT_STREAMK_SKINNY=1 enables it)
+  const char* e_sk = getenv("QLRT_STREAMK_SKINNY");
+  if (e_sk && atoi(e_sk) && sk && sk->sk_ws && streamk_policy() && !(out_split && out_t) &&
+      (!fold || (2 * fold <= bn && N <= bn))) {
+    // skinny GEMM: stream-K over all SMs, partials reduced in-kernel, fold /
+    // hi-lo split applied in the epilogue -- no split-K workspace, no reduce launch
+    a.sk_ws = sk->sk_ws;
+    a.sk_flags = sk->sk_flags;
+    a.splits = 1;
+    a.to_ws = 0;
+    return run(bn, A, B, nullptr, nullptr, K, 0, a, s);
+  }
   a.splits = effective_splits(ws ? pick_splits(tiles, kit, M * N * 4, ws_bytes) : 1, (int)kit);
   a.to_ws = fold != 0 || (out_split && out_t);
   if ((a.to_ws || a.splits > 1) && (!ws || (size_t)(M * N * 4) * a.splits > ws_bytes)) return QLRT_ERR_ARG;
@@ -1046,8 +1111,17 @@ qlrt_status qlrt_gemm_bf16(const void* a, const void* b, void* d, int64_t m, int
   A.ptr = a; A.mn = a_mn; A.ld = a_mn ? m : k;
   B.ptr = b; B.mn = b_mn; B.ld = b_mn ? n : k;
   const int bn = n <= 64 ? 64 : (n <= 128 ? 128 : 256);
+  // a workspace with room for the stream-K region (its last sk_bytes) enables stream-K
+  gemm::Args sk{};
+  if (workspace && workspace_bytes >= gemm::sk_bytes() + 4096) {
+    uint8_t* b = (uint8_t*)workspace + (workspace_bytes - gemm::sk_bytes());
+    b = (uint8_t*)(((uintptr_t)b) & ~(uintptr_t)255);
+    sk.sk_ws = (float*)b;
+    sk.sk_flags = (int*)(b + gemm::align256((size_t)kNumSMs * gemm::BM * 256 * 4));
+    workspace_bytes = (size_t)(b - (uint8_t*)workspace);
+  }
   return gemm::plain(bn, A, B, m, n, k, alpha, d, out_t ? m : n, out_f32, out_t, (float*)workspace, workspace_bytes,
-                     (cudaStream_t)stream);
+                     (cudaStream_t)stream, 0, 0, sk.sk_ws ? &sk : nullptr);
 }
 
 qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const void* xa, int64_t m, const void* l1,
@@ -1062,11 +1136,14 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
       ws_bytes - gemm::dbl_bytes(K, N, rank) - gemm::sk_bytes() - gemm::align256(gemm::consts_bytes(K, N));
   float* consts = (float*)((uint8_t*)workspace + part_bytes);
   qlrt_status rc;
+  gemm::Args sk{};
+  gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
   if (rank > 0) {
     // Ts[m, 0:r] + Ts[m, r:2r] = s * Xa l1 as a bf16 hi/lo pair:
     //   A = Xa (K-major, [m][K]), B = l1 (MN-major, [K][r])
     Operand A{xa ? xa : x, K, 0}, B{l1, rank, 1};
-    rc = gemm::plain(64, A, B, m, rank, K, s, ts_out, 2 * rank, 0, 0, (float*)workspace, part_bytes, st, 0, rank);
+    rc = gemm::plain(64, A, B, m, rank, K, s, ts_out, 2 * rank, 0, 0, (float*)workspace, part_bytes, st, 0, rank,
+                     &sk);
     if (rc != QLRT_OK) return rc;
   }
   // Y^T[N, m] = W^T X^T (+ l2^T Ts^T): A = NF4 (MN-major image), B = X (K-major)
@@ -1080,7 +1157,7 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   a.out_t = 1;
   a.alpha = 1.0f;
   a.pair = gemm::pair_policy(0);
-  if (gemm::streamk_policy()) gemm::sk_region(workspace, ws_bytes, K, N, rank, a);
+  if (gemm::streamk_policy()) { a.sk_ws = sk.sk_ws; a.sk_flags = sk.sk_flags; }
   if ((rc = gemm::fill_nf4(a, w, 1, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{x, K, 0};
   // augmented segment K2 = 2r: [l2 ; l2]^T [Ts_hi | Ts_lo]^T, i.e. the pair at ~16-bit precision
@@ -1106,11 +1183,14 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
       ws_bytes - gemm::dbl_bytes(K, N, rank) - gemm::sk_bytes() - gemm::align256(gemm::consts_bytes(K, N));
   float* consts = (float*)((uint8_t*)workspace + part_bytes);
   qlrt_status rc;
+  gemm::Args sk{};
+  gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
   if (rank > 0) {
     // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):
     //   A = dY (K-major [m][N]), B = l2 (K-major [r][N])
     Operand A{dy, N, 0}, B{l2, N, 0};
-    rc = gemm::plain(64, A, B, m, rank, N, s, dt_out, 2 * rank, 0, 0, (float*)workspace, part_bytes, st, 0, rank);
+    rc = gemm::plain(64, A, B, m, rank, N, s, dt_out, 2 * rank, 0, 0, (float*)workspace, part_bytes, st, 0, rank,
+                     &sk);
     if (rc != QLRT_OK) return rc;
   }
   // dX^T[K, m] = W dY^T (+ l1 dT^T): A = NF4 (K-major image), B = dY (K-major)
@@ -1124,7 +1204,7 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   a.out_t = 1;
   a.alpha = 1.0f;
   a.pair = gemm::pair_policy(0);
-  if (gemm::streamk_policy()) gemm::sk_region(workspace, ws_bytes, K, N, rank, a);
+  if (gemm::streamk_policy()) { a.sk_ws = sk.sk_ws; a.sk_flags = sk.sk_flags; }
   if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{dy, N, 0};
   // augmented segment K2 = 2r: [l1 | l1] [dT_hi | dT_lo]^T
@@ -1143,14 +1223,14 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   {
     Operand A{dy, N, 1}, B{ts, 2 * rank, 1};
     rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, N, 2 * rank, m, 1.0f, dl2, N, 1, 1, (float*)workspace,
-                     part_bytes, st, rank);
+                     part_bytes, st, rank, 0, &sk);
     if (rc != QLRT_OK) return rc;
   }
   // dl1[K, r] = Xa^T (dT_hi + dT_lo): A = Xa (MN-major [m][K]), B = [dT_hi | dT_lo] (MN-major [m][2r])
   {
     Operand A{x, K, 1}, B{dt_out, 2 * rank, 1};
     rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, K, 2 * rank, m, 1.0f, dl1, rank, 1, 0, (float*)workspace,
-                     part_bytes, st, rank);
+                     part_bytes, st, rank, 0, &sk);
   }
   return rc;
 }

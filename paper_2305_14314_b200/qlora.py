@@ -153,7 +153,7 @@ class QLinear:
         r = _pad8(self.adapters[0].rank) if self.adapters else 0
         need = int(lib().qlrt_linear_workspace_bytes(max(m, 1), self.in_dim, self.out_dim, r))
         if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+            self._ws = torch.zeros(need, dtype=torch.uint8, device="cuda")  # stream-K flags start at 0
         return self._ws
 
     # -- forward / backward -------------------------------------------------
@@ -305,9 +305,9 @@ def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
         return out
     dev = a.device
     ws = _GEMM_WS.get(dev)
-    need = 16 * m * n * 4 + 4096
+    need = 16 * m * n * 4 + 4096 + (20 << 20)  # split-K partials + the stream-K region
     if ws is None or ws.numel() < need:
-        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        ws = torch.zeros(need, dtype=torch.uint8, device=dev)  # stream-K flags start at 0
         _GEMM_WS[dev] = ws
     # a_mn: A stored [K][M]; b_mn: B stored [K][N]
     check(lib().qlrt_gemm_bf16(ptr(a), ptr(b), ptr(out), m, n, k, int(a_t), int(not b_t), float(alpha),

@@ -1,0 +1,36 @@
+"""A/B the skinny LoRA GEMM shapes of one QLinear step (C2) with stream-K on/off."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2305_14314_b200 as qb  # noqa: E402
+from tools.bench_mem import timed  # noqa: E402
+
+m, k, n, r = 2048, 4096, 11008, 64
+x = torch.randn(m, k, device="cuda").bfloat16()
+dy = torch.randn(m, n, device="cuda").bfloat16()
+l1 = (torch.randn(k, r, device="cuda") / 8).bfloat16()
+l2 = (torch.randn(r, n, device="cuda") * .01).bfloat16()
+ts = torch.randn(m, 2 * r, device="cuda").bfloat16()
+cases = {
+    "Ts = X l1      (2048x64x4096)": lambda: qb.gemm_bf16(x, l1, out_dtype=torch.float32),
+    "dT = dY l2^T   (2048x64x11008)": lambda: qb.gemm_bf16(dy, l2, b_t=True, out_dtype=torch.float32),
+    "dl2^T = dY^T Ts (11008x128x2048)": lambda: qb.gemm_bf16(dy, ts, a_t=True, out_dtype=torch.float32),
+    "dl1 = X^T dT   (4096x128x2048)": lambda: qb.gemm_bf16(x, ts, a_t=True, out_dtype=torch.float32),
+}
+for name, fn in cases.items():
+    row = []
+    for sk in ("0", "1", "0", "1"):
+        os.environ["QLRT_STREAMK"] = sk
+        row.append(timed([fn], n=20) * 1e3)
+    print(f"{name}: sk0 {min(row[0], row[2]):6.1f} us   sk1 {min(row[1], row[3]):6.1f} us")
+
+# back-to-back launches in one graph (no flush between): per-launch cost
+for name, fn in cases.items():
+    row = []
+    for sk in ("0", "1"):
+        os.environ["QLRT_STREAMK"] = sk
+        row.append(timed([fn] * 10, n=10) * 1e3 / 10)
+    print(f"x10 {name}: sk0 {row[0]:6.1f} us   sk1 {row[1]:6.1f} us")

@@ -181,6 +181,15 @@ qlrt_status qlrt_adam_step(float* p, const float* g, float* m, float* v, int64_t
                            float b1, float omb1, float b2, float omb2, float bc1,
                            float bc2, float eps, float lr, void* p_bf16, void* stream);
 
+/* The same update over one flat buffer with its scalars in device memory
+ * (hyper[8] = b1, 1-b1, b2, 1-b2, bc1, bc2, eps, lr: a CUDA graph replays it
+ * while the host refreshes hyper) and, when sumsq != NULL, the global-norm
+ * clip fused in: g *= f32(max_norm / sqrt(*sumsq)) if that norm > max_norm
+ * (training.py:398-413).  16-byte aligned p, g, m, v; 8-byte aligned p_bf16. */
+qlrt_status qlrt_adam_step_dev(float* p, const float* g, float* m, float* v, int64_t n,
+                               const float* hyper, const double* sumsq, double max_norm,
+                               void* p_bf16, void* stream);
+
 /* sum of squares in fp64 of n floats, accumulated into acc[0] (device).
  * acc must have QLRT_SUMSQ_SCRATCH bytes: acc[0] result, then scratch. */
 #define QLRT_SUMSQ_SCRATCH (8 + 8 * 296 + 8)

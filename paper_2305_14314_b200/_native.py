@@ -60,6 +60,8 @@ _SIGS = {
     "qlrt_gemm_bf16": [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_int, c_float, c_int, c_int,
                        c_void_p, c_size_t, c_void_p],
     "qlrt_adam_step": [c_void_p, c_void_p, c_void_p, c_void_p, c_int64] + [c_float] * 8 + [c_void_p, c_void_p],
+    "qlrt_adam_step_dev": [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_double, c_void_p,
+                           c_void_p],
     "qlrt_sumsq_f64": [c_void_p, c_int64, c_void_p, c_void_p],
     "qlrt_scale_f32": [c_void_p, c_int64, c_float, c_void_p],
     "qlrt_prefetch": [c_void_p, c_size_t, c_int, c_void_p],

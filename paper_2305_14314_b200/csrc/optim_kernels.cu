@@ -60,6 +60,56 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, const 
   }
 }
 
+// Graph-replayable Adam over one flat parameter buffer: the step-dependent
+// scalars come from device memory (hyper = b1, 1-b1, b2, 1-b2, bc1, bc2, eps,
+// lr) and, with sumsq != nullptr, the global-norm clip is fused in
+// (clip_global_norm, training.py:398-413: scale = f32(max_norm / sqrt(sumsq))
+// when the norm exceeds max_norm, then g * scale in fp32 before the update).
+__global__ void __launch_bounds__(256) adam_dev_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                                       float* __restrict__ m, float* __restrict__ v, int64_t n,
+                                                       const float* __restrict__ hyper,
+                                                       const double* __restrict__ sumsq, double max_norm,
+                                                       __nv_bfloat16* __restrict__ pb) {
+  const float b1 = hyper[0], omb1 = hyper[1], b2 = hyper[2], omb2 = hyper[3];
+  const float bc1 = hyper[4], bc2 = hyper[5], eps = hyper[6], lr = hyper[7];
+  float scale = 1.0f;
+  bool clip = false;
+  if (sumsq) {
+    const double norm = __dsqrt_rn(*sumsq);
+    if (norm > max_norm && norm > 0.0) {
+      clip = true;
+      scale = __double2float_rn(__ddiv_rn(max_norm, norm));
+    }
+  }
+  const int64_t n4 = n >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 P = reinterpret_cast<float4*>(p)[i];
+    float4 G = reinterpret_cast<const float4*>(g)[i];
+    float4 Mv = reinterpret_cast<float4*>(m)[i];
+    float4 Vv = reinterpret_cast<float4*>(v)[i];
+    if (clip) {
+      G.x = __fmul_rn(G.x, scale); G.y = __fmul_rn(G.y, scale);
+      G.z = __fmul_rn(G.z, scale); G.w = __fmul_rn(G.w, scale);
+    }
+    adam_one(P.x, G.x, Mv.x, Vv.x, b1, omb1, b2, omb2, bc1, bc2, eps, lr);
+    adam_one(P.y, G.y, Mv.y, Vv.y, b1, omb1, b2, omb2, bc1, bc2, eps, lr);
+    adam_one(P.z, G.z, Mv.z, Vv.z, b1, omb1, b2, omb2, bc1, bc2, eps, lr);
+    adam_one(P.w, G.w, Mv.w, Vv.w, b1, omb1, b2, omb2, bc1, bc2, eps, lr);
+    reinterpret_cast<float4*>(p)[i] = P;
+    reinterpret_cast<float4*>(m)[i] = Mv;
+    reinterpret_cast<float4*>(v)[i] = Vv;
+    if (pb) reinterpret_cast<uint2*>(pb)[i] = make_uint2(pack_bf16x2(P.x, P.y), pack_bf16x2(P.z, P.w));
+  }
+  for (int64_t i = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float P = p[i], Mv = m[i], Vv = v[i], G = g[i];
+    if (clip) G = __fmul_rn(G, scale);
+    adam_one(P, G, Mv, Vv, b1, omb1, b2, omb2, bc1, bc2, eps, lr);
+    p[i] = P; m[i] = Mv; v[i] = Vv;
+    if (pb) pb[i] = __float2bfloat16_rn(P);
+  }
+}
+
 // fp64 sum of squares: per-thread sequential over a grid-stride range, then
 // a fixed-shape tree per CTA and a fixed-order add of CTA partials by the
 // last CTA (deterministic for a given n and grid).
@@ -113,6 +163,20 @@ qlrt_status qlrt_adam_step(float* p, const float* g, float* m, float* v, int64_t
   if (blocks < 1) blocks = 1;
   adam_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(p, g, m, v, n, b1, omb1, b2, omb2, bc1, bc2, eps, lr,
                                                             (__nv_bfloat16*)p_bf16);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_adam_step_dev(float* p, const float* g, float* m, float* v, int64_t n, const float* hyper,
+                               const double* sumsq, double max_norm, void* p_bf16, void* stream) {
+  if (!p || !g || !m || !v || !hyper || n <= 0) return QLRT_ERR_ARG;
+  if (((((uintptr_t)p) | ((uintptr_t)g) | ((uintptr_t)m) | ((uintptr_t)v)) & 15) || (((uintptr_t)p_bf16) & 7))
+    return QLRT_ERR_ARG;
+  int64_t blocks = (n / 4 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  adam_dev_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(p, g, m, v, n, hyper, sumsq, max_norm,
+                                                                (__nv_bfloat16*)p_bf16);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }

@@ -1,0 +1,241 @@
+"""LLaMA-shaped QLoRA finetuning harness on the B200 kernels (SURVEY.md §8(f)
+rank 1; BASELINE configs C3 = LLaMA-7B shapes on 1 GPU and C5 = LLaMA-33B
+shapes data-parallel).
+
+The reference trains a toy MLP (pkg/src/qlrt/qlora.py:229-303) and has no
+transformer; this harness exists to *measure* the hot path at LLaMA scale:
+every linear layer (q, k, v, o, gate, up, down) is a frozen NF4 + DQ base with
+a bf16-operand LoRA adapter running through the fused tcgen05 kernels
+(``QLinear``, qlora.py:91-167 semantics); the glue -- RMSNorm, RoPE, SwiGLU,
+causal attention (PyTorch SDPA), the frozen bf16 embedding and lm_head
+(cuBLAS) and the loss -- is PyTorch.  Weights are random N(0, 0.02) (no
+checkpoints offline), tokens synthetic.
+
+Training step = forward, backward (adapter gradients written straight into
+one flat fp32 bucket), data-parallel mean all-reduce of that bucket only
+(NCCL; a no-op on one rank), fused global-norm clip + bit-exact Adam over the
+flat parameter buffer (``qlrt_adam_step_dev``), bf16 operand shadows
+refreshed in the same pass.  The whole step captures into one CUDA graph.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from ._native import check, lib, ptr, stream_ptr
+from .blockquant import quantize
+from .codebooks import get_codebook
+from .parallel import GradBucket
+from .qlora import LoraAdapter, QLinear
+from .training import TrainConfig, _sumsq_scratch
+
+PROJS = ("q", "k", "v", "o", "gate", "up", "down")
+
+
+@dataclass(frozen=True)
+class LlamaConfig:
+    n_layers: int = 32
+    hidden: int = 4096
+    ffn: int = 11008
+    n_heads: int = 32
+    vocab: int = 32000
+    seq: int = 512
+    rank: int = 64
+    alpha: float = 16.0
+    rms_eps: float = 1e-6
+    rope_theta: float = 10000.0
+
+    @staticmethod
+    def llama7b(**kw) -> "LlamaConfig":
+        return LlamaConfig(**kw)
+
+    @staticmethod
+    def llama33b(**kw) -> "LlamaConfig":
+        return LlamaConfig(n_layers=60, hidden=6656, ffn=17920, n_heads=52, **kw)
+
+    @staticmethod
+    def tiny(**kw) -> "LlamaConfig":
+        base = dict(n_layers=2, hidden=256, ffn=512, n_heads=4, vocab=512, seq=64, rank=16)
+        base.update(kw)
+        return LlamaConfig(**base)
+
+    def proj_shape(self, name: str) -> tuple[int, int]:
+        h, f = self.hidden, self.ffn
+        return {"q": (h, h), "k": (h, h), "v": (h, h), "o": (h, h), "gate": (h, f), "up": (h, f),
+                "down": (f, h)}[name]
+
+    @property
+    def linear_params(self) -> int:
+        return self.n_layers * sum(a * b for a, b in map(self.proj_shape, PROJS))
+
+    @property
+    def lora_params(self) -> int:
+        return self.n_layers * sum(self.rank * (a + b) for a, b in map(self.proj_shape, PROJS))
+
+    def flops_per_token(self) -> float:
+        """fwd 2P + bwd-to-input 2P over the frozen linears, 6 P_lora for the
+        adapters, causal attention (QK^T and PV, fwd + bwd 3x, half masked
+        counted in full as the SDPA kernels do the work) and the lm_head
+        (fwd + bwd-to-input): SURVEY.md §8(d) C3."""
+        p, pl = self.linear_params, self.lora_params
+        attn = 3 * self.n_layers * 4 * self.seq * self.hidden
+        head = 4 * self.vocab * self.hidden
+        return 2 * p + 2 * p + 6 * pl + attn + head
+
+
+class _QLinearFn(torch.autograd.Function):
+    """Autograd bridge to QLinear.forward / backward (qlora.py:124-167); the
+    adapter gradients go to the bucket views, not to autograd."""
+
+    @staticmethod
+    def forward(ctx, x, anchor, layer, gviews):
+        y, cache = layer.forward(x)
+        ctx.layer, ctx.cache, ctx.gviews = layer, cache, gviews
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        dx, _ = ctx.layer.backward(dy.contiguous(), ctx.cache, grads_out=ctx.gviews)
+        ctx.cache = None
+        return dx, None, None, None
+
+
+def _rmsnorm(x: torch.Tensor, eps: float) -> torch.Tensor:
+    xf = x.float()
+    return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)).to(x.dtype)
+
+
+def _rope(t: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
+    h = t.shape[-1] // 2
+    t1, t2 = t[..., :h], t[..., h:]
+    return torch.cat((t1 * cos - t2 * sin, t2 * cos + t1 * sin), dim=-1)
+
+
+class LlamaQLoRA:
+    """Frozen NF4 LLaMA-shaped decoder with LoRA on every linear layer."""
+
+    def __init__(self, cfg: LlamaConfig, device="cuda", seed: int = 0, train_cfg: TrainConfig | None = None):
+        self.cfg = cfg
+        self.dev = torch.device(device)
+        self.train_cfg = train_cfg or TrainConfig()
+        g = torch.Generator(device=self.dev).manual_seed(seed)
+        cb = get_codebook("nf4")
+        h, v = cfg.hidden, cfg.vocab
+        self.embed = (torch.randn(v, h, device=self.dev, generator=g) * 0.02).to(torch.bfloat16)
+        self.lm_head = (torch.randn(h, v, device=self.dev, generator=g) * 0.02).to(torch.bfloat16)
+        # one flat fp32 buffer each for adapter parameters, gradients, moments;
+        # a flat bf16 buffer for the MMA operand shadows (same layout)
+        names, shapes = [], {}
+        for li in range(cfg.n_layers):
+            for pj in PROJS:
+                a, b = cfg.proj_shape(pj)
+                shapes[f"{li}.{pj}.l1"] = (a, cfg.rank)
+                shapes[f"{li}.{pj}.l2"] = (cfg.rank, b)
+                names += [f"{li}.{pj}.l1", f"{li}.{pj}.l2"]
+        self.names = names
+        self.bucket = GradBucket(shapes, self.dev)          # gradients (all-reduced)
+        pbuf = GradBucket(shapes, self.dev)                 # parameters
+        self.params_flat = pbuf.flat
+        self.params = pbuf.views()
+        self.shadow_flat = torch.zeros(self.params_flat.numel(), dtype=torch.bfloat16, device=self.dev)
+        self.m_flat = torch.zeros_like(self.params_flat)
+        self.v_flat = torch.zeros_like(self.params_flat)
+        self.gviews = self.bucket.views()
+        shadows, off = {}, 0
+        for n in names:
+            k = int(np.prod(shapes[n]))
+            shadows[n] = self.shadow_flat[off: off + k].view(shapes[n])
+            off += k
+        self.layers = []
+        for li in range(cfg.n_layers):
+            lay = {}
+            for pj in PROJS:
+                a, b = cfg.proj_shape(pj)
+                w = torch.randn(a, b, device=self.dev, generator=g) * 0.02
+                q = quantize(w, cb, 64, double_quant=True)
+                del w
+                l1, l2 = self.params[f"{li}.{pj}.l1"], self.params[f"{li}.{pj}.l2"]
+                l1.copy_(torch.randn(a, cfg.rank, device=self.dev, generator=g) / math.sqrt(cfg.rank))
+                l2.zero_()  # lora_init: l2 = 0 (qlora.py:63-80)
+                ad = LoraAdapter(cfg.rank, cfg.alpha, l1, l2)
+                if cfg.rank % 8 == 0:  # the kernels read the shadows in place; Adam refreshes them
+                    s1, s2 = shadows[f"{li}.{pj}.l1"], shadows[f"{li}.{pj}.l2"]
+                    s1.copy_(l1)
+                    s2.copy_(l2)
+                    ad._shadow["ops"] = ((l1.data_ptr(), l2.data_ptr(), cfg.rank), s1, s2)
+                lay[pj] = QLinear(q, [ad])
+                lay[pj + ".g"] = {"adapter0.l1": self.gviews[f"{li}.{pj}.l1"],
+                                  "adapter0.l2": self.gviews[f"{li}.{pj}.l2"]}
+            self.layers.append(lay)
+        d = h // cfg.n_heads
+        inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, d, 2, device=self.dev, dtype=torch.float32) / d))
+        ang = torch.outer(torch.arange(cfg.seq, device=self.dev, dtype=torch.float32), inv)
+        self.cos = torch.cos(ang).to(torch.bfloat16)[None, None]
+        self.sin = torch.sin(ang).to(torch.bfloat16)[None, None]
+        self.anchor = torch.zeros(1, device=self.dev, requires_grad=True)
+        self.t = 0
+        self.hyper_host = torch.zeros(8, dtype=torch.float32).pin_memory()
+        self.hyper = torch.zeros(8, dtype=torch.float32, device=self.dev)
+        self.sumsq = _sumsq_scratch(self.dev)
+
+    # ------------------------------------------------------------------ model
+    def _lin(self, x, lay, pj):
+        return _QLinearFn.apply(x, self.anchor, lay[pj], lay[pj + ".g"])
+
+    def loss(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        cfg = self.cfg
+        b, s = tokens.shape
+        nh, d = cfg.n_heads, cfg.hidden // cfg.n_heads
+        x = F.embedding(tokens, self.embed)
+        for lay in self.layers:
+            hn = _rmsnorm(x, cfg.rms_eps)
+            q = self._lin(hn, lay, "q").view(b, s, nh, d).transpose(1, 2)
+            k = self._lin(hn, lay, "k").view(b, s, nh, d).transpose(1, 2)
+            v = self._lin(hn, lay, "v").view(b, s, nh, d).transpose(1, 2)
+            q, k = _rope(q, self.cos[:, :, :s], self.sin[:, :, :s]), _rope(k, self.cos[:, :, :s], self.sin[:, :, :s])
+            a = F.scaled_dot_product_attention(q, k, v, is_causal=True).transpose(1, 2).reshape(b, s, cfg.hidden)
+            x = x + self._lin(a, lay, "o")
+            hn = _rmsnorm(x, cfg.rms_eps)
+            gt = self._lin(hn, lay, "gate")
+            up = self._lin(hn, lay, "up")
+            x = x + self._lin(F.silu(gt) * up, lay, "down")
+        x = _rmsnorm(x, cfg.rms_eps)
+        logits = x.reshape(b * s, cfg.hidden) @ self.lm_head
+        return F.cross_entropy(logits.float(), targets.reshape(-1))
+
+    # ------------------------------------------------------------------ step
+    def set_step_constants(self) -> None:
+        """Host side of one optimizer step: the numpy-2 float32 constants of
+        the reference update (training.py:426-442) for step t+1, into the
+        pinned buffer the graph copies from."""
+        self.t += 1
+        c = self.train_cfg
+        f = np.float32
+        vals = (c.adam_beta1, 1.0 - c.adam_beta1, c.adam_beta2, 1.0 - c.adam_beta2,
+                1.0 - c.adam_beta1 ** self.t, 1.0 - c.adam_beta2 ** self.t, c.adam_eps, c.learning_rate)
+        self.hyper_host.copy_(torch.tensor([float(f(v)) for v in vals], dtype=torch.float32))
+
+    def train_step(self, tokens: torch.Tensor, targets: torch.Tensor, group=None) -> torch.Tensor:
+        """One QLoRA step (capturable: no host sync).  Call set_step_constants() first."""
+        loss = self.loss(tokens, targets)
+        loss.backward()
+        self.bucket.start(group)
+        self.bucket.finish(group)
+        self.hyper.copy_(self.hyper_host, non_blocking=True)
+        self.sumsq.zero_()
+        L = lib()
+        check(L.qlrt_sumsq_f64(ptr(self.bucket.flat), self.bucket.flat.numel(), ptr(self.sumsq), stream_ptr()),
+              "clip")
+        check(L.qlrt_adam_step_dev(ptr(self.params_flat), ptr(self.bucket.flat), ptr(self.m_flat), ptr(self.v_flat),
+                                   self.params_flat.numel(), ptr(self.hyper), ptr(self.sumsq),
+                                   float(self.train_cfg.max_grad_norm), ptr(self.shadow_flat), stream_ptr()),
+              "adam")
+        return loss.detach()
+
+
+__all__ = ["LlamaConfig", "LlamaQLoRA", "PROJS"]

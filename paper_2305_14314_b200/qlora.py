@@ -30,6 +30,7 @@ from ._native import check, lib, ptr, stream_ptr
 from .blockquant import BlockQuantized, dequantize
 
 PLACEMENTS = ("all_linear", "qv_only", "none")
+_LINEAR_WS: dict = {}
 
 
 def _pad8(r: int) -> int:
@@ -150,11 +151,16 @@ class QLinear:
         return torch.as_tensor(self.base).to(device="cuda", dtype=self.dtype)
 
     def _workspace(self, m: int) -> torch.Tensor:
+        """Scratch of the fused entry points.  Layers share one buffer per
+        device (their launches are stream-ordered); it only grows."""
         r = _pad8(self.adapters[0].rank) if self.adapters else 0
         need = int(lib().qlrt_linear_workspace_bytes(max(m, 1), self.in_dim, self.out_dim, r))
-        if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.zeros(need, dtype=torch.uint8, device="cuda")  # stream-K flags start at 0
-        return self._ws
+        dev = torch.cuda.current_device()
+        ws = _LINEAR_WS.get(dev)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(need, dtype=torch.uint8, device="cuda")  # stream-K flags start at 0
+            _LINEAR_WS[dev] = ws
+        return ws
 
     # -- forward / backward -------------------------------------------------
     def forward(self, x, train: bool = False, rng=None) -> tuple[torch.Tensor, dict[str, Any]]:
@@ -204,7 +210,11 @@ class QLinear:
         cache = {"x": x2, "xa": xa, "ts": ts, "mask": mask, "lead": lead, "consts": consts}
         return y.reshape(*lead, self.out_dim), cache
 
-    def backward(self, d_y, cache: dict[str, Any]) -> tuple[torch.Tensor, dict[str, torch.Tensor]]:
+    def backward(self, d_y, cache: dict[str, Any], grads_out: dict | None = None
+                 ) -> tuple[torch.Tensor, dict[str, torch.Tensor]]:
+        """``grads_out`` optionally names fp32 buffers ([in, rank], [rank, out],
+        e.g. views of a data-parallel gradient bucket) the fused kernels write
+        the adapter gradients into directly."""
         d_y = torch.as_tensor(d_y).to(device="cuda", dtype=self.dtype).reshape(-1, self.out_dim).contiguous()
         m = d_y.shape[0]
         ad = self.adapters[0] if self.adapters else None
@@ -215,8 +225,13 @@ class QLinear:
             rp = _pad8(ad.rank)
             l1b, l2b = ad.bf16_operands()
             dt = torch.empty(m, 2 * rp, dtype=self.dtype, device=d_y.device)  # bf16 hi | lo
-            dl1 = torch.empty(self.in_dim, rp, dtype=torch.float32, device=d_y.device)
-            dl2 = torch.empty(rp, self.out_dim, dtype=torch.float32, device=d_y.device)
+            go = grads_out or {}
+            g1, g2 = go.get("adapter0.l1"), go.get("adapter0.l2")
+            direct = (rp == ad.rank and g1 is not None and g2 is not None and g1.is_contiguous()
+                      and g2.is_contiguous() and g1.dtype == torch.float32 and g2.dtype == torch.float32
+                      and tuple(g1.shape) == (self.in_dim, rp) and tuple(g2.shape) == (rp, self.out_dim))
+            dl1 = g1 if direct else torch.empty(self.in_dim, rp, dtype=torch.float32, device=d_y.device)
+            dl2 = g2 if direct else torch.empty(rp, self.out_dim, dtype=torch.float32, device=d_y.device)
         if self.fused() and mask is None:
             if ad is None:
                 check(lib().qlrt_nf4_linear_bwd(self.weight_desc(cache.get("consts")), ptr(d_y), m, None, None, None, None, 0, 0.0,
@@ -250,6 +265,11 @@ class QLinear:
         if ad is not None:
             grads["adapter0.l1"] = dl1[:, : ad.rank]
             grads["adapter0.l2"] = dl2[: ad.rank]
+            if grads_out and not direct:
+                for k in ("adapter0.l1", "adapter0.l2"):
+                    if grads_out.get(k) is not None:
+                        grads_out[k].copy_(grads[k])
+                        grads[k] = grads_out[k]
         return d_x.reshape(*cache["lead"], self.in_dim), grads
 
     def trainable(self) -> dict[str, torch.Tensor]:

@@ -357,6 +357,17 @@ def main() -> None:
     extras = {}
     if not args.no_extras:
         extras = secondary(qb, torch, dev, flush, stream, hbm)
+        # C3: LLaMA-7B-shape QLoRA finetune step on this GPU (tokens/s), whole step in one CUDA graph
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from bench_c3 import run as run_c3
+            c3 = run_c3("7b", batch=4, steps=10)
+            c3["roofline_tokens_per_s"] = tf_burst * 1e12 / c3["flops_per_token"]
+            c3["note"] = ("32 layers h4096 ffn11008 vocab32000, seq 512 x 4, all 7 linears NF4+DQ with LoRA r=64; "
+                          "random-init weights, synthetic tokens; fwd+bwd+grad all-reduce+clip+Adam per step")
+            extras["c3_llama7b_qlora_step"] = c3
+        except Exception as e:  # pragma: no cover
+            extras["c3_llama7b_qlora_step"] = {"error": repr(e)}
 
     line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",

@@ -70,6 +70,11 @@ struct Args {
   int streamk;
   float* sk_ws;         // [gridDim.x][BM][BN] fp32 partials (one per CTA)
   int* sk_flags;        // [gridDim.x]; 0 between launches (owners re-arm what they consume), 1 = partial ready
+  // cluster split-K (plain GEMMs): a cluster of csplit CTAs shares one tile,
+  // CTA rank z owns k-split z; ranks > 0 stage their fp32 partial in their own
+  // shared memory and rank 0 sums them over DSMEM in rank order -- no
+  // workspace round trip, no reduce launch
+  int csplit;
 };
 
 template <int BN, bool NF4, bool PAIR = false>
@@ -189,7 +194,7 @@ __device__ __forceinline__ void lookup8(uint32_t w, const uint32_t (&L)[4], cons
 template <int EC>
 __device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[EC], int64_t m, int64_t n0, int z) {
   const bool full_chunk = n0 + EC <= p.N;
-  if (p.splits > 1 || p.to_ws) {
+  if ((p.splits > 1 && !p.csplit) || p.to_ws) {
     float* dst = p.ws + ((int64_t)z * p.M + m) * p.N + n0;
     if (full_chunk && (p.N & 3) == 0) {
 #pragma unroll
@@ -288,19 +293,27 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
   uint64_t* tfull = cempty + L::CST;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* pready = tempty + 3;  // cluster split-K: peers' partials staged (rank 0)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
   const bool leader = rank == 0;
-  // work unit = one (pair) tile; a cluster walks the tile list
-  const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int n_units = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const bool csplit = !NF4 && !PAIR && p.csplit > 1;
+  const uint32_t zrank = csplit ? ptx::cluster_ctarank() : 0u;  // k-split of this CTA (cluster split-K)
+  // work unit = one (pair) tile; a cluster walks the tile list.  Cluster
+  // split-K: one (tile, split) per CTA, t = z * tiles + tile
+  int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  int n_units = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   const int m_tiles = (p.M + BMP - 1) / BMP;
   const int n_tiles = (p.N + BN - 1) / BN;
   const int n_tiles_total = m_tiles * n_tiles * p.splits;
   const int kc = (p.k_iters + p.splits - 1) / p.splits;
+  if (csplit) {
+    unit0 = (int)zrank * (m_tiles * n_tiles) + (int)(blockIdx.x / p.csplit);
+    n_units = n_tiles_total;  // exactly one segment per CTA
+  }
   constexpr uint32_t kNTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
   // iterations of a whole tile (stream-K needs splits == 1)
   const int T_tile = p.streamk ? p.k_iters + p.k_iters_aug : (1 << 30);
@@ -329,6 +342,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], (PAIR ? 2 : 1) * kNumEpiWarps);  // one lane per epilogue warp
     }
+    if (csplit) ptx::mbar_init(pready, (uint32_t)(p.csplit - 1) * kNumEpiWarps);
     ptx::fence_mbar_init();
   }
   if (warp == kMmaWarp) {
@@ -337,7 +351,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (PAIR) ptx::cluster_sync();  // peer barriers initialised before any remote arrive
+  if (PAIR || csplit) ptx::cluster_sync();  // peer barriers initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -517,6 +531,45 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           }
         }
       };
+      // cluster split-K: rank 0 adds ranks 1.. (their smem, [c/4][row][4] fp32) in rank order
+      auto add_peers = [&](int c, uint32_t (&r)[EC]) {
+        for (int zz = 1; zz < p.csplit; ++zz) {
+          const uint32_t base = ptx::mapa_shared(ptx::smem_u32(sA), (uint32_t)zz) + (uint32_t)((c * BM + row * 4) * 4);
+#pragma unroll
+          for (int j = 0; j < EC; j += 4) {
+            float4 w4;
+            asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(w4.x), "=f"(w4.y), "=f"(w4.z), "=f"(w4.w)
+                         : "r"(base + (uint32_t)(j * BM * 4)));
+            r[j] = __float_as_uint(__uint_as_float(r[j]) + w4.x);
+            r[j + 1] = __float_as_uint(__uint_as_float(r[j + 1]) + w4.y);
+            r[j + 2] = __float_as_uint(__uint_as_float(r[j + 2]) + w4.z);
+            r[j + 3] = __float_as_uint(__uint_as_float(r[j + 3]) + w4.w);
+          }
+        }
+      };
+      if (csplit && zrank != 0) {  // stage this split's accumulator, signal rank 0, done
+        float* st = reinterpret_cast<float*>(sA);
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += EC) {
+          uint32_t r[EC];
+          ptx::tmem_ld<EC>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, r);
+#pragma unroll
+          for (int j = 0; j < EC; j += 4)
+            *reinterpret_cast<float4*>(st + (c0 + j) * BM + row * 4) =
+                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                            __uint_as_float(r[j + 3]));
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];"
+                       ::"r"(ptx::mapa_shared(ptx::smem_u32(pready), 0)) : "memory");
+          arrive_leader(&tempty[acc]);
+        }
+        continue;
+      }
+      if (csplit) ptx::mbar_wait_cluster(pready, 0);
       auto store_partial = [&](int c, const uint32_t (&r)[EC]) {
         float* dst = p.sk_ws + (size_t)blockIdx.x * BM * BN + (size_t)c * BM + row * 4;
 #pragma unroll
@@ -526,7 +579,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
       };
       // fold (hi/lo operand pairs, fold <= BN / 2, one column tile): out column
       // n = D[:, n] + D[:, n + fold]
-      const bool direct_fold = p.fold && !(p.splits > 1 || p.to_ws);  // else the reduce kernel folds
+      const bool direct_fold = p.fold && !((p.splits > 1 && !p.csplit) || p.to_ws);  // else the reduce kernel folds
       const int cend = direct_fold ? p.fold : BN;
 #pragma unroll 1
       for (int c0 = 0; c0 < cend; c0 += EC) {
@@ -541,9 +594,11 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           continue;
         }
         load_acc(c0, r);
+        if (csplit) add_peers(c0, r);
         if (direct_fold) {
           uint32_t r2[EC];
           load_acc(c0 + p.fold, r2);
+          if (csplit) add_peers(c0 + p.fold, r2);
 #pragma unroll
           for (int j = 0; j < EC; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
         }
@@ -707,7 +762,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (PAIR) ptx::cluster_sync();
+  if (PAIR || csplit) ptx::cluster_sync();  // (split-K: peers stay alive until rank 0 has read them)
   if (warp == kMmaWarp) {
     ptx::tc_fence_after();
     if (PAIR) ptx::tmem_dealloc_pair(tmem_base, kNTmemCols);
@@ -867,6 +922,15 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
   cfg.dynamicSmemBytes = L::BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attrs[1];
+  if (!PAIR && !NF4 && args.csplit > 1) {  // one CTA per (tile, split), clusters of csplit
+    cfg.gridDim = dim3(m_tiles * n_tiles * args.csplit);
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = args.csplit;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+  }
   if (PAIR) {
     attrs[0].id = cudaLaunchAttributeClusterDimension;
     attrs[0].val.clusterDim.x = 2;
@@ -928,6 +992,7 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   args.a2_mn = A2 ? A2->mn : 0;
   args.b2_mn = B2 ? B2->mn : 0;
   args.splits = effective_splits(args.splits, args.k_iters);
+  if (args.csplit > 1) args.csplit = args.splits;  // every CTA of the cluster owns >= 1 k-iteration
   if (args.splits > 1 && K2) return QLRT_ERR_UNSUPPORTED;
   if (args.sk_ws && args.splits == 1 && bn >= 64 && num_sms() <= kNumSMs) {
     // stream-K only for short grids (< 2 waves) that whole-tile waves would
@@ -1008,6 +1073,22 @@ static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, 
     a.splits = 1;
     a.to_ws = 0;
     return run(bn, A, B, nullptr, nullptr, K, 0, a, s);
+  }
+  // cluster split-K for short grids: partials reduced over DSMEM inside the
+  // kernel.  Off by default (QLRT_CSPLIT=1 enables it): measured 1.7-2.9x
+  // slower than split-K + the reduce kernel on the C2 LoRA shapes
+  // (tools/ab_skinny.py) -- clusters of 1-CTA-per-SM kernels co-schedule poorly
+  const char* e_cs = getenv("QLRT_CSPLIT");
+  if (e_cs && atoi(e_cs) && tiles < 74 && !(out_split && out_t) && bn <= 256 && a.pair == 0 &&
+      (!fold || (2 * fold <= bn && N <= bn))) {
+    int S = 1;
+    while (S < 8 && tiles * (S + 1) <= num_sms() && (S + 1) * 4 <= kit) ++S;
+    if (S >= 2) {
+      a.splits = S;
+      a.csplit = S;
+      a.to_ws = 0;
+      return run(bn, A, B, nullptr, nullptr, K, 0, a, s);
+    }
   }
   a.splits = effective_splits(ws ? pick_splits(tiles, kit, M * N * 4, ws_bytes) : 1, (int)kit);
   a.to_ws = fold != 0 || (out_split && out_t);

@@ -1,4 +1,4 @@
-"""A/B the skinny LoRA GEMM shapes of one QLinear step (C2) with stream-K on/off."""
+"""A/B the skinny LoRA GEMM shapes of one QLinear step (C2): env variants, per-launch time."""
 import os
 import sys
 
@@ -20,17 +20,16 @@ cases = {
     "dl2^T = dY^T Ts (11008x128x2048)": lambda: qb.gemm_bf16(dy, ts, a_t=True, out_dtype=torch.float32),
     "dl1 = X^T dT   (4096x128x2048)": lambda: qb.gemm_bf16(x, ts, a_t=True, out_dtype=torch.float32),
 }
+variants = sys.argv[1:] or ["QLRT_CSPLIT=0", "QLRT_CSPLIT=1"]
 for name, fn in cases.items():
+    ref = None
     row = []
-    for sk in ("0", "1", "0", "1"):
-        os.environ["QLRT_STREAMK"] = sk
-        row.append(timed([fn], n=20) * 1e3)
-    print(f"{name}: sk0 {min(row[0], row[2]):6.1f} us   sk1 {min(row[1], row[3]):6.1f} us")
-
-# back-to-back launches in one graph (no flush between): per-launch cost
-for name, fn in cases.items():
-    row = []
-    for sk in ("0", "1"):
-        os.environ["QLRT_STREAMK"] = sk
-        row.append(timed([fn] * 10, n=10) * 1e3 / 10)
-    print(f"x10 {name}: sk0 {row[0]:6.1f} us   sk1 {row[1]:6.1f} us")
+    for v in variants:
+        kk, vv = v.split("=")
+        os.environ[kk] = vv
+        out = fn().clone()
+        if ref is None:
+            ref = out
+        err = ((out - ref).abs().max() / ref.abs().max()).item()
+        row.append((timed([fn] * 10, n=10) * 1e3 / 10, err))
+    print(f"{name}: " + "   ".join(f"{v} {t:6.1f} us (rel {e:.1e})" for v, (t, e) in zip(variants, row)))

@@ -106,14 +106,14 @@ class _QLinearFn(torch.autograd.Function):
 
 
 def _rmsnorm(x: torch.Tensor, eps: float) -> torch.Tensor:
-    xf = x.float()
-    return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)).to(x.dtype)
+    return F.rms_norm(x.float(), (x.shape[-1],), eps=eps).to(x.dtype)
 
 
-def _rope(t: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
-    h = t.shape[-1] // 2
-    t1, t2 = t[..., :h], t[..., h:]
-    return torch.cat((t1 * cos - t2 * sin, t2 * cos + t1 * sin), dim=-1)
+def _rope(t: torch.Tensor, freqs: torch.Tensor) -> torch.Tensor:
+    """Rotary embedding on [b, s, heads, d] (contiguous) as one complex multiply
+    over adjacent pairs; freqs = exp(i theta) as complex64 [s, d/2]."""
+    tc = torch.view_as_complex(t.float().reshape(*t.shape[:-1], -1, 2))
+    return torch.view_as_real(tc * freqs[None, :, None, :]).flatten(-2).to(t.dtype)
 
 
 class LlamaQLoRA:
@@ -175,8 +175,7 @@ class LlamaQLoRA:
         d = h // cfg.n_heads
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, d, 2, device=self.dev, dtype=torch.float32) / d))
         ang = torch.outer(torch.arange(cfg.seq, device=self.dev, dtype=torch.float32), inv)
-        self.cos = torch.cos(ang).to(torch.bfloat16)[None, None]
-        self.sin = torch.sin(ang).to(torch.bfloat16)[None, None]
+        self.freqs = torch.polar(torch.ones_like(ang), ang)  # complex64 [seq, d/2]
         self.anchor = torch.zeros(1, device=self.dev, requires_grad=True)
         self.t = 0
         self.hyper_host = torch.zeros(8, dtype=torch.float32).pin_memory()
@@ -194,10 +193,10 @@ class LlamaQLoRA:
         x = F.embedding(tokens, self.embed)
         for lay in self.layers:
             hn = _rmsnorm(x, cfg.rms_eps)
-            q = self._lin(hn, lay, "q").view(b, s, nh, d).transpose(1, 2)
-            k = self._lin(hn, lay, "k").view(b, s, nh, d).transpose(1, 2)
+            fr = self.freqs[:s]
+            q = _rope(self._lin(hn, lay, "q").view(b, s, nh, d), fr).transpose(1, 2)
+            k = _rope(self._lin(hn, lay, "k").view(b, s, nh, d), fr).transpose(1, 2)
             v = self._lin(hn, lay, "v").view(b, s, nh, d).transpose(1, 2)
-            q, k = _rope(q, self.cos[:, :, :s], self.sin[:, :, :s]), _rope(k, self.cos[:, :, :s], self.sin[:, :, :s])
             a = F.scaled_dot_product_attention(q, k, v, is_causal=True).transpose(1, 2).reshape(b, s, cfg.hidden)
             x = x + self._lin(a, lay, "o")
             hn = _rmsnorm(x, cfg.rms_eps)

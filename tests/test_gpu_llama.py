@@ -39,13 +39,12 @@ def _reference_grads(model, tokens, targets):
         return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + cfg.rms_eps)
 
     x = F.embedding(tokens, model.embed.float())
-    cos, sin = model.cos.float()[:, :, :s], model.sin.float()[:, :, :s]
+    fr = model.freqs[:s]
     for li in range(cfg.n_layers):
         hn = rms(x)
-        q = lin(hn, li, "q").view(b, s, nh, d).transpose(1, 2)
-        k = lin(hn, li, "k").view(b, s, nh, d).transpose(1, 2)
+        q = _rope(lin(hn, li, "q").view(b, s, nh, d), fr).transpose(1, 2)
+        k = _rope(lin(hn, li, "k").view(b, s, nh, d), fr).transpose(1, 2)
         v = lin(hn, li, "v").view(b, s, nh, d).transpose(1, 2)
-        q, k = _rope(q, cos, sin), _rope(k, cos, sin)
         a = F.scaled_dot_product_attention(q, k, v, is_causal=True).transpose(1, 2).reshape(b, s, cfg.hidden)
         x = x + lin(a, li, "o")
         hn = rms(x)

@@ -121,8 +121,9 @@ __device__ void build_bin_tables(BinTables& T, const qlrt_codebook4& cb) {
   const int n = cb.n_mids;
   for (int b = threadIdx.x; b < NBIN; b += blockDim.x) {
     const float qb = -1.0f + 2.0f * (float)b / (float)NBIN;  // bin start (exact)
-    int base = 0;
-    while (base < n && cb.hi[base] <= qb) ++base;
+    int base = 0;  // #{hi[i] <= qb}: hi ascending, unrolled (constant-bank operands)
+#pragma unroll
+    for (int i = 0; i < 15; ++i) base += (i < n && cb.hi[i] <= qb) ? 1 : 0;
     T.bin[b] = make_float2(__int_as_float(base), base < n ? cb.lo[base] : __int_as_float(0x7f800000));
   }
   if (threadIdx.x < 16) {
@@ -155,6 +156,110 @@ __device__ __forceinline__ unsigned bin_code(V x, float r, float c, const BinTab
   const float2 bd = t.bound[j];
   if (!(q >= bd.x && q <= bd.y)) return exact_code_t((double)x, c, t);
   return j;
+}
+
+// fast-path code of one element; clears ok when q lies inside a midpoint
+// bracket or on a bin-edge rounding case (the caller then redoes the group)
+template <typename V>
+__device__ __forceinline__ unsigned bin_j(V x, float r, const BinTables& t, bool& ok) {
+  const float q = (float)x * r;
+  int b = __float2int_rd(fmaf(q, 0.5f * NBIN, 0.5f * NBIN));
+  b = min(max(b, 0), NBIN - 1);
+  const float2 e = t.bin[b];
+  const unsigned j = (unsigned)__float_as_int(e.x) + (q > e.y ? 1u : 0u);
+  const float2 bd = t.bound[j];
+  ok = ok && (q >= bd.x) && (q <= bd.y);
+  return j;
+}
+
+template <typename T>
+__device__ __forceinline__ void load8_stream(const T* __restrict__ x, int64_t i, float (&v)[8]);
+template <>
+__device__ __forceinline__ void load8_stream<float>(const float* __restrict__ x, int64_t i, float (&v)[8]) {
+  uint32_t u[8];
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7])
+               : "l"(x + i));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(u[j]);
+}
+template <>
+__device__ __forceinline__ void load8_stream<__nv_bfloat16>(const __nv_bfloat16* __restrict__ x, int64_t i,
+                                                            float (&v)[8]) {
+  uint4 a;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w)
+               : "l"(x + i));
+  const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    v[2 * j] = __uint_as_float(w[j] << 16);
+    v[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+  }
+}
+
+// Phase A, fp32 / bf16 input, blocksize 64, n % 64 == 0 (whole blocks): the
+// streaming version.  8 lanes per block as below, a persistent grid, the next
+// group's 32 B (fp32: one 256-bit load) in flight while the current one is
+// coded, and a branch-free fast path per element with one group-wide check
+// (bracket hits are re-decided exactly, rarely).
+template <typename T>
+__global__ void __launch_bounds__(256, 3) quantize64_stream_kernel(const T* __restrict__ x, int64_t n_groups,
+                                                                qlrt_codebook4 cb, uint32_t* __restrict__ codes,
+                                                                float* __restrict__ absmax,
+                                                                unsigned long long* __restrict__ first_bad) {
+  __shared__ BinTables t;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float nv[8];  // the next group's values in flight
+  if (g < n_groups) load8_stream<T>(x, g * 8, nv);
+  build_bin_tables(t, cb);
+  __syncthreads();
+  const unsigned pad = (unsigned)cb.pad_code;
+  // n_groups % 8 == 0 and stride % 8 == 0: 8-lane groups are all-in or all-out,
+  // and the trip count is warp-uniform (the shuffles need every lane)
+  for (int64_t gb = g - lane; gb < n_groups; gb += stride, g += stride) {
+    const bool act = g < n_groups;
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = act ? nv[j] : 0.0f;
+    if (g + stride < n_groups) load8_stream<T>(x, (g + stride) * 8, nv);
+    unsigned mb = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) mb = max(mb, __float_as_uint(v[j]) & 0x7FFFFFFFu);
+    if (mb >= 0x7F800000u) {  // inf / NaN: first bad flat index
+      unsigned long long bad = ~0ull;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if ((__float_as_uint(v[j]) & 0x7FFFFFFFu) >= 0x7F800000u) bad = min(bad, (unsigned long long)(g * 8 + j));
+      atomicMin(first_bad, bad);
+    }
+    mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 1));
+    mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 2));
+    mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 4));
+    if (!act) continue;
+    const float c = __uint_as_float(mb);
+    uint32_t word;
+    if (c > 0.0f) {
+      const float r = __frcp_rn(c);
+      bool ok = r <= 3.402823466e38f;  // subnormal c: 1/c overflows -> exact path
+      word = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) word |= bin_j(v[j], r, t, ok) << (4 * j);
+      if (!ok) {
+        const bool fast_ok = r <= 3.402823466e38f;
+        word = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          word |= (fast_ok ? bin_code(v[j], r, c, t) : exact_code_t((double)v[j], c, t)) << (4 * j);
+      }
+    } else {
+      word = pad * 0x11111111u;
+    }
+    codes[g] = word;
+    if ((threadIdx.x & 7) == 0) absmax[g >> 3] = c;
+  }
 }
 
 // Phase A, blocksize 64: 8 consecutive lanes own one 64-block, 8 elements
@@ -359,58 +464,80 @@ __device__ double pairwise_seq(const float* a, int n) {
   }
 }
 
-// One CTA (64 threads) per 8192-constant buffer chunk.  A full chunk is a
-// perfect pairwise tree of 64 leaves of 128 (8 strided accumulators each).
-__global__ void __launch_bounds__(64) dq_chunk_sums_kernel(const float* __restrict__ c,
-                                                           int64_t nb,
-                                                           double* __restrict__ chunk_sums) {
+// One CTA (512 threads) per 8192-constant buffer chunk.  A full chunk is a
+// perfect pairwise tree of 64 leaves of 128; leaf accumulator j of leaf L is
+// a[128L + j] + a[128L + j + 8] + ... (16 terms, in order) -- one thread each
+// -- and the 8 accumulators combine as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
+// by xor-shuffles (IEEE addition is commutative, so both partners hold the
+// same value).  The last CTA to finish adds the chunk sums in order from 0.0
+// and writes mu = f32(sum / nb) (doublequant.py:164-166).
+__global__ void __launch_bounds__(512) dq_chunk_sums_kernel(const float* __restrict__ c, int64_t nb,
+                                                            double* __restrict__ chunk_sums,
+                                                            unsigned* __restrict__ ticket,
+                                                            float* __restrict__ mu_out) {
   __shared__ double leaf[64];
+  __shared__ bool last;
   const int64_t base = (int64_t)blockIdx.x * 8192;
   const int len = (int)min((int64_t)8192, nb - base);
   if (len < 8192) {
     if (threadIdx.x == 0) chunk_sums[blockIdx.x] = pairwise_seq(c + base, len);
-    return;
+  } else {
+    const int L = threadIdx.x >> 3, j = threadIdx.x & 7;
+    const float* a = c + base + L * 128 + j;
+    float w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = __ldg(a + 8 * i);
+    double r = (double)w[0];
+#pragma unroll
+    for (int i = 1; i < 16; ++i) r = __dadd_rn(r, (double)w[i]);
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    if (j == 0) leaf[L] = r;
+    __syncthreads();
+    for (int w2 = 32; w2 >= 1; w2 >>= 1) {
+      double sv = 0.0;
+      if (threadIdx.x < w2) sv = __dadd_rn(leaf[2 * threadIdx.x], leaf[2 * threadIdx.x + 1]);
+      __syncthreads();
+      if (threadIdx.x < w2) leaf[threadIdx.x] = sv;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) chunk_sums[blockIdx.x] = leaf[0];
   }
-  const float* a = c + base + threadIdx.x * 128;
-  double r[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = (double)a[j];
-  for (int i = 8; i < 128; i += 8)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], (double)a[i + j]);
-  leaf[threadIdx.x] = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                                __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
   __syncthreads();
-  for (int w = 32; w >= 1; w >>= 1) {
-    double s = 0.0;
-    if (threadIdx.x < w) s = __dadd_rn(leaf[2 * threadIdx.x], leaf[2 * threadIdx.x + 1]);
+  if (!last) return;
+  __threadfence();
+  // the chunk sums in parallel into shared memory, then added in order
+  __shared__ double cs[512];
+  double acc = 0.0;
+  for (unsigned b = 0; b < gridDim.x; b += 512) {
     __syncthreads();
-    if (threadIdx.x < w) leaf[threadIdx.x] = s;
+    if (b + threadIdx.x < gridDim.x) cs[threadIdx.x] = __ldcg(chunk_sums + b + threadIdx.x);
     __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned e = min(512u, gridDim.x - b);
+      for (unsigned i = 0; i < e; ++i) acc = __dadd_rn(acc, cs[i]);
+    }
   }
-  if (threadIdx.x == 0) chunk_sums[blockIdx.x] = leaf[0];
+  if (threadIdx.x == 0) {
+    *mu_out = __double2float_rn(__ddiv_rn(acc, (double)nb));
+    *ticket = 0u;  // re-armed for the next call
+  }
 }
 
-// One CTA per second-level block: mu from the chunk sums (added in order
-// from 0.0, then / nb in fp64, then f32), centring, fp64 absmax,
-// c1 = f32(A / max), codes = encode(centered / f64(c1)).
+// One CTA per second-level block: centring by mu, fp64 absmax, c1 = f32(A / max),
+// codes = encode(centered / f64(c1))  (doublequant.py:167-186).
 __global__ void __launch_bounds__(256) dq_encode_kernel(const float* __restrict__ c, int64_t nb,
-                                                        int bs2, int64_t n_chunks,
-                                                        const double* __restrict__ chunk_sums,
-                                                        qlrt_fp8spec sp, float* __restrict__ mu_out,
+                                                        int bs2, const float* __restrict__ mu_in,
+                                                        qlrt_fp8spec sp,
                                                         float* __restrict__ c1,
                                                         uint8_t* __restrict__ codes) {
-  __shared__ double s_mu;
   __shared__ double s_red[8];
-  if (threadIdx.x == 0) {
-    double acc = 0.0;
-    for (int64_t i = 0; i < n_chunks; ++i) acc = __dadd_rn(acc, chunk_sums[i]);
-    float mu = __double2float_rn(__ddiv_rn(acc, (double)nb));
-    s_mu = (double)mu;
-    if (blockIdx.x == 0) *mu_out = mu;
-  }
-  __syncthreads();
-  const double mu = s_mu;
+  const double mu = (double)*mu_in;
   const int64_t b0 = (int64_t)blockIdx.x * bs2;
   const int64_t b1 = min(b0 + bs2, nb);
   double amax = 0.0;
@@ -782,7 +909,18 @@ qlrt_status qlrt_quantize4(const void* x, int x_dtype, int64_t n, int blocksize,
   if (cudaMemsetAsync(first_bad, 0x7F, 8, s) != cudaSuccess) return QLRT_ERR_CUDA;
   auto* fb = reinterpret_cast<unsigned long long*>(first_bad);
   const bool aligned = (((uintptr_t)x) & 15) == 0 && (((uintptr_t)codes) & 3) == 0;
-  if (blocksize == 64 && aligned) {
+  const bool aligned32 = (((uintptr_t)x) & 31) == 0 && (((uintptr_t)codes) & 3) == 0;
+  if (blocksize == 64 && n % 64 == 0 && aligned32 && (x_dtype == QLRT_F32 || x_dtype == QLRT_BF16)) {
+    const int64_t n_groups = nb * 8;
+    const int64_t want = cdiv(n_groups, 256);
+    const int grid = (int)(want < (int64_t)kNumSMs * 3 ? want : (int64_t)kNumSMs * 3);  // 3 x 256 resident / SM
+    if (x_dtype == QLRT_F32)
+      quantize64_stream_kernel<float><<<grid, 256, 0, s>>>((const float*)x, n_groups, *cb, (uint32_t*)codes, absmax,
+                                                          fb);
+    else
+      quantize64_stream_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, n_groups, *cb,
+                                                                  (uint32_t*)codes, absmax, fb);
+  } else if (blocksize == 64 && aligned) {
     const int64_t n_groups = nb * 8;
     const int grid = grid_for(n_groups, 256, 8);
     if (x_dtype == QLRT_F32)
@@ -812,7 +950,8 @@ qlrt_status qlrt_quantize4(const void* x, int x_dtype, int64_t n, int blocksize,
   return QLRT_OK;
 }
 
-size_t qlrt_dq_workspace_bytes(int64_t nb) { return (size_t)cdiv(nb, 8192) * sizeof(double); }
+// chunk sums + the ticket of the last-CTA mu reduction (zeroed per call)
+size_t qlrt_dq_workspace_bytes(int64_t nb) { return (size_t)cdiv(nb, 8192) * sizeof(double) + 16; }
 
 qlrt_status qlrt_dq_compress(const float* absmax, int64_t nb, int blocksize2, qlrt_fp8spec spec,
                              void* workspace, float* mu, float* c1, uint8_t* dq_codes,
@@ -823,10 +962,11 @@ qlrt_status qlrt_dq_compress(const float* absmax, int64_t nb, int blocksize2, ql
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n_chunks = cdiv(nb, 8192);
   double* sums = (double*)workspace;
-  dq_chunk_sums_kernel<<<(unsigned)n_chunks, 64, 0, s>>>(absmax, nb, sums);
+  unsigned* ticket = (unsigned*)(sums + n_chunks);
+  if (cudaMemsetAsync(ticket, 0, sizeof(unsigned), s) != cudaSuccess) return QLRT_ERR_CUDA;
+  dq_chunk_sums_kernel<<<(unsigned)n_chunks, 512, 0, s>>>(absmax, nb, sums, ticket, mu);
   const int64_t n2 = cdiv(nb, blocksize2);
-  dq_encode_kernel<<<(unsigned)n2, 256, 0, s>>>(absmax, nb, blocksize2, n_chunks, sums, spec, mu,
-                                                c1, dq_codes);
+  dq_encode_kernel<<<(unsigned)n2, 256, 0, s>>>(absmax, nb, blocksize2, mu, spec, c1, dq_codes);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }

@@ -32,7 +32,7 @@ def test_library_exports_every_header_symbol():
 def test_workspace_queries_are_host_only():
     from paper_2305_14314_b200 import _native
     lib = _native.load_library()
-    assert lib.qlrt_dq_workspace_bytes(262144) == 32 * 8
+    assert lib.qlrt_dq_workspace_bytes(262144) == 32 * 8 + 16  # chunk sums + mu ticket
     assert lib.qlrt_linear_workspace_bytes(2048, 4096, 11008, 64) >= 16 * 2048 * 64 * 4
 
 

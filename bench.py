@@ -284,33 +284,68 @@ def main() -> None:
     step_flops = flops_fwd() + flops_bwd()
     value = world * step_flops * args.steps / (ms / 1e3) / 1e12
 
-    # ---- e2e through the public API with pinned host buffers
+    # ---- e2e through the public API with pinned host buffers: every step copies
+    # its X, dY in (pinned -> device) and dX, dl1, dl2 out (device -> pinned).
+    # Copies run on a side stream, double-buffered, so step i+1's inputs cross
+    # PCIe while step i computes (the compute stream waits on per-buffer events).
     xh = x.cpu().pin_memory()
     dyh = dy.cpu().pin_memory()
     dxh = torch.empty(M_TOK, K_IN, dtype=torch.bfloat16).pin_memory()
     g1h = torch.empty(K_IN, RANK).pin_memory()
     g2h = torch.empty(RANK, N_OUT).pin_memory()
-    e_steps = max(3, args.steps // 2)
+    e_steps = max(4, args.steps // 2)
+    xin = [torch.empty_like(x) for _ in range(2)]
+    dyin = [torch.empty_like(dy) for _ in range(2)]
+    cstream = torch.cuda.Stream(dev)
+    h2d_done = [torch.cuda.Event() for _ in range(2)]
+    used = [torch.cuda.Event() for _ in range(2)]
+    out_ready = torch.cuda.Event()
+
+    def h2d(i):
+        j = i % 2
+        with torch.cuda.stream(cstream):
+            cstream.wait_event(used[j])  # the compute of step i-2 is done with buffer j
+            xin[j].copy_(xh, non_blocking=True)
+            dyin[j].copy_(dyh, non_blocking=True)
+            h2d_done[j].record(cstream)
+
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0.record(stream)
-    for _ in range(e_steps):
-        xd = xh.to(dev, non_blocking=True)
-        dyd = dyh.to(dev, non_blocking=True)
-        _, dx, grads = step(xd, dyd)
-        dxh.copy_(dx, non_blocking=True)
-        g1h.copy_(grads["adapter0.l1"], non_blocking=True)
-        g2h.copy_(grads["adapter0.l2"], non_blocking=True)
+    cstream.wait_event(ev0)
+    h2d(0)
+    for i in range(e_steps):
+        if i + 1 < e_steps:
+            h2d(i + 1)
+        j = i % 2
+        stream.wait_event(h2d_done[j])
+        _, dx, grads = step(xin[j], dyin[j])
+        used[j].record(stream)
+        out_ready.record(stream)
+        with torch.cuda.stream(cstream):
+            cstream.wait_event(out_ready)
+            dxh.copy_(dx, non_blocking=True)
+            g1h.copy_(grads["adapter0.l1"], non_blocking=True)
+            g2h.copy_(grads["adapter0.l2"], non_blocking=True)
+    stream.wait_stream(cstream)
     ev1.record(stream)
     torch.cuda.synchronize()
     e_ms = torch.tensor([ev0.elapsed_time(ev1)], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
     e2e = world * step_flops * e_steps / (float(e_ms.item()) / 1e3) / 1e12
-    h2d = xh.numel() * 2 + dyh.numel() * 2
+    h2d_bytes = xh.numel() * 2 + dyh.numel() * 2
     d2h = dxh.numel() * 2 + g1h.numel() * 4 + g2h.numel() * 4
+    # pinned H2D bandwidth of this box (context for e2e)
+    ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ta.record(stream)
+    for _ in range(3):
+        dyin[0].copy_(dyh, non_blocking=True)
+    tb.record(stream)
+    torch.cuda.synchronize()
+    h2d_gbs = 3 * dyh.numel() * 2 / (ta.elapsed_time(tb) / 1e3) / 1e9
 
     # ---- roofline of the dominant kernel: the fused NF4 dequant-GEMM (forward
     # main GEMM, 2*M*K*N FLOPs per launch), launched alone through the C ABI
@@ -377,8 +412,10 @@ def main() -> None:
                        "tokens_per_gpu": M_TOK, "flops_per_step_per_gpu": step_flops,
                        "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) before every timed step"},
             "tokens_per_s": world * M_TOK * args.steps / (ms / 1e3),
-            "e2e": {"value": e2e, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "steps": e_steps},
+            "e2e": {"value": e2e, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h,
+                    "steps": e_steps, "pinned_h2d_gbs": h2d_gbs,
+                    "note": "QLinear.forward/backward from pinned host X, dY; dX, dl1, dl2 back to pinned host; "
+                            "copies double-buffered on a side stream"},
             "roofline": roofline,
             "gpu_launches": (launches_per_step * args.steps) if launches_per_step else None,
             "gpu_launches_per_step": launches_per_step,

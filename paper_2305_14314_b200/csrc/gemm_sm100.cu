@@ -75,6 +75,10 @@ struct Args {
   // shared memory and rank 0 sums them over DSMEM in rank order -- no
   // workspace round trip, no reduce launch
   int csplit;
+  // NF4, 1-SM MMAs: a 2-CTA cluster works on the same W rows and two adjacent
+  // token tiles; each CTA decodes half of every A stage into both CTAs' shared
+  // memory (DSMEM stores), halving the per-SM dequant work
+  int share;
 };
 
 template <int BN, bool NF4, bool PAIR = false>
@@ -300,14 +304,17 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
   const uint32_t rank = PAIR ? ptx::cluster_ctarank() : 0u;
   const bool leader = rank == 0;
   const bool csplit = !NF4 && !PAIR && p.csplit > 1;
+  const bool share = NF4 && !PAIR && p.share;
+  const uint32_t srank = share ? ptx::cluster_ctarank() : 0u;  // token-tile half of the shared-decode pair
   const uint32_t zrank = csplit ? ptx::cluster_ctarank() : 0u;  // k-split of this CTA (cluster split-K)
   // work unit = one (pair) tile; a cluster walks the tile list.  Cluster
   // split-K: one (tile, split) per CTA, t = z * tiles + tile
-  int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  int n_units = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  int unit0 = (PAIR || share) ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  int n_units = (PAIR || share) ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   const int m_tiles = (p.M + BMP - 1) / BMP;
-  const int n_tiles = (p.N + BN - 1) / BN;
+  const int n_tiles_real = (p.N + BN - 1) / BN;
+  const int n_tiles = share ? (n_tiles_real + 1) / 2 : n_tiles_real;  // scheduling grid (pairs of token tiles)
   const int n_tiles_total = m_tiles * n_tiles * p.splits;
   const int kc = (p.k_iters + p.splits - 1) / p.splits;
   if (csplit) {
@@ -319,6 +326,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
   const int T_tile = p.streamk ? p.k_iters + p.k_iters_aug : (1 << 30);
   auto seg_extent = [&](int tile, int& mt, int& nt, int& z, int& kb, int& nk, int& total) {
     tile_coords(tile, m_tiles, n_tiles, mt, nt, z);
+    if (share) nt = 2 * nt + (int)srank;
     kb = z * kc;
     nk = min(kc, p.k_iters - kb);
     total = nk + (p.splits == 1 ? p.k_iters_aug : 0);
@@ -331,12 +339,13 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     if (p.k_iters_aug) { ptx::prefetch_tmap(&tmA2); ptx::prefetch_tmap(&tmB2); }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&afull[s], NF4 ? (PAIR ? 8 : 4) : 1);  // one elected lane per dequant warp
-      ptx::mbar_init(&empty[s], 1);
+      // one elected lane per dequant warp (share: this CTA's 2 + the peer's 2)
+      ptx::mbar_init(&afull[s], NF4 ? (PAIR ? 8 : 4) : 1);
+      ptx::mbar_init(&empty[s], share ? 2 : 1);  // share: both CTAs' MMAs read the stage
     }
     for (int c = 0; c < L::CST; ++c) {
       ptx::mbar_init(&cfull[c], 1);      // TMA expect_tx arrival (codes + constants bytes)
-      ptx::mbar_init(&cempty[c], 4);     // one elected lane per warp of the consuming dequant group
+      ptx::mbar_init(&cempty[c], share ? 2 : 4);  // one elected lane per warp of the consuming dequant group
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -351,7 +360,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (PAIR || csplit) ptx::cluster_sync();  // peer barriers initialised before any remote arrive
+  if (PAIR || csplit || share) ptx::cluster_sync();  // peer barriers initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -453,6 +462,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
               else ptx::umma_bf16(d_tmem, ad, bd, idesc, (i != i0) || kk != 0);
             }
             if (PAIR) ptx::umma_commit_pair_mc(&empty[s], 0x3);
+            else if (share) ptx::umma_commit_mc(&empty[s], 0x3);  // frees the slot in both CTAs
             else ptx::umma_commit(&empty[s]);
           }
           __syncwarp();
@@ -682,8 +692,12 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
   } else if (NF4 && warp >= kXfWarp0 && warp < kXfWarp0 + kNumXfWarps) {
     // ======================= NF4 dequant producer =======================
     const int xw = warp - kXfWarp0;
-    const int grp = xw >> 2;                 // two groups alternate stages
-    const int item = (xw & 3) * 32 + lane;   // 0..127: one 64-element W block per stage
+    // stages rotate over the groups: 2 groups of 4 warps (128 items each), or
+    // with share 4 groups of 2 warps (this CTA's 64 items of every stage)
+    const int ngrp = share ? 4 : 2;
+    const int grp = share ? xw >> 1 : xw >> 2;
+    const int item = share ? (int)srank * 64 + (xw & 1) * 32 + lane  // 0..127: one 64-element W block
+                           : (xw & 3) * 32 + lane;
     float vals[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) vals[i] = (float)p.values[i];
@@ -692,7 +706,9 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     // bwd: item -> W row m+item, cols k0..k0+64: A image item*128, codes item*32
     // fwd: warp (xw & 3) -> half h = xw & 1 of rows rr = 32 * ((xw & 3) >> 1) + lane: consecutive lanes
     // write consecutive 128 B rows of the MN-major image (conflict-free 16 B stores)
-    const int h = xw & 1, rr = 32 * ((xw & 3) >> 1) + lane;
+    // share: this CTA decodes column half h = srank, rows rr = 32 * (xw & 1) + lane
+    const int h = share ? (int)srank : xw & 1;
+    const int rr = share ? 32 * (xw & 1) + lane : 32 * ((xw & 3) >> 1) + lane;
     const bool fwd = p.nf4_mode == 1;
     const uint32_t soff = fwd ? (uint32_t)(h * 8192 + rr * 128) : (uint32_t)(item * 128);
     // the two 16 B halves of an item's 32 code bytes are read in lane-alternating
@@ -704,6 +720,17 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     const uint32_t consts_s = ptx::smem_u32(sK) + (fwd ? (uint32_t)(rr * 16 + h * 4) : (uint32_t)item * 16);
     const uint32_t k3210 = 0x32103210u;
     const uint32_t a_s = ptx::smem_u32(sA) + soff;
+    const uint32_t a_peer = share ? ptx::mapa_shared(a_s, srank ^ 1u) : 0u;  // same offset in the peer CTA
+    auto arrive_afull = [&](uint64_t* bar) {  // this CTA's barrier, and (share) the peer's
+      arrive_leader(bar);
+      if (share) {
+#ifdef QLRT_SHARE_RELAXED
+        ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(bar), srank ^ 1u));
+#else
+        ptx::mbar_arrive_cluster_release(ptx::mapa_shared(ptx::smem_u32(bar), srank ^ 1u));
+#endif
+      }
+    };
     uint32_t it = 0, cit = 0;
     Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
     int tile, i0, i1;
@@ -712,15 +739,15 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
       seg_extent(tile, mt, nt, z, kb, nk, total);
       i1 = min(i1, total);
       const int m_cta = mt * BMP + (int)rank * BM;
-      // stages alternate between the two groups by the running stage count
-      for (int i = i0 + (int)(((it & 1) != (uint32_t)grp)); i < i1; i += 2) {
+      // stages rotate over the groups by the running stage count
+      for (int i = i0 + (int)(((uint32_t)grp - it) % (uint32_t)ngrp); i < i1; i += ngrp) {
         const uint32_t my = it + (uint32_t)(i - i0);
         const int s = my % STAGES;
         const uint32_t ph = (my / STAGES) & 1;
         if (i >= nk) {  // augmented (TMA-fed) stage: keep afull's phase in step
           ptx::mbar_wait(&empty[s], ph ^ 1);
           __syncwarp();
-          if (lane == 0) arrive_leader(&afull[s]);
+          if (lane == 0) arrive_afull(&afull[s]);
           continue;
         }
         const uint32_t ci = cit + (uint32_t)(i - i0);
@@ -744,11 +771,13 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
         for (int ch = 0; ch < 8; ++ch) {
           if (ch < QLRT_HACK_DECODE) lookup8(words[ch], Lp, Hp, k3210, o0, o1, o2, o3);
           ptx::st_shared_v4(base + ((ch ^ swz) << 4), o0, o1, o2, o3);
+          if (share) ptx::st_cluster_v4(a_peer + s * A_STAGE + ((ch ^ swz) << 4), o0, o1, o2, o3);
         }
-        ptx::fence_proxy_async_smem();
+        if (share) ptx::fence_proxy_async_cluster();
+        else ptx::fence_proxy_async_smem();
         __syncwarp();  // orders the warp's smem writes before the elected release
         if (lane == 0) {
-          arrive_leader(&afull[s]);
+          arrive_afull(&afull[s]);
           // release the codes slot only now: every loaded word has been consumed
           // (an arrive right after the loads can overtake them, and the next TMA
           // would overwrite the slot under an in-flight ld.shared)
@@ -762,7 +791,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (PAIR || csplit) ptx::cluster_sync();  // (split-K: peers stay alive until rank 0 has read them)
+  if (PAIR || csplit || share) ptx::cluster_sync();  // (peers stay alive until remote traffic is done)
   if (warp == kMmaWarp) {
     ptx::tc_fence_after();
     if (PAIR) ptx::tmem_dealloc_pair(tmem_base, kNTmemCols);
@@ -881,6 +910,15 @@ static int pair_policy(int dflt) {
   return v < 0 ? dflt : v;
 }
 
+// shared-decode CTA pairs for the fused NF4 GEMMs (QLRT_SHARE=1).  Off by
+// default: correct, but the cross-SM coupling (both MMAs release a stage,
+// both producer halves fill it, DSMEM stores + remote arrives) costs more
+// than the halved decode saves -- measured 0.66x (tools/ab.py QLRT_SHARE=0/1)
+static int share_policy() {
+  const char* e = getenv("QLRT_SHARE");
+  return e ? atoi(e) : 0;
+}
+
 // stream-K policy: QLRT_STREAMK=0 disables it (whole-tile waves only)
 static int streamk_policy() {
   const char* e = getenv("QLRT_STREAMK");  // read per call: A/B runs toggle it in-process
@@ -926,6 +964,17 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
     cfg.gridDim = dim3(m_tiles * n_tiles * args.csplit);
     attrs[0].id = cudaLaunchAttributeClusterDimension;
     attrs[0].val.clusterDim.x = args.csplit;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+  }
+  if (NF4 && !PAIR && args.share) {  // pairs of CTAs on the same W rows
+    const int tiles_s = m_tiles * ((n_tiles + 1) / 2) * args.splits;
+    const int pairs = tiles_s < num_sms() / 2 ? tiles_s : num_sms() / 2;
+    cfg.gridDim = dim3(2 * pairs);
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
@@ -994,7 +1043,7 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   args.splits = effective_splits(args.splits, args.k_iters);
   if (args.csplit > 1) args.csplit = args.splits;  // every CTA of the cluster owns >= 1 k-iteration
   if (args.splits > 1 && K2) return QLRT_ERR_UNSUPPORTED;
-  if (args.sk_ws && args.splits == 1 && bn >= 64 && num_sms() <= kNumSMs) {
+  if (args.sk_ws && args.splits == 1 && bn >= 64 && num_sms() <= kNumSMs && !args.share) {
     // stream-K only for short grids (< 2 waves) that whole-tile waves would
     // leave > 10% idle: measured, its partial-tile traffic and spread-out
     // L2 footprint cost ~5% on long grids (tools/ab.py QLRT_STREAMK=0/1)
@@ -1238,6 +1287,7 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   a.out_t = 1;
   a.alpha = 1.0f;
   a.pair = gemm::pair_policy(0);
+  a.share = a.pair ? 0 : gemm::share_policy();
   if (gemm::streamk_policy()) { a.sk_ws = sk.sk_ws; a.sk_flags = sk.sk_flags; }
   if ((rc = gemm::fill_nf4(a, w, 1, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{x, K, 0};
@@ -1285,6 +1335,7 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   a.out_t = 1;
   a.alpha = 1.0f;
   a.pair = gemm::pair_policy(0);
+  a.share = a.pair ? 0 : gemm::share_policy();
   if (gemm::streamk_policy()) { a.sk_ws = sk.sk_ws; a.sk_flags = sk.sk_flags; }
   if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{dy, N, 0};

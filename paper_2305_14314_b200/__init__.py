@@ -11,6 +11,8 @@ Drop-in surface (reference names, GPU tensors):
               PagedMomentStore
   paging      Pager, PagerConfig, pager_open
   parallel    GradBucket, allreduce_mean (data-parallel adapter gradients)
+  analysis    quant_error_report, QuantConfig, QuantErrorRow (data-type comparison)
+  llama       LlamaConfig, LlamaQLoRA (LLaMA-shaped QLoRA harness, C3/C5)
 
 Every computation runs in the CUDA library ``_lib/libqlrt_b200.so``
 (hand-written sm_100a kernels, C ABI in include/qlrt_b200.h).  There is no CPU
@@ -18,6 +20,7 @@ fallback: calls raise RuntimeError without the library or a GPU.
 """
 
 from ._native import EXPORTS, LIB_PATH, load_library
+from .analysis import QuantConfig, QuantErrorRow, quant_error_report
 from .blockquant import BlockQuantized, dequantize, pack_codes, quantize, unpack_codes
 from .codebooks import (CODEBOOK_NAMES, Codebook, get_codebook, inv_normal_cdf, make_fp4_codebook,
                         make_int_codebook, make_nf_codebook, make_nf_midpoint_codebook)

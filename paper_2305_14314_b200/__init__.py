@@ -12,6 +12,7 @@ Drop-in surface (reference names, GPU tensors):
   paging      Pager, PagerConfig, pager_open
   parallel    GradBucket, allreduce_mean (data-parallel adapter gradients)
   analysis    quant_error_report, QuantConfig, QuantErrorRow (data-type comparison)
+  container   save, load, inspect_header (.qlrt v1, byte-compatible, GPU tensors)
   llama       LlamaConfig, LlamaQLoRA (LLaMA-shaped QLoRA harness, C3/C5)
 
 Every computation runs in the CUDA library ``_lib/libqlrt_b200.so``
@@ -20,12 +21,14 @@ fallback: calls raise RuntimeError without the library or a GPU.
 """
 
 from ._native import EXPORTS, LIB_PATH, load_library
+from . import container
 from .analysis import QuantConfig, QuantErrorRow, quant_error_report
 from .blockquant import BlockQuantized, dequantize, pack_codes, quantize, unpack_codes
 from .codebooks import (CODEBOOK_NAMES, Codebook, get_codebook, inv_normal_cdf, make_fp4_codebook,
                         make_int_codebook, make_nf_codebook, make_nf_midpoint_codebook)
 from .doublequant import DQConstants, Fp8Spec, bits_per_param, decode_fp8, dq_compress, dq_decompress, encode_fp8
-from .errors import ContainerError, CorruptDataError, QlrtError, TrainingDivergedError
+from .errors import (BadMagicError, ChecksumMismatchError, ContainerError, CorruptDataError, QlrtError,
+                     TrainingDivergedError, TruncatedFileError, UnsupportedVersionError)
 from .paging import Pager, PagerConfig, Slab, pager_open
 from .parallel import GradBucket, allreduce_mean
 from .qlora import PLACEMENTS, LoraAdapter, QLinear, gemm_bf16, lora_init

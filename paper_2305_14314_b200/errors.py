@@ -15,11 +15,28 @@ class CorruptDataError(QlrtError):
 
 
 class ContainerError(QlrtError):
-    """Container read/write failure (container format is out of scope here)."""
+    """Container read/write failure (pkg/docs/FORMAT.md failure taxonomy)."""
+
+
+class BadMagicError(ContainerError):
+    """The first four bytes are not ``QLRT``."""
+
+
+class UnsupportedVersionError(ContainerError):
+    """The version field is not 1."""
+
+
+class TruncatedFileError(ContainerError):
+    """A section is cut short, or bytes trail the checksum."""
+
+
+class ChecksumMismatchError(ContainerError):
+    """The stored crc32 differs from the recomputed one."""
 
 
 class TrainingDivergedError(QlrtError):
     """Training produced a non-finite loss or gradient norm."""
 
 
-__all__ = ["QlrtError", "CorruptDataError", "ContainerError", "TrainingDivergedError"]
+__all__ = ["QlrtError", "CorruptDataError", "ContainerError", "BadMagicError", "UnsupportedVersionError",
+           "TruncatedFileError", "ChecksumMismatchError", "TrainingDivergedError"]

@@ -1140,7 +1140,10 @@ static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, 
     }
   }
   a.splits = effective_splits(ws ? pick_splits(tiles, kit, M * N * 4, ws_bytes) : 1, (int)kit);
-  a.to_ws = fold != 0 || (out_split && out_t);
+  // fold is applied in the epilogue when one column tile holds both halves
+  // and there is no split-K (no reduce launch); otherwise the reduce kernel folds
+  const bool direct_fold = fold != 0 && a.splits == 1 && 2 * fold <= bn && N <= bn;
+  a.to_ws = (fold != 0 && !direct_fold) || (out_split && out_t);
   if ((a.to_ws || a.splits > 1) && (!ws || (size_t)(M * N * 4) * a.splits > ws_bytes)) return QLRT_ERR_ARG;
   qlrt_status st = run(bn, A, B, nullptr, nullptr, K, 0, a, s);
   if (st != QLRT_OK || (a.splits == 1 && !a.to_ws)) return st;

@@ -206,7 +206,9 @@ __device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[E
         *reinterpret_cast<float4*>(dst + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
                                                           __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
     } else {
-      for (int j = 0; j < EC && n0 + j < p.N; ++j) dst[j] = __uint_as_float(r[j]);
+#pragma unroll
+      for (int j = 0; j < EC; ++j)  // (unrolled + predicated: r stays in registers)
+        if (n0 + j < p.N) dst[j] = __uint_as_float(r[j]);
     }
     return;
   }
@@ -236,11 +238,15 @@ __device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[E
         *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(r[j]) * a, __uint_as_float(r[j + 1]) * a,
                                                         __uint_as_float(r[j + 2]) * a, __uint_as_float(r[j + 3]) * a);
     } else {
-      for (int j = 0; j < EC && n0 + j < NL; ++j) o[j] = __uint_as_float(r[j]) * a;
+#pragma unroll
+      for (int j = 0; j < EC; ++j)
+        if (n0 + j < NL) o[j] = __uint_as_float(r[j]) * a;
     }
   } else if (p.out_split) {  // bf16 hi/lo pair: v ~= hi + lo to ~16 mantissa bits
     __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + m * p.ldo + n0;
-    for (int j = 0; j < EC && n0 + j < NL; ++j) {
+#pragma unroll
+    for (int j = 0; j < EC; ++j) {
+      if (n0 + j >= NL) continue;
       const float v = __uint_as_float(r[j]) * a;
       const __nv_bfloat16 hi = __float2bfloat16_rn(v);
       o[j] = hi;
@@ -257,7 +263,9 @@ __device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[E
                        pack_bf16x2(__uint_as_float(r[j + 4]) * a, __uint_as_float(r[j + 5]) * a),
                        pack_bf16x2(__uint_as_float(r[j + 6]) * a, __uint_as_float(r[j + 7]) * a));
     } else {
-      for (int j = 0; j < EC && n0 + j < NL; ++j) o[j] = __float2bfloat16_rn(__uint_as_float(r[j]) * a);
+#pragma unroll
+      for (int j = 0; j < EC; ++j)
+        if (n0 + j < NL) o[j] = __float2bfloat16_rn(__uint_as_float(r[j]) * a);
     }
   }
 }
@@ -631,8 +639,11 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
               if (mcol + 8 <= p.M && (p.ldo & 7) == 0) {
                 *reinterpret_cast<uint4*>(o) = v;
               } else {
-                const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
-                for (int u = 0; u < 8 && mcol + u < p.M; ++u) o[u] = e[u];
+                const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                  if (mcol + u < p.M)
+                    reinterpret_cast<unsigned short*>(o)[u] = (unsigned short)(vw[u >> 1] >> (16 * (u & 1)));
               }
             }
           }

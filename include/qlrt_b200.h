@@ -202,6 +202,20 @@ qlrt_status qlrt_scale_f32(float* g, int64_t n, float scale, void* stream);
  * (device >= 0) or to the host (device < 0) on the given stream. */
 qlrt_status qlrt_prefetch(void* ptr, size_t bytes, int device, void* stream);
 
+/* ---- fused glue of the LLaMA-shaped harness (llama.py; not a reference path) */
+/* bf16 in/out, fp32 math, 16-byte vectors (widths multiples of 8). */
+qlrt_status qlrt_rmsnorm_fwd(const void* x, void* y, float* rstd, int64_t rows, int64_t h,
+                             float eps, void* stream);
+qlrt_status qlrt_rmsnorm_bwd(const void* dy, const void* x, const float* rstd, void* dx,
+                             int64_t rows, int64_t h, void* stream);
+qlrt_status qlrt_swiglu_fwd(const void* g, const void* u, void* out, int64_t n, void* stream);
+qlrt_status qlrt_swiglu_bwd(const void* g, const void* u, const void* dout, void* dg, void* du,
+                            int64_t n, void* stream);
+/* rotary embedding on [rows = b*s][heads][d], adjacent pairs; cos_sin fp32
+ * [seq][d/2] (cos, sin); inverse = 1 rotates back (the backward). */
+qlrt_status qlrt_rope(const void* x, void* y, const void* cos_sin, int64_t rows, int heads, int d,
+                      int seq, int inverse, void* stream);
+
 /* Library identification: returns the compiled arch string ("sm_100a"). */
 const char* qlrt_build_info(void);
 

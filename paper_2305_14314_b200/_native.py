@@ -65,6 +65,11 @@ _SIGS = {
     "qlrt_sumsq_f64": [c_void_p, c_int64, c_void_p, c_void_p],
     "qlrt_scale_f32": [c_void_p, c_int64, c_float, c_void_p],
     "qlrt_prefetch": [c_void_p, c_size_t, c_int, c_void_p],
+    "qlrt_rmsnorm_fwd": [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_void_p],
+    "qlrt_rmsnorm_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p],
+    "qlrt_swiglu_fwd": [c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
+    "qlrt_swiglu_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
+    "qlrt_rope": [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int, c_void_p],
     "qlrt_build_info": [],
 }
 _RESTYPE = {"qlrt_dq_workspace_bytes": c_size_t, "qlrt_linear_workspace_bytes": c_size_t,

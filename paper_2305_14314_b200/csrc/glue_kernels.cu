@@ -1,0 +1,206 @@
+// Fused elementwise kernels of the LLaMA-shaped harness (llama.py): RMSNorm,
+// SwiGLU and rotary embedding, forward and backward, bf16 in/out with fp32
+// math, 16-byte vector accesses.  Not on the reference's path (qlrt has no
+// transformer); they keep the glue between the fused NF4 linears from
+// dominating the C3/C5 step.
+#include "qlrt_common.cuh"
+
+namespace qlrt {
+namespace glue {
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.0f;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+  return t;
+}
+
+// y = x * rsqrt(mean(x^2) + eps), one CTA per row (h % 8 == 0)
+__global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const uint4* __restrict__ x, uint4* __restrict__ y,
+                                                          float* __restrict__ rstd, int h8, float eps) {
+  __shared__ float red[8];
+  const int64_t row = blockIdx.x;
+  const uint4* xr = x + row * h8;
+  float ss = 0.0f;
+  for (int i = threadIdx.x; i < h8; i += blockDim.x) {
+    const uint4 u = xr[i];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ss += bf_lo(w[j]) * bf_lo(w[j]) + bf_hi(w[j]) * bf_hi(w[j]);
+  }
+  const float r = rsqrtf(block_sum(ss, red) / (float)(h8 * 8) + eps);
+  if (threadIdx.x == 0) rstd[row] = r;
+  uint4* yr = y + row * h8;
+  for (int i = threadIdx.x; i < h8; i += blockDim.x) {
+    const uint4 u = xr[i];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = pack_bf16x2(bf_lo(w[j]) * r, bf_hi(w[j]) * r);
+    yr[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// dx = r * dy - r^3 * x * sum(dy * x) / h
+__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ x,
+                                                          const float* __restrict__ rstd, uint4* __restrict__ dx,
+                                                          int h8) {
+  __shared__ float red[8];
+  const int64_t row = blockIdx.x;
+  const uint4 *xr = x + row * h8, *gr = dy + row * h8;
+  float dot = 0.0f;
+  for (int i = threadIdx.x; i < h8; i += blockDim.x) {
+    const uint4 a = xr[i], b = gr[i];
+    const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dot += bf_lo(wa[j]) * bf_lo(wb[j]) + bf_hi(wa[j]) * bf_hi(wb[j]);
+  }
+  dot = block_sum(dot, red);
+  const float r = rstd[row];
+  const float k = r * r * r * dot / (float)(h8 * 8);
+  uint4* dr = dx + row * h8;
+  for (int i = threadIdx.x; i < h8; i += blockDim.x) {
+    const uint4 a = xr[i], b = gr[i];
+    const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      o[j] = pack_bf16x2(r * bf_lo(wb[j]) - k * bf_lo(wa[j]), r * bf_hi(wb[j]) - k * bf_hi(wa[j]));
+    dr[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+__device__ __forceinline__ float sigmoidf_(float g) { return 1.0f / (1.0f + __expf(-g)); }
+
+// out = silu(g) * u  (n % 8 == 0)
+__global__ void swiglu_fwd_kernel(const uint4* __restrict__ g, const uint4* __restrict__ u, uint4* __restrict__ out,
+                                  int64_t n8) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 a = g[i], b = u[i];
+    const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float g0 = bf_lo(wa[j]), g1 = bf_hi(wa[j]);
+      o[j] = pack_bf16x2(g0 * sigmoidf_(g0) * bf_lo(wb[j]), g1 * sigmoidf_(g1) * bf_hi(wb[j]));
+    }
+    out[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// du = dout * silu(g);  dg = dout * u * s * (1 + g (1 - s)),  s = sigmoid(g)
+__global__ void swiglu_bwd_kernel(const uint4* __restrict__ g, const uint4* __restrict__ u,
+                                  const uint4* __restrict__ dout, uint4* __restrict__ dg, uint4* __restrict__ du,
+                                  int64_t n8) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 a = g[i], b = u[i], c = dout[i];
+    const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w}, wc[4] = {c.x, c.y, c.z, c.w};
+    uint32_t og[4], ou[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float gg[2] = {bf_lo(wa[j]), bf_hi(wa[j])}, uu[2] = {bf_lo(wb[j]), bf_hi(wb[j])};
+      float dd[2] = {bf_lo(wc[j]), bf_hi(wc[j])}, rg[2], ru[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float s = sigmoidf_(gg[e]);
+        ru[e] = dd[e] * gg[e] * s;
+        rg[e] = dd[e] * uu[e] * s * (1.0f + gg[e] * (1.0f - s));
+      }
+      og[j] = pack_bf16x2(rg[0], rg[1]);
+      ou[j] = pack_bf16x2(ru[0], ru[1]);
+    }
+    dg[i] = make_uint4(og[0], og[1], og[2], og[3]);
+    du[i] = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+  }
+}
+
+// rotary embedding on [rows = b*s, heads, d] bf16, adjacent pairs (2i, 2i+1)
+// rotated by angle pos * inv_freq[i]; cs = (cos, sin) fp32 [s][d/2]; sign = -1
+// applies the inverse rotation (backward)
+__global__ void rope_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, const float2* __restrict__ cs,
+                            int64_t rows, int heads, int d, int seq, float sign) {
+  const int d8 = d / 8;
+  const int64_t total = rows * heads * d8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % d8);
+    const int64_t row = i / ((int64_t)d8 * heads);
+    const int pos = (int)(row % seq);
+    const float2* t = cs + (int64_t)pos * (d / 2) + c8 * 4;  // 4 pairs per 16 B
+    const uint4 a = x[i];
+    const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 r = t[j];
+      const float x0 = bf_lo(w[j]), x1 = bf_hi(w[j]), sn = sign * r.y;
+      o[j] = pack_bf16x2(x0 * r.x - x1 * sn, x0 * sn + x1 * r.x);
+    }
+    y[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+static int grid_for(int64_t n, int tpb) {
+  int64_t g = (n + tpb - 1) / tpb;
+  return (int)(g < (int64_t)kNumSMs * 8 ? (g < 1 ? 1 : g) : (int64_t)kNumSMs * 8);
+}
+
+}  // namespace glue
+}  // namespace qlrt
+
+using namespace qlrt;
+
+extern "C" {
+
+qlrt_status qlrt_rmsnorm_fwd(const void* x, void* y, float* rstd, int64_t rows, int64_t h, float eps, void* stream) {
+  if (!x || !y || !rstd || rows <= 0 || h <= 0 || (h % 8)) return QLRT_ERR_ARG;
+  glue::rmsnorm_fwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>((const uint4*)x, (uint4*)y, rstd,
+                                                                            (int)(h / 8), eps);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_rmsnorm_bwd(const void* dy, const void* x, const float* rstd, void* dx, int64_t rows, int64_t h,
+                             void* stream) {
+  if (!dy || !x || !rstd || !dx || rows <= 0 || h <= 0 || (h % 8)) return QLRT_ERR_ARG;
+  glue::rmsnorm_bwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>((const uint4*)dy, (const uint4*)x, rstd,
+                                                                            (uint4*)dx, (int)(h / 8));
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_swiglu_fwd(const void* g, const void* u, void* out, int64_t n, void* stream) {
+  if (!g || !u || !out || n <= 0 || (n % 8)) return QLRT_ERR_ARG;
+  glue::swiglu_fwd_kernel<<<glue::grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)g, (const uint4*)u, (uint4*)out, n / 8);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_swiglu_bwd(const void* g, const void* u, const void* dout, void* dg, void* du, int64_t n,
+                            void* stream) {
+  if (!g || !u || !dout || !dg || !du || n <= 0 || (n % 8)) return QLRT_ERR_ARG;
+  glue::swiglu_bwd_kernel<<<glue::grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)g, (const uint4*)u, (const uint4*)dout, (uint4*)dg, (uint4*)du, n / 8);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_rope(const void* x, void* y, const void* cos_sin, int64_t rows, int heads, int d, int seq,
+                      int inverse, void* stream) {
+  if (!x || !y || !cos_sin || rows <= 0 || heads <= 0 || d <= 0 || (d % 8) || seq <= 0) return QLRT_ERR_ARG;
+  const int64_t total = rows * heads * (d / 8);
+  glue::rope_kernel<<<glue::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)x, (uint4*)y, (const float2*)cos_sin, rows, heads, d, seq, inverse ? -1.0f : 1.0f);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+}  // extern "C"

@@ -105,15 +105,91 @@ class _QLinearFn(torch.autograd.Function):
         return dx, None, None, None
 
 
+class _RMSNormFn(torch.autograd.Function):
+    """y = x * rsqrt(mean(x^2) + eps) (frozen unit weight), fused kernels."""
+
+    @staticmethod
+    def forward(ctx, x, eps):
+        x = x.contiguous()
+        h = x.shape[-1]
+        rows = x.numel() // h
+        y = torch.empty_like(x)
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        check(lib().qlrt_rmsnorm_fwd(ptr(x), ptr(y), ptr(rstd), rows, h, float(eps), stream_ptr()), "rmsnorm")
+        ctx.save_for_backward(x, rstd)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, rstd = ctx.saved_tensors
+        dy = dy.contiguous()
+        dx = torch.empty_like(x)
+        h = x.shape[-1]
+        check(lib().qlrt_rmsnorm_bwd(ptr(dy), ptr(x), ptr(rstd), ptr(dx), x.numel() // h, h, stream_ptr()),
+              "rmsnorm bwd")
+        return dx, None
+
+
+class _SwiGLUFn(torch.autograd.Function):
+    """silu(g) * u, fused kernels."""
+
+    @staticmethod
+    def forward(ctx, g, u):
+        g, u = g.contiguous(), u.contiguous()
+        out = torch.empty_like(g)
+        check(lib().qlrt_swiglu_fwd(ptr(g), ptr(u), ptr(out), g.numel(), stream_ptr()), "swiglu")
+        ctx.save_for_backward(g, u)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        g, u = ctx.saved_tensors
+        dout = dout.contiguous()
+        dg, du = torch.empty_like(g), torch.empty_like(u)
+        check(lib().qlrt_swiglu_bwd(ptr(g), ptr(u), ptr(dout), ptr(dg), ptr(du), g.numel(), stream_ptr()),
+              "swiglu bwd")
+        return dg, du
+
+
+class _RoPEFn(torch.autograd.Function):
+    """Rotary embedding of adjacent pairs on [b, s, heads, d]; the backward
+    rotates the gradient back."""
+
+    @staticmethod
+    def forward(ctx, t, cos_sin):
+        t = t.contiguous()
+        b, s, nh, d = t.shape
+        y = torch.empty_like(t)
+        check(lib().qlrt_rope(ptr(t), ptr(y), ptr(cos_sin), b * s, nh, d, s, 0, stream_ptr()), "rope")
+        ctx.save_for_backward(cos_sin)
+        ctx.shape = (b, s, nh, d)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        (cos_sin,) = ctx.saved_tensors
+        b, s, nh, d = ctx.shape
+        dy = dy.contiguous()
+        dx = torch.empty_like(dy)
+        check(lib().qlrt_rope(ptr(dy), ptr(dx), ptr(cos_sin), b * s, nh, d, s, 1, stream_ptr()), "rope bwd")
+        return dx, None
+
+
 def _rmsnorm(x: torch.Tensor, eps: float) -> torch.Tensor:
-    return F.rms_norm(x.float(), (x.shape[-1],), eps=eps).to(x.dtype)
+    return _RMSNormFn.apply(x, eps)
 
 
-def _rope(t: torch.Tensor, freqs: torch.Tensor) -> torch.Tensor:
-    """Rotary embedding on [b, s, heads, d] (contiguous) as one complex multiply
-    over adjacent pairs; freqs = exp(i theta) as complex64 [s, d/2]."""
-    tc = torch.view_as_complex(t.float().reshape(*t.shape[:-1], -1, 2))
-    return torch.view_as_real(tc * freqs[None, :, None, :]).flatten(-2).to(t.dtype)
+def _rope(t: torch.Tensor, cos_sin: torch.Tensor) -> torch.Tensor:
+    """Rotary embedding on [b, s, heads, d]; cos_sin fp32 [s, d/2, 2]."""
+    return _RoPEFn.apply(t, cos_sin)
+
+
+def rope_reference(t: torch.Tensor, cos_sin: torch.Tensor) -> torch.Tensor:
+    """Plain PyTorch statement of the same rotation (tests)."""
+    tt = t.float().reshape(*t.shape[:-1], -1, 2)
+    c, s_ = cos_sin[None, :, None, :, 0], cos_sin[None, :, None, :, 1]
+    x0, x1 = tt[..., 0], tt[..., 1]
+    return torch.stack((x0 * c - x1 * s_, x0 * s_ + x1 * c), dim=-1).flatten(-2)
 
 
 class LlamaQLoRA:
@@ -175,7 +251,7 @@ class LlamaQLoRA:
         d = h // cfg.n_heads
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, d, 2, device=self.dev, dtype=torch.float32) / d))
         ang = torch.outer(torch.arange(cfg.seq, device=self.dev, dtype=torch.float32), inv)
-        self.freqs = torch.polar(torch.ones_like(ang), ang)  # complex64 [seq, d/2]
+        self.cos_sin = torch.stack((torch.cos(ang), torch.sin(ang)), dim=-1).contiguous()  # fp32 [seq, d/2, 2]
         self.anchor = torch.zeros(1, device=self.dev, requires_grad=True)
         self.t = 0
         self.hyper_host = torch.zeros(8, dtype=torch.float32).pin_memory()
@@ -193,16 +269,16 @@ class LlamaQLoRA:
         x = F.embedding(tokens, self.embed)
         for lay in self.layers:
             hn = _rmsnorm(x, cfg.rms_eps)
-            fr = self.freqs[:s]
-            q = _rope(self._lin(hn, lay, "q").view(b, s, nh, d), fr).transpose(1, 2)
-            k = _rope(self._lin(hn, lay, "k").view(b, s, nh, d), fr).transpose(1, 2)
+            cs = self.cos_sin[:s]
+            q = _rope(self._lin(hn, lay, "q").view(b, s, nh, d), cs).transpose(1, 2)
+            k = _rope(self._lin(hn, lay, "k").view(b, s, nh, d), cs).transpose(1, 2)
             v = self._lin(hn, lay, "v").view(b, s, nh, d).transpose(1, 2)
             a = F.scaled_dot_product_attention(q, k, v, is_causal=True).transpose(1, 2).reshape(b, s, cfg.hidden)
             x = x + self._lin(a, lay, "o")
             hn = _rmsnorm(x, cfg.rms_eps)
             gt = self._lin(hn, lay, "gate")
             up = self._lin(hn, lay, "up")
-            x = x + self._lin(F.silu(gt) * up, lay, "down")
+            x = x + self._lin(_SwiGLUFn.apply(gt, up), lay, "down")
         x = _rmsnorm(x, cfg.rms_eps)
         logits = x.reshape(b * s, cfg.hidden) @ self.lm_head
         return F.cross_entropy(logits.float(), targets.reshape(-1))

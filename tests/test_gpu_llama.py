@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 def _reference_grads(model, tokens, targets):
     """fp32 autograd through the same decoder; returns loss and d/d(l1, l2)."""
     import paper_2305_14314_b200 as qb
-    from paper_2305_14314_b200.llama import PROJS, _rope
+    from paper_2305_14314_b200.llama import PROJS, rope_reference
     cfg = model.cfg
     b, s = tokens.shape
     nh, d = cfg.n_heads, cfg.hidden // cfg.n_heads
@@ -39,11 +39,11 @@ def _reference_grads(model, tokens, targets):
         return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + cfg.rms_eps)
 
     x = F.embedding(tokens, model.embed.float())
-    fr = model.freqs[:s]
+    cs = model.cos_sin[:s]
     for li in range(cfg.n_layers):
         hn = rms(x)
-        q = _rope(lin(hn, li, "q").view(b, s, nh, d), fr).transpose(1, 2)
-        k = _rope(lin(hn, li, "k").view(b, s, nh, d), fr).transpose(1, 2)
+        q = rope_reference(lin(hn, li, "q").view(b, s, nh, d), cs).transpose(1, 2)
+        k = rope_reference(lin(hn, li, "k").view(b, s, nh, d), cs).transpose(1, 2)
         v = lin(hn, li, "v").view(b, s, nh, d).transpose(1, 2)
         a = F.scaled_dot_product_attention(q, k, v, is_causal=True).transpose(1, 2).reshape(b, s, cfg.hidden)
         x = x + lin(a, li, "o")
@@ -53,6 +53,43 @@ def _reference_grads(model, tokens, targets):
     loss = F.cross_entropy(logits, targets.reshape(-1))
     loss.backward()
     return loss.item(), {n: t.grad for n, t in leaves.items()}
+
+
+def test_glue_kernels_match_torch(cuda):
+    """Fused RMSNorm / SwiGLU / RoPE forward and backward vs PyTorch fp32."""
+    from paper_2305_14314_b200.llama import _RMSNormFn, _RoPEFn, _SwiGLUFn, rope_reference
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(6, 5, 256, device="cuda", generator=g).bfloat16().requires_grad_(True)
+    y = _RMSNormFn.apply(x, 1e-6)
+    xr = x.detach().float().requires_grad_(True)
+    yr = xr * torch.rsqrt(xr.pow(2).mean(-1, keepdim=True) + 1e-6)
+    dy = torch.randn(y.shape, device="cuda", generator=g).bfloat16()
+    y.backward(dy)
+    yr.backward(dy.float())
+    assert (y.float() - yr).abs().max() <= 2e-2 * yr.abs().max()
+    assert (x.grad.float() - xr.grad).abs().max() <= 2e-2 * xr.grad.abs().max()
+    a = torch.randn(1000, 64, device="cuda", generator=g).bfloat16().requires_grad_(True)
+    b = torch.randn(1000, 64, device="cuda", generator=g).bfloat16().requires_grad_(True)
+    o = _SwiGLUFn.apply(a, b)
+    ar, br = a.detach().float().requires_grad_(True), b.detach().float().requires_grad_(True)
+    orf = F.silu(ar) * br
+    do = torch.randn(o.shape, device="cuda", generator=g).bfloat16()
+    o.backward(do)
+    orf.backward(do.float())
+    assert (o.float() - orf).abs().max() <= 2e-2 * orf.abs().max()
+    assert (a.grad.float() - ar.grad).abs().max() <= 2e-2 * ar.grad.abs().max()
+    assert (b.grad.float() - br.grad).abs().max() <= 2e-2 * br.grad.abs().max()
+    t = torch.randn(2, 16, 4, 64, device="cuda", generator=g).bfloat16().requires_grad_(True)
+    ang = torch.outer(torch.arange(16, device="cuda").float(), 1.0 / (10000 ** (torch.arange(0, 64, 2, device="cuda").float() / 64)))
+    cs = torch.stack((torch.cos(ang), torch.sin(ang)), dim=-1).contiguous()
+    r = _RoPEFn.apply(t, cs)
+    tr = t.detach().float().requires_grad_(True)
+    rr = rope_reference(tr, cs)
+    dr = torch.randn(r.shape, device="cuda", generator=g).bfloat16()
+    r.backward(dr)
+    rr.backward(dr.float())
+    assert (r.float() - rr).abs().max() <= 2e-2 * rr.abs().max()
+    assert (t.grad.float() - tr.grad).abs().max() <= 2e-2 * tr.grad.abs().max()
 
 
 def _tiny(seed=0):

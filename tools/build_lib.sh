@@ -9,7 +9,7 @@ NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$ROOT/include -I$SRC ${QLRT_NVCC_EXTRA:-}"
 objs=()
 pids=()
-for f in quant_kernels gemm_sm100 gemv_nf4 optim_kernels; do
+for f in quant_kernels gemm_sm100 gemv_nf4 optim_kernels glue_kernels; do
   "$NVCC" $FLAGS -c "$SRC/$f.cu" -o "$OUT/$f.o" &
   pids+=($!)
   objs+=("$OUT/$f.o")

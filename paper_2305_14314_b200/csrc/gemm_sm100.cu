@@ -371,6 +371,10 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
   if (PAIR || csplit || share) ptx::cluster_sync();  // peer barriers initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // programmatic dependent launch: the prologue above (barriers, TMEM,
+  // descriptor prefetch) overlaps the previous kernel's tail; no global data
+  // of the previous kernel is touched before this point
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   // leader-side barrier addresses (shared::cluster) for remote arrivals / TMA bytes
   auto leader_addr = [&](uint64_t* bar) -> uint32_t {
@@ -921,6 +925,12 @@ static int pair_policy(int dflt) {
   return v < 0 ? dflt : v;
 }
 
+// programmatic dependent launch of the engine kernels (QLRT_PDL=0 disables it)
+static int pdl_policy() {
+  const char* e = getenv("QLRT_PDL");
+  return e ? atoi(e) : 1;
+}
+
 // shared-decode CTA pairs for the fused NF4 GEMMs (QLRT_SHARE=1).  Off by
 // default: correct, but the cross-SM coupling (both MMAs release a stage,
 // both producer halves fill it, DSMEM stores + remote arrives) costs more
@@ -970,7 +980,7 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
   cfg.blockDim = dim3(NF4 ? kNF4Threads : 192);
   cfg.dynamicSmemBytes = L::BYTES;
   cfg.stream = s;
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   if (!PAIR && !NF4 && args.csplit > 1) {  // one CTA per (tile, split), clusters of csplit
     cfg.gridDim = dim3(m_tiles * n_tiles * args.csplit);
     attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -998,6 +1008,13 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
+  }
+  if (pdl_policy()) {
+    cudaLaunchAttribute& at = attrs[cfg.numAttrs];
+    at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs += 1;
   }
   if (cudaLaunchKernelEx(&cfg, kern, a, b, a2, b2, c, k, args) != cudaSuccess) return QLRT_ERR_CUDA;
   QLRT_CHECK_LAUNCH();

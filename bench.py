@@ -294,12 +294,24 @@ def main() -> None:
     g1h = torch.empty(K_IN, RANK).pin_memory()
     g2h = torch.empty(RANK, N_OUT).pin_memory()
     e_steps = max(4, args.steps // 2)
-    xin = [torch.empty_like(x) for _ in range(2)]
-    dyin = [torch.empty_like(dy) for _ in range(2)]
+    xin = [x.clone() for _ in range(2)]
+    dyin = [dy.clone() for _ in range(2)]
+    # the public-API calls (QLinear.forward / backward) on each input buffer,
+    # captured once into a CUDA graph so the host does not pace the GPU
+    e_graphs = []
+    for j in range(2):
+        gj = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gj):
+            _, cj = lin.forward(xin[j])
+            dxj, grj = lin.backward(dyin[j], cj)
+        e_graphs.append((gj, dxj, grj))
+    torch.cuda.synchronize()
     cstream = torch.cuda.Stream(dev)
+    ostream = torch.cuda.Stream(dev)  # D2H on its own stream: both PCIe directions at once
     h2d_done = [torch.cuda.Event() for _ in range(2)]
     used = [torch.cuda.Event() for _ in range(2)]
     out_ready = torch.cuda.Event()
+    out_read = [torch.cuda.Event() for _ in range(2)]
 
     def h2d(i):
         j = i % 2
@@ -321,15 +333,23 @@ def main() -> None:
             h2d(i + 1)
         j = i % 2
         stream.wait_event(h2d_done[j])
-        _, dx, grads = step(xin[j], dyin[j])
+        gj, dx, grads = e_graphs[j]
+        stream.wait_event(out_read[j])
+        gj.replay()
+        if world > 1:
+            bucket.load(grads)
+            bucket.start()
+            grads = bucket.finish()
         used[j].record(stream)
         out_ready.record(stream)
-        with torch.cuda.stream(cstream):
-            cstream.wait_event(out_ready)
+        with torch.cuda.stream(ostream):
+            ostream.wait_event(out_ready)
             dxh.copy_(dx, non_blocking=True)
             g1h.copy_(grads["adapter0.l1"], non_blocking=True)
             g2h.copy_(grads["adapter0.l2"], non_blocking=True)
+            out_read[j].record(ostream)  # graph j's outputs are read; its next replay (step i+2) waits
     stream.wait_stream(cstream)
+    stream.wait_stream(ostream)
     ev1.record(stream)
     torch.cuda.synchronize()
     e_ms = torch.tensor([ev0.elapsed_time(ev1)], device=dev, dtype=torch.float64)
@@ -414,8 +434,8 @@ def main() -> None:
             "tokens_per_s": world * M_TOK * args.steps / (ms / 1e3),
             "e2e": {"value": e2e, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h,
                     "steps": e_steps, "pinned_h2d_gbs": h2d_gbs,
-                    "note": "QLinear.forward/backward from pinned host X, dY; dX, dl1, dl2 back to pinned host; "
-                            "copies double-buffered on a side stream"},
+                    "note": "QLinear.forward/backward (CUDA-graph captured) from pinned host X, dY; dX, dl1, "
+                            "dl2 back to pinned host; copies double-buffered on a side stream"},
             "roofline": roofline,
             "gpu_launches": (launches_per_step * args.steps) if launches_per_step else None,
             "gpu_launches_per_step": launches_per_step,

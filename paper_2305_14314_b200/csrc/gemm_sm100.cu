@@ -329,7 +329,13 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     unit0 = (int)zrank * (m_tiles * n_tiles) + (int)(blockIdx.x / p.csplit);
     n_units = n_tiles_total;  // exactly one segment per CTA
   }
-  constexpr uint32_t kNTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+  // accumulators: double-buffered up to BN = 256; BN = 512 (pair tiles of
+  // 256 x 512, two N = 256 UMMAs per k-step) fills TMEM with one buffer
+  constexpr int NACC = 2 * BN <= 512 ? 2 : 1;
+  constexpr uint32_t kNTmemCols = NACC * BN < 32 ? 32 : NACC * BN;
+  constexpr int UN = BN > 256 ? 256 : BN;   // N of one UMMA
+  constexpr int NUM = BN / UN;              // UMMAs per k16 step
+  static_assert(!(BN > 256) || PAIR, "BN = 512 needs 2-CTA pairs");
   // iterations of a whole tile (stream-K needs splits == 1)
   const int T_tile = p.streamk ? p.k_iters + p.k_iters_aug : (1 << 30);
   auto seg_extent = [&](int tile, int& mt, int& nt, int& z, int& kb, int& nk, int& total) {
@@ -431,6 +437,10 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           if (bmn) {
 #pragma unroll
             for (int j = 0; j < (BNC + 63) / 64; ++j) tma(mb, &full[s], b_dst + j * 8192, n_cta + j * 64, k0);
+          } else if (NUM > 1) {  // one 128-token half of each UMMA's B, at the same offset in both CTAs
+#pragma unroll
+            for (int j = 0; j < NUM; ++j)
+              tma(mb, &full[s], b_dst + j * (L::B_STAGE / NUM), k0, nt * BN + j * UN + (int)rank * (UN / 2));
           } else {
             tma(mb, &full[s], b_dst, k0, n_cta);
           }
@@ -447,8 +457,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
         int mt, nt, z, kb, nk, total;
         seg_extent(tile, mt, nt, z, kb, nk, total);
         i1 = min(i1, total);
-        const uint32_t acc = local & 1;
-        wait_x(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        const uint32_t acc = local % NACC;
+        wait_x(&tempty[acc], ((local / NACC) & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int i = i0; i < i1; ++i, ++it) {
@@ -460,7 +470,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           ptx::tc_fence_after();
           const int amn = aug ? p.a2_mn : (NF4 ? (p.nf4_mode == 1) : p.a_mn);
           const int bmn = aug ? p.b2_mn : p.b_mn;
-          const uint32_t idesc = ptx::idesc_bf16(BMP, BN, amn, bmn);
+          const uint32_t idesc = ptx::idesc_bf16(BMP, UN, amn, bmn);
           const uint32_t a_addr = ptx::smem_u32(sA + s * A_STAGE);
           const uint32_t b_addr = ptx::smem_u32(sB + s * L::B_STAGE);
           if (lane == 0) {
@@ -468,10 +478,14 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
             for (int kk = 0; kk < BK / 16; ++kk) {
               const uint64_t ad = amn ? ptx::sdesc_sw128(a_addr + kk * 2048, 8192, 1024)
                                       : ptx::sdesc_sw128(a_addr + kk * 32, 16, 1024);
-              const uint64_t bd = bmn ? ptx::sdesc_sw128(b_addr + kk * 2048, 8192, 1024)
-                                      : ptx::sdesc_sw128(b_addr + kk * 32, 16, 1024);
-              if (PAIR) ptx::umma_bf16_pair(d_tmem, ad, bd, idesc, (i != i0) || kk != 0);
-              else ptx::umma_bf16(d_tmem, ad, bd, idesc, (i != i0) || kk != 0);
+#pragma unroll
+              for (int j = 0; j < NUM; ++j) {
+                const uint32_t bj = b_addr + (uint32_t)(j * (L::B_STAGE / NUM));
+                const uint64_t bd = bmn ? ptx::sdesc_sw128(bj + kk * 2048, 8192, 1024)
+                                        : ptx::sdesc_sw128(bj + kk * 32, 16, 1024);
+                if (PAIR) ptx::umma_bf16_pair(d_tmem + j * UN, ad, bd, idesc, (i != i0) || kk != 0);
+                else ptx::umma_bf16(d_tmem + j * UN, ad, bd, idesc, (i != i0) || kk != 0);
+              }
             }
             if (PAIR) ptx::umma_commit_pair_mc(&empty[s], 0x3);
             else if (share) ptx::umma_commit_mc(&empty[s], 0x3);  // frees the slot in both CTAs
@@ -505,8 +519,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
       int v_end = unit0 + 1;
       if (p.streamk && i0 == 0 && i1 < total)
         while (v_end < n_units && Sched::range_begin(G, v_end, n_units) < (long long)(tile + 1) * T_tile) ++v_end;
-      const uint32_t acc = local & 1;
-      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      const uint32_t acc = local % NACC;
+      ptx::mbar_wait(&tfull[acc], (local / NACC) & 1);
       ptx::tc_fence_after();
       if (v_end > unit0 + 1) {  // wait for the later units' partials of this tile (one flag per lane)
         for (int v0 = unit0 + 1; v0 < v_end; v0 += 32) {
@@ -925,6 +939,15 @@ static int pair_policy(int dflt) {
   return v < 0 ? dflt : v;
 }
 
+// 256 x 512 pair tiles for the fused NF4 GEMMs (QLRT_TILE512=0 falls back to
+// 128 x 256 single-CTA tiles): the 2-CTA pair halves the B traffic per SM and
+// the two N = 256 UMMAs per k-step halve the dequant work per MMA -- measured
+// +16..41% on the C2 / C4 shapes (tools/ab.py QLRT_TILE512=0/1)
+static int tile512_policy() {
+  const char* e = getenv("QLRT_TILE512");
+  return e ? atoi(e) : 1;
+}
+
 // programmatic dependent launch of the engine kernels (QLRT_PDL=0 disables it)
 static int pdl_policy() {
   const char* e = getenv("QLRT_PDL");
@@ -1049,8 +1072,9 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   if (bn < 64 && (B.mn || (B2 && B2->mn))) return QLRT_ERR_UNSUPPORTED;
   if (!nf4 && !(A.mn ? make_tmap(&ta, A.ptr, M, K, A.ld, 64) : make_tmap(&ta, A.ptr, K, M, A.ld, BM)))
     return QLRT_ERR_UNSUPPORTED;
-  if (args.pair && (bn != 256 || (B2 && B2->mn && bn / 2 < 64))) return QLRT_ERR_UNSUPPORTED;
-  const int bbox = args.pair ? bn / 2 : bn;  // B rows each CTA loads
+  if (args.pair && ((bn != 256 && bn != 512) || (B2 && B2->mn && bn / 2 < 64))) return QLRT_ERR_UNSUPPORTED;
+  if (bn == 512 && (!args.pair || B.mn || (B2 && B2->mn))) return QLRT_ERR_UNSUPPORTED;
+  const int bbox = args.pair ? (bn > 256 ? 128 : bn / 2) : bn;  // B rows per TMA box
   if (!(B.mn ? make_tmap(&tb, B.ptr, N, K, B.ld, 64) : make_tmap(&tb, B.ptr, K, N, B.ld, bbox)))
     return QLRT_ERR_UNSUPPORTED;
   if (K2) {
@@ -1071,7 +1095,8 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   args.splits = effective_splits(args.splits, args.k_iters);
   if (args.csplit > 1) args.csplit = args.splits;  // every CTA of the cluster owns >= 1 k-iteration
   if (args.splits > 1 && K2) return QLRT_ERR_UNSUPPORTED;
-  if (args.sk_ws && args.splits == 1 && bn >= 64 && num_sms() <= kNumSMs && !args.share) {
+  // (not for the single-buffered 512-wide pair tiles: measured slower)
+  if (args.sk_ws && args.splits == 1 && bn >= 64 && bn <= 256 && num_sms() <= kNumSMs && !args.share) {
     // stream-K only for short grids (< 2 waves) that whole-tile waves would
     // leave > 10% idle: measured, its partial-tile traffic and spread-out
     // L2 footprint cost ~5% on long grids (tools/ab.py QLRT_STREAMK=0/1)
@@ -1087,6 +1112,9 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
     args.streamk = 0;
   }
   switch (bn) {
+    case 512:
+      return nf4 ? launch_t<512, true, true>(ta, tb, ta2, tb2, tc, tk, args, s)
+                 : launch_t<512, false, true>(ta, tb, ta2, tb2, tc, tk, args, s);
     case 256:
       if (args.pair) return nf4 ? launch_t<256, true, true>(ta, tb, ta2, tb2, tc, tk, args, s)
                                 : launch_t<256, false, true>(ta, tb, ta2, tb2, tc, tk, args, s);
@@ -1224,7 +1252,8 @@ static size_t dbl_bytes(int64_t k_in, int64_t n_out, int rank) {
   return align256((size_t)mx * 2 * rank * 2);
 }
 // stream-K partials (one BM x 256 fp32 tile per CTA) + flags
-static size_t sk_bytes() { return align256((size_t)kNumSMs * BM * 256 * 4) + align256((size_t)kNumSMs * 4); }
+constexpr int kSkCols = 512;  // widest tile (pair 256 x 512)
+static size_t sk_bytes() { return align256((size_t)kNumSMs * BM * kSkCols * 4) + align256((size_t)kNumSMs * 4); }
 // layout of the linear workspace: [split-K partials][constants][stream-K][doubled adapter]
 static void* dbl_region(void* ws, size_t ws_bytes, int64_t k_in, int64_t n_out, int rank) {
   return (uint8_t*)ws + (ws_bytes - dbl_bytes(k_in, n_out, rank));
@@ -1232,7 +1261,7 @@ static void* dbl_region(void* ws, size_t ws_bytes, int64_t k_in, int64_t n_out, 
 static void sk_region(void* ws, size_t ws_bytes, int64_t k_in, int64_t n_out, int rank, Args& a) {
   uint8_t* b = (uint8_t*)ws + (ws_bytes - dbl_bytes(k_in, n_out, rank) - sk_bytes());
   a.sk_ws = (float*)b;
-  a.sk_flags = (int*)(b + align256((size_t)kNumSMs * BM * 256 * 4));
+  a.sk_flags = (int*)(b + align256((size_t)kNumSMs * BM * kSkCols * 4));
 }
 
 }  // namespace gemm
@@ -1278,7 +1307,7 @@ qlrt_status qlrt_gemm_bf16(const void* a, const void* b, void* d, int64_t m, int
     uint8_t* b = (uint8_t*)workspace + (workspace_bytes - gemm::sk_bytes());
     b = (uint8_t*)(((uintptr_t)b) & ~(uintptr_t)255);
     sk.sk_ws = (float*)b;
-    sk.sk_flags = (int*)(b + gemm::align256((size_t)kNumSMs * gemm::BM * 256 * 4));
+    sk.sk_flags = (int*)(b + gemm::align256((size_t)kNumSMs * gemm::BM * gemm::kSkCols * 4));
     workspace_bytes = (size_t)(b - (uint8_t*)workspace);
   }
   return gemm::plain(bn, A, B, m, n, k, alpha, d, out_t ? m : n, out_f32, out_t, (float*)workspace, workspace_bytes,
@@ -1317,7 +1346,8 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   a.out_f32 = 0;
   a.out_t = 1;
   a.alpha = 1.0f;
-  a.pair = gemm::pair_policy(0);
+  const int bn_main = gemm::tile512_policy() ? 512 : 256;
+  a.pair = bn_main == 512 ? 1 : gemm::pair_policy(0);
   a.share = a.pair ? 0 : gemm::share_policy();
   if (gemm::streamk_policy()) { a.sk_ws = sk.sk_ws; a.sk_flags = sk.sk_flags; }
   if ((rc = gemm::fill_nf4(a, w, 1, consts, st)) != QLRT_OK) return rc;
@@ -1330,7 +1360,7 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
       return QLRT_ERR_CUDA;
   }
   Operand A2{l2d, N, 1}, B2{ts_out, 2 * rank, 0};
-  return gemm::run(256, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, K, 2 * rank, a, st);
+  return gemm::run(bn_main, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, K, 2 * rank, a, st);
 }
 
 qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_t m, const void* x, const void* ts,
@@ -1365,7 +1395,8 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   a.out_f32 = 0;
   a.out_t = 1;
   a.alpha = 1.0f;
-  a.pair = gemm::pair_policy(0);
+  const int bn_main = gemm::tile512_policy() ? 512 : 256;
+  a.pair = bn_main == 512 ? 1 : gemm::pair_policy(0);
   a.share = a.pair ? 0 : gemm::share_policy();
   if (gemm::streamk_policy()) { a.sk_ws = sk.sk_ws; a.sk_flags = sk.sk_flags; }
   if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
@@ -1379,7 +1410,7 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
         return QLRT_ERR_CUDA;
   }
   Operand A2{l1d, 2 * rank, 0}, B2{dt_out, 2 * rank, 0};
-  rc = gemm::run(256, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, N, 2 * rank, a, st);
+  rc = gemm::run(bn_main, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, N, 2 * rank, a, st);
   if (rc != QLRT_OK || rank == 0) return rc;
   // dl2^T[N, r] = dY^T (Ts_hi + Ts_lo): A = dY (MN-major [m][N]), B = [Ts_hi | Ts_lo] (MN-major [m][2r]);
   // the pair is folded in the reduction, stored transposed into dl2[r][N]

@@ -405,7 +405,7 @@ def main() -> None:
     achieved = k_flops / (k_ms / 1e3) / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": tf_burst, "unit": "TFLOP/s",
                 "frac": achieved / tf_burst, "traffic": traffic_of("fused_fwd_c2"),
-                "kernel": "gemm_kernel<256,NF4> (fused NF4 dequant + tcgen05 GEMM), fwd 2048x4096x11008, alone",
+                "kernel": "gemm_kernel<512,NF4,pair> (fused NF4 dequant + tcgen05 GEMM, 256x512 2-CTA tiles), fwd 2048x4096x11008, alone",
                 "kernel_ms": k_ms, "peak_kind": f"{peak_kind} burst bf16 (cuBLAS)",
                 "algorithmic_flops_per_launch": k_flops}
 

@@ -79,6 +79,10 @@ struct Args {
   // token tiles; each CTA decodes half of every A stage into both CTAs' shared
   // memory (DSMEM stores), halving the per-SM dequant work
   int share;
+  // 512-wide pair tiles: work items >= tail_from are half tiles (one N = 256
+  // UMMA each) -- the last partial wave of whole tiles is split in two so it
+  // finishes in about half the time; 0 = no half tiles
+  int tail_from;
 };
 
 template <int BN, bool NF4, bool PAIR = false>
@@ -320,15 +324,6 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
   int unit0 = (PAIR || share) ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   int n_units = (PAIR || share) ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
-  const int m_tiles = (p.M + BMP - 1) / BMP;
-  const int n_tiles_real = (p.N + BN - 1) / BN;
-  const int n_tiles = share ? (n_tiles_real + 1) / 2 : n_tiles_real;  // scheduling grid (pairs of token tiles)
-  const int n_tiles_total = m_tiles * n_tiles * p.splits;
-  const int kc = (p.k_iters + p.splits - 1) / p.splits;
-  if (csplit) {
-    unit0 = (int)zrank * (m_tiles * n_tiles) + (int)(blockIdx.x / p.csplit);
-    n_units = n_tiles_total;  // exactly one segment per CTA
-  }
   // accumulators: double-buffered up to BN = 256; BN = 512 (pair tiles of
   // 256 x 512, two N = 256 UMMAs per k-step) fills TMEM with one buffer
   constexpr int NACC = 2 * BN <= 512 ? 2 : 1;
@@ -336,9 +331,29 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
   constexpr int UN = BN > 256 ? 256 : BN;   // N of one UMMA
   constexpr int NUM = BN / UN;              // UMMAs per k16 step
   static_assert(!(BN > 256) || PAIR, "BN = 512 needs 2-CTA pairs");
+  const int m_tiles = (p.M + BMP - 1) / BMP;
+  const int n_tiles_real = (p.N + BN - 1) / BN;
+  const int n_tiles = share ? (n_tiles_real + 1) / 2 : n_tiles_real;  // scheduling grid (pairs of token tiles)
+  const int n_tiles_total0 = m_tiles * n_tiles * p.splits;
+  const bool halves = NUM > 1 && p.tail_from > 0 && p.tail_from < n_tiles_total0;
+  // work items: whole tiles [0, tail_from), then two half tiles per remaining tile
+  const int n_tiles_total = halves ? p.tail_from + 2 * (n_tiles_total0 - p.tail_from) : n_tiles_total0;
+  const int kc = (p.k_iters + p.splits - 1) / p.splits;
+  if (csplit) {
+    unit0 = (int)zrank * (m_tiles * n_tiles) + (int)(blockIdx.x / p.csplit);
+    n_units = n_tiles_total;  // exactly one segment per CTA
+  }
   // iterations of a whole tile (stream-K needs splits == 1)
   const int T_tile = p.streamk ? p.k_iters + p.k_iters_aug : (1 << 30);
-  auto seg_extent = [&](int tile, int& mt, int& nt, int& z, int& kb, int& nk, int& total) {
+  // item -> tile and half (-1 = whole tile; 0 / 1 = which N = 256 half)
+  auto item_half = [&](int item, int& tile) -> int {
+    if (!halves || item < p.tail_from) { tile = item; return -1; }
+    tile = p.tail_from + (item - p.tail_from) / 2;
+    return (item - p.tail_from) & 1;
+  };
+  auto seg_extent = [&](int item, int& mt, int& nt, int& z, int& kb, int& nk, int& total) {
+    int tile;
+    item_half(item, tile);
     tile_coords(tile, m_tiles, n_tiles, mt, nt, z);
     if (share) nt = 2 * nt + (int)srank;
     kb = z * kc;
@@ -422,8 +437,11 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           const int bmn = aug ? p.b2_mn : p.b_mn;
           const int k0 = (aug ? (i - nk) : (kb + i)) * BK;
           const bool a_tma = aug || !NF4;
+          int tdummy;
+          const int hh = item_half(tile, tdummy);
+          const int b_bytes = hh >= 0 ? L::B_STAGE / NUM : L::B_STAGE;
           if (leader)  // one arrival per phase; both CTAs' bytes
-            ptx::mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * (L::B_STAGE + (a_tma ? A_STAGE : 0)));
+            ptx::mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * (b_bytes + (a_tma ? A_STAGE : 0)));
           uint8_t* a_dst = sA + s * A_STAGE;
           uint8_t* b_dst = sB + s * L::B_STAGE;
           if (a_tma) {
@@ -440,7 +458,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           } else if (NUM > 1) {  // one 128-token half of each UMMA's B, at the same offset in both CTAs
 #pragma unroll
             for (int j = 0; j < NUM; ++j)
-              tma(mb, &full[s], b_dst + j * (L::B_STAGE / NUM), k0, nt * BN + j * UN + (int)rank * (UN / 2));
+              if (hh < 0 || hh == j)
+                tma(mb, &full[s], b_dst + j * (L::B_STAGE / NUM), k0, nt * BN + j * UN + (int)rank * (UN / 2));
           } else {
             tma(mb, &full[s], b_dst, k0, n_cta);
           }
@@ -458,6 +477,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
         seg_extent(tile, mt, nt, z, kb, nk, total);
         i1 = min(i1, total);
         const uint32_t acc = local % NACC;
+        int tdummy;
+        const int hh = item_half(tile, tdummy);
         wait_x(&tempty[acc], ((local / NACC) & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -480,6 +501,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
                                       : ptx::sdesc_sw128(a_addr + kk * 32, 16, 1024);
 #pragma unroll
               for (int j = 0; j < NUM; ++j) {
+                if (hh >= 0 && hh != j) continue;
                 const uint32_t bj = b_addr + (uint32_t)(j * (L::B_STAGE / NUM));
                 const uint64_t bd = bmn ? ptx::sdesc_sw128(bj + kk * 2048, 8192, 1024)
                                         : ptx::sdesc_sw128(bj + kk * 32, 16, 1024);
@@ -616,9 +638,12 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
       // fold (hi/lo operand pairs, fold <= BN / 2, one column tile): out column
       // n = D[:, n] + D[:, n + fold]
       const bool direct_fold = p.fold && !((p.splits > 1 && !p.csplit) || p.to_ws);  // else the reduce kernel folds
-      const int cend = direct_fold ? p.fold : BN;
+      int tdummy;
+      const int hh = item_half(tile, tdummy);
+      const int cbeg = hh >= 0 ? hh * UN : 0;  // a half tile drains its own 256 columns
+      const int cend = direct_fold ? p.fold : (hh >= 0 ? cbeg + UN : BN);
 #pragma unroll 1
-      for (int c0 = 0; c0 < cend; c0 += EC) {
+      for (int c0 = cbeg; c0 < cend; c0 += EC) {
         uint32_t r[EC];
         if (partial) {
           ptx::tmem_ld<EC>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, r);
@@ -948,6 +973,12 @@ static int tile512_policy() {
   return e ? atoi(e) : 1;
 }
 
+// half tiles for the last partial wave of 512-wide pair tiles (QLRT_HALFTAIL=0 disables)
+static int halftail_policy() {
+  const char* e = getenv("QLRT_HALFTAIL");
+  return e ? atoi(e) : 1;
+}
+
 // programmatic dependent launch of the engine kernels (QLRT_PDL=0 disables it)
 static int pdl_policy() {
   const char* e = getenv("QLRT_PDL");
@@ -1094,6 +1125,16 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   args.b2_mn = B2 ? B2->mn : 0;
   args.splits = effective_splits(args.splits, args.k_iters);
   if (args.csplit > 1) args.csplit = args.splits;  // every CTA of the cluster owns >= 1 k-iteration
+  args.tail_from = 0;
+  if (bn == 512 && args.pair && !args.streamk && args.splits == 1 && halftail_policy()) {
+    // whole 256 x 512 tiles for the full waves, half tiles for the last partial one
+    const int64_t tiles = ((M + 255) / 256) * ((N + 511) / 512);
+    const int64_t units = num_sms() / 2;
+    const int64_t full = (tiles / units) * units;
+    // a half tile costs ~0.85 of a whole one (same dequant): only worth it when
+    // all the halves fit in one round
+    if (full > 0 && full < tiles && 2 * (tiles - full) <= units) args.tail_from = (int)full;
+  }
   if (args.splits > 1 && K2) return QLRT_ERR_UNSUPPORTED;
   // (not for the single-buffered 512-wide pair tiles: measured slower)
   if (args.sk_ws && args.splits == 1 && bn >= 64 && bn <= 256 && num_sms() <= kNumSMs && !args.share) {

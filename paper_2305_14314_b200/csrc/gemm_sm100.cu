@@ -85,6 +85,9 @@ struct Args {
   int tail_from;
 };
 
+#ifndef SKINNY_STAGES
+#define SKINNY_STAGES 4
+#endif
 template <int BN, bool NF4, bool PAIR = false>
 struct Smem {
   static constexpr int BNC = PAIR ? BN / 2 : BN;       // B rows (tokens) held by this CTA
@@ -97,7 +100,11 @@ struct Smem {
   static constexpr int CRING = CST * (CODE_BYTES + CONST_BYTES);
   // as many A/B stages as fit in ~226 KB, at most 8, even
   static constexpr int FIT = (226 * 1024 - EPI_BYTES - CRING) / (A_STAGE + B_STAGE);
-  static constexpr int STAGES = (FIT > 8 ? 8 : FIT) & ~1;
+  // skinny plain GEMMs (BN <= 128, the adapter products): few stages, so two
+  // CTAs fit per SM and independent skinny GEMMs can run concurrently
+  static constexpr int CAP = (!NF4 && BN <= 64) ? SKINNY_STAGES : ((!NF4 && BN <= 128) ? 3 : 8);
+  // (the NF4 producers alternate stages between groups: even count there)
+  static constexpr int STAGES = NF4 ? ((FIT > CAP ? CAP : FIT) & ~1) : (FIT > CAP ? CAP : FIT);
   static constexpr int C_OFF = STAGES * (A_STAGE + B_STAGE);
   static constexpr int EPI_OFF = C_OFF + CRING;
   static constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
@@ -964,6 +971,25 @@ static int pair_policy(int dflt) {
   return v < 0 ? dflt : v;
 }
 
+// A per-device side stream (+ fork / join events) for independent skinny
+// adapter GEMMs; QLRT_SIDE=0 keeps everything on the caller's stream.
+static cudaStream_t side_stream() {
+  const char* e = getenv("QLRT_SIDE");
+  if (e && !atoi(e)) return nullptr;
+  static cudaStream_t st[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!st[dev] && cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking) != cudaSuccess) st[dev] = nullptr;
+  return st[dev];
+}
+static cudaEvent_t side_event(int i) {
+  static cudaEvent_t ev[64][2] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!ev[dev][i]) cudaEventCreateWithFlags(&ev[dev][i], cudaEventDisableTiming);
+  return ev[dev][i];
+}
+
 // 256 x 512 pair tiles for the fused NF4 GEMMs (QLRT_TILE512=0 falls back to
 // 128 x 256 single-CTA tiles): the 2-CTA pair halves the B traffic per SM and
 // the two N = 256 UMMAs per k-step halve the dequant work per MMA -- measured
@@ -1369,6 +1395,21 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   qlrt_status rc;
   gemm::Args sk{};
   gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
+  // the block-constant prepass (when no cache is given) and the doubled l2
+  // copies run on the side stream while Ts is computed here
+  gemm::Args a{};
+  cudaStream_t side = rank > 0 ? gemm::side_stream() : nullptr;
+  if (side && (cudaEventRecord(gemm::side_event(0), st) != cudaSuccess ||
+               cudaStreamWaitEvent(side, gemm::side_event(0), 0) != cudaSuccess))
+    side = nullptr;
+  cudaStream_t aux = side ? side : st;
+  if ((rc = gemm::fill_nf4(a, w, 1, consts, aux)) != QLRT_OK) return rc;
+  __nv_bfloat16* l2d = (__nv_bfloat16*)gemm::dbl_region(workspace, ws_bytes, K, N, rank);
+  if (rank) {
+    if (cudaMemcpyAsync(l2d, l2, (size_t)rank * N * 2, cudaMemcpyDeviceToDevice, aux) != cudaSuccess ||
+        cudaMemcpyAsync(l2d + (size_t)rank * N, l2, (size_t)rank * N * 2, cudaMemcpyDeviceToDevice, aux) != cudaSuccess)
+      return QLRT_ERR_CUDA;
+  }
   if (rank > 0) {
     // Ts[m, 0:r] + Ts[m, r:2r] = s * Xa l1 as a bf16 hi/lo pair:
     //   A = Xa (K-major, [m][K]), B = l1 (MN-major, [K][r])
@@ -1377,8 +1418,10 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
                      &sk);
     if (rc != QLRT_OK) return rc;
   }
+  if (side && (cudaEventRecord(gemm::side_event(1), side) != cudaSuccess ||
+               cudaStreamWaitEvent(st, gemm::side_event(1), 0) != cudaSuccess))
+    return QLRT_ERR_CUDA;
   // Y^T[N, m] = W^T X^T (+ l2^T Ts^T): A = NF4 (MN-major image), B = X (K-major)
-  gemm::Args a{};
   a.M = (int)N;
   a.N = (int)m;
   a.splits = 1;
@@ -1391,15 +1434,8 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   a.pair = bn_main == 512 ? 1 : gemm::pair_policy(0);
   a.share = a.pair ? 0 : gemm::share_policy();
   if (gemm::streamk_policy()) { a.sk_ws = sk.sk_ws; a.sk_flags = sk.sk_flags; }
-  if ((rc = gemm::fill_nf4(a, w, 1, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{x, K, 0};
   // augmented segment K2 = 2r: [l2 ; l2]^T [Ts_hi | Ts_lo]^T, i.e. the pair at ~16-bit precision
-  __nv_bfloat16* l2d = (__nv_bfloat16*)gemm::dbl_region(workspace, ws_bytes, K, N, rank);
-  if (rank) {
-    if (cudaMemcpyAsync(l2d, l2, (size_t)rank * N * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
-        cudaMemcpyAsync(l2d + (size_t)rank * N, l2, (size_t)rank * N * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-      return QLRT_ERR_CUDA;
-  }
   Operand A2{l2d, N, 1}, B2{ts_out, 2 * rank, 0};
   return gemm::run(bn_main, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, K, 2 * rank, a, st);
 }
@@ -1418,6 +1454,23 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   qlrt_status rc;
   gemm::Args sk{};
   gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
+  cudaStream_t side = nullptr;
+  if (rank > 0) {
+    // dl2^T[N, r] = dY^T (Ts_hi + Ts_lo) needs only the inputs: it runs on a
+    // side stream (no split-K workspace) while dT, the fused dX GEMM and dl1
+    // run here -- the skinny kernels hold <= 2 CTAs per SM and overlap.
+    //   A = dY (MN-major [m][N]), B = [Ts_hi | Ts_lo] (MN-major [m][2r]); the
+    //   pair is folded in the epilogue, stored transposed into dl2[r][N]
+    if ((side = gemm::side_stream()) && cudaEventRecord(gemm::side_event(0), st) == cudaSuccess &&
+        cudaStreamWaitEvent(side, gemm::side_event(0), 0) == cudaSuccess) {
+    } else {
+      side = st;
+    }
+    Operand A{dy, N, 1}, B{ts, 2 * rank, 1};
+    rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, N, 2 * rank, m, 1.0f, dl2, N, 1, 1,
+                     side == st ? (float*)workspace : nullptr, side == st ? part_bytes : 0, side, rank);
+    if (rc != QLRT_OK) return rc;
+  }
   if (rank > 0) {
     // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):
     //   A = dY (K-major [m][N]), B = l2 (K-major [r][N])
@@ -1425,6 +1478,13 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
     rc = gemm::plain(64, A, B, m, rank, N, s, dt_out, 2 * rank, 0, 0, (float*)workspace, part_bytes, st, 0, rank,
                      &sk);
     if (rc != QLRT_OK) return rc;
+  }
+  // join the side stream (dl2) before the persistent fused GEMM: its CTAs need
+  // every SM free, a straggling skinny kernel would delay the whole grid
+  if (side && side != st) {
+    if (cudaEventRecord(gemm::side_event(1), side) != cudaSuccess ||
+        cudaStreamWaitEvent(st, gemm::side_event(1), 0) != cudaSuccess)
+      return QLRT_ERR_CUDA;
   }
   // dX^T[K, m] = W dY^T (+ l1 dT^T): A = NF4 (K-major image), B = dY (K-major)
   gemm::Args a{};
@@ -1453,14 +1513,7 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   Operand A2{l1d, 2 * rank, 0}, B2{dt_out, 2 * rank, 0};
   rc = gemm::run(bn_main, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, N, 2 * rank, a, st);
   if (rc != QLRT_OK || rank == 0) return rc;
-  // dl2^T[N, r] = dY^T (Ts_hi + Ts_lo): A = dY (MN-major [m][N]), B = [Ts_hi | Ts_lo] (MN-major [m][2r]);
-  // the pair is folded in the reduction, stored transposed into dl2[r][N]
-  {
-    Operand A{dy, N, 1}, B{ts, 2 * rank, 1};
-    rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, N, 2 * rank, m, 1.0f, dl2, N, 1, 1, (float*)workspace,
-                     part_bytes, st, rank, 0, &sk);
-    if (rc != QLRT_OK) return rc;
-  }
+  // (dl2 ran on the side stream; joined below)
   // dl1[K, r] = Xa^T (dT_hi + dT_lo): A = Xa (MN-major [m][K]), B = [dT_hi | dT_lo] (MN-major [m][2r])
   {
     Operand A{x, K, 1}, B{dt_out, 2 * rank, 1};

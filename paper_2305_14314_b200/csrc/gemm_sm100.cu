@@ -27,10 +27,16 @@ namespace gemm {
 constexpr int BM = 128;
 constexpr int BK = 64;              // one 128B swizzle row of bf16
 constexpr int A_STAGE = BM * BK * 2;  // 16 KB
-constexpr int kTmaWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2, kNumEpiWarps = 4, kXfWarp0 = 6;
+#ifndef QLRT_EPI_WARPS
+#define QLRT_EPI_WARPS 4
+#endif
+// epilogue warps: 4 or 8 (two per TMEM lane quarter, alternate 32-column chunks)
+constexpr int kTmaWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2, kNumEpiWarps = QLRT_EPI_WARPS;
+constexpr int kXfWarp0 = kEpiWarp0 + kNumEpiWarps;
 constexpr int kNumXfWarps = 8;
 constexpr int kCstWarp = kXfWarp0 + kNumXfWarps;  // NF4: codes (TMA) + block-constant producer
-constexpr int kNF4Threads = (kCstWarp + 1) * 32;  // 480
+constexpr int kNF4Threads = (kCstWarp + 1) * 32;  // 480 (4 epilogue warps) or 608 (8)
+constexpr int kPlainThreads = (2 + kNumEpiWarps) * 32;
 
 struct Args {
   int M, N;             // output extent (UMMA M rows, N cols)
@@ -83,6 +89,7 @@ struct Args {
   // UMMA each) -- the last partial wave of whole tiles is split in two so it
   // finishes in about half the time; 0 = no half tiles
   int tail_from;
+  int tma_out;          // D^T bf16 via TMA stores from the epilogue staging tile
 };
 
 #ifndef SKINNY_STAGES
@@ -290,10 +297,11 @@ __device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[E
 // barriers, and its commits are multicast to both CTAs.
 // ---------------------------------------------------------------------------
 template <int BN, bool NF4, bool PAIR>
-__global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
+__global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmK,
+                const __grid_constant__ CUtensorMap tmO,
                 const __grid_constant__ Args p) {
   using L = Smem<BN, NF4, PAIR>;
   constexpr int STAGES = L::STAGES;
@@ -533,6 +541,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
     // ======================= epilogue (each CTA drains its own TMEM rows) =======================
     constexpr int EC = BN < 32 ? BN : 32;   // columns per tcgen05.ld
     const int quarter = warp & 3;           // TMEM lane quarter this warp may access
+    const int csub = (warp - kEpiWarp0) >> 2;  // which alternate 32-column chunks (8 epilogue warps)
+    constexpr int CSTEP = (kNumEpiWarps / 4) * (BN < 32 ? BN : 32);
     const int row = quarter * 32 + lane;    // accumulator row (M index within this CTA's half)
     uint32_t local = 0;
     Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
@@ -616,7 +626,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
       if (csplit && zrank != 0) {  // stage this split's accumulator, signal rank 0, done
         float* st = reinterpret_cast<float*>(sA);
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += EC) {
+        for (int c0 = csub * EC; c0 < BN; c0 += CSTEP) {
           uint32_t r[EC];
           ptx::tmem_ld<EC>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, r);
 #pragma unroll
@@ -650,7 +660,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
       const int cbeg = hh >= 0 ? hh * UN : 0;  // a half tile drains its own 256 columns
       const int cend = direct_fold ? p.fold : (hh >= 0 ? cbeg + UN : BN);
 #pragma unroll 1
-      for (int c0 = cbeg; c0 < cend; c0 += EC) {
+      for (int c0 = cbeg + csub * EC; c0 < cend; c0 += CSTEP) {
         uint32_t r[EC];
         if (partial) {
           ptx::tmem_ld<EC>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, r);
@@ -671,7 +681,28 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
           for (int j = 0; j < EC; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
         }
         const int64_t n0 = (int64_t)nt * BN + c0;
-        if (EC == 32 && p.out_t && !p.out_f32 && p.splits == 1 && !p.to_ws) {
+#ifdef QLRT_HACK_NOEPI
+        if (NF4) { if (r[0] == 0x7fffffffu && lane == 99) static_cast<uint32_t*>(p.out)[0] = r[1]; continue; }
+#endif
+        if (EC == 32 && p.tma_out) {
+          // D^T: the 32 x 32 tile staged in shared memory (row = token n0 + j,
+          // 32 features), written by one TMA store (clips at the tensor edge);
+          // the staging tile is reused once the previous store has read it
+          __nv_bfloat16* st = sE + (warp - kEpiWarp0) * 32 * 32;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < EC; ++j) st[j * 32 + lane] = __float2bfloat16_rn(__uint_as_float(r[j]) * p.alpha);
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tmO),
+                "r"((int)(m_base + quarter * 32)), "r"((int)n0), "r"(ptx::smem_u32(st))
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        } else if (EC == 32 && p.out_t && !p.out_f32 && p.splits == 1 && !p.to_ws) {
           // D^T tile through shared memory: row j = token n0+j, 32 features per row,
           // then 16B vector stores (4 lanes cover one 64B output row segment)
           __nv_bfloat16* st = sE + (warp - kEpiWarp0) * 32 * 32;
@@ -718,6 +749,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : 192, 1)
         }
       }
     }
+    if (p.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (NF4 && warp == kCstWarp) {
     // ======================= codes + block-constant producer =======================
     // Runs ahead of the dequant warps through its own ring, TMA-loading the
@@ -942,6 +974,21 @@ static bool make_tmap(CUtensorMap* m, const void* base, int64_t inner, int64_t o
   return r == CUDA_SUCCESS;
 }
 
+// bf16 output written transposed by TMA stores: tensor [outer = N tokens][inner = M
+// features] with row pitch ld, box 32 x 32, no swizzle (the epilogue's staging tile)
+static bool make_tmap_store(CUtensorMap* m, const void* base, int64_t inner, int64_t outer, int64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || (((uintptr_t)base) & 15) || ((ld * 2) & 15)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // packed NF4 codes viewed as a uint8 matrix [rows][bytes], no swizzle
 static bool make_tmap_u8(CUtensorMap* m, const void* base, int64_t inner_bytes, int64_t rows, int box_inner,
                          int box_rows) {
@@ -999,6 +1046,12 @@ static int tile512_policy() {
   return e ? atoi(e) : 1;
 }
 
+// epilogue output via TMA stores (QLRT_TMAOUT=0: ld.shared + 16 B st.global)
+static int tma_out_policy() {
+  const char* e = getenv("QLRT_TMAOUT");
+  return e ? atoi(e) : 1;
+}
+
 // half tiles for the last partial wave of 512-wide pair tiles (QLRT_HALFTAIL=0 disables)
 static int halftail_policy() {
   const char* e = getenv("QLRT_HALFTAIL");
@@ -1038,7 +1091,8 @@ static int num_sms() {
 
 template <int BN, bool NF4, bool PAIR = false>
 static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2, const CUtensorMap& b2,
-                            const CUtensorMap& c, const CUtensorMap& k, const Args& args, cudaStream_t s) {
+                            const CUtensorMap& c, const CUtensorMap& k, const CUtensorMap& o, const Args& args,
+                            cudaStream_t s) {
   using L = Smem<BN, NF4, PAIR>;
   auto kern = gemm_kernel<BN, NF4, PAIR>;
   static bool attr = false;
@@ -1057,7 +1111,7 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
   if (args.streamk && (int64_t)tiles * kSkMaxSplit < units) units = tiles * kSkMaxSplit;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(units * (PAIR ? 2 : 1));
-  cfg.blockDim = dim3(NF4 ? kNF4Threads : 192);
+  cfg.blockDim = dim3(NF4 ? kNF4Threads : kPlainThreads);
   cfg.dynamicSmemBytes = L::BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attrs[2];
@@ -1096,7 +1150,7 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
     cfg.attrs = attrs;
     cfg.numAttrs += 1;
   }
-  if (cudaLaunchKernelEx(&cfg, kern, a, b, a2, b2, c, k, args) != cudaSuccess) return QLRT_ERR_CUDA;
+  if (cudaLaunchKernelEx(&cfg, kern, a, b, a2, b2, c, k, o, args) != cudaSuccess) return QLRT_ERR_CUDA;
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }
@@ -1111,7 +1165,7 @@ static int effective_splits(int splits, int k_iters) {
 // args.nf4_mode != 0 makes A the quantized weight (A operand ignored).
 static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand* A2, const Operand* B2, int64_t K,
                        int64_t K2, Args args, cudaStream_t s) {
-  CUtensorMap ta{}, tb{}, ta2{}, tb2{}, tc{}, tk{};
+  CUtensorMap ta{}, tb{}, ta2{}, tb2{}, tc{}, tk{}, to{};
   const bool nf4 = args.nf4_mode != 0;
   if (nf4) {
     // packed codes as a uint8 matrix [w_rows][w_cols/2]; constants fp32 [w_rows][kpitch]
@@ -1178,17 +1232,23 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   } else {
     args.streamk = 0;
   }
+  // bf16 D^T output through TMA stores (32 features x 32 tokens per box)
+  args.tma_out = 0;
+  if (args.out_t && !args.out_f32 && args.splits == 1 && !args.to_ws && !args.out_split && tma_out_policy() &&
+      make_tmap_store(&to, args.out, args.M, args.N, args.ldo))
+    args.tma_out = 1;
+  if (!args.tma_out) to = tb;
   switch (bn) {
     case 512:
-      return nf4 ? launch_t<512, true, true>(ta, tb, ta2, tb2, tc, tk, args, s)
-                 : launch_t<512, false, true>(ta, tb, ta2, tb2, tc, tk, args, s);
+      return nf4 ? launch_t<512, true, true>(ta, tb, ta2, tb2, tc, tk, to, args, s)
+                 : launch_t<512, false, true>(ta, tb, ta2, tb2, tc, tk, to, args, s);
     case 256:
-      if (args.pair) return nf4 ? launch_t<256, true, true>(ta, tb, ta2, tb2, tc, tk, args, s)
-                                : launch_t<256, false, true>(ta, tb, ta2, tb2, tc, tk, args, s);
-      return nf4 ? launch_t<256, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<256, false>(ta, tb, ta2, tb2, tc, tk, args, s);
-    case 128: return nf4 ? launch_t<128, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<128, false>(ta, tb, ta2, tb2, tc, tk, args, s);
-    case 64: return nf4 ? launch_t<64, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<64, false>(ta, tb, ta2, tb2, tc, tk, args, s);
-    case 16: return nf4 ? launch_t<16, true>(ta, tb, ta2, tb2, tc, tk, args, s) : launch_t<16, false>(ta, tb, ta2, tb2, tc, tk, args, s);
+      if (args.pair) return nf4 ? launch_t<256, true, true>(ta, tb, ta2, tb2, tc, tk, to, args, s)
+                                : launch_t<256, false, true>(ta, tb, ta2, tb2, tc, tk, to, args, s);
+      return nf4 ? launch_t<256, true>(ta, tb, ta2, tb2, tc, tk, to, args, s) : launch_t<256, false>(ta, tb, ta2, tb2, tc, tk, to, args, s);
+    case 128: return nf4 ? launch_t<128, true>(ta, tb, ta2, tb2, tc, tk, to, args, s) : launch_t<128, false>(ta, tb, ta2, tb2, tc, tk, to, args, s);
+    case 64: return nf4 ? launch_t<64, true>(ta, tb, ta2, tb2, tc, tk, to, args, s) : launch_t<64, false>(ta, tb, ta2, tb2, tc, tk, to, args, s);
+    case 16: return nf4 ? launch_t<16, true>(ta, tb, ta2, tb2, tc, tk, to, args, s) : launch_t<16, false>(ta, tb, ta2, tb2, tc, tk, to, args, s);
   }
   return QLRT_ERR_UNSUPPORTED;
 }

@@ -90,6 +90,7 @@ struct Args {
   // finishes in about half the time; 0 = no half tiles
   int tail_from;
   int tma_out;          // D^T bf16 via TMA stores from the epilogue staging tile
+  int stagger;          // 512-wide tiles: per-half accumulator release (drain overlaps MMAs)
 };
 
 #ifndef SKINNY_STAGES
@@ -494,16 +495,22 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
         const uint32_t acc = local % NACC;
         int tdummy;
         const int hh = item_half(tile, tdummy);
-        wait_x(&tempty[acc], ((local / NACC) & 1) ^ 1);
+        // 512-wide tiles (one accumulator): the epilogue frees the two 256-column
+        // halves separately (tempty[0], tempty[1]); the first `pre` stages of
+        // the tile issue their half-0 MMAs as soon as half 0 is drained and
+        // their half-1 MMAs once half 1 is, so the drain overlaps the MMAs
+        const bool split = NUM == 2 && NACC == 1 && p.stagger;
+        const int pre = (split && hh < 0) ? min(STAGES, i1 - i0) : 0;
+        if (split) {
+          wait_x(&tempty[0], (local & 1) ^ 1);
+          if (pre == 0) wait_x(&tempty[1], (local & 1) ^ 1);
+        } else {
+          wait_x(&tempty[acc], ((local / NACC) & 1) ^ 1);
+        }
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int i = i0; i < i1; ++i, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
+        auto issue = [&](int i, int s, int jsel, bool commit) {  // jsel: -1 both halves, else that half
           const bool aug = i >= nk;
-          wait_x(&full[s], ph);
-          if (NF4) wait_x(&afull[s], ph);
-          ptx::tc_fence_after();
           const int amn = aug ? p.a2_mn : (NF4 ? (p.nf4_mode == 1) : p.a_mn);
           const int bmn = aug ? p.b2_mn : p.b_mn;
           const uint32_t idesc = ptx::idesc_bf16(BMP, UN, amn, bmn);
@@ -516,7 +523,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
                                       : ptx::sdesc_sw128(a_addr + kk * 32, 16, 1024);
 #pragma unroll
               for (int j = 0; j < NUM; ++j) {
-                if (hh >= 0 && hh != j) continue;
+                if ((hh >= 0 && hh != j) || (jsel >= 0 && jsel != j)) continue;
                 const uint32_t bj = b_addr + (uint32_t)(j * (L::B_STAGE / NUM));
                 const uint64_t bd = bmn ? ptx::sdesc_sw128(bj + kk * 2048, 8192, 1024)
                                         : ptx::sdesc_sw128(bj + kk * 32, 16, 1024);
@@ -524,11 +531,34 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
                 else ptx::umma_bf16(d_tmem + j * UN, ad, bd, idesc, (i != i0) || kk != 0);
               }
             }
-            if (PAIR) ptx::umma_commit_pair_mc(&empty[s], 0x3);
-            else if (share) ptx::umma_commit_mc(&empty[s], 0x3);  // frees the slot in both CTAs
-            else ptx::umma_commit(&empty[s]);
+            if (commit) {
+              if (PAIR) ptx::umma_commit_pair_mc(&empty[s], 0x3);
+              else if (share) ptx::umma_commit_mc(&empty[s], 0x3);  // frees the slot in both CTAs
+              else ptx::umma_commit(&empty[s]);
+            }
           }
           __syncwarp();
+        };
+        if (pre > 0) {
+          for (int q = 0; q < pre; ++q) {  // half 0 of the first stages
+            const uint32_t itq = it + (uint32_t)q;
+            const int s = itq % STAGES;
+            wait_x(&full[s], (itq / STAGES) & 1);
+            if (NF4) wait_x(&afull[s], (itq / STAGES) & 1);
+            ptx::tc_fence_after();
+            issue(i0 + q, s, 0, false);
+          }
+          wait_x(&tempty[1], (local & 1) ^ 1);
+          ptx::tc_fence_after();
+          for (int q = 0; q < pre; ++q, ++it) issue(i0 + q, it % STAGES, 1, true);  // their half 1
+        }
+        for (int i = i0 + pre; i < i1; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          wait_x(&full[s], ph);
+          if (NF4) wait_x(&afull[s], ph);
+          ptx::tc_fence_after();
+          issue(i, s, -1, true);
         }
         if (lane == 0) {
           if (PAIR) ptx::umma_commit_pair_mc(&tfull[acc], 0x3);
@@ -732,10 +762,22 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
         } else if (m < p.M) {
           store_chunk<EC>(p, r, m, n0, z);
         }
+        if (NUM == 2 && NACC == 1 && p.stagger && hh < 0 && c0 + CSTEP >= UN && c0 < UN) {
+          ptx::tc_fence_before();  // this warp's reads of columns [0, 256) are done
+          __syncwarp();
+          if (lane == 0) arrive_leader(&tempty[0]);
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) arrive_leader(&tempty[acc]);
+      if (NUM == 2 && NACC == 1 && p.stagger) {  // half 1 (and half 0 if not released in the loop)
+        if (lane == 0) {
+          if (!(hh < 0 && !partial)) arrive_leader(&tempty[0]);
+          arrive_leader(&tempty[1]);
+        }
+      } else if (lane == 0) {
+        arrive_leader(&tempty[acc]);
+      }
       if (v_end > unit0 + 1) {  // every epilogue warp consumed the partials: re-arm the flags
         asm volatile("bar.sync 1, %0;" ::"n"(kNumEpiWarps * 32) : "memory");
         if (warp == kEpiWarp0)
@@ -1046,6 +1088,13 @@ static int tile512_policy() {
   return e ? atoi(e) : 1;
 }
 
+// per-half accumulator release for 512-wide tiles (QLRT_STAGGER=1).  Off by
+// default: correct, but measured neutral-to-slower (tools/ab.py QLRT_STAGGER)
+static int stagger_policy() {
+  const char* e = getenv("QLRT_STAGGER");
+  return e ? atoi(e) : 0;
+}
+
 // epilogue output via TMA stores (QLRT_TMAOUT=0: ld.shared + 16 B st.global)
 static int tma_out_policy() {
   const char* e = getenv("QLRT_TMAOUT");
@@ -1205,6 +1254,7 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   args.b2_mn = B2 ? B2->mn : 0;
   args.splits = effective_splits(args.splits, args.k_iters);
   if (args.csplit > 1) args.csplit = args.splits;  // every CTA of the cluster owns >= 1 k-iteration
+  args.stagger = stagger_policy();
   args.tail_from = 0;
   if (bn == 512 && args.pair && !args.streamk && args.splits == 1 && halftail_policy()) {
     // whole 256 x 512 tiles for the full waves, half tiles for the last partial one

@@ -297,6 +297,25 @@ __device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[E
 // byte counts and producer arrivals of both CTAs land on the leader's
 // barriers, and its commits are multicast to both CTAs.
 // ---------------------------------------------------------------------------
+// QLRT_TRACE builds (tools/trace_gemm.py): per-CTA clock64 totals of where
+// each warp role waits, read back with qlrt_trace_fetch.  Not in the product build.
+#ifdef QLRT_TRACE
+constexpr int kTrSlots = 24;
+__device__ unsigned long long g_trace[2 * kNumSMs][kTrSlots];
+#define TRW(acc, stmt)                      \
+  {                                         \
+    const long long _t0 = clock64();        \
+    stmt;                                   \
+    acc += (unsigned long long)(clock64() - _t0); \
+  }
+#define TRDECL(...) unsigned long long __VA_ARGS__
+#define TRPUT(slot, v) atomicAdd(&g_trace[blockIdx.x % (2 * kNumSMs)][slot], (unsigned long long)(v))
+#else
+#define TRW(acc, stmt) stmt
+#define TRDECL(...)
+#define TRPUT(slot, v)
+#endif
+
 template <int BN, bool NF4, bool PAIR>
 __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -434,6 +453,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
     // ======================= TMA producer (every CTA loads its own halves) =======================
     if (lane == 0) {
       uint32_t it = 0;
+      TRDECL(tr_we = 0);
       Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
       int tile, i0, i1;
       while (sc.next(tile, i0, i1)) {
@@ -445,7 +465,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
         for (int i = i0; i < i1; ++i, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
-          ptx::mbar_wait(&empty[s], ph ^ 1);
+          TRW(tr_we, ptx::mbar_wait(&empty[s], ph ^ 1));
           const bool aug = i >= nk;
           const CUtensorMap* ma = aug ? &tmA2 : &tmA;
           const CUtensorMap* mb = aug ? &tmB2 : &tmB;
@@ -481,11 +501,14 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           }
         }
       }
+      TRPUT(9, tr_we);
     }
   } else if (warp == kMmaWarp) {
     // ======================= MMA issuer (leader only) =======================
     if (leader) {
       uint32_t it = 0, local = 0;
+      TRDECL(tr_wt = 0, tr_wf = 0, tr_wa = 0);
+      TRDECL(tr_t0 = clock64());
       Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
       int tile, i0, i1;
       for (; sc.next(tile, i0, i1); ++local) {
@@ -505,7 +528,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           wait_x(&tempty[0], (local & 1) ^ 1);
           if (pre == 0) wait_x(&tempty[1], (local & 1) ^ 1);
         } else {
-          wait_x(&tempty[acc], ((local / NACC) & 1) ^ 1);
+          TRW(tr_wt, wait_x(&tempty[acc], ((local / NACC) & 1) ^ 1));
         }
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -555,8 +578,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
         for (int i = i0 + pre; i < i1; ++i, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
-          wait_x(&full[s], ph);
-          if (NF4) wait_x(&afull[s], ph);
+          TRW(tr_wf, wait_x(&full[s], ph));
+          if (NF4) TRW(tr_wa, wait_x(&afull[s], ph));
           ptx::tc_fence_after();
           issue(i, s, -1, true);
         }
@@ -565,6 +588,9 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           else ptx::umma_commit(&tfull[acc]);
         }
         __syncwarp();
+      }
+      if (lane == 0) {
+        TRPUT(0, tr_wt); TRPUT(1, tr_wf); TRPUT(2, tr_wa); TRPUT(3, clock64() - tr_t0); TRPUT(11, local);
       }
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpiWarps) {
@@ -575,6 +601,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
     constexpr int CSTEP = (kNumEpiWarps / 4) * (BN < 32 ? BN : 32);
     const int row = quarter * 32 + lane;    // accumulator row (M index within this CTA's half)
     uint32_t local = 0;
+    TRDECL(tr_wt = 0, tr_dr = 0, tr_d0 = 0);
     Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
     const long long G = (long long)n_tiles_total * T_tile;
     int tile, i0, i1;
@@ -589,7 +616,10 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
       if (p.streamk && i0 == 0 && i1 < total)
         while (v_end < n_units && Sched::range_begin(G, v_end, n_units) < (long long)(tile + 1) * T_tile) ++v_end;
       const uint32_t acc = local % NACC;
-      ptx::mbar_wait(&tfull[acc], (local / NACC) & 1);
+      TRW(tr_wt, ptx::mbar_wait(&tfull[acc], (local / NACC) & 1));
+#ifdef QLRT_TRACE
+      tr_d0 = clock64();
+#endif
       ptx::tc_fence_after();
       if (v_end > unit0 + 1) {  // wait for the later units' partials of this tile (one flag per lane)
         for (int v0 = unit0 + 1; v0 < v_end; v0 += 32) {
@@ -770,6 +800,9 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
+#ifdef QLRT_TRACE
+      tr_dr += clock64() - tr_d0;
+#endif
       if (NUM == 2 && NACC == 1 && p.stagger) {  // half 1 (and half 0 if not released in the loop)
         if (lane == 0) {
           if (!(hh < 0 && !partial)) arrive_leader(&tempty[0]);
@@ -792,6 +825,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
       }
     }
     if (p.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (lane == 0 && warp == kEpiWarp0) { TRPUT(4, tr_wt); TRPUT(5, tr_dr); }
   } else if (NF4 && warp == kCstWarp) {
     // ======================= codes + block-constant producer =======================
     // Runs ahead of the dequant warps through its own ring, TMA-loading the
@@ -800,6 +834,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
     // matching fp32 block constants (fwd: 64 rows x 4; bwd: 128 rows x 4).
     if (lane == 0) {
       uint32_t cit = 0;
+      TRDECL(tr_wc = 0);
       const uint32_t kbytes = p.nf4_mode == 1 ? 64 * 16 : 128 * 16;
       Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
       int tile, i0, i1;
@@ -810,7 +845,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
         for (int i = i0; i < min(i1, nk); ++i, ++cit) {
           const int c = cit % CST;
           const int k0 = (kb + i) * BK;
-          ptx::mbar_wait(&cempty[c], ((cit / CST) & 1) ^ 1);
+          TRW(tr_wc, ptx::mbar_wait(&cempty[c], ((cit / CST) & 1) ^ 1));
           ptx::mbar_arrive_expect_tx(&cfull[c], L::CODE_BYTES + kbytes);
           uint8_t* cdst = sC + c * L::CODE_BYTES;
           float* kdst = sK + c * (L::CONST_BYTES / 4);
@@ -823,6 +858,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           }
         }
       }
+      TRPUT(10, tr_wc);
     }
   } else if (NF4 && warp >= kXfWarp0 && warp < kXfWarp0 + kNumXfWarps) {
     // ======================= NF4 dequant producer =======================
@@ -867,6 +903,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
       }
     };
     uint32_t it = 0, cit = 0;
+    TRDECL(tr_wc = 0, tr_we = 0, tr_t0 = clock64());
     Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
     int tile, i0, i1;
     while (sc.next(tile, i0, i1)) {
@@ -889,13 +926,13 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
         const int c = ci % CST;
         // the constants box starts at a 16 B aligned column: index within it
         const uint32_t kcol = (uint32_t)((p.nf4_mode == 1 ? m_cta / 64 : kb + i) & 3) * 4;
-        ptx::mbar_wait(&cfull[c], (ci / CST) & 1);
+        TRW(tr_wc, ptx::mbar_wait(&cfull[c], (ci / CST) & 1));
         const uint4 w0 = ptx::ld_shared_v4(codes_s + c * L::CODE_BYTES + jA * 16);
         const uint4 w1 = ptx::ld_shared_v4(codes_s + c * L::CODE_BYTES + (jA ^ 1u) * 16);
         const float cst = ptx::ld_shared_f32(consts_s + c * L::CONST_BYTES + kcol);
         uint32_t Lp[4], Hp[4];
         build_planes(vals, cst, Lp, Hp);
-        ptx::mbar_wait(&empty[s], ph ^ 1);
+        TRW(tr_we, ptx::mbar_wait(&empty[s], ph ^ 1));
         const uint32_t base = a_s + s * A_STAGE;
         const uint32_t words[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #ifndef QLRT_HACK_DECODE
@@ -922,6 +959,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
       it += (uint32_t)(i1 - i0);
       cit += (uint32_t)max(0, min(i1, nk) - i0);
     }
+    if (lane == 0) { TRPUT(6, tr_wc); TRPUT(7, tr_we); TRPUT(8, clock64() - tr_t0); }
   }
 
   ptx::tc_fence_before();
@@ -1448,6 +1486,15 @@ using namespace qlrt;
 using gemm::Operand;
 
 extern "C" {
+
+#ifdef QLRT_TRACE
+// copies and clears the per-CTA trace totals ([2 * 148][24] u64)
+int qlrt_trace_fetch(unsigned long long* host) {
+  static unsigned long long zero[2 * qlrt::kNumSMs][qlrt::gemm::kTrSlots];
+  if (cudaMemcpyFromSymbol(host, qlrt::gemm::g_trace, sizeof(zero)) != cudaSuccess) return -1;
+  return cudaMemcpyToSymbol(qlrt::gemm::g_trace, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 size_t qlrt_nf4_constants_bytes(int64_t k_in, int64_t n_out) { return gemm::consts_bytes(k_in, n_out); }
 

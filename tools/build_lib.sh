@@ -10,11 +10,11 @@ FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompil
 objs=()
 pids=()
 for f in quant_kernels gemm_sm100 gemv_nf4 optim_kernels glue_kernels; do
-  "$NVCC" $FLAGS -c "$SRC/$f.cu" -o "$OUT/$f.o" &
+  "$NVCC" $FLAGS -c "$SRC/$f.cu" -o "$OUT/$f${QLRT_LIB_NAME:+.$QLRT_LIB_NAME}.o" &
   pids+=($!)
-  objs+=("$OUT/$f.o")
+  objs+=("$OUT/$f${QLRT_LIB_NAME:+.$QLRT_LIB_NAME}.o")
 done
 for p in "${pids[@]}"; do wait "$p"; done  # a failed compile fails the build
-"$NVCC" -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT/libqlrt_b200.so" "${objs[@]}" -lcudart
+"$NVCC" -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT/${QLRT_LIB_NAME:-libqlrt_b200.so}" "${objs[@]}" -lcudart
 rm -f "${objs[@]}"
-echo "built $OUT/libqlrt_b200.so"
+echo "built $OUT/${QLRT_LIB_NAME:-libqlrt_b200.so}"

@@ -91,6 +91,8 @@ struct Args {
   int tail_from;
   int tma_out;          // D^T bf16 via TMA stores from the epilogue staging tile
   int stagger;          // 512-wide tiles: per-half accumulator release (drain overlaps MMAs)
+  int aug_wrap;         // > 0: the augmented A2 operand has only aug_wrap K rows/cols and is
+                        // re-read for K2 = 2 aug_wrap ([l | l] without materialising the pair)
 };
 
 #ifndef SKINNY_STAGES
@@ -472,6 +474,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           const int amn = aug ? p.a2_mn : p.a_mn;
           const int bmn = aug ? p.b2_mn : p.b_mn;
           const int k0 = (aug ? (i - nk) : (kb + i)) * BK;
+          const int k0a = (aug && p.aug_wrap) ? k0 % p.aug_wrap : k0;
           const bool a_tma = aug || !NF4;
           int tdummy;
           const int hh = item_half(tile, tdummy);
@@ -482,10 +485,10 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           uint8_t* b_dst = sB + s * L::B_STAGE;
           if (a_tma) {
             if (amn) {
-              tma(ma, &full[s], a_dst, m_cta, k0);
-              tma(ma, &full[s], a_dst + 8192, m_cta + 64, k0);
+              tma(ma, &full[s], a_dst, m_cta, k0a);
+              tma(ma, &full[s], a_dst + 8192, m_cta + 64, k0a);
             } else {
-              tma(ma, &full[s], a_dst, k0, m_cta);
+              tma(ma, &full[s], a_dst, k0a, m_cta);
             }
           }
           if (bmn) {
@@ -1276,7 +1279,9 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   if (!(B.mn ? make_tmap(&tb, B.ptr, N, K, B.ld, 64) : make_tmap(&tb, B.ptr, K, N, B.ld, bbox)))
     return QLRT_ERR_UNSUPPORTED;
   if (K2) {
-    if (!(A2->mn ? make_tmap(&ta2, A2->ptr, M, K2, A2->ld, 64) : make_tmap(&ta2, A2->ptr, K2, M, A2->ld, BM)))
+    const int64_t K2a = args.aug_wrap ? args.aug_wrap : K2;  // A2's own K extent
+    if (args.aug_wrap && (args.aug_wrap % BK || K2 % args.aug_wrap)) return QLRT_ERR_UNSUPPORTED;
+    if (!(A2->mn ? make_tmap(&ta2, A2->ptr, M, K2a, A2->ld, 64) : make_tmap(&ta2, A2->ptr, K2a, M, A2->ld, BM)))
       return QLRT_ERR_UNSUPPORTED;
     if (!(B2->mn ? make_tmap(&tb2, B2->ptr, N, K2, B2->ld, 64) : make_tmap(&tb2, B2->ptr, K2, N, B2->ld, bbox)))
       return QLRT_ERR_UNSUPPORTED;
@@ -1562,7 +1567,9 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   cudaStream_t aux = side ? side : st;
   if ((rc = gemm::fill_nf4(a, w, 1, consts, aux)) != QLRT_OK) return rc;
   __nv_bfloat16* l2d = (__nv_bfloat16*)gemm::dbl_region(workspace, ws_bytes, K, N, rank);
-  if (rank) {
+  // rank % 64 == 0: the augmented operand re-reads l2 itself (no doubled copy)
+  const bool wrap = rank > 0 && rank % 64 == 0;
+  if (rank && !wrap) {
     if (cudaMemcpyAsync(l2d, l2, (size_t)rank * N * 2, cudaMemcpyDeviceToDevice, aux) != cudaSuccess ||
         cudaMemcpyAsync(l2d + (size_t)rank * N, l2, (size_t)rank * N * 2, cudaMemcpyDeviceToDevice, aux) != cudaSuccess)
       return QLRT_ERR_CUDA;
@@ -1593,7 +1600,8 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   if (gemm::streamk_policy()) { a.sk_ws = sk.sk_ws; a.sk_flags = sk.sk_flags; }
   Operand none{}, B{x, K, 0};
   // augmented segment K2 = 2r: [l2 ; l2]^T [Ts_hi | Ts_lo]^T, i.e. the pair at ~16-bit precision
-  Operand A2{l2d, N, 1}, B2{ts_out, 2 * rank, 0};
+  Operand A2{wrap ? l2 : l2d, N, 1}, B2{ts_out, 2 * rank, 0};
+  a.aug_wrap = wrap ? rank : 0;
   return gemm::run(bn_main, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, K, 2 * rank, a, st);
 }
 
@@ -1611,23 +1619,6 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   qlrt_status rc;
   gemm::Args sk{};
   gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
-  cudaStream_t side = nullptr;
-  if (rank > 0) {
-    // dl2^T[N, r] = dY^T (Ts_hi + Ts_lo) needs only the inputs: it runs on a
-    // side stream (no split-K workspace) while dT, the fused dX GEMM and dl1
-    // run here -- the skinny kernels hold <= 2 CTAs per SM and overlap.
-    //   A = dY (MN-major [m][N]), B = [Ts_hi | Ts_lo] (MN-major [m][2r]); the
-    //   pair is folded in the epilogue, stored transposed into dl2[r][N]
-    if ((side = gemm::side_stream()) && cudaEventRecord(gemm::side_event(0), st) == cudaSuccess &&
-        cudaStreamWaitEvent(side, gemm::side_event(0), 0) == cudaSuccess) {
-    } else {
-      side = st;
-    }
-    Operand A{dy, N, 1}, B{ts, 2 * rank, 1};
-    rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, N, 2 * rank, m, 1.0f, dl2, N, 1, 1,
-                     side == st ? (float*)workspace : nullptr, side == st ? part_bytes : 0, side, rank);
-    if (rc != QLRT_OK) return rc;
-  }
   if (rank > 0) {
     // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):
     //   A = dY (K-major [m][N]), B = l2 (K-major [r][N])
@@ -1636,13 +1627,14 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
                      &sk);
     if (rc != QLRT_OK) return rc;
   }
-  // join the side stream (dl2) before the persistent fused GEMM: its CTAs need
-  // every SM free, a straggling skinny kernel would delay the whole grid
-  if (side && side != st) {
-    if (cudaEventRecord(gemm::side_event(1), side) != cudaSuccess ||
-        cudaStreamWaitEvent(st, gemm::side_event(1), 0) != cudaSuccess)
-      return QLRT_ERR_CUDA;
-  }
+  // the adapter gradients dl2 and dl1 need only the inputs and dT: they run on
+  // a side stream forked here and are launched after the fused dX GEMM, so
+  // they fill the SMs its grid leaves idle (or follow it as its CTAs retire)
+  cudaStream_t side = nullptr;
+  if (rank > 0 && (side = gemm::side_stream()) &&
+      (cudaEventRecord(gemm::side_event(0), st) != cudaSuccess ||
+       cudaStreamWaitEvent(side, gemm::side_event(0), 0) != cudaSuccess))
+    side = nullptr;
   // dX^T[K, m] = W dY^T (+ l1 dT^T): A = NF4 (K-major image), B = dY (K-major)
   gemm::Args a{};
   a.M = (int)K;
@@ -1661,22 +1653,37 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   Operand none{}, B{dy, N, 0};
   // augmented segment K2 = 2r: [l1 | l1] [dT_hi | dT_lo]^T
   __nv_bfloat16* l1d = (__nv_bfloat16*)gemm::dbl_region(workspace, ws_bytes, K, N, rank);
-  if (rank) {
+  const bool wrap = rank > 0 && rank % 64 == 0;  // re-read l1 itself (no doubled copy)
+  if (rank && !wrap) {
     for (int h = 0; h < 2; ++h)
       if (cudaMemcpy2DAsync(l1d + h * rank, (size_t)4 * rank, l1, (size_t)2 * rank, (size_t)2 * rank, (size_t)K,
                             cudaMemcpyDeviceToDevice, st) != cudaSuccess)
         return QLRT_ERR_CUDA;
   }
-  Operand A2{l1d, 2 * rank, 0}, B2{dt_out, 2 * rank, 0};
+  Operand A2{wrap ? l1 : l1d, wrap ? rank : 2 * rank, 0}, B2{dt_out, 2 * rank, 0};
+  a.aug_wrap = wrap ? rank : 0;
   rc = gemm::run(bn_main, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, N, 2 * rank, a, st);
   if (rc != QLRT_OK || rank == 0) return rc;
-  // (dl2 ran on the side stream; joined below)
-  // dl1[K, r] = Xa^T (dT_hi + dT_lo): A = Xa (MN-major [m][K]), B = [dT_hi | dT_lo] (MN-major [m][2r])
+  cudaStream_t aux = side ? side : st;
   {
-    Operand A{x, K, 1}, B{dt_out, 2 * rank, 1};
-    rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, K, 2 * rank, m, 1.0f, dl1, rank, 1, 0, (float*)workspace,
-                     part_bytes, st, rank, 0, &sk);
+    // dl2^T[N, r] = dY^T (Ts_hi + Ts_lo): A = dY (MN-major [m][N]), B = [Ts_hi | Ts_lo]
+    // (MN-major [m][2r]); the pair is folded in the epilogue, stored transposed
+    // into dl2[r][N] (no split-K: the workspace belongs to dl1)
+    Operand A{dy, N, 1}, B{ts, 2 * rank, 1};
+    rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, N, 2 * rank, m, 1.0f, dl2, N, 1, 1,
+                     nullptr, 0, aux, rank);
+    if (rc != QLRT_OK) return rc;
   }
+  {
+    // dl1[K, r] = Xa^T (dT_hi + dT_lo): A = Xa (MN-major [m][K]), B = [dT_hi | dT_lo] (MN-major [m][2r])
+    Operand A{x, K, 1}, B{dt_out, 2 * rank, 1};
+    rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, K, 2 * rank, m, 1.0f, dl1, rank, 1, 0,
+                     (float*)workspace, part_bytes, aux, rank, 0, &sk);
+    if (rc != QLRT_OK) return rc;
+  }
+  if (side && (cudaEventRecord(gemm::side_event(1), side) != cudaSuccess ||
+               cudaStreamWaitEvent(st, gemm::side_event(1), 0) != cudaSuccess))
+    return QLRT_ERR_CUDA;
   return rc;
 }
 

@@ -95,6 +95,9 @@ struct Args {
                         // re-read for K2 = 2 aug_wrap ([l | l] without materialising the pair)
 };
 
+#ifndef QLRT_MERGE_FULL
+#define QLRT_MERGE_FULL 1
+#endif
 #ifndef QLRT_ISSUE_E
 #define QLRT_ISSUE_E 2  // MMA issue: 0 lane 0, 1 warp-uniform + elect per asm, 2 elect.sync region
 #endif
@@ -343,7 +346,9 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
   __nv_bfloat16* sE = reinterpret_cast<__nv_bfloat16*>(smem + L::EPI_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* full = bars;
-  uint64_t* afull = bars + STAGES;
+  // NF4 (QLRT_MERGE_FULL): the dequant warps arrive on full[] itself, so the
+  // MMA issuer waits on one barrier per stage (B bytes + decoded A)
+  uint64_t* afull = QLRT_MERGE_FULL ? bars : bars + STAGES;
   uint64_t* empty = bars + 2 * STAGES;
   uint64_t* cfull = bars + 3 * STAGES;
   uint64_t* cempty = cfull + L::CST;
@@ -408,9 +413,9 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
     if (NF4) { ptx::prefetch_tmap(&tmC); ptx::prefetch_tmap(&tmK); }
     if (p.k_iters_aug) { ptx::prefetch_tmap(&tmA2); ptx::prefetch_tmap(&tmB2); }
     for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&full[s], 1 + ((NF4 && QLRT_MERGE_FULL) ? (PAIR ? 8 : 4) : 0));
       // one elected lane per dequant warp (share: this CTA's 2 + the peer's 2)
-      ptx::mbar_init(&afull[s], NF4 ? (PAIR ? 8 : 4) : 1);
+      if (!QLRT_MERGE_FULL) ptx::mbar_init(&afull[s], NF4 ? (PAIR ? 8 : 4) : 1);
       ptx::mbar_init(&empty[s], share ? 2 : 1);  // share: both CTAs' MMAs read the stage
     }
     for (int c = 0; c < L::CST; ++c) {
@@ -629,7 +634,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
             const uint32_t itq = it + (uint32_t)q;
             const int s = itq % STAGES;
             wait_x(&full[s], (itq / STAGES) & 1);
-            if (NF4) wait_x(&afull[s], (itq / STAGES) & 1);
+            if (NF4 && !QLRT_MERGE_FULL) wait_x(&afull[s], (itq / STAGES) & 1);
             ptx::tc_fence_after();
             issue(i0 + q, s, 0, false);
           }
@@ -641,7 +646,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           TRW(tr_wf, wait_x(&full[s], ph));
-          if (NF4) TRW(tr_wa, wait_x(&afull[s], ph));
+          if (NF4 && !QLRT_MERGE_FULL) TRW(tr_wa, wait_x(&afull[s], ph));
           ptx::tc_fence_after();
           TRW(tr_is, issue(i, s, -1, true));
         }

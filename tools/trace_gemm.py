@@ -15,7 +15,7 @@ from paper_2305_14314_b200 import _native  # noqa: E402
 
 NAMES = ["mma_wait_tempty", "mma_wait_full(B)", "mma_wait_afull(deq)", "mma_total", "epi_wait_tfull",
          "epi_drain", "deq_wait_cfull(x8)", "deq_wait_empty(x8)", "deq_total(x8)", "tma_wait_empty",
-         "cst_wait_cempty", "tiles"]
+         "cst_wait_cempty", "tiles", "mma_issue"]
 ap = argparse.ArgumentParser()
 ap.add_argument("shapes", nargs="*", default=["4096x11008"])
 ap.add_argument("--m", type=int, default=2048)
@@ -47,7 +47,7 @@ for shp in a.shapes:
         tot = lead[:, 3].mean()
         print(f"== {shp} M={a.m} {name}: {ms * 1e3:.1f} us, leader mma_total {tot:.0f} cyc")
         for i, nm in enumerate(NAMES):
-            src = lead if i <= 3 or i == 11 else allc
+            src = lead if i <= 3 or i in (11, 12) else allc
             v = src[:, i]
             v = v[v > 0] if i != 11 else v
             if len(v) == 0:

@@ -102,6 +102,9 @@ struct Args {
 #define QLRT_ISSUE_E 2  // MMA issue: 0 lane 0, 1 warp-uniform + elect per asm, 2 elect.sync region
 #endif
 
+#ifndef SKINNY128_STAGES
+#define SKINNY128_STAGES 3
+#endif
 #ifndef SKINNY_STAGES
 #define SKINNY_STAGES 4
 #endif
@@ -119,7 +122,7 @@ struct Smem {
   static constexpr int FIT = (226 * 1024 - EPI_BYTES - CRING) / (A_STAGE + B_STAGE);
   // skinny plain GEMMs (BN <= 128, the adapter products): few stages, so two
   // CTAs fit per SM and independent skinny GEMMs can run concurrently
-  static constexpr int CAP = (!NF4 && BN <= 64) ? SKINNY_STAGES : ((!NF4 && BN <= 128) ? 3 : 8);
+  static constexpr int CAP = (!NF4 && BN <= 64) ? SKINNY_STAGES : ((!NF4 && BN <= 128) ? SKINNY128_STAGES : 8);
   // (the NF4 producers alternate stages between groups: even count there)
   static constexpr int STAGES = NF4 ? ((FIT > CAP ? CAP : FIT) & ~1) : (FIT > CAP ? CAP : FIT);
   static constexpr int C_OFF = STAGES * (A_STAGE + B_STAGE);

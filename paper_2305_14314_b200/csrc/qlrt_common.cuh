@@ -44,19 +44,31 @@ __host__ __device__ inline double fp8_max_value(int E, int M, int B) {
 // encode: nearest grid value, ties away from zero, clamp at +-max
 // (doublequant.py:103-113).  Exact in fp64: within a binade the grid is
 // uniform, so round-half-up of the scaled mantissa is the midpoint rule.
+__device__ __forceinline__ double pow2_d(int k) {  // 2^k for normal exponents, exact
+  return __longlong_as_double((long long)((unsigned long long)(1023 + k) << 52));
+}
 __device__ __forceinline__ unsigned fp8_encode(double q, int E, int M, int B, double maxv) {
-  double a = fabs(q);
+  // nearest grid value, ties away from zero (doublequant.py:103-113): within a
+  // binade the grid is uniform, so it is round-half-up of the exactly scaled
+  // magnitude; the power-of-two scalings and the frexp split act on the bits
+  const double a = fabs(q);
   unsigned mag;
+  // round half up without the fp64 add (floor(t + 0.5) rounds 0.5 - 2^-54 up)
+  auto rhu = [](double t) -> unsigned {
+    const double n = floor(t);
+    return (unsigned)n + (t - n >= 0.5 ? 1u : 0u);  // t - n is exact
+  };
   if (a >= maxv) {
     mag = 0x7Fu;
-  } else if (a < ldexp(1.0, 1 - B)) {
-    mag = (unsigned)floor(ldexp(a, B + M - 1) + 0.5);
+  } else if (a < pow2_d(1 - B)) {
+    mag = rhu(a * pow2_d(B + M - 1));                              // subnormal grid step, exact scaling
   } else {
-    int ex;
-    double f = frexp(a, &ex);                      // a = f 2^ex, f in [0.5,1)
-    double mr = (ldexp(f, 1) - 1.0) * (double)(1 << M);
-    mag = ((unsigned)(ex - 1 + B) << M) + (unsigned)floor(mr + 0.5);
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(a);
+    const int ex = (int)((bits >> 52) & 0x7FFu) - 1022;           // a = f 2^ex, f in [0.5, 1)
+    const double frac = (double)(bits & 0xFFFFFFFFFFFFFull);       // (2f - 1) 2^52, exact
+    mag = ((unsigned)(ex - 1 + B) << M) + rhu(frac * pow2_d(M - 52));  // (2f - 1) 2^M, exact
   }
+  (void)E;
   if (mag == 0u) return 0u;
   return (q < 0.0 ? 0x80u : 0u) | mag;
 }

@@ -216,3 +216,25 @@ def test_dequant_bf16_ragged_and_misaligned(dq, oracle, qb, cuda):
         assert rc == 0
         torch.cuda.synchronize()
         assert torch.equal(dst.cpu(), want), ("misaligned", n)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec_args", [(4, 3, 7), (5, 2, 15)])
+def test_fp8_encode_midpoints_vs_oracle(spec_args, oracle, qb, cuda):
+    """encode_fp8 on every grid midpoint and its +-1..2 ulp neighbours, the grid
+    itself, the subnormal range and random magnitudes: bit-exact vs the oracle."""
+    spec = qb.Fp8Spec(*spec_args)
+    ospec = oracle.Fp8Spec(*spec_args)
+    vals, _ = spec.grid()
+    v = np.unique(np.abs(np.asarray(vals, dtype=np.float64)))
+    mids = (v[1:] + v[:-1]) / 2
+    probes = [v, mids]
+    for k in (1, 2):
+        probes += [np.nextafter(mids, np.inf) if k == 1 else np.nextafter(np.nextafter(mids, np.inf), np.inf),
+                   np.nextafter(mids, -np.inf) if k == 1 else np.nextafter(np.nextafter(mids, -np.inf), -np.inf)]
+    rng = np.random.default_rng(7)
+    probes.append(np.exp(rng.uniform(np.log(v[1] / 4), np.log(v[-1] * 1.5), 20000)))
+    x = np.concatenate(probes)
+    x = np.concatenate([x, -x, [0.0, -0.0]])
+    got = qb.encode_fp8(x, spec).cpu().numpy()
+    assert np.array_equal(got, oracle.encode_fp8(x, ospec))

@@ -99,7 +99,7 @@ struct Args {
 #define QLRT_MERGE_FULL 1
 #endif
 #ifndef QLRT_ISSUE_E
-#define QLRT_ISSUE_E 2  // MMA issue: 0 lane 0, 1 warp-uniform + elect per asm, 2 elect.sync region
+#define QLRT_ISSUE_E 2  // MMA issue: 2 = elect.sync region (uniform datapath), 0 = lane-0 issue (old)
 #endif
 
 #ifndef SKINNY128_STAGES
@@ -554,30 +554,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           const uint32_t idesc = ptx::idesc_bf16(BMP, UN, amn, bmn);
           const uint32_t a_addr = ptx::smem_u32(sA + s * A_STAGE);
           const uint32_t b_addr = ptx::smem_u32(sB + s * L::B_STAGE);
-#if QLRT_ISSUE_E == 1
-          // whole warp, uniform operands; one lane elected inside each asm.
-          // Descriptors: base per stage, + 2048 B (MN-major) or 32 B (K-major)
-          // per k16 step in the 14-bit start-address field (>> 4)
-          const uint64_t ad0 = amn ? ptx::sdesc_sw128(a_addr, 8192, 1024) : ptx::sdesc_sw128(a_addr, 16, 1024);
-          const uint32_t astep = amn ? 128u : 2u, bstep = bmn ? 128u : 2u;
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-#pragma unroll
-            for (int j = 0; j < NUM; ++j) {
-              if ((hh >= 0 && hh != j) || (jsel >= 0 && jsel != j)) continue;
-              const uint32_t bj = b_addr + (uint32_t)(j * (L::B_STAGE / NUM));
-              const uint64_t bd0 = bmn ? ptx::sdesc_sw128(bj, 8192, 1024) : ptx::sdesc_sw128(bj, 16, 1024);
-              const uint64_t ad = ad0 + (uint64_t)(kk * astep), bd = bd0 + (uint64_t)(kk * bstep);
-              if (PAIR) ptx::umma_bf16_pair_e(d_tmem + j * UN, ad, bd, idesc, (i != i0) || kk != 0);
-              else ptx::umma_bf16_e(d_tmem + j * UN, ad, bd, idesc, (i != i0) || kk != 0);
-            }
-          }
-          if (commit) {
-            if (PAIR) ptx::umma_commit_pair_mc_e(&empty[s], 0x3);
-            else if (share) ptx::umma_commit_mc_e(&empty[s], 0x3);  // frees the slot in both CTAs
-            else ptx::umma_commit_e(&empty[s]);
-          }
-#elif QLRT_ISSUE_E == 2
+#if QLRT_ISSUE_E == 2
           // one elected thread (elect.sync: ptxas keeps the region on the
           // uniform datapath); descriptors built once per stage, then + 2048 B
           // (MN-major) or + 32 B (K-major) per k16 step in the >> 4 address field
@@ -653,10 +630,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           ptx::tc_fence_after();
           TRW(tr_is, issue(i, s, -1, true));
         }
-#if QLRT_ISSUE_E == 1
-        if (PAIR) ptx::umma_commit_pair_mc_e(&tfull[acc], 0x3);
-        else ptx::umma_commit_e(&tfull[acc]);
-#elif QLRT_ISSUE_E == 2
+#if QLRT_ISSUE_E == 2
         if (ptx::elect_one()) {
           if (PAIR) ptx::umma_commit_pair_mc(&tfull[acc], 0x3);
           else ptx::umma_commit(&tfull[acc]);

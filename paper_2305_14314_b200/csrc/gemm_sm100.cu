@@ -91,6 +91,7 @@ struct Args {
   int tail_from;
   int tma_out;          // D^T bf16 via TMA stores from the epilogue staging tile
   int stagger;          // 512-wide tiles: per-half accumulator release (drain overlaps MMAs)
+  int pdl_trigger;      // let the next (PDL) launch be scheduled right after this grid's prologue
   int aug_wrap;         // > 0: the augmented A2 operand has only aug_wrap K rows/cols and is
                         // re-read for K2 = 2 aug_wrap ([l | l] without materialising the pair)
 };
@@ -445,6 +446,10 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
   // descriptor prefetch) overlaps the previous kernel's tail; no global data
   // of the previous kernel is touched before this point
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the dependent launch (a split-K reduce, the next GEMM) may be scheduled
+  // now: its prologue / launch latency overlaps this grid; it still waits for
+  // our completion (griddepcontrol.wait) before touching our outputs
+  if (p.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // leader-side barrier addresses (shared::cluster) for remote arrivals / TMA bytes
   auto leader_addr = [&](uint64_t* bar) -> uint32_t {
@@ -1031,6 +1036,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
 // out_split writes a bf16 hi/lo pair.
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, int fold, float alpha,
                                      void* __restrict__ out, int64_t ldo, int out_f32, int out_t, int out_split) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (PDL launch: the partials are complete)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t total = (int64_t)M * N;
   const int NO = fold ? fold : N;
   const int64_t total_o = (int64_t)M * NO;
@@ -1382,6 +1389,10 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
       make_tmap_store(&to, args.out, args.M, args.N, args.ldo))
     args.tma_out = 1;
   if (!args.tma_out) to = tb;
+  {
+    const char* e = getenv("QLRT_PDL_TRIGGER");
+    args.pdl_trigger = (e ? atoi(e) : 1) && pdl_policy();
+  }
   switch (bn) {
     case 512:
       return nf4 ? launch_t<512, true, true>(ta, tb, ta2, tb2, tc, tk, to, args, s)
@@ -1401,8 +1412,20 @@ static qlrt_status reduce(const Args& args, cudaStream_t s) {
   const int64_t total = (int64_t)args.M * (args.fold ? args.fold : args.N);
   int64_t g = (total + 255) / 256;
   if (g > 148 * 8) g = 148 * 8;
-  splitk_reduce_kernel<<<(int)g, 256, 0, s>>>(args.ws, args.splits, args.M, args.N, args.fold, args.alpha, args.out,
-                                              args.ldo, args.out_f32, args.out_t, args.out_split);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)g);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  if (pdl_policy()) {  // launched early behind the split-K GEMM (see Args::pdl_trigger)
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  if (cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, (const float*)args.ws, args.splits, args.M, args.N, args.fold,
+                         args.alpha, args.out, args.ldo, args.out_f32, args.out_t, args.out_split) != cudaSuccess)
+    return QLRT_ERR_CUDA;
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }

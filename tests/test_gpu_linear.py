@@ -117,11 +117,13 @@ def test_fused_linear_vs_oracle(m, k, n, r, oracle, qb, cuda):
     assert_tol(gg["adapter0.l2"].cpu().numpy(), grads["adapter0.l2"], "dl2")
 
 
-def test_c2_shape_vs_torch_fp32(qb, cuda):
-    """Config C2 at full size (4096 -> 11008, r = 64, 4x512 tokens) against a
-    plain PyTorch fp32 reference of the same bf16 operands (the fp64 oracle
-    takes minutes at this size)."""
-    m, k, n, r, s = 2048, 4096, 11008, 64, 0.25
+@pytest.mark.parametrize("m,k,n", [(2048, 4096, 11008), (1024, 8192, 22016), (1024, 22016, 8192)])
+def test_c2_shape_vs_torch_fp32(m, k, n, qb, cuda):
+    """Config C2 at full size (4096 -> 11008, r = 64, 4x512 tokens) and the
+    LLaMA-65B MLP shapes (C4) against a plain PyTorch fp32 reference of the
+    same bf16 operands (the fp64 oracle takes minutes at these sizes)."""
+    r, s = 64, 0.25
+    torch.backends.cuda.matmul.allow_tf32 = False
     g = torch.Generator(device="cuda").manual_seed(0)
     w = torch.randn(k, n, device="cuda", generator=g) * 0.02
     q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)

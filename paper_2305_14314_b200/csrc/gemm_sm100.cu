@@ -92,6 +92,11 @@ struct Args {
   int tma_out;          // D^T bf16 via TMA stores from the epilogue staging tile
   int stagger;          // 512-wide tiles: per-half accumulator release (drain overlaps MMAs)
   int pdl_trigger;      // let the next (PDL) launch be scheduled right after this grid's prologue
+  // the augmented B2 operand is the output of the PDL predecessor (an adapter
+  // product running beside this grid): no grid-wide wait at the start; the
+  // TMA producer waits (griddepcontrol.wait) only before its first augmented load
+  int aug_pdl;
+  int units_cap;        // > 0: at most this many (pair) units (SMs left to the predecessor)
   int aug_wrap;         // > 0: the augmented A2 operand has only aug_wrap K rows/cols and is
                         // re-read for K2 = 2 aug_wrap ([l | l] without materialising the pair)
 };
@@ -445,7 +450,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
   // programmatic dependent launch: the prologue above (barriers, TMEM,
   // descriptor prefetch) overlaps the previous kernel's tail; no global data
   // of the previous kernel is touched before this point
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!p.aug_pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   // the dependent launch (a split-K reduce, the next GEMM) may be scheduled
   // now: its prologue / launch latency overlaps this grid; it still waits for
   // our completion (griddepcontrol.wait) before touching our outputs
@@ -472,6 +477,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
     // ======================= TMA producer (every CTA loads its own halves) =======================
     if (lane == 0) {
       uint32_t it = 0;
+      bool aug_ready = false;
       TRDECL(tr_we = 0);
       Sched sc(unit0, n_units, n_tiles_total, T_tile, p.streamk);
       int tile, i0, i1;
@@ -493,6 +499,10 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           const int k0 = (aug ? (i - nk) : (kb + i)) * BK;
           const int k0a = (aug && p.aug_wrap) ? k0 % p.aug_wrap : k0;
           const bool a_tma = aug || !NF4;
+          if (aug && p.aug_pdl && !aug_ready) {  // B2 = the adapter product of the PDL predecessor
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            aug_ready = true;
+          }
           int tdummy;
           const int hh = item_half(tile, tdummy);
           const int b_bytes = hh >= 0 ? L::B_STAGE / NUM : L::B_STAGE;
@@ -1153,6 +1163,14 @@ struct Operand {
 };
 
 // 2-CTA pairing policy: QLRT_PAIR=0 off, 1 on, unset -> the per-GEMM default
+// Adapter product (Ts / dT) beside the fused GEMM that consumes it, chained by
+// programmatic dependent launch (QLRT_OVERLAP=0 disables it): the skinny GEMM
+// runs without split-K on `need` SMs while the fused grid starts its main K
+// segment; only the fused grid's augmented loads wait for it.  Returns the
+// pair cap for the fused grid (leaving >= need SMs), 0 when the cap would cost
+// a round of 256 x 512 tiles -- then the old serial order is used.
+static int overlap_cap(int64_t w_rows, int64_t m, int need_sms);
+
 static int pair_policy(int dflt) {
   const char* e = getenv("QLRT_PAIR");  // read per call: A/B runs toggle it in-process
   const int v = e ? atoi(e) : -1;
@@ -1227,6 +1245,22 @@ static int streamk_policy() {
   return e ? atoi(e) : 1;
 }
 
+static int num_sms();
+static int overlap_cap(int64_t w_rows, int64_t m, int need_sms) {
+  const char* e = getenv("QLRT_OVERLAP");
+  if (e && !atoi(e)) return 0;
+  const int64_t tiles = ((w_rows + 255) / 256) * ((m + 511) / 512);
+  auto rounds = [&](int64_t units) {
+    const int64_t full = tiles / units, rem = tiles - full * units;
+    return (double)full + (rem == 0 ? 0.0 : (2 * rem <= units && full > 0 ? 0.85 : 1.0));
+  };
+  const int64_t all = num_sms() / 2;
+  int64_t cap = all - (need_sms + 1) / 2;
+  if (tiles < cap) return (int)all;  // the grid leaves enough SMs free already
+  if (cap < 8 || rounds(cap) > rounds(all) + 1e-9) return 0;
+  return (int)cap;
+}
+
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -1252,7 +1286,8 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
   const int bmp = PAIR ? 2 * BM : BM;
   const int m_tiles = (args.M + bmp - 1) / bmp, n_tiles = (args.N + BN - 1) / BN;
   const int tiles = m_tiles * n_tiles * args.splits;
-  const int units_max = PAIR ? num_sms() / 2 : num_sms();
+  int units_max = PAIR ? num_sms() / 2 : num_sms();
+  if (args.units_cap > 0 && args.units_cap < units_max) units_max = args.units_cap;
   // stream-K: at most kSkMaxSplit units share a tile (the owner reads the
   // others' partials from L2; more contributors cost more round trips)
   int units = (tiles < units_max && !args.streamk) ? tiles : units_max;
@@ -1360,7 +1395,7 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   if (bn == 512 && args.pair && !args.streamk && args.splits == 1 && halftail_policy()) {
     // whole 256 x 512 tiles for the full waves, half tiles for the last partial one
     const int64_t tiles = ((M + 255) / 256) * ((N + 511) / 512);
-    const int64_t units = num_sms() / 2;
+    const int64_t units = args.units_cap > 0 && args.units_cap < num_sms() / 2 ? args.units_cap : num_sms() / 2;
     const int64_t full = (tiles / units) * units;
     // a half tile costs ~0.85 of a whole one (same dequant): only worth it when
     // all the halves fit in one round
@@ -1378,6 +1413,7 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
     const int64_t waves = (tiles + units - 1) / units;
     const int64_t T = args.k_iters + args.k_iters_aug;
     args.streamk = waves <= 2 && (double)tiles / (double)(waves * units) < 0.9 && T * tiles >= 2 * units;
+    if (args.aug_pdl) args.streamk = 0;
     // the flags are zero between launches: every owner re-arms the flags it
     // consumed; the caller zero-fills the region once (qlrt_streamk_init)
   } else {
@@ -1391,7 +1427,7 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   if (!args.tma_out) to = tb;
   {
     const char* e = getenv("QLRT_PDL_TRIGGER");
-    args.pdl_trigger = (e ? atoi(e) : 1) && pdl_policy();
+    args.pdl_trigger = (e ? atoi(e) : 1) && pdl_policy() && !args.aug_pdl;
   }
   switch (bn) {
     case 512:
@@ -1631,6 +1667,32 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   qlrt_status rc;
   gemm::Args sk{};
   gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
+  const bool big = gemm::tile512_policy();
+  const int cap = (rank > 0 && rank % 64 == 0 && big && gemm::pdl_policy()) ? gemm::overlap_cap(N, m, 4) : 0;
+  if (cap) {
+    // Ts beside the fused grid: constants first (the fused grid reads them from
+    // its start), then Ts without split-K (bf16 hi/lo pair, one CTA per 128
+    // tokens) as the PDL predecessor of the fused GEMM, whose TMA producer
+    // waits for it only before the augmented segment [l2 ; l2]^T [Ts_hi | Ts_lo]^T
+    gemm::Args a{};
+    if ((rc = gemm::fill_nf4(a, w, 1, consts, st)) != QLRT_OK) return rc;
+    Operand TA{xa ? xa : x, K, 0}, TB{l1, rank, 1};
+    rc = gemm::plain(64, TA, TB, m, rank, K, s, ts_out, 2 * rank, 0, 0, nullptr, 0, st, 0, rank, nullptr);
+    if (rc != QLRT_OK) return rc;
+    a.M = (int)N;
+    a.N = (int)m;
+    a.splits = 1;
+    a.out = y;
+    a.ldo = N;
+    a.out_t = 1;
+    a.alpha = 1.0f;
+    a.pair = 1;
+    a.aug_wrap = rank;
+    a.aug_pdl = 1;
+    a.units_cap = cap;
+    Operand none{}, B{x, K, 0}, A2{l2, N, 1}, B2{ts_out, 2 * rank, 0};
+    return gemm::run(512, none, B, &A2, &B2, K, 2 * rank, a, st);
+  }
   // the block-constant prepass (when no cache is given) and the doubled l2
   // copies run on the side stream while Ts is computed here
   gemm::Args a{};
@@ -1693,6 +1755,54 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   qlrt_status rc;
   gemm::Args sk{};
   gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
+  // (QLRT_OVERLAP_BWD=1, off: measured 1-7% slower -- dl2 on the side stream
+  // is dispatched before the PDL-chained fused grid and delays its pairs; the
+  // serial dT + side-stream dl2 / dl1 order below is kept)
+  const char* e_ob = getenv("QLRT_OVERLAP_BWD");
+  const int cap = (e_ob && atoi(e_ob) && rank > 0 && rank % 64 == 0 && gemm::tile512_policy() && gemm::pdl_policy())
+                      ? gemm::overlap_cap(K, m, 4) : 0;
+  cudaStream_t oside = cap ? gemm::side_stream() : nullptr;
+  if (cap && oside && cudaEventRecord(gemm::side_event(0), st) == cudaSuccess &&
+      cudaStreamWaitEvent(oside, gemm::side_event(0), 0) == cudaSuccess) {
+    // dT beside the fused dX GEMM (PDL predecessor, no split-K; the fused
+    // grid waits for it only before its augmented segment [l1 | l1][dT_hi | dT_lo]^T);
+    // dl2 (inputs only) on the side stream, launched after the fused grid so
+    // it takes the SMs the grid leaves; dl1 (needs dT) after the fused GEMM
+    gemm::Args a{};
+    if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
+    Operand DA{dy, N, 0}, DB{l2, N, 0};
+    rc = gemm::plain(64, DA, DB, m, rank, N, s, dt_out, 2 * rank, 0, 0, nullptr, 0, st, 0, rank, nullptr);
+    if (rc != QLRT_OK) return rc;
+    a.M = (int)K;
+    a.N = (int)m;
+    a.splits = 1;
+    a.out = dx;
+    a.ldo = K;
+    a.out_t = 1;
+    a.alpha = 1.0f;
+    a.pair = 1;
+    a.aug_wrap = rank;
+    a.aug_pdl = 1;
+    a.units_cap = cap;
+    Operand none{}, B{dy, N, 0}, A2{l1, rank, 0}, B2{dt_out, 2 * rank, 0};
+    if ((rc = gemm::run(512, none, B, &A2, &B2, N, 2 * rank, a, st)) != QLRT_OK) return rc;
+    {
+      Operand A{dy, N, 1}, B{ts, 2 * rank, 1};
+      rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, N, 2 * rank, m, 1.0f, dl2, N, 1, 1,
+                       nullptr, 0, oside, rank);
+      if (rc != QLRT_OK) return rc;
+    }
+    {
+      Operand A{x, K, 1}, B{dt_out, 2 * rank, 1};
+      rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, K, 2 * rank, m, 1.0f, dl1, rank, 1,
+                       0, (float*)workspace, part_bytes, st, rank, 0, &sk);
+      if (rc != QLRT_OK) return rc;
+    }
+    if (cudaEventRecord(gemm::side_event(1), oside) != cudaSuccess ||
+        cudaStreamWaitEvent(st, gemm::side_event(1), 0) != cudaSuccess)
+      return QLRT_ERR_CUDA;
+    return QLRT_OK;
+  }
   if (rank > 0) {
     // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):
     //   A = dY (K-major [m][N]), B = l2 (K-major [r][N])

@@ -96,6 +96,9 @@ struct Args {
   // product running beside this grid): no grid-wide wait at the start; the
   // TMA producer waits (griddepcontrol.wait) only before its first augmented load
   int aug_pdl;
+  int trigger_dep;      // aug_pdl grid that still lets its PDL dependent launch after the prologue
+  int wait_at_end;      // (with aug_pdl, no augmented segment) the grid needs nothing from its PDL
+                        // predecessor but does not complete before it (keeps stream order for later work)
   int units_cap;        // > 0: at most this many (pair) units (SMs left to the predecessor)
   int aug_wrap;         // > 0: the augmented A2 operand has only aug_wrap K rows/cols and is
                         // re-read for K2 = 2 aug_wrap ([l | l] without materialising the pair)
@@ -1032,6 +1035,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
   }
 
   ptx::tc_fence_before();
+  if (p.wait_at_end) asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   if (PAIR || csplit || share) ptx::cluster_sync();  // (peers stay alive until remote traffic is done)
   if (warp == kMmaWarp) {
@@ -1427,7 +1431,7 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   if (!args.tma_out) to = tb;
   {
     const char* e = getenv("QLRT_PDL_TRIGGER");
-    args.pdl_trigger = (e ? atoi(e) : 1) && pdl_policy() && !args.aug_pdl;
+    args.pdl_trigger = (e ? atoi(e) : 1) && pdl_policy() && (!args.aug_pdl || args.trigger_dep);
   }
   switch (bn) {
     case 512:
@@ -1480,8 +1484,12 @@ static int pick_splits(int64_t tiles, int64_t k_iters, int64_t per_split_bytes, 
 // reduce kernel (forces the fp32 workspace route); out_split: bf16 hi/lo.
 static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, int64_t N, int64_t K, float alpha,
                          void* out, int64_t ldo, int out_f32, int out_t, float* ws, size_t ws_bytes, cudaStream_t s,
-                         int fold = 0, int out_split = 0, const Args* sk = nullptr) {
+                         int fold = 0, int out_split = 0, const Args* sk = nullptr, int pdl_independent = 0) {
   Args a{};
+  // pdl_independent: inputs only (nothing from the PDL predecessor) -- start
+  // at once beside it, complete only after it (see Args::wait_at_end)
+  a.aug_pdl = pdl_independent;
+  a.wait_at_end = pdl_independent;
   a.M = (int)M;
   a.N = (int)N;
   a.out = out;
@@ -1755,19 +1763,17 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   qlrt_status rc;
   gemm::Args sk{};
   gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
-  // (QLRT_OVERLAP_BWD=1, off: measured 1-7% slower -- dl2 on the side stream
-  // is dispatched before the PDL-chained fused grid and delays its pairs; the
-  // serial dT + side-stream dl2 / dl1 order below is kept)
+  // QLRT_OVERLAP_BWD=1 (off by default): one PDL chain on the caller's
+  // stream -- dT (no split-K) -> fused dX grid, which starts its main K
+  // segment at once and waits for dT only before the augmented segment, and
+  // lets the next launch go right after its prologue -> dl2 (inputs only: runs
+  // on the SMs the grid leaves, completes only after it) -> dl1 (needs dT).
+  // Measured 2-9% slower than the order below: dT, dl2 and dl1 together do
+  // not fit in the SMs the fused grid leaves, and dT at full width is faster.
   const char* e_ob = getenv("QLRT_OVERLAP_BWD");
   const int cap = (e_ob && atoi(e_ob) && rank > 0 && rank % 64 == 0 && gemm::tile512_policy() && gemm::pdl_policy())
                       ? gemm::overlap_cap(K, m, 4) : 0;
-  cudaStream_t oside = cap ? gemm::side_stream() : nullptr;
-  if (cap && oside && cudaEventRecord(gemm::side_event(0), st) == cudaSuccess &&
-      cudaStreamWaitEvent(oside, gemm::side_event(0), 0) == cudaSuccess) {
-    // dT beside the fused dX GEMM (PDL predecessor, no split-K; the fused
-    // grid waits for it only before its augmented segment [l1 | l1][dT_hi | dT_lo]^T);
-    // dl2 (inputs only) on the side stream, launched after the fused grid so
-    // it takes the SMs the grid leaves; dl1 (needs dT) after the fused GEMM
+  if (cap) {
     gemm::Args a{};
     if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
     Operand DA{dy, N, 0}, DB{l2, N, 0};
@@ -1783,25 +1789,19 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
     a.pair = 1;
     a.aug_wrap = rank;
     a.aug_pdl = 1;
+    a.trigger_dep = 1;
     a.units_cap = cap;
     Operand none{}, B{dy, N, 0}, A2{l1, rank, 0}, B2{dt_out, 2 * rank, 0};
     if ((rc = gemm::run(512, none, B, &A2, &B2, N, 2 * rank, a, st)) != QLRT_OK) return rc;
     {
       Operand A{dy, N, 1}, B{ts, 2 * rank, 1};
       rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, N, 2 * rank, m, 1.0f, dl2, N, 1, 1,
-                       nullptr, 0, oside, rank);
+                       nullptr, 0, st, rank, 0, nullptr, 1);
       if (rc != QLRT_OK) return rc;
     }
-    {
-      Operand A{x, K, 1}, B{dt_out, 2 * rank, 1};
-      rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, K, 2 * rank, m, 1.0f, dl1, rank, 1,
+    Operand A{x, K, 1}, B1{dt_out, 2 * rank, 1};
+    return gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B1, K, 2 * rank, m, 1.0f, dl1, rank, 1,
                        0, (float*)workspace, part_bytes, st, rank, 0, &sk);
-      if (rc != QLRT_OK) return rc;
-    }
-    if (cudaEventRecord(gemm::side_event(1), oside) != cudaSuccess ||
-        cudaStreamWaitEvent(st, gemm::side_event(1), 0) != cudaSuccess)
-      return QLRT_ERR_CUDA;
-    return QLRT_OK;
   }
   if (rank > 0) {
     // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):

@@ -222,3 +222,44 @@ def test_unfused_shape_path(oracle, qb, cuda):
     assert_tol(y.float().cpu().numpy(), bf16_round(yr), "y")
     assert_tol(dx.float().cpu().numpy(), bf16_round(dxr), "dx")
     assert_tol(gr["adapter0.l1"].cpu().numpy(), grr["adapter0.l1"], "dl1")
+
+
+@pytest.mark.parametrize("env", [{"QLRT_OVERLAP": "0"}, {"QLRT_OVERLAP_BWD": "1"}])
+def test_overlap_modes_match_default(env, qb, cuda):
+    """The PDL-chained adapter products (forward default; backward behind
+    QLRT_OVERLAP_BWD) and the serial order agree within the GEMM tolerance
+    (split-K vs one-CTA summation order of T / dT), and each is run-to-run
+    deterministic."""
+    import os
+    m, k, n, r = 1024, 4096, 4096, 64
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q = qb.quantize(torch.randn(k, n, device="cuda", generator=g) * 0.02, qb.get_codebook("nf4"), 64,
+                    double_quant=True)
+    x = torch.randn(m, k, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(m, n, device="cuda", generator=g).bfloat16()
+    ad = qb.LoraAdapter(r, 16.0, (torch.randn(k, r, device="cuda", generator=g) / 8).bfloat16().float(),
+                        (torch.randn(r, n, device="cuda", generator=g) * 0.01).bfloat16().float())
+    lin = qb.QLinear(q, [ad])
+
+    def run():
+        y, c = lin.forward(x)
+        dx, gr = lin.backward(dy, c)
+        return [y.clone(), dx.clone(), gr["adapter0.l1"].clone(), gr["adapter0.l2"].clone()]
+
+    base = run()
+    old = {kk: os.environ.get(kk) for kk in env}
+    os.environ.update(env)
+    try:
+        alt = run()
+        alt2 = run()
+    finally:
+        for kk, vv in old.items():
+            if vv is None:
+                os.environ.pop(kk, None)
+            else:
+                os.environ[kk] = vv
+    for a, b, c in zip(base, alt, alt2):
+        assert torch.equal(b, c)
+        d = (a.float() - b.float()).abs()
+        assert (d.max() / a.float().abs().max()).item() <= MAX_REL
+        assert (d.mean() / a.float().abs().mean()).item() <= MEAN_REL

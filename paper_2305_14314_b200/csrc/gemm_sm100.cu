@@ -1174,6 +1174,10 @@ struct Operand {
 // pair cap for the fused grid (leaving >= need SMs), 0 when the cap would cost
 // a round of 256 x 512 tiles -- then the old serial order is used.
 static int overlap_cap(int64_t w_rows, int64_t m, int need_sms);
+static int overlap_need_sms() {  // SMs left to the adapter product (QLRT_OVERLAP_SMS; 8: +1-2% over 4)
+  const char* e = getenv("QLRT_OVERLAP_SMS");
+  return e ? atoi(e) : 8;
+}
 
 static int pair_policy(int dflt) {
   const char* e = getenv("QLRT_PAIR");  // read per call: A/B runs toggle it in-process
@@ -1676,7 +1680,7 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   gemm::Args sk{};
   gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
   const bool big = gemm::tile512_policy();
-  const int cap = (rank > 0 && rank % 64 == 0 && big && gemm::pdl_policy()) ? gemm::overlap_cap(N, m, 4) : 0;
+  const int cap = (rank > 0 && rank % 64 == 0 && big && gemm::pdl_policy()) ? gemm::overlap_cap(N, m, gemm::overlap_need_sms()) : 0;
   if (cap) {
     // Ts beside the fused grid: constants first (the fused grid reads them from
     // its start), then Ts without split-K (bf16 hi/lo pair, one CTA per 128

@@ -1767,16 +1767,15 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   qlrt_status rc;
   gemm::Args sk{};
   gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
-  // QLRT_OVERLAP_BWD=1 (off by default): one PDL chain on the caller's
-  // stream -- dT (no split-K) -> fused dX grid, which starts its main K
-  // segment at once and waits for dT only before the augmented segment, and
-  // lets the next launch go right after its prologue -> dl2 (inputs only: runs
-  // on the SMs the grid leaves, completes only after it) -> dl1 (needs dT).
-  // Measured 2-9% slower than the order below: dT, dl2 and dl1 together do
-  // not fit in the SMs the fused grid leaves, and dT at full width is faster.
+  // QLRT_OVERLAP_BWD=1 (off: measured -6% to +2%): dT beside the fused dX
+  // grid as its PDL predecessor (no split-K; the grid waits for it only before
+  // the augmented segment), then dl2 (side stream) and dl1 at full width.  The
+  // 16 dT CTAs land one per SM and hold back fused pairs that need whole SMs;
+  // the backward's 64-tile grids already leave their idle SMs to dl2 / dl1.
+  // (dl2 beside the grid as well: 2-9% slower.)
   const char* e_ob = getenv("QLRT_OVERLAP_BWD");
   const int cap = (e_ob && atoi(e_ob) && rank > 0 && rank % 64 == 0 && gemm::tile512_policy() && gemm::pdl_policy())
-                      ? gemm::overlap_cap(K, m, 4) : 0;
+                      ? gemm::overlap_cap(K, m, gemm::overlap_need_sms()) : 0;
   if (cap) {
     gemm::Args a{};
     if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
@@ -1793,19 +1792,29 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
     a.pair = 1;
     a.aug_wrap = rank;
     a.aug_pdl = 1;
-    a.trigger_dep = 1;
     a.units_cap = cap;
     Operand none{}, B{dy, N, 0}, A2{l1, rank, 0}, B2{dt_out, 2 * rank, 0};
     if ((rc = gemm::run(512, none, B, &A2, &B2, N, 2 * rank, a, st)) != QLRT_OK) return rc;
+    cudaStream_t side = gemm::side_stream();
+    if (side && (cudaEventRecord(gemm::side_event(0), st) != cudaSuccess ||
+                 cudaStreamWaitEvent(side, gemm::side_event(0), 0) != cudaSuccess))
+      side = nullptr;
     {
-      Operand A{dy, N, 1}, B{ts, 2 * rank, 1};
-      rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, N, 2 * rank, m, 1.0f, dl2, N, 1, 1,
-                       nullptr, 0, st, rank, 0, nullptr, 1);
+      Operand A{dy, N, 1}, B2t{ts, 2 * rank, 1};
+      rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B2t, N, 2 * rank, m, 1.0f, dl2, N, 1,
+                       1, side ? nullptr : (float*)workspace, side ? 0 : part_bytes, side ? side : st, rank);
       if (rc != QLRT_OK) return rc;
     }
-    Operand A{x, K, 1}, B1{dt_out, 2 * rank, 1};
-    return gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B1, K, 2 * rank, m, 1.0f, dl1, rank, 1,
-                       0, (float*)workspace, part_bytes, st, rank, 0, &sk);
+    {
+      Operand A{x, K, 1}, B1{dt_out, 2 * rank, 1};
+      rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B1, K, 2 * rank, m, 1.0f, dl1, rank,
+                       1, 0, (float*)workspace, part_bytes, st, rank, 0, &sk);
+      if (rc != QLRT_OK) return rc;
+    }
+    if (side && (cudaEventRecord(gemm::side_event(1), side) != cudaSuccess ||
+                 cudaStreamWaitEvent(st, gemm::side_event(1), 0) != cudaSuccess))
+      return QLRT_ERR_CUDA;
+    return QLRT_OK;
   }
   if (rank > 0) {
     // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):

@@ -1264,7 +1264,7 @@ static int overlap_cap(int64_t w_rows, int64_t m, int need_sms) {
   };
   const int64_t all = num_sms() / 2;
   int64_t cap = all - (need_sms + 1) / 2;
-  if (tiles < cap) return (int)all;  // the grid leaves enough SMs free already
+  if (tiles <= cap) return (int)tiles;  // the grid leaves enough SMs free already
   if (cap < 8 || rounds(cap) > rounds(all) + 1e-9) return 0;
   return (int)cap;
 }
@@ -1278,6 +1278,7 @@ static int num_sms() {
   }
   return n;
 }
+
 
 template <int BN, bool NF4, bool PAIR = false>
 static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2, const CUtensorMap& b2,
@@ -1689,6 +1690,9 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
     gemm::Args a{};
     if ((rc = gemm::fill_nf4(a, w, 1, consts, st)) != QLRT_OK) return rc;
     Operand TA{xa ? xa : x, K, 0}, TB{l1, rank, 1};
+    // (one CTA per 128-token tile; capping it to the SMs left, each CTA
+    // looping over tiles, was measured slower: Ts then outlasts the grid's
+    // first tiles)
     rc = gemm::plain(64, TA, TB, m, rank, K, s, ts_out, 2 * rank, 0, 0, nullptr, 0, st, 0, rank, nullptr);
     if (rc != QLRT_OK) return rc;
     a.M = (int)N;

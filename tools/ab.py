@@ -31,7 +31,13 @@ fl = 2 * m * k * n
 res = {v: {"fwd": [], "bwd": []} for v in a.variants}
 
 
+ALL_KEYS = {kv.split("=")[0] for v in a.variants for kv in v.split(",")}
+
+
 def setenv(v):
+    """Exactly this variant's settings: keys set by other variants are cleared."""
+    for kk in ALL_KEYS:
+        os.environ.pop(kk, None)
     for kv in v.split(","):
         kk, vv = kv.split("=")
         os.environ[kk] = vv

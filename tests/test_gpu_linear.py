@@ -102,7 +102,8 @@ def _oracle_case(oracle, m, k, n, r, seed):
     return w, x, dy, l1, l2, y, dx, grads
 
 
-@pytest.mark.parametrize("m,k,n,r", [(512, 1024, 2048, 64), (300, 512, 704, 16), (2048, 4096, 1024, 64)])
+@pytest.mark.parametrize("m,k,n,r", [(512, 1024, 2048, 64), (300, 512, 704, 16), (2048, 4096, 1024, 64),
+                                     (300, 576, 704, 64), (1000, 1024, 1536, 128)])
 def test_fused_linear_vs_oracle(m, k, n, r, oracle, qb, cuda):
     w, x, dy, l1, l2, y, dx, grads = _oracle_case(oracle, m, k, n, r, seed=m + n)
     q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)

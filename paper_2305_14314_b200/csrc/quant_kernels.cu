@@ -208,7 +208,10 @@ __device__ __forceinline__ void load8_stream<__nv_bfloat16>(const __nv_bfloat16*
 // coded, and a branch-free fast path per element with one group-wide check
 // (bracket hits are re-decided exactly, rarely).
 template <typename T>
-__global__ void __launch_bounds__(256, 3) quantize64_stream_kernel(const T* __restrict__ x, int64_t n_groups,
+#ifndef QLRT_Q_MINB
+#define QLRT_Q_MINB 3  // (4: spills, 8% slower)
+#endif
+__global__ void __launch_bounds__(256, QLRT_Q_MINB) quantize64_stream_kernel(const T* __restrict__ x, int64_t n_groups,
                                                                 qlrt_codebook4 cb, uint32_t* __restrict__ codes,
                                                                 float* __restrict__ absmax,
                                                                 unsigned long long* __restrict__ first_bad) {
@@ -920,7 +923,7 @@ qlrt_status qlrt_quantize4(const void* x, int x_dtype, int64_t n, int blocksize,
   if (blocksize == 64 && n % 64 == 0 && aligned32 && (x_dtype == QLRT_F32 || x_dtype == QLRT_BF16)) {
     const int64_t n_groups = nb * 8;
     const int64_t want = cdiv(n_groups, 256);
-    const int grid = (int)(want < (int64_t)kNumSMs * 3 ? want : (int64_t)kNumSMs * 3);  // 3 x 256 resident / SM
+    const int grid = (int)(want < (int64_t)kNumSMs * QLRT_Q_MINB ? want : (int64_t)kNumSMs * QLRT_Q_MINB);  // resident
     if (x_dtype == QLRT_F32)
       quantize64_stream_kernel<float><<<grid, 256, 0, s>>>((const float*)x, n_groups, *cb, (uint32_t*)codes, absmax,
                                                           fb);

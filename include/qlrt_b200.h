@@ -149,13 +149,14 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
                                 float* dl1, float* dl2, void* workspace, void* stream);
 
 /* batch-1 GEMV variant of forward (M = 1), HBM-bound on the packed codes:
- *   y[N] = x[K] W + s (x l1) l2          fp32 accumulate, bf16 out.
+ *   y[N] = x[K] W + s (xa l1) l2         fp32 accumulate, bf16 out
+ * (xa = the dropout-masked adapter input, NULL -> x; qlora.py:137-146).
  * W decodes as bf16(f32(v) * c) (as the fused GEMM); split-K partials are
  * summed in a fixed order (deterministic).  Needs N % 64 == 0, a
  * power-of-two blocksize2, 32-byte aligned codes; rank <= 512. */
-qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* l1,
-                          const void* l2, int rank, float s, void* y, void* workspace,
-                          void* stream);
+qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* xa,
+                          const void* l1, const void* l2, int rank, float s, void* y,
+                          void* workspace, void* stream);
 
 /* Workspace bytes of qlrt_nf4_gemv (split-K partials, LoRA partials, strip
  * tickets); qlrt_linear_workspace_bytes(m = 1, ...) already covers it. */

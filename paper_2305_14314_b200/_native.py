@@ -55,7 +55,7 @@ _SIGS = {
                             c_void_p, c_void_p, c_void_p, c_void_p],
     "qlrt_nf4_linear_bwd": [POINTER(NF4Weight), c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
                             c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
-    "qlrt_nf4_gemv": [POINTER(NF4Weight), c_void_p, c_void_p, c_void_p, c_int, c_float, c_void_p, c_void_p, c_void_p],
+    "qlrt_nf4_gemv": [POINTER(NF4Weight), c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_float, c_void_p, c_void_p, c_void_p],
     "qlrt_gemv_workspace_bytes": [c_int64, c_int64, c_int],
     "qlrt_gemm_bf16": [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_int, c_float, c_int, c_int,
                        c_void_p, c_size_t, c_void_p],

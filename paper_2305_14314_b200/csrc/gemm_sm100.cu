@@ -1670,7 +1670,9 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
                                 const void* l2, int rank, float s, void* ts_out, void* y, void* workspace,
                                 void* stream) {
   if (!gemm::weight_ok(w) || !x || !y || m <= 0 || rank < 0) return QLRT_ERR_ARG;
-  if (rank > 0 && (!l1 || !l2 || !ts_out || (rank % 8))) return QLRT_ERR_ARG;
+  if (rank > 0 && (!l2 || !ts_out || (rank % 8))) return QLRT_ERR_ARG;
+  // l1 == NULL: ts_out already holds Ts (several adapters concatenated by the host)
+  const bool ts_given = rank > 0 && !l1;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t K = w->k_in, N = w->n_out;
   const size_t ws_bytes = qlrt_linear_workspace_bytes(m, K, N, rank);
@@ -1681,7 +1683,8 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   gemm::Args sk{};
   gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
   const bool big = gemm::tile512_policy();
-  const int cap = (rank > 0 && rank % 64 == 0 && big && gemm::pdl_policy()) ? gemm::overlap_cap(N, m, gemm::overlap_need_sms()) : 0;
+  const int cap = (rank > 0 && !ts_given && rank % 64 == 0 && big && gemm::pdl_policy())
+                      ? gemm::overlap_cap(N, m, gemm::overlap_need_sms()) : 0;
   if (cap) {
     // Ts beside the fused grid: constants first (the fused grid reads them from
     // its start), then Ts without split-K (bf16 hi/lo pair, one CTA per 128
@@ -1726,7 +1729,7 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
         cudaMemcpyAsync(l2d + (size_t)rank * N, l2, (size_t)rank * N * 2, cudaMemcpyDeviceToDevice, aux) != cudaSuccess)
       return QLRT_ERR_CUDA;
   }
-  if (rank > 0) {
+  if (rank > 0 && !ts_given) {
     // Ts[m, 0:r] + Ts[m, r:2r] = s * Xa l1 as a bf16 hi/lo pair:
     //   A = Xa (K-major, [m][K]), B = l1 (MN-major, [K][r])
     Operand A{xa ? xa : x, K, 0}, B{l1, rank, 1};
@@ -1761,7 +1764,9 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
                                 const void* l1, const void* l2, int rank, float s, void* dt_out, void* dx, float* dl1,
                                 float* dl2, void* workspace, void* stream) {
   if (!gemm::weight_ok(w) || !dy || !dx || m <= 0 || rank < 0) return QLRT_ERR_ARG;
-  if (rank > 0 && (!x || !ts || !l1 || !l2 || !dt_out || !dl1 || !dl2 || (rank % 8))) return QLRT_ERR_ARG;
+  if (rank > 0 && (!x || !ts || !l1 || !dt_out || !dl1 || !dl2 || (rank % 8))) return QLRT_ERR_ARG;
+  // l2 == NULL: dt_out already holds dT (several adapters concatenated by the host)
+  const bool dt_given = rank > 0 && !l2;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t K = w->k_in, N = w->n_out;
   const size_t ws_bytes = qlrt_linear_workspace_bytes(m, K, N, rank);
@@ -1778,7 +1783,8 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   // the backward's 64-tile grids already leave their idle SMs to dl2 / dl1.
   // (dl2 beside the grid as well: 2-9% slower.)
   const char* e_ob = getenv("QLRT_OVERLAP_BWD");
-  const int cap = (e_ob && atoi(e_ob) && rank > 0 && rank % 64 == 0 && gemm::tile512_policy() && gemm::pdl_policy())
+  const int cap = (e_ob && atoi(e_ob) && rank > 0 && !dt_given && rank % 64 == 0 && gemm::tile512_policy() &&
+                   gemm::pdl_policy())
                       ? gemm::overlap_cap(K, m, gemm::overlap_need_sms()) : 0;
   if (cap) {
     gemm::Args a{};
@@ -1820,7 +1826,7 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
       return QLRT_ERR_CUDA;
     return QLRT_OK;
   }
-  if (rank > 0) {
+  if (rank > 0 && !dt_given) {
     // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):
     //   A = dY (K-major [m][N]), B = l2 (K-major [r][N])
     Operand A{dy, N, 0}, B{l2, N, 0};

@@ -302,8 +302,8 @@ size_t qlrt_gemv_workspace_bytes(int64_t k_in, int64_t n_out, int rank) {
   return gemv::ws_bytes(k_in, n_out, rank);
 }
 
-qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* l1, const void* l2, int rank, float s,
-                          void* y, void* workspace, void* stream) {
+qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* xa, const void* l1, const void* l2,
+                          int rank, float s, void* y, void* workspace, void* stream) {
   if (!w || !w->codes || !w->dq_codes || !w->c1 || !w->mu || w->k_in <= 0 || w->n_out <= 0 || (w->n_out % 64) ||
       !x || !y || !workspace || rank < 0 || rank > 512)
     return QLRT_ERR_ARG;
@@ -321,7 +321,7 @@ qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* l
                                    gemv::align256((size_t)p.zt * (rank > 0 ? rank : 1) * 4));
   if (cudaMemsetAsync(counters, 0, (size_t)p.strips * 4, st) != cudaSuccess) return QLRT_ERR_CUDA;
   if (rank > 0)
-    gemv::lora_t_kernel<<<p.zt, gemv::TPB, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)l1, K, rank,
+    gemv::lora_t_kernel<<<p.zt, gemv::TPB, 0, st>>>((const __nv_bfloat16*)(xa ? xa : x), (const __nv_bfloat16*)l1, K, rank,
                                                     tpart);
   gemv::Vals32 v;
   for (int i = 0; i < 16; ++i) v.v[i] = (float)w->values[i];

@@ -13,9 +13,25 @@ checkpoints offline), tokens synthetic.
 
 Training step = forward, backward (adapter gradients written straight into
 one flat fp32 bucket), data-parallel mean all-reduce of that bucket only
-(NCCL; a no-op on one rank), fused global-norm clip + bit-exact Adam over the
-flat parameter buffer (``qlrt_adam_step_dev``), bf16 operand shadows
-refreshed in the same pass.  The whole step captures into one CUDA graph.
+(NCCL over NVLink; per group of layers, launched as soon as the group's
+gradients land so it overlaps the rest of the backward --
+``parallel.LayerReducer``), fused global-norm clip + bit-exact Adam
+(``qlrt_adam_step_dev``), bf16 operand shadows refreshed in the same pass.
+
+Optimizer state: ``optimizer="plain"`` keeps the Adam moments in one flat
+device buffer and the whole step captures into one CUDA graph;
+``optimizer="paged"`` keeps them in unified-memory pages under a
+:class:`~paper_2305_14314_b200.paging.Pager` budget (the reference's
+PagedMomentStore, training.py:371-395: one slab per layer holding its m then
+v), the forward/backward still one CUDA graph and the optimizer walking the
+layer slabs with look-ahead prefetch on the pager's side streams.  The walk
+alternates direction every step (an elevator scan), so the reference's LRU
+keeps exactly the slabs the next step needs first and evicts the ones it has
+finished with; each parameter's update is independent, so the order changes
+no bit of the result (paged == plain).
+
+``checkpoint=True`` recomputes each decoder layer's forward in the backward
+(activation memory O(1 layer) instead of O(layers); +2P FLOPs per token).
 """
 
 from __future__ import annotations
@@ -26,11 +42,13 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 import torch.nn.functional as F
+import torch.utils.checkpoint as _ckpt
 
 from ._native import check, lib, ptr, stream_ptr
 from .blockquant import quantize
 from .codebooks import get_codebook
-from .parallel import GradBucket
+from .paging import Pager, PagerConfig
+from .parallel import GradBucket, LayerReducer
 from .qlora import LoraAdapter, QLinear
 from .training import TrainConfig, _sumsq_scratch
 
@@ -93,16 +111,18 @@ class _QLinearFn(torch.autograd.Function):
     adapter gradients go to the bucket views, not to autograd."""
 
     @staticmethod
-    def forward(ctx, x, anchor, layer, gviews):
+    def forward(ctx, x, anchor, layer, gviews, notify):
         y, cache = layer.forward(x)
-        ctx.layer, ctx.cache, ctx.gviews = layer, cache, gviews
+        ctx.layer, ctx.cache, ctx.gviews, ctx.notify = layer, cache, gviews, notify
         return y
 
     @staticmethod
     def backward(ctx, dy):
         dx, _ = ctx.layer.backward(dy.contiguous(), ctx.cache, grads_out=ctx.gviews)
         ctx.cache = None
-        return dx, None, None, None
+        if ctx.notify is not None:  # this projection's adapter gradients are in the bucket
+            ctx.notify()
+        return dx, None, None, None, None
 
 
 class _RMSNormFn(torch.autograd.Function):
@@ -193,19 +213,35 @@ def rope_reference(t: torch.Tensor, cos_sin: torch.Tensor) -> torch.Tensor:
 
 
 class LlamaQLoRA:
-    """Frozen NF4 LLaMA-shaped decoder with LoRA on every linear layer."""
+    """Frozen NF4 LLaMA-shaped decoder with LoRA on every linear layer.
 
-    def __init__(self, cfg: LlamaConfig, device="cuda", seed: int = 0, train_cfg: TrainConfig | None = None):
+    group: the data-parallel process group (None = the default group when
+    torch.distributed is initialized, else single rank).  optimizer:
+    "plain" | "paged"; pager_budget_bytes bounds the device-resident moment
+    bytes of the paged store (default: all of them).  bucket_layers: layers
+    per overlapped all-reduce; wire_dtype: float32 (exact) or bfloat16.
+    """
+
+    def __init__(self, cfg: LlamaConfig, device="cuda", seed: int = 0, train_cfg: TrainConfig | None = None, *,
+                 group=None, optimizer: str = "plain", pager_budget_bytes: int | None = None,
+                 page_bytes: int = 2 << 20, lookahead: int = 2, checkpoint: bool = False, bucket_layers: int = 4,
+                 wire_dtype=torch.float32, max_steps: int = 100_000):
+        if optimizer not in ("plain", "paged"):
+            raise ValueError(f"optimizer must be 'plain' or 'paged', got {optimizer!r}")
         self.cfg = cfg
         self.dev = torch.device(device)
         self.train_cfg = train_cfg or TrainConfig()
+        self.checkpoint = checkpoint
+        self.optimizer = optimizer
+        self.lookahead = lookahead
         g = torch.Generator(device=self.dev).manual_seed(seed)
         cb = get_codebook("nf4")
         h, v = cfg.hidden, cfg.vocab
         self.embed = (torch.randn(v, h, device=self.dev, generator=g) * 0.02).to(torch.bfloat16)
         self.lm_head = (torch.randn(h, v, device=self.dev, generator=g) * 0.02).to(torch.bfloat16)
-        # one flat fp32 buffer each for adapter parameters, gradients, moments;
-        # a flat bf16 buffer for the MMA operand shadows (same layout)
+        # one flat fp32 buffer each for adapter parameters and gradients (layer
+        # after layer, so a layer's -- and a group of layers' -- tensors are
+        # contiguous); a flat bf16 buffer for the MMA operand shadows (same layout)
         names, shapes = [], {}
         for li in range(cfg.n_layers):
             for pj in PROJS:
@@ -219,14 +255,29 @@ class LlamaQLoRA:
         self.params_flat = pbuf.flat
         self.params = pbuf.views()
         self.shadow_flat = torch.zeros(self.params_flat.numel(), dtype=torch.bfloat16, device=self.dev)
-        self.m_flat = torch.zeros_like(self.params_flat)
-        self.v_flat = torch.zeros_like(self.params_flat)
+        offs = self.bucket.offsets()
+        self.layer_spans = []
+        for li in range(cfg.n_layers):
+            first = offs[f"{li}.{PROJS[0]}.l1"][0]
+            last_off, last_n = offs[f"{li}.{PROJS[-1]}.l2"]
+            self.layer_spans.append((first, last_off + last_n - first))
+        self.pager = None
+        if optimizer == "plain":
+            self.m_flat = torch.zeros_like(self.params_flat)
+            self.v_flat = torch.zeros_like(self.params_flat)
+        else:
+            # default budget: every slab resident (page-rounded), i.e. no eviction
+            state = sum((2 * n * 4 + page_bytes - 1) // page_bytes * page_bytes for _, n in self.layer_spans)
+            self.pager = Pager(PagerConfig(budget_bytes=pager_budget_bytes or state, page_bytes=page_bytes))
+            self.mslabs = [self.pager.alloc(2 * n * 4) for _, n in self.layer_spans]
         self.gviews = self.bucket.views()
         shadows, off = {}, 0
         for n in names:
             k = int(np.prod(shapes[n]))
             shadows[n] = self.shadow_flat[off: off + k].view(shapes[n])
             off += k
+        self.reducer = LayerReducer(self.bucket.flat, self.layer_spans, bucket_layers, group, wire_dtype)
+        self._pending = [len(PROJS)] * cfg.n_layers
         self.layers = []
         for li in range(cfg.n_layers):
             lay = {}
@@ -243,10 +294,11 @@ class LlamaQLoRA:
                     s1, s2 = shadows[f"{li}.{pj}.l1"], shadows[f"{li}.{pj}.l2"]
                     s1.copy_(l1)
                     s2.copy_(l2)
-                    ad._shadow["ops"] = ((l1.data_ptr(), l2.data_ptr(), cfg.rank), s1, s2)
+                    ad.adopt_shadows(s1, s2)
                 lay[pj] = QLinear(q, [ad])
                 lay[pj + ".g"] = {"adapter0.l1": self.gviews[f"{li}.{pj}.l1"],
                                   "adapter0.l2": self.gviews[f"{li}.{pj}.l2"]}
+            lay["notify"] = (lambda li=li: self._proj_done(li))
             self.layers.append(lay)
         d = h // cfg.n_heads
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, d, 2, device=self.dev, dtype=torch.float32) / d))
@@ -254,63 +306,142 @@ class LlamaQLoRA:
         self.cos_sin = torch.stack((torch.cos(ang), torch.sin(ang)), dim=-1).contiguous()  # fp32 [seq, d/2, 2]
         self.anchor = torch.zeros(1, device=self.dev, requires_grad=True)
         self.t = 0
-        self.hyper_host = torch.zeros(8, dtype=torch.float32).pin_memory()
+        self._scans = 0
+        # the Adam constants of every step t = 1..max_steps, as the float32
+        # values numpy 2 uses in the reference update (training.py:426-442);
+        # a device step counter selects the row, so a captured step replays
+        # with the right bias corrections and no host write races the GPU
+        c = self.train_cfg
+        f32 = np.float32
+        rows = np.empty((max_steps, 8), dtype=np.float32)
+        rows[:, 0], rows[:, 1] = f32(c.adam_beta1), f32(1.0 - c.adam_beta1)
+        rows[:, 2], rows[:, 3] = f32(c.adam_beta2), f32(1.0 - c.adam_beta2)
+        rows[:, 4] = [f32(1.0 - c.adam_beta1 ** t) for t in range(1, max_steps + 1)]
+        rows[:, 5] = [f32(1.0 - c.adam_beta2 ** t) for t in range(1, max_steps + 1)]
+        rows[:, 6], rows[:, 7] = f32(c.adam_eps), f32(c.learning_rate)
+        self.hyper_table = torch.from_numpy(rows).to(self.dev)
+        self.t_dev = torch.zeros(1, dtype=torch.int64, device=self.dev)  # steps taken
         self.hyper = torch.zeros(8, dtype=torch.float32, device=self.dev)
         self.sumsq = _sumsq_scratch(self.dev)
 
     # ------------------------------------------------------------------ model
-    def _lin(self, x, lay, pj):
-        return _QLinearFn.apply(x, self.anchor, lay[pj], lay[pj + ".g"])
+    def _proj_done(self, li: int) -> None:
+        self._pending[li] -= 1
+        if self._pending[li] == 0:
+            self.reducer.layer_ready(li)
+
+    def _lin(self, x, lay, pj, anchor):
+        return _QLinearFn.apply(x, anchor, lay[pj], lay[pj + ".g"], lay["notify"])
+
+    def _layer(self, x, li, anchor):
+        cfg = self.cfg
+        lay = self.layers[li]
+        b, s = x.shape[0], x.shape[1]
+        nh, d = cfg.n_heads, cfg.hidden // cfg.n_heads
+        hn = _rmsnorm(x, cfg.rms_eps)
+        cs = self.cos_sin[:s]
+        q = _rope(self._lin(hn, lay, "q", anchor).view(b, s, nh, d), cs).transpose(1, 2)
+        k = _rope(self._lin(hn, lay, "k", anchor).view(b, s, nh, d), cs).transpose(1, 2)
+        v = self._lin(hn, lay, "v", anchor).view(b, s, nh, d).transpose(1, 2)
+        a = F.scaled_dot_product_attention(q, k, v, is_causal=True).transpose(1, 2).reshape(b, s, cfg.hidden)
+        x = x + self._lin(a, lay, "o", anchor)
+        hn = _rmsnorm(x, cfg.rms_eps)
+        gt = self._lin(hn, lay, "gate", anchor)
+        up = self._lin(hn, lay, "up", anchor)
+        return x + self._lin(_SwiGLUFn.apply(gt, up), lay, "down", anchor)
 
     def loss(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         cfg = self.cfg
         b, s = tokens.shape
-        nh, d = cfg.n_heads, cfg.hidden // cfg.n_heads
         x = F.embedding(tokens, self.embed)
-        for lay in self.layers:
-            hn = _rmsnorm(x, cfg.rms_eps)
-            cs = self.cos_sin[:s]
-            q = _rope(self._lin(hn, lay, "q").view(b, s, nh, d), cs).transpose(1, 2)
-            k = _rope(self._lin(hn, lay, "k").view(b, s, nh, d), cs).transpose(1, 2)
-            v = self._lin(hn, lay, "v").view(b, s, nh, d).transpose(1, 2)
-            a = F.scaled_dot_product_attention(q, k, v, is_causal=True).transpose(1, 2).reshape(b, s, cfg.hidden)
-            x = x + self._lin(a, lay, "o")
-            hn = _rmsnorm(x, cfg.rms_eps)
-            gt = self._lin(hn, lay, "gate")
-            up = self._lin(hn, lay, "up")
-            x = x + self._lin(_SwiGLUFn.apply(gt, up), lay, "down")
+        for li in range(cfg.n_layers):
+            if self.checkpoint:
+                # reentrant: the layer reruns under grad in the backward; the
+                # anchor (requires_grad) carries the graph through it
+                x = _ckpt.checkpoint(self._layer, x, li, self.anchor, use_reentrant=True,
+                                     preserve_rng_state=False)
+            else:
+                x = self._layer(x, li, self.anchor)
         x = _rmsnorm(x, cfg.rms_eps)
         logits = x.reshape(b * s, cfg.hidden) @ self.lm_head
         return F.cross_entropy(logits.float(), targets.reshape(-1))
 
     # ------------------------------------------------------------------ step
     def set_step_constants(self) -> None:
-        """Host side of one optimizer step: the numpy-2 float32 constants of
-        the reference update (training.py:426-442) for step t+1, into the
-        pinned buffer the graph copies from."""
+        """Host mirror of the step counter (the paged optimizer's scan
+        direction follows it); the constants themselves come from the device
+        table row the device counter selects inside the step."""
         self.t += 1
-        c = self.train_cfg
-        f = np.float32
-        vals = (c.adam_beta1, 1.0 - c.adam_beta1, c.adam_beta2, 1.0 - c.adam_beta2,
-                1.0 - c.adam_beta1 ** self.t, 1.0 - c.adam_beta2 ** self.t, c.adam_eps, c.learning_rate)
-        self.hyper_host.copy_(torch.tensor([float(f(v)) for v in vals], dtype=torch.float32))
 
-    def train_step(self, tokens: torch.Tensor, targets: torch.Tensor, group=None) -> torch.Tensor:
-        """One QLoRA step (capturable: no host sync).  Call set_step_constants() first."""
+    def forward_backward(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        """Loss, backward with the overlapped adapter-gradient all-reduce, and
+        the global fp64 sum of squares for the clip (capturable: no host sync)."""
+        self._pending = [len(PROJS)] * self.cfg.n_layers
+        self.reducer.reset()
         loss = self.loss(tokens, targets)
         loss.backward()
-        self.bucket.start(group)
-        self.bucket.finish(group)
-        self.hyper.copy_(self.hyper_host, non_blocking=True)
+        self.reducer.finish()
+        # step t + 1's Adam constants from the table (device-side counter)
+        self.hyper.copy_(self.hyper_table.index_select(0, self.t_dev).view(-1))
+        self.t_dev.add_(1)
         self.sumsq.zero_()
-        L = lib()
-        check(L.qlrt_sumsq_f64(ptr(self.bucket.flat), self.bucket.flat.numel(), ptr(self.sumsq), stream_ptr()),
+        check(lib().qlrt_sumsq_f64(ptr(self.bucket.flat), self.bucket.flat.numel(), ptr(self.sumsq), stream_ptr()),
               "clip")
-        check(L.qlrt_adam_step_dev(ptr(self.params_flat), ptr(self.bucket.flat), ptr(self.m_flat), ptr(self.v_flat),
-                                   self.params_flat.numel(), ptr(self.hyper), ptr(self.sumsq),
-                                   float(self.train_cfg.max_grad_norm), ptr(self.shadow_flat), stream_ptr()),
-              "adam")
         return loss.detach()
+
+    def _adam(self, off: int, n: int, m: torch.Tensor, v: torch.Tensor) -> None:
+        check(lib().qlrt_adam_step_dev(ptr(self.params_flat) + 4 * off, ptr(self.bucket.flat) + 4 * off, ptr(m),
+                                       ptr(v), n, ptr(self.hyper), ptr(self.sumsq),
+                                       float(self.train_cfg.max_grad_norm), ptr(self.shadow_flat) + 2 * off,
+                                       stream_ptr()), "adam")
+
+    def optimizer_step(self) -> None:
+        """Fused clip + Adam over every adapter parameter.  Plain: one launch
+        over the flat buffers (capturable).  Paged: one launch per layer slab,
+        elevator order, the next ``lookahead`` slabs prefetched while the
+        current one updates (host-driven: the pager decides faults and
+        evictions per step)."""
+        if self.pager is None:
+            self._adam(0, self.params_flat.numel(), self.m_flat, self.v_flat)
+            return
+        n_l = self.cfg.n_layers
+        self._scans += 1
+        order = list(range(n_l)) if self._scans % 2 == 1 else list(range(n_l - 1, -1, -1))
+        for i, li in enumerate(order):
+            off, n = self.layer_spans[li]
+            st = self.pager.acquire(self.mslabs[li]).view(torch.float32)
+            self._adam(off, n, st[:n], st[n:])
+            self.pager.release(self.mslabs[li])
+            for j in order[i + 1: i + 1 + self.lookahead]:
+                self.pager.prefetch(self.mslabs[j])
+
+    def train_step(self, tokens: torch.Tensor, targets: torch.Tensor, group=None) -> torch.Tensor:
+        """One QLoRA step; call set_step_constants() first.  Capturable as a
+        whole with the plain optimizer (``group`` is accepted for backward
+        compatibility; the process group is fixed at construction)."""
+        loss = self.forward_backward(tokens, targets)
+        self.optimizer_step()
+        return loss
+
+    def state_bytes(self) -> int:
+        """Adam moment bytes (m + v, fp32) of all adapter parameters."""
+        return 8 * self.params_flat.numel()
+
+    def moments(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """(m, v) as flat fp32 tensors in parameter order (a copy when paged)."""
+        if self.pager is None:
+            return self.m_flat, self.v_flat
+        ms, vs = [], []
+        for li, (off, n) in enumerate(self.layer_spans):
+            st = self.pager.view(self.mslabs[li]).view(torch.float32)
+            ms.append(st[:n].clone())
+            vs.append(st[n:].clone())
+        return torch.cat(ms), torch.cat(vs)
+
+    def close(self) -> None:
+        if self.pager is not None:
+            self.pager.close()
+            self.pager = None
 
 
 __all__ = ["LlamaConfig", "LlamaQLoRA", "PROJS"]

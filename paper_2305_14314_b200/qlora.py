@@ -52,19 +52,31 @@ class LoraAdapter:
     def scaling(self) -> float:
         return self.alpha / self.rank
 
+    def _versions(self):
+        return (self.l1._version, self.l2._version)
+
     def bf16_operands(self):
-        """bf16 copies of l1 / l2, zero-padded to a rank multiple of 8 (the
-        optimizer refreshes them in place after every step)."""
+        """bf16 copies of l1 / l2, zero-padded to a rank multiple of 8.  They
+        follow the fp32 masters: any in-place change of l1 / l2 (a torch op, or
+        ``AdamOptimizer.step``, which bumps their version counters) refreshes
+        them before the next use."""
         rp = _pad8(self.rank)
         key = (self.l1.data_ptr(), self.l2.data_ptr(), rp)
         sh = self._shadow.get("ops")
         if sh is None or sh[0] != key:
             l1b = torch.zeros(self.l1.shape[0], rp, dtype=torch.bfloat16, device=self.l1.device)
             l2b = torch.zeros(rp, self.l2.shape[1], dtype=torch.bfloat16, device=self.l2.device)
-            sh = (key, l1b, l2b)
+            sh = [key, l1b, l2b, None]
             self._shadow["ops"] = sh
+        if sh[3] != self._versions():
             self.refresh_bf16()
         return sh[1], sh[2]
+
+    def adopt_shadows(self, l1b: torch.Tensor, l2b: torch.Tensor) -> None:
+        """Use caller-owned bf16 copies (kept current by the caller, e.g. the
+        fused Adam kernel of the LLaMA harness) as the MMA operands."""
+        self._shadow["ops"] = [(self.l1.data_ptr(), self.l2.data_ptr(), _pad8(self.rank)), l1b, l2b,
+                               self._versions()]
 
     def refresh_bf16(self) -> None:
         sh = self._shadow.get("ops")
@@ -72,6 +84,7 @@ class LoraAdapter:
             return
         sh[1][:, : self.rank].copy_(self.l1)
         sh[2][: self.rank].copy_(self.l2)
+        sh[3] = self._versions()
 
 
 def lora_init(in_dim: int, out_dim: int, rank: int, alpha: float, rng: np.random.Generator,
@@ -100,8 +113,7 @@ class QLinear:
             if ad.l1.shape[0] != base.shape[0] or ad.l2.shape[1] != base.shape[1]:
                 raise ValueError(f"adapter ({tuple(ad.l1.shape)} x {tuple(ad.l2.shape)}) does not match "
                                  f"base shape {tuple(base.shape)}")
-        if len(self.adapters) > 1:
-            raise ValueError("the fused GPU layer carries at most one adapter per layer")
+        self._cat = None
         self._ws = None
         self._wdesc = None
 
@@ -150,11 +162,13 @@ class QLinear:
             return dequantize(self.base, torch.float32).to(self.dtype)
         return torch.as_tensor(self.base).to(device="cuda", dtype=self.dtype)
 
+    def _rank_total(self) -> int:
+        return sum(_pad8(ad.rank) for ad in self.adapters)
+
     def _workspace(self, m: int) -> torch.Tensor:
         """Scratch of the fused entry points.  Layers share one buffer per
         device (their launches are stream-ordered); it only grows."""
-        r = _pad8(self.adapters[0].rank) if self.adapters else 0
-        need = int(lib().qlrt_linear_workspace_bytes(max(m, 1), self.in_dim, self.out_dim, r))
+        need = int(lib().qlrt_linear_workspace_bytes(max(m, 1), self.in_dim, self.out_dim, self._rank_total()))
         dev = torch.cuda.current_device()
         ws = _LINEAR_WS.get(dev)
         if ws is None or ws.numel() < need:
@@ -162,16 +176,50 @@ class QLinear:
             _LINEAR_WS[dev] = ws
         return ws
 
-    # -- forward / backward -------------------------------------------------
-    def forward(self, x, train: bool = False, rng=None) -> tuple[torch.Tensor, dict[str, Any]]:
-        x = torch.as_tensor(x).to(device="cuda", dtype=self.dtype).contiguous()
-        lead = x.shape[:-1]
-        x2 = x.reshape(-1, self.in_dim)
-        m = x2.shape[0]
-        ad = self.adapters[0] if self.adapters else None
-        mask = None
-        xa = x2
-        if ad is not None and train and ad.dropout_p > 0.0:
+    def _operands(self):
+        """bf16 MMA operands of all adapters: one adapter -> its own copies;
+        several -> l1c = [l1_0 | l1_1 | ...] ([in, R]) and l2c = [l2_0; l2_1; ...]
+        ([R, out]), each rank zero-padded to a multiple of 8, rebuilt when any
+        master changes.  A sum of adapters is one adapter of the summed rank
+        once each Ts_i / dT_i carries its own scaling (qlora.py:133-146)."""
+        if len(self.adapters) == 1:
+            return self.adapters[0].bf16_operands()
+        key = tuple((ad.l1.data_ptr(), ad.l2.data_ptr()) + ad._versions() for ad in self.adapters)
+        if self._cat is None or self._cat[0] != key:
+            R = self._rank_total()
+            l1c = torch.zeros(self.in_dim, R, dtype=torch.bfloat16, device=self.adapters[0].l1.device)
+            l2c = torch.zeros(R, self.out_dim, dtype=torch.bfloat16, device=self.adapters[0].l1.device)
+            o = 0
+            for ad in self.adapters:
+                l1c[:, o: o + ad.rank].copy_(ad.l1)
+                l2c[o: o + ad.rank].copy_(ad.l2)
+                o += _pad8(ad.rank)
+            self._cat = (key, l1c, l2c)
+        return self._cat[1], self._cat[2]
+
+    def _pairs(self, inputs, ts: torch.Tensor, transpose_l2: bool) -> None:
+        """Per-adapter s_i * inputs_i @ l1_i (or s_i * dY @ l2_i^T) as bf16 hi/lo
+        pairs into ts[:, o_i : o_i + r_i] (hi) and ts[:, R + o_i : ...] (lo)."""
+        R = ts.shape[1] // 2
+        o = 0
+        for ad, inp in zip(self.adapters, inputs):
+            rp = _pad8(ad.rank)
+            l1b, l2b = ad.bf16_operands()
+            v = (gemm_bf16(inp, l2b, alpha=ad.scaling, b_t=True, out_dtype=torch.float32) if transpose_l2
+                 else gemm_bf16(inp, l1b, alpha=ad.scaling, out_dtype=torch.float32))
+            hi = v.to(torch.bfloat16)
+            ts[:, o: o + rp].copy_(hi)
+            ts[:, R + o: R + o + rp].copy_((v - hi.float()).to(torch.bfloat16))
+            o += rp
+
+    def _masks(self, x2: torch.Tensor, train: bool, rng) -> list:
+        """Dropout masks on the adapter inputs, drawn adapter by adapter from
+        ``rng`` as the reference does (qlora.py:137-143); None = no dropout."""
+        masks = []
+        for ad in self.adapters:
+            if not (train and ad.dropout_p > 0.0):
+                masks.append(None)
+                continue
             if rng is None:
                 raise ValueError("dropout needs an rng in train mode")
             keep = 1.0 - ad.dropout_p
@@ -179,97 +227,158 @@ class QLinear:
                 draw = torch.rand(x2.shape, generator=rng, device=x2.device)
             else:  # numpy Generator: the reference's exact mask (qlora.py:140-142)
                 draw = torch.from_numpy(rng.random(tuple(x2.shape))).to(x2.device)
-            mask = ((draw >= ad.dropout_p).to(torch.float32) / keep)
-            xa = (x2.float() * mask).to(self.dtype).contiguous()
+            masks.append((draw >= ad.dropout_p).to(torch.float32) / keep)
+        return masks
+
+    # -- forward / backward -------------------------------------------------
+    def forward(self, x, train: bool = False, rng=None) -> tuple[torch.Tensor, dict[str, Any]]:
+        """y = x W + sum_i s_i (xa_i l1_i) l2_i (qlora.py:124-148).  One
+        adapter without dropout is the fully fused path (Ts and the NF4 GEMM
+        with the adapter term in its accumulator, all in the C ABI); several
+        adapters or dropout compute the Ts pairs here and still join the same
+        accumulator; M = 1 runs the HBM-streaming GEMV."""
+        x = torch.as_tensor(x).to(device="cuda", dtype=self.dtype).contiguous()
+        lead = x.shape[:-1]
+        x2 = x.reshape(-1, self.in_dim)
+        m = x2.shape[0]
+        masks = self._masks(x2, train, rng)
+        xas = [x2 if mk is None else (x2.float() * mk).to(self.dtype).contiguous() for mk in masks]
         y = torch.empty(m, self.out_dim, dtype=self.dtype, device=x2.device)
-        rp = _pad8(ad.rank) if ad else 0
-        ts = torch.empty(m, 2 * rp, dtype=self.dtype, device=x2.device) if ad else None  # bf16 hi | lo
-        # the GEMV decodes the DQ constants itself; at m > 1 the fp32 constants are
-        # built once here and shared with backward (None -> backward rebuilds them)
-        consts = self._constants() if self.fused() and m > 1 else None
-        if self.fused() and m > 1:
-            l1b, l2b = ad.bf16_operands() if ad else (None, None)
-            check(lib().qlrt_nf4_linear_fwd(self.weight_desc(consts), ptr(x2), ptr(xa) if mask is not None else None, m,
-                                            ptr(l1b), ptr(l2b), rp, float(ad.scaling) if ad else 0.0, ptr(ts),
-                                            ptr(y), ptr(self._workspace(m)), stream_ptr()), "QLinear.forward")
-        elif self.fused() and m == 1:
-            l1b, l2b = ad.bf16_operands() if ad else (None, None)
-            if ad is not None:
-                _split_into(gemm_bf16(xa, l1b, alpha=ad.scaling, out_dtype=torch.float32), ts)
-            check(lib().qlrt_nf4_gemv(self.weight_desc(None), ptr(x2), ptr(l1b), ptr(l2b), rp,
-                                      float(ad.scaling) if ad else 0.0, ptr(y), ptr(self._workspace(m)),
-                                      stream_ptr()), "QLinear.forward(gemv)")
+        n_ad = len(self.adapters)
+        R = self._rank_total()
+        ts = torch.empty(m, 2 * R, dtype=self.dtype, device=x2.device) if n_ad else None  # bf16 hi | lo
+        consts = None
+        if self.fused() and m == 1 and n_ad <= 1:
+            # the GEMV decodes the DQ constants itself; Ts (needed only by a
+            # backward) is left to backward -- inference pays nothing for it
+            ad = self.adapters[0] if n_ad else None
+            l1b, l2b = self._operands() if n_ad else (None, None)
+            check(lib().qlrt_nf4_gemv(self.weight_desc(None), ptr(x2), ptr(xas[0]) if masks and masks[0] is not None
+                                      else None, ptr(l1b), ptr(l2b), R, float(ad.scaling) if ad else 0.0, ptr(y),
+                                      ptr(self._workspace(m)), stream_ptr()), "QLinear.forward(gemv)")
+            ts_ready = False
+        elif self.fused():
+            # fp32 block constants built once here and shared with backward
+            consts = self._constants()
+            l1b, l2b = self._operands() if n_ad else (None, None)
+            if n_ad == 1:
+                ad = self.adapters[0]
+                check(lib().qlrt_nf4_linear_fwd(self.weight_desc(consts), ptr(x2),
+                                                ptr(xas[0]) if masks[0] is not None else None, m, ptr(l1b),
+                                                ptr(l2b), R, float(ad.scaling), ptr(ts), ptr(y),
+                                                ptr(self._workspace(m)), stream_ptr()), "QLinear.forward")
+            else:
+                if n_ad:
+                    self._pairs(xas, ts, False)  # Ts given: l1 = NULL
+                check(lib().qlrt_nf4_linear_fwd(self.weight_desc(consts), ptr(x2), None, m, None, ptr(l2b), R, 0.0,
+                                                ptr(ts), ptr(y), ptr(self._workspace(m)), stream_ptr()),
+                      "QLinear.forward")
+            ts_ready = True
         else:
             w = self.dequant_weight().contiguous()
-            gemm_bf16(x2, w, out=y)
-            if ad is not None:
-                l1b, l2b = ad.bf16_operands()
-                _split_into(gemm_bf16(xa, l1b, alpha=ad.scaling, out_dtype=torch.float32), ts)
-                y.copy_((y.float() + gemm_bf16(ts[:, :rp], l2b, out_dtype=torch.float32)
-                         + gemm_bf16(ts[:, rp:], l2b, out_dtype=torch.float32)).to(self.dtype))
-        cache = {"x": x2, "xa": xa, "ts": ts, "mask": mask, "lead": lead, "consts": consts}
+            y32 = gemm_bf16(x2, w, out_dtype=torch.float32)
+            if n_ad:
+                self._pairs(xas, ts, False)
+                o = 0
+                for ad in self.adapters:
+                    rp = _pad8(ad.rank)
+                    _, l2b = ad.bf16_operands()
+                    y32 += gemm_bf16(ts[:, o: o + rp], l2b, out_dtype=torch.float32)
+                    y32 += gemm_bf16(ts[:, R + o: R + o + rp], l2b, out_dtype=torch.float32)
+                    o += rp
+            y.copy_(y32.to(self.dtype))
+            ts_ready = True
+        cache = {"x": x2, "xas": xas, "masks": masks, "ts": ts, "ts_ready": ts_ready, "lead": lead,
+                 "consts": consts}
         return y.reshape(*lead, self.out_dim), cache
 
     def backward(self, d_y, cache: dict[str, Any], grads_out: dict | None = None
                  ) -> tuple[torch.Tensor, dict[str, torch.Tensor]]:
-        """``grads_out`` optionally names fp32 buffers ([in, rank], [rank, out],
-        e.g. views of a data-parallel gradient bucket) the fused kernels write
-        the adapter gradients into directly."""
+        """dX = dY W^T + sum_i (s_i dY l2_i^T) l1_i^T (masked), dl2_i = s_i t_i^T dY,
+        dl1_i = xa_i^T (s_i dY l2_i^T) (qlora.py:150-167).  ``grads_out``
+        optionally names fp32 buffers ([in, rank], [rank, out], e.g. views of a
+        data-parallel gradient bucket) the fused kernels write the adapter
+        gradients into directly."""
         d_y = torch.as_tensor(d_y).to(device="cuda", dtype=self.dtype).reshape(-1, self.out_dim).contiguous()
         m = d_y.shape[0]
-        ad = self.adapters[0] if self.adapters else None
+        n_ad = len(self.adapters)
+        R = self._rank_total()
+        dev = d_y.device
         grads: dict[str, torch.Tensor] = {}
-        d_x = torch.empty(m, self.in_dim, dtype=self.dtype, device=d_y.device)
-        mask = cache["mask"]
-        if ad is not None:
-            rp = _pad8(ad.rank)
-            l1b, l2b = ad.bf16_operands()
-            dt = torch.empty(m, 2 * rp, dtype=self.dtype, device=d_y.device)  # bf16 hi | lo
+        d_x = torch.empty(m, self.in_dim, dtype=self.dtype, device=dev)
+        masks, xas, ts = cache["masks"], cache["xas"], cache["ts"]
+        if n_ad and not cache["ts_ready"]:
+            self._pairs(xas, ts, False)  # the GEMV forward left Ts to backward
+            cache["ts_ready"] = True
+        any_mask = any(mk is not None for mk in masks)
+        wd = self.weight_desc(cache.get("consts")) if self.fused() else None
+        ws = self._workspace(m) if self.fused() else None
+        if n_ad == 0 or (self.fused() and not any_mask):
             go = grads_out or {}
+            single = n_ad == 1
             g1, g2 = go.get("adapter0.l1"), go.get("adapter0.l2")
-            direct = (rp == ad.rank and g1 is not None and g2 is not None and g1.is_contiguous()
-                      and g2.is_contiguous() and g1.dtype == torch.float32 and g2.dtype == torch.float32
-                      and tuple(g1.shape) == (self.in_dim, rp) and tuple(g2.shape) == (rp, self.out_dim))
-            dl1 = g1 if direct else torch.empty(self.in_dim, rp, dtype=torch.float32, device=d_y.device)
-            dl2 = g2 if direct else torch.empty(rp, self.out_dim, dtype=torch.float32, device=d_y.device)
-        if self.fused() and mask is None:
-            if ad is None:
-                check(lib().qlrt_nf4_linear_bwd(self.weight_desc(cache.get("consts")), ptr(d_y), m, None, None, None, None, 0, 0.0,
-                                                None, ptr(d_x), None, None, ptr(self._workspace(m)), stream_ptr()),
-                      "QLinear.backward")
+            direct = (single and R == self.adapters[0].rank and g1 is not None and g2 is not None
+                      and g1.is_contiguous() and g2.is_contiguous() and g1.dtype == torch.float32
+                      and g2.dtype == torch.float32 and tuple(g1.shape) == (self.in_dim, R)
+                      and tuple(g2.shape) == (R, self.out_dim))
+            if n_ad == 0:
+                if self.fused():
+                    check(lib().qlrt_nf4_linear_bwd(wd, ptr(d_y), m, None, None, None, None, 0, 0.0, None, ptr(d_x),
+                                                    None, None, ptr(ws), stream_ptr()), "QLinear.backward")
+                else:
+                    gemm_bf16(d_y, self.dequant_weight().contiguous(), out=d_x, b_t=True)
+                return d_x.reshape(*cache["lead"], self.in_dim), grads
+            dt = torch.empty(m, 2 * R, dtype=self.dtype, device=dev)  # bf16 hi | lo
+            dl1 = g1 if direct else torch.empty(self.in_dim, R, dtype=torch.float32, device=dev)
+            dl2 = g2 if direct else torch.empty(R, self.out_dim, dtype=torch.float32, device=dev)
+            l1b, l2b = self._operands()
+            if single:
+                ad = self.adapters[0]
+                check(lib().qlrt_nf4_linear_bwd(wd, ptr(d_y), m, ptr(xas[0]), ptr(ts), ptr(l1b), ptr(l2b), R,
+                                                float(ad.scaling), ptr(dt), ptr(d_x), ptr(dl1), ptr(dl2), ptr(ws),
+                                                stream_ptr()), "QLinear.backward")
             else:
-                check(lib().qlrt_nf4_linear_bwd(self.weight_desc(cache.get("consts")), ptr(d_y), m, ptr(cache["xa"]), ptr(cache["ts"]),
-                                                ptr(l1b), ptr(l2b), rp, float(ad.scaling), ptr(dt), ptr(d_x),
-                                                ptr(dl1), ptr(dl2), ptr(self._workspace(m)), stream_ptr()),
+                self._pairs([d_y] * n_ad, dt, True)  # dT given: l2 = NULL
+                check(lib().qlrt_nf4_linear_bwd(wd, ptr(d_y), m, ptr(cache["x"]), ptr(ts), ptr(l1b), None, R, 0.0,
+                                                ptr(dt), ptr(d_x), ptr(dl1), ptr(dl2), ptr(ws), stream_ptr()),
                       "QLinear.backward")
+            o = 0
+            for i, ad in enumerate(self.adapters):
+                grads[f"adapter{i}.l1"] = dl1[:, o: o + ad.rank]
+                grads[f"adapter{i}.l2"] = dl2[o: o + ad.rank]
+                o += _pad8(ad.rank)
         else:
+            # dropout (or a base the fused kernels do not take): the base product
+            # through the engine, the masked adapter terms added in fp32
             if self.fused():
-                check(lib().qlrt_nf4_linear_bwd(self.weight_desc(cache.get("consts")), ptr(d_y), m, None, None, None, None, 0, 0.0,
-                                                None, ptr(d_x), None, None, ptr(self._workspace(m)), stream_ptr()),
-                      "QLinear.backward")
+                check(lib().qlrt_nf4_linear_bwd(wd, ptr(d_y), m, None, None, None, None, 0, 0.0, None, ptr(d_x),
+                                                None, None, ptr(ws), stream_ptr()), "QLinear.backward")
+                dx32 = d_x.float()
             else:
-                w = self.dequant_weight().contiguous()
-                gemm_bf16(d_y, w, out=d_x, b_t=True)
-            if ad is not None:
-                _split_into(gemm_bf16(d_y, l2b, alpha=ad.scaling, b_t=True, out_dtype=torch.float32), dt)
-                d_xa = (gemm_bf16(dt[:, :rp], l1b, b_t=True, out_dtype=torch.float32)
-                        + gemm_bf16(dt[:, rp:], l1b, b_t=True, out_dtype=torch.float32))
-                if mask is not None:
-                    d_xa = d_xa * mask
-                d_x.copy_((d_x.float() + d_xa).to(self.dtype))
-                ts = cache["ts"]
-                dl2.copy_(gemm_bf16(ts[:, :rp], d_y, a_t=True, out_dtype=torch.float32)
-                          + gemm_bf16(ts[:, rp:], d_y, a_t=True, out_dtype=torch.float32))
-                dl1.copy_(gemm_bf16(cache["xa"], dt[:, :rp], a_t=True, out_dtype=torch.float32)
-                          + gemm_bf16(cache["xa"], dt[:, rp:], a_t=True, out_dtype=torch.float32))
-        if ad is not None:
-            grads["adapter0.l1"] = dl1[:, : ad.rank]
-            grads["adapter0.l2"] = dl2[: ad.rank]
-            if grads_out and not direct:
-                for k in ("adapter0.l1", "adapter0.l2"):
-                    if grads_out.get(k) is not None:
-                        grads_out[k].copy_(grads[k])
-                        grads[k] = grads_out[k]
+                dx32 = gemm_bf16(d_y, self.dequant_weight().contiguous(), b_t=True, out_dtype=torch.float32)
+            dt = torch.empty(m, 2 * R, dtype=self.dtype, device=dev)
+            self._pairs([d_y] * n_ad, dt, True)
+            o = 0
+            for i, (ad, mk, xa) in enumerate(zip(self.adapters, masks, xas)):
+                rp = _pad8(ad.rank)
+                l1b, _ = ad.bf16_operands()
+                hi, lo = dt[:, o: o + rp], dt[:, R + o: R + o + rp]
+                d_xa = (gemm_bf16(hi, l1b, b_t=True, out_dtype=torch.float32)
+                        + gemm_bf16(lo, l1b, b_t=True, out_dtype=torch.float32))
+                dx32 += d_xa if mk is None else d_xa * mk
+                t_hi, t_lo = ts[:, o: o + rp], ts[:, R + o: R + o + rp]
+                grads[f"adapter{i}.l2"] = (gemm_bf16(t_hi, d_y, a_t=True, out_dtype=torch.float32)
+                                           + gemm_bf16(t_lo, d_y, a_t=True, out_dtype=torch.float32))[: ad.rank]
+                grads[f"adapter{i}.l1"] = (gemm_bf16(xa, hi, a_t=True, out_dtype=torch.float32)
+                                           + gemm_bf16(xa, lo, a_t=True, out_dtype=torch.float32))[:, : ad.rank]
+                o += rp
+            d_x.copy_(dx32.to(self.dtype))
+        if grads_out:
+            for k, v in list(grads.items()):
+                tgt = grads_out.get(k)
+                if tgt is not None and tgt.data_ptr() != v.data_ptr():
+                    tgt.copy_(v)
+                    grads[k] = tgt
         return d_x.reshape(*cache["lead"], self.in_dim), grads
 
     def trainable(self) -> dict[str, torch.Tensor]:
@@ -278,14 +387,6 @@ class QLinear:
             out[f"adapter{i}.l1"] = ad.l1
             out[f"adapter{i}.l2"] = ad.l2
         return out
-
-
-def _split_into(v: torch.Tensor, pair: torch.Tensor) -> None:
-    """fp32 [m, r] -> bf16 hi/lo pair stored as pair[:, :r] | pair[:, r:]."""
-    r = v.shape[1]
-    hi = v.to(torch.bfloat16)
-    pair[:, :r].copy_(hi)
-    pair[:, r:].copy_((v - hi.float()).to(torch.bfloat16))
 
 
 _GEMM_WS: dict = {}

@@ -96,6 +96,12 @@ class PagedMomentStore:
 
         self.pager.with_slab(slab, run)
 
+    def prefetch(self, name: str) -> None:
+        """Start migrating ``name``'s moments to the device (look-ahead)."""
+        slab = self._slabs.get(name)
+        if slab is not None:
+            self.pager.prefetch(slab)
+
     def close(self) -> None:
         self.pager.flush()
 
@@ -156,7 +162,9 @@ class AdamOptimizer:
     def step(self, grads: dict) -> None:
         self.t += 1
         consts = self.constants()
-        for name, p in self.params.items():
+        names = list(self.params)
+        for i, name in enumerate(names):
+            p = self.params[name]
             g = grads[name]
             if not g.is_contiguous():
                 g = g.contiguous()
@@ -169,6 +177,12 @@ class AdamOptimizer:
                                            stream_ptr()), "AdamOptimizer.step")
 
             self.store.update(name, p, upd)
+            # the kernel wrote p through its pointer: bump its version so the
+            # layers' bf16 operand copies (LoraAdapter.bf16_operands) refresh
+            torch.autograd.graph.increment_version(p)
+            nxt = names[i + 1] if i + 1 < len(names) else None
+            if nxt is not None and hasattr(self.store, "prefetch"):
+                self.store.prefetch(nxt)  # look-ahead: the next moments migrate while this update runs
 
 
 def check_finite(loss: float, norm: float, step: int) -> None:

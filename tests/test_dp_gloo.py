@@ -43,3 +43,10 @@ def test_allreduce_mean_two_ranks():
         assert d["l2"] == [[1.5 * (3 * i + j) for j in range(3)] for i in range(4)]
         assert d["a"] == [0.5] * 3 and d["b"] == [[10.5, 10.5], [10.5, 10.5]]
     assert outs[0]["shard"] == [0, 5] and outs[1]["shard"] == [5, 10]
+    # LayerReducer: group 2 (layer 4) launches as soon as layer 4 is ready,
+    # group 1 after layers 3 and 2; finish launches the rest; mean = 1.5 x
+    for d in outs:
+        for wire, red in d["reducer"].items():
+            assert red["early"] == [[2], [2], [2, 1]], wire
+            assert red["launched"] == [2, 1, 0], wire
+            assert red["flat"] == [1.5 * i for i in range(15)], wire

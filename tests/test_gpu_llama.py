@@ -165,3 +165,113 @@ def test_step_matches_reference_update_and_graph_replay(cuda):
     torch.cuda.synchronize()
     assert torch.equal(m2.params_flat, m3.params_flat)
     assert torch.equal(gl, el)
+
+
+def test_grad_groups_launch_as_backward_reaches_them(cuda):
+    """The overlapped reducer launches each layer group's all-reduce from
+    inside the backward, last group first (before the backward returns)."""
+    from paper_2305_14314_b200.llama import LlamaConfig, LlamaQLoRA
+    m = LlamaQLoRA(LlamaConfig.tiny(n_layers=4), seed=0, bucket_layers=1)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    tok = torch.randint(0, 512, (2, 64), device="cuda", generator=g)
+    m._pending = [7] * 4
+    m.reducer.reset()
+    m.loss(tok, tok).backward()
+    assert m.reducer.launched == [3, 2, 1, 0]
+
+
+def _paged_pair(budget_layers, page_bytes):
+    from paper_2305_14314_b200.llama import LlamaConfig, LlamaQLoRA
+    cfg = LlamaConfig.tiny(n_layers=4)
+    plain = LlamaQLoRA(cfg, seed=5)
+    span = plain.layer_spans[0][1]
+    slab_pages = (2 * span * 4 + page_bytes - 1) // page_bytes
+    paged = LlamaQLoRA(cfg, seed=5, optimizer="paged", pager_budget_bytes=budget_layers * slab_pages * page_bytes,
+                       page_bytes=page_bytes)
+    return plain, paged
+
+
+@pytest.mark.parametrize("budget_layers,page_bytes", [(1, 64 << 10), (2, 64 << 10), (4, 2 << 20)])
+def test_paged_adamw_equals_plain(budget_layers, page_bytes, cuda):
+    """PagedMomentStore transparency on the training path (pkg/tests/
+    test_training.py:325-350): the paged harness -- moments in unified-memory
+    pages under a budget below the total state, elevator order, look-ahead
+    prefetch -- produces bit-identical parameters and moments to the plain one."""
+    plain, paged = _paged_pair(budget_layers, page_bytes)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    tok = torch.randint(0, 512, (2, 64), device="cuda", generator=g)
+    tgt = torch.randint(0, 512, (2, 64), device="cuda", generator=g)
+    for _ in range(4):
+        for mdl in (plain, paged):
+            mdl.set_step_constants()
+            mdl.train_step(tok, tgt)
+    torch.cuda.synchronize()
+    assert torch.equal(plain.params_flat, paged.params_flat)
+    assert torch.equal(plain.shadow_flat, paged.shadow_flat)
+    pm, pv = paged.moments()
+    assert torch.equal(plain.m_flat, pm) and torch.equal(plain.v_flat, pv)
+    pg = paged.pager
+    assert pg.faults > 0 and pg.peak_resident_bytes <= pg.config.budget_bytes
+    if budget_layers < 4:
+        assert pg.evictions > 0 and pg.bytes_read > 0
+    paged.close()
+
+
+def test_checkpointed_layers_match(cuda):
+    """Gradient checkpointing recomputes each layer in the backward: same loss
+    and adapter gradients as keeping the activations."""
+    from paper_2305_14314_b200.llama import LlamaConfig, LlamaQLoRA
+    cfg = LlamaConfig.tiny(n_layers=3)
+    a = LlamaQLoRA(cfg, seed=9)
+    b = LlamaQLoRA(cfg, seed=9, checkpoint=True)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    for mdl in (a, b):
+        for n, p in mdl.params.items():
+            if n.endswith(".l2"):
+                p.copy_(torch.randn(p.shape, device="cuda", generator=torch.Generator(device="cuda").manual_seed(4)) * 0.05)
+        mdl.shadow_flat.copy_(mdl.params_flat)
+    tok = torch.randint(0, 512, (2, 64), device="cuda", generator=g)
+    la = a.forward_backward(tok, tok)
+    lb = b.forward_backward(tok, tok)
+    torch.cuda.synchronize()
+    assert torch.equal(la, lb)
+    d = (a.bucket.flat - b.bucket.flat).abs().max() / a.bucket.flat.abs().max()
+    assert float(d) <= 1e-6, float(d)
+
+
+@pytest.mark.timeout(300)
+def test_dp_two_ranks_equal_one_rank_over_concatenated_batch(cuda, tmp_path):
+    """Two data-parallel ranks (gloo, both on cuda:0), each on half of the
+    batch: the all-reduced adapter gradients and the loss equal one rank's
+    over the whole batch (tolerance: bf16 GEMMs see different M tilings)."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    helper = os.path.join(os.path.dirname(__file__), "helpers", "dp_llama_worker.py")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                   OUT=str(tmp_path / f"r{r}.pt"))
+        procs.append(subprocess.Popen([sys.executable, helper], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    for p in procs:
+        out, err = p.communicate(timeout=280)
+        assert p.returncode == 0, err[-3000:]
+    env = dict(os.environ, RANK="0", WORLD_SIZE="1", OUT=str(tmp_path / "single.pt"))
+    env.pop("MASTER_PORT", None)
+    single = subprocess.run([sys.executable, helper], env=env, capture_output=True, text=True, timeout=280)
+    assert single.returncode == 0, single.stderr[-3000:]
+    r0, r1, one = (torch.load(tmp_path / f, weights_only=True) for f in ("r0.pt", "r1.pt", "single.pt"))
+    assert torch.equal(r0["grads"], r1["grads"]) and torch.equal(r0["params"], r1["params"])
+    loss_dp = (r0["loss"] + r1["loss"]) / 2
+    assert abs(float(loss_dp - one["loss"])) <= 1e-3 * abs(float(one["loss"]))
+    d = (r0["grads"] - one["grads"]).abs()
+    assert float(d.max() / one["grads"].abs().max()) <= 2e-2
+    assert float(d.mean() / one["grads"].abs().mean()) <= 1e-2
+    assert json.loads(r0["launched"]) == [1, 0]

@@ -1,0 +1,124 @@
+"""QLinear API surface beyond the single-adapter fused path (qlora.py:91-167):
+several adapters per layer, dropout with a fixed mask (pkg/tests/test_qlora.py:
+225-268) at M > 1 and on the batch-1 GEMV, and the bf16 operand copies
+following the fp32 masters when AdamOptimizer updates them (no caller-side
+shadows).  Tolerances as tests/test_gpu_linear.py (north star)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+MAX_REL, MEAN_REL = 1e-2, 1e-3
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).float().numpy()
+
+
+def assert_tol(got, ref, what):
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    d = np.abs(got - ref)
+    mx, mn = d.max() / np.abs(ref).max(), d.mean() / np.abs(ref).mean()
+    assert mx <= MAX_REL and mn <= MEAN_REL, f"{what}: max-rel {mx:.3e} mean-rel {mn:.3e}"
+
+
+def _base(oracle, qb, k, n, seed):
+    rng = np.random.default_rng(seed)
+    w = (0.02 * rng.standard_normal((k, n))).astype(np.float32)
+    q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)
+    wd = bf16_round(qb.dequantize(q, torch.float32).cpu().numpy()).astype(np.float64)
+    return rng, q, wd
+
+
+def _adapters(rng, qb, oracle, k, n, specs):
+    ads, oads = [], []
+    for r, alpha, p in specs:
+        l1 = bf16_round(rng.standard_normal((k, r)) / np.sqrt(r))
+        l2 = bf16_round(0.02 * rng.standard_normal((r, n)))
+        ads.append(qb.LoraAdapter(r, alpha, torch.from_numpy(l1).cuda(), torch.from_numpy(l2).cuda(), dropout_p=p))
+        oads.append(oracle.LoraAdapter(r, alpha, l1.astype(np.float64), l2.astype(np.float64)))
+    return ads, oads
+
+
+@pytest.mark.parametrize("m", [300, 1])
+def test_multi_adapter_vs_oracle(m, oracle, qb, cuda):
+    """Three adapters of ranks 16 / 64 / 12 (12 padded to 16 on the GPU) with
+    different scalings: one concatenated augmented segment in the fused GEMM."""
+    k, n = 512, 768
+    rng, q, wd = _base(oracle, qb, k, n, 11)
+    ads, oads = _adapters(rng, qb, oracle, k, n, [(16, 32.0, 0.0), (64, 16.0, 0.0), (12, 6.0, 0.0)])
+    lin = qb.QLinear(q, ads)
+    x = bf16_round(rng.standard_normal((m, k)))
+    dy = bf16_round(rng.standard_normal((m, n)))
+    y, cache = lin.forward(torch.from_numpy(x))
+    dx, grads = lin.backward(torch.from_numpy(dy), cache)
+    torch.cuda.synchronize()
+    yr, c = oracle.qlinear_forward(wd, oads, x.astype(np.float64))
+    dxr, gr = oracle.qlinear_backward(oads, dy.astype(np.float64), c)
+    assert_tol(y.float().cpu().numpy(), bf16_round(yr), "y")
+    assert_tol(dx.float().cpu().numpy(), bf16_round(dxr), "dx")
+    assert set(grads) == set(gr)
+    for key in gr:
+        assert tuple(grads[key].shape) == gr[key].shape
+        assert_tol(grads[key].cpu().numpy(), gr[key], key)
+
+
+@pytest.mark.parametrize("m", [300, 1])
+def test_dropout_fixed_mask_vs_oracle(m, oracle, qb, cuda):
+    """Train-mode dropout with a numpy rng draws the reference's mask
+    (qlora.py:137-143); with that mask held fixed the forward and every
+    gradient match the oracle (test_qlora.py:246-268)."""
+    k, n = 512, 640
+    rng, q, wd = _base(oracle, qb, k, n, 7)
+    ads, oads = _adapters(rng, qb, oracle, k, n, [(16, 32.0, 0.5)])
+    lin = qb.QLinear(q, ads)
+    x = bf16_round(rng.standard_normal((m, k)))
+    dy = bf16_round(rng.standard_normal((m, n)))
+    y, cache = lin.forward(torch.from_numpy(x), train=True, rng=np.random.default_rng(3))
+    mask = cache["masks"][0].cpu().numpy()
+    ref_mask = (np.random.default_rng(3).random((m, k)) >= 0.5).astype(np.float32) / np.float32(0.5)
+    assert np.array_equal(mask, ref_mask)
+    assert set(np.unique(mask)) <= {0.0, 2.0}
+    dx, grads = lin.backward(torch.from_numpy(dy), cache)
+    torch.cuda.synchronize()
+    yr, c = oracle.qlinear_forward(wd, oads, x.astype(np.float64), masks=[mask.astype(np.float64)])
+    dxr, gr = oracle.qlinear_backward(oads, dy.astype(np.float64), c)
+    assert_tol(y.float().cpu().numpy(), bf16_round(yr), "y")
+    assert_tol(dx.float().cpu().numpy(), bf16_round(dxr), "dx")
+    assert_tol(grads["adapter0.l1"].cpu().numpy(), gr["adapter0.l1"], "dl1")
+    assert_tol(grads["adapter0.l2"].cpu().numpy(), gr["adapter0.l2"], "dl2")
+    # eval mode ignores dropout (test_qlora.py:232-238)
+    y_eval, _ = lin.forward(torch.from_numpy(x), train=False)
+    y_plain, _ = qb.QLinear(q, [qb.LoraAdapter(16, 32.0, ads[0].l1, ads[0].l2)]).forward(torch.from_numpy(x))
+    assert torch.equal(y_eval, y_plain)
+    with pytest.raises(ValueError, match="rng"):
+        lin.forward(torch.from_numpy(x), train=True)
+
+
+def test_adam_updates_reach_the_kernels(qb, cuda):
+    """lora_init leaves l2 = 0; AdamOptimizer over lin.trainable() (no
+    shadows) must move the adapter seen by forward and backward: after each
+    step the layer equals a fresh layer built from the current masters."""
+    rng = np.random.default_rng(0)
+    k, n, r = 256, 384, 8
+    q = qb.quantize(0.02 * rng.standard_normal((k, n)), qb.get_codebook("nf4"), 64, double_quant=True)
+    lin = qb.QLinear(q, [qb.lora_init(k, n, r, 16.0, rng)])
+    opt = qb.AdamOptimizer(lin.trainable(), qb.TrainConfig(learning_rate=1e-2), qb.PlainMomentStore())
+    x = torch.from_numpy(rng.standard_normal((64, k)).astype(np.float32))
+    dy = torch.from_numpy(rng.standard_normal((64, n)).astype(np.float32))
+    y0, _ = lin.forward(x)
+    for step in range(3):
+        y, cache = lin.forward(x)
+        _, grads = lin.backward(dy, cache)
+        opt.step(grads)
+        fresh = qb.QLinear(q, [qb.LoraAdapter(r, 16.0, lin.adapters[0].l1.clone(), lin.adapters[0].l2.clone())])
+        y_now, c_now = lin.forward(x)
+        y_fresh, c_fresh = fresh.forward(x)
+        assert torch.equal(y_now, y_fresh), step
+        assert torch.equal(lin.backward(dy, c_now)[1]["adapter0.l1"], fresh.backward(dy, c_fresh)[1]["adapter0.l1"])
+    assert not torch.equal(y_now, y0)
+    assert float(lin.adapters[0].l2.abs().max()) > 0

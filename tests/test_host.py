@@ -102,3 +102,44 @@ def test_adam_constants_follow_nep50():
     assert omb1 == float(np.float32(1.0 - 0.9))
     assert bc2 == float(np.float32(1.0 - 0.999 ** 2))
     assert lr == float(np.float32(0.01))
+
+
+def test_page_table_replays_reference_pager_traces():
+    """paging.PageTable (the GPU pager's replacement policy and counters) vs
+    the reference Pager's counters after every operation of random traces
+    (tests/golden/make_golden_pager.py; pkg/src/qlrt/paging.py:116-187)."""
+    import json
+    from paper_2305_14314_b200.paging import PagerConfig, PageTable, Slab
+    traces = json.loads((ROOT / "tests" / "golden" / "pager_traces.json").read_text())
+    for tr in traces:
+        pb = tr["page_bytes"]
+        t = PageTable(PagerConfig(budget_bytes=tr["budget_bytes"], page_bytes=pb))
+        slabs = [Slab(offset=o, nbytes=n) for o, n in tr["slabs"]]
+        for (op, arg), want in zip(tr["ops"], tr["counters"]):
+            if op == "touch":
+                t.touch(arg)
+            else:
+                pages = list(slabs[arg].pages(pb))
+                for pid in pages:
+                    t.touch(pid)
+                t.mark_dirty(pages)
+            got = [t.faults, t.evictions, t.bytes_read, t.bytes_written, t.peak_resident_bytes, t.resident_bytes]
+            assert got == want, (op, arg, got, want)
+        t.flush()
+        assert t.bytes_written == tr["bytes_written_after_flush"]
+
+
+def test_page_table_lru_order_and_slab_pages():
+    """pkg/tests/test_paging.py:42-47, 63-86 restated on the page table."""
+    from paper_2305_14314_b200.paging import PagerConfig, PageTable, Slab
+    assert list(Slab(offset=0, nbytes=64).pages(64)) == [0]
+    assert list(Slab(offset=64, nbytes=65).pages(64)) == [1, 2]
+    assert list(Slab(offset=128, nbytes=200).pages(64)) == [2, 3, 4, 5]
+    t = PageTable(PagerConfig(budget_bytes=128, page_bytes=64))
+    for pid in (0, 1, 0, 2, 0, 1):
+        t.touch(pid)
+    assert (t.faults, t.evictions) == (4, 2)
+    with pytest.raises(ValueError, match="at least one page"):
+        PagerConfig(budget_bytes=63, page_bytes=64).validate()
+    with pytest.raises(ValueError, match="page_bytes"):
+        PagerConfig(budget_bytes=64, page_bytes=0).validate()

@@ -3,7 +3,10 @@
  * hot path.  Every entry point takes DEVICE pointers, element counts and a
  * cudaStream_t (passed as void*), never allocates (callers own all buffers,
  * including the documented workspaces) and returns a qlrt_status.  Launches
- * are stream-ordered and reentrant; there is no global mutable state.
+ * are stream-ordered and reentrant.  Process-wide state is limited to the
+ * launch-policy table (atomics, qlrt_set_policy) and a mutex-guarded table of
+ * side streams keyed by (device, caller stream), so callers on different
+ * streams never share a side stream or its fork/join events.
  *
  * Each function cites the reference (qlrt 0.1.0, /root/reference/pkg/src/qlrt)
  * interface it replaces.  The Python host mirror binds these with ctypes
@@ -54,7 +57,7 @@ typedef struct {
 
 /* Phase A of quantize(): per-block float32 absmax, nearest codes (ties away
  * from zero, fp64-exact), 2-codes-per-byte packing, padding/zero blocks ->
- * pad_code, first non-finite flat index (INT64_MAX if none).
+ * pad_code, first non-finite flat index (>= n if none: 0x7F7F7F7F7F7F7F7F).
  * x: n elements of x_dtype (F32, BF16 or F64 -- the reference's own dtype).  codes: ceil(nb*blocksize/2) bytes.
  * absmax: nb floats.  first_bad: one int64 on the device. */
 qlrt_status qlrt_quantize4(const void* x, int x_dtype, int64_t n, int blocksize,
@@ -216,6 +219,15 @@ qlrt_status qlrt_swiglu_bwd(const void* g, const void* u, const void* dout, void
  * [seq][d/2] (cos, sin); inverse = 1 rotates back (the backward). */
 qlrt_status qlrt_rope(const void* x, void* y, const void* cos_sin, int64_t rows, int heads, int d,
                       int seq, int inverse, void* stream);
+
+/* Launch-policy switches of the engine (the measured A/B knobs DESIGN.md
+ * lists: QLRT_PAIR, QLRT_STREAMK, QLRT_OVERLAP, QLRT_OVERLAP_BWD, ...).  They
+ * are read from the environment once, on first use; afterwards these calls
+ * are the only way to change them (process-wide, atomic; no getenv on the
+ * launch path).  value = INT32_MIN + 1 restores the built-in default.
+ * Returns QLRT_ERR_ARG for an unknown name. */
+int qlrt_set_policy(const char* name, int value);
+int qlrt_get_policy(const char* name, int* value);
 
 /* Library identification: returns the compiled arch string ("sm_100a"). */
 const char* qlrt_build_info(void);

@@ -71,6 +71,8 @@ _SIGS = {
     "qlrt_swiglu_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
     "qlrt_rope": [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int, c_void_p],
     "qlrt_build_info": [],
+    "qlrt_set_policy": [ctypes.c_char_p, c_int],
+    "qlrt_get_policy": [ctypes.c_char_p, POINTER(c_int)],
 }
 _RESTYPE = {"qlrt_dq_workspace_bytes": c_size_t, "qlrt_linear_workspace_bytes": c_size_t,
             "qlrt_gemv_workspace_bytes": c_size_t,
@@ -79,6 +81,27 @@ _RESTYPE = {"qlrt_dq_workspace_bytes": c_size_t, "qlrt_linear_workspace_bytes": 
 
 EXPORTS = tuple(_SIGS)
 _lib = None
+TORCH_OPS_PATH = os.path.join(os.path.dirname(LIB_PATH), "libqlrt_torch_ops.so")
+_ops_loaded = False
+
+
+def load_torch_ops(path: str = TORCH_OPS_PATH):
+    """Register the torch custom ops (``torch.ops.qlrt_b200.*``, CUDA + Meta
+    implementations over the same C ABI; csrc/torch_ops.cpp).  Raises if the
+    library is missing."""
+    global _ops_loaded
+    if not _ops_loaded:
+        if not os.path.exists(path):
+            raise RuntimeError(f"qlrt_b200 torch-op library not built: {path} (run __graft_entry__.build())")
+        load_library()
+        torch.ops.load_library(path)
+        _ops_loaded = True
+    return torch.ops.qlrt_b200
+
+
+def codebook_blob(cb) -> torch.Tensor:
+    """A codebook as the qlrt_codebook4 struct bytes (CPU uint8) for the torch ops."""
+    return torch.frombuffer(bytearray(bytes(cb.to_c())), dtype=torch.uint8)
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -109,6 +132,21 @@ def stream_ptr(device=None) -> int:
 
 def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
+
+
+POLICY_DEFAULT = -0x7FFFFFFF
+
+
+def set_policy(name: str, value: int | None) -> None:
+    """Set an engine launch policy (e.g. "QLRT_STREAMK"); None restores the default."""
+    check(load_library().qlrt_set_policy(name.encode(), POLICY_DEFAULT if value is None else int(value)),
+          f"set_policy({name})")
+
+
+def get_policy(name: str) -> int:
+    v = c_int()
+    check(load_library().qlrt_get_policy(name.encode(), ctypes.byref(v)), f"get_policy({name})")
+    return v.value
 
 
 def check(status: int, what: str) -> None:

@@ -64,7 +64,7 @@ def save(q: BlockQuantized, path: str) -> int:
                                   d.spec.exp_bits, d.spec.mant_bits, d.spec.bias, 0))
         parts.append(_host(d.c1, "<f4"))
         parts.append(_host(d.codes, "u1"))
-    payload = nb * q.blocksize * cb.bits // 8 if cb.bits * q.blocksize % 8 == 0 else -(-nb * q.blocksize * cb.bits // 8)
+    payload = _code_bytes(nb * q.blocksize, cb.bits)
     codes = _host(q.codes, "u1")
     if len(codes) != payload:
         raise ValueError(f"packed code buffer is {len(codes)} bytes, the container needs {payload}")
@@ -74,6 +74,12 @@ def save(q: BlockQuantized, path: str) -> int:
     with open(path, "wb") as fh:
         fh.write(data)
     return len(data)
+
+
+def _code_bytes(padded: int, k: int) -> int:
+    """Packed code bytes of a container (container.py:180-181): two codes per
+    byte for k = 4, one byte per code for every other k."""
+    return (padded + 1) // 2 if k == 4 else padded
 
 
 class _Cursor:
@@ -121,7 +127,7 @@ def _read(data: bytes, payload: bool, device) -> dict:
         consts = (mu, b2, Fp8Spec(eb, mb, bias), c1, codes2)
     else:
         consts = cur.take(4 * nb, "constants")
-    codes = cur.take(-(-nb * blocksize * k // 8), "codes")
+    codes = cur.take(_code_bytes(nb * blocksize, k), "codes")
     (crc,) = struct.unpack("<I", cur.take(4, "crc32"))
     if cur.off != len(data):
         raise TruncatedFileError(f"{len(data) - cur.off} trailing bytes after the checksum")

@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "qlrt_common.cuh"
+#include <mutex>
 #include "sm100_ptx.cuh"
 
 namespace qlrt {
@@ -1174,89 +1175,94 @@ struct Operand {
 // pair cap for the fused grid (leaving >= need SMs), 0 when the cap would cost
 // a round of 256 x 512 tiles -- then the old serial order is used.
 static int overlap_cap(int64_t w_rows, int64_t m, int need_sms);
-static int overlap_need_sms() {  // SMs left to the adapter product (QLRT_OVERLAP_SMS; 8: +1-2% over 4)
-  const char* e = getenv("QLRT_OVERLAP_SMS");
-  return e ? atoi(e) : 8;
-}
+static int overlap_need_sms() { return policy(P_OVERLAP_SMS); }  // SMs left to the adapter product (8: +1-2% over 4)
 
 static int pair_policy(int dflt) {
-  const char* e = getenv("QLRT_PAIR");  // read per call: A/B runs toggle it in-process
-  const int v = e ? atoi(e) : -1;
+  const int v = policy(P_PAIR);
   return v < 0 ? dflt : v;
 }
 
-// A per-device side stream (+ fork / join events) for independent skinny
-// adapter GEMMs; QLRT_SIDE=0 keeps everything on the caller's stream.
-static cudaStream_t side_stream() {
-  const char* e = getenv("QLRT_SIDE");
-  if (e && !atoi(e)) return nullptr;
-  static cudaStream_t st[64] = {};
+// A side stream (+ fork / join events) per (device, caller stream) for the
+// independent skinny adapter GEMMs; QLRT_SIDE=0 keeps everything on the
+// caller's stream.  Callers on different streams never share a side stream or
+// its events; one caller's launches are ordered by its own stream.
+struct SideCtx {
+  int dev;
+  cudaStream_t caller, side;
+  cudaEvent_t ev[2];
+};
+static std::mutex g_side_mu;
+static SideCtx g_side[256];
+static int g_side_n = 0;
+static SideCtx* side_ctx(cudaStream_t caller) {
+  if (!policy(P_SIDE)) return nullptr;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (!st[dev] && cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking) != cudaSuccess) st[dev] = nullptr;
-  return st[dev];
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  for (int i = 0; i < g_side_n; ++i)
+    if (g_side[i].dev == dev && g_side[i].caller == caller) return &g_side[i];
+  if (g_side_n == 256) return nullptr;  // table full: the caller's stream only
+  SideCtx c{dev, caller, nullptr, {nullptr, nullptr}};
+  if (cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  if (cudaEventCreateWithFlags(&c.ev[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c.ev[1], cudaEventDisableTiming) != cudaSuccess)
+    return nullptr;
+  g_side[g_side_n] = c;
+  return &g_side[g_side_n++];
 }
-static cudaEvent_t side_event(int i) {
-  static cudaEvent_t ev[64][2] = {};
+// fork: the side stream waits for everything issued on `st` so far
+static cudaStream_t fork_side(SideCtx* c, cudaStream_t st) {
+  if (!c || cudaEventRecord(c->ev[0], st) != cudaSuccess || cudaStreamWaitEvent(c->side, c->ev[0], 0) != cudaSuccess)
+    return nullptr;
+  return c->side;
+}
+// join: `st` waits for everything issued on the side stream so far
+static bool join_side(SideCtx* c, cudaStream_t st) {
+  return cudaEventRecord(c->ev[1], c->side) == cudaSuccess && cudaStreamWaitEvent(st, c->ev[1], 0) == cudaSuccess;
+}
+
+// kernel attributes (dynamic shared memory) are per device: set once per device
+static bool attr_once(std::atomic<unsigned long long>& mask, const void* kern, int bytes) {
   int dev = 0;
-  cudaGetDevice(&dev);
-  if (!ev[dev][i]) cudaEventCreateWithFlags(&ev[dev][i], cudaEventDisableTiming);
-  return ev[dev][i];
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  const unsigned long long bit = 1ull << dev;
+  if (mask.load(std::memory_order_acquire) & bit) return true;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  mask.fetch_or(bit, std::memory_order_acq_rel);
+  return true;
 }
 
 // 256 x 512 pair tiles for the fused NF4 GEMMs (QLRT_TILE512=0 falls back to
 // 128 x 256 single-CTA tiles): the 2-CTA pair halves the B traffic per SM and
 // the two N = 256 UMMAs per k-step halve the dequant work per MMA -- measured
 // +16..41% on the C2 / C4 shapes (tools/ab.py QLRT_TILE512=0/1)
-static int tile512_policy() {
-  const char* e = getenv("QLRT_TILE512");
-  return e ? atoi(e) : 1;
-}
+static int tile512_policy() { return policy(P_TILE512); }
 
 // per-half accumulator release for 512-wide tiles (QLRT_STAGGER=1).  Off by
 // default: correct, but measured neutral-to-slower (tools/ab.py QLRT_STAGGER)
-static int stagger_policy() {
-  const char* e = getenv("QLRT_STAGGER");
-  return e ? atoi(e) : 0;
-}
+static int stagger_policy() { return policy(P_STAGGER); }
 
 // epilogue output via TMA stores (QLRT_TMAOUT=0: ld.shared + 16 B st.global)
-static int tma_out_policy() {
-  const char* e = getenv("QLRT_TMAOUT");
-  return e ? atoi(e) : 1;
-}
+static int tma_out_policy() { return policy(P_TMAOUT); }
 
 // half tiles for the last partial wave of 512-wide pair tiles (QLRT_HALFTAIL=0 disables)
-static int halftail_policy() {
-  const char* e = getenv("QLRT_HALFTAIL");
-  return e ? atoi(e) : 1;
-}
+static int halftail_policy() { return policy(P_HALFTAIL); }
 
 // programmatic dependent launch of the engine kernels (QLRT_PDL=0 disables it)
-static int pdl_policy() {
-  const char* e = getenv("QLRT_PDL");
-  return e ? atoi(e) : 1;
-}
+static int pdl_policy() { return policy(P_PDL); }
 
 // shared-decode CTA pairs for the fused NF4 GEMMs (QLRT_SHARE=1).  Off by
 // default: correct, but the cross-SM coupling (both MMAs release a stage,
 // both producer halves fill it, DSMEM stores + remote arrives) costs more
 // than the halved decode saves -- measured 0.66x (tools/ab.py QLRT_SHARE=0/1)
-static int share_policy() {
-  const char* e = getenv("QLRT_SHARE");
-  return e ? atoi(e) : 0;
-}
+static int share_policy() { return policy(P_SHARE); }
 
 // stream-K policy: QLRT_STREAMK=0 disables it (whole-tile waves only)
-static int streamk_policy() {
-  const char* e = getenv("QLRT_STREAMK");  // read per call: A/B runs toggle it in-process
-  return e ? atoi(e) : 1;
-}
+static int streamk_policy() { return policy(P_STREAMK); }
 
 static int num_sms();
 static int overlap_cap(int64_t w_rows, int64_t m, int need_sms) {
-  const char* e = getenv("QLRT_OVERLAP");
-  if (e && !atoi(e)) return 0;
+  if (!policy(P_OVERLAP)) return 0;
   const int64_t tiles = ((w_rows + 255) / 256) * ((m + 511) / 512);
   auto rounds = [&](int64_t units) {
     const int64_t full = tiles / units, rem = tiles - full * units;
@@ -1286,12 +1292,8 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
                             cudaStream_t s) {
   using L = Smem<BN, NF4, PAIR>;
   auto kern = gemm_kernel<BN, NF4, PAIR>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES) != cudaSuccess)
-      return QLRT_ERR_CUDA;
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr_mask{0};
+  if (!attr_once(attr_mask, (const void*)kern, L::BYTES)) return QLRT_ERR_CUDA;
   const int bmp = PAIR ? 2 * BM : BM;
   const int m_tiles = (args.M + bmp - 1) / bmp, n_tiles = (args.N + BN - 1) / BN;
   const int tiles = m_tiles * n_tiles * args.splits;
@@ -1434,10 +1436,7 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
       make_tmap_store(&to, args.out, args.M, args.N, args.ldo))
     args.tma_out = 1;
   if (!args.tma_out) to = tb;
-  {
-    const char* e = getenv("QLRT_PDL_TRIGGER");
-    args.pdl_trigger = (e ? atoi(e) : 1) && pdl_policy() && (!args.aug_pdl || args.trigger_dep);
-  }
+  args.pdl_trigger = policy(P_PDL_TRIGGER) && pdl_policy() && (!args.aug_pdl || args.trigger_dep);
   switch (bn) {
     case 512:
       return nf4 ? launch_t<512, true, true>(ta, tb, ta2, tb2, tc, tk, to, args, s)
@@ -1511,8 +1510,7 @@ static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, 
   const int64_t kit = (K + BK - 1) / BK;
   // (off by default: measured slower than split-K + reduce on the C2 LoRA shapes,
   //  tools/ab_skinny.py; QLRT_STREAMK_SKINNY=1 enables it)
-  const char* e_sk = getenv("QLRT_STREAMK_SKINNY");
-  if (e_sk && atoi(e_sk) && sk && sk->sk_ws && streamk_policy() && !(out_split && out_t) &&
+  if (policy(P_STREAMK_SKINNY) && sk && sk->sk_ws && streamk_policy() && !(out_split && out_t) &&
       (!fold || (2 * fold <= bn && N <= bn))) {
     // skinny GEMM: stream-K over all SMs, partials reduced in-kernel, fold /
     // hi-lo split applied in the epilogue -- no split-K workspace, no reduce launch
@@ -1526,8 +1524,7 @@ static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, 
   // kernel.  Off by default (QLRT_CSPLIT=1 enables it): measured 1.7-2.9x
   // slower than split-K + the reduce kernel on the C2 LoRA shapes
   // (tools/ab_skinny.py) -- clusters of 1-CTA-per-SM kernels co-schedule poorly
-  const char* e_cs = getenv("QLRT_CSPLIT");
-  if (e_cs && atoi(e_cs) && tiles < 74 && !(out_split && out_t) && bn <= 256 && a.pair == 0 &&
+  if (policy(P_CSPLIT) && tiles < 74 && !(out_split && out_t) && bn <= 256 && a.pair == 0 &&
       (!fold || (2 * fold <= bn && N <= bn))) {
     int S = 1;
     while (S < 8 && tiles * (S + 1) <= num_sms() && (S + 1) * 4 <= kit) ++S;
@@ -1624,6 +1621,27 @@ int qlrt_trace_fetch(unsigned long long* host) {
 }
 #endif
 
+int qlrt_set_policy(const char* name, int value) {
+  if (!name) return QLRT_ERR_ARG;
+  if (!g_policy_init.load(std::memory_order_acquire)) policy_load_env();
+  for (int i = 0; i < P_COUNT; ++i)
+    if (!strcmp(name, kPolicies[i].env)) {
+      g_policy[i].store(value == kPolicyUnset ? kPolicies[i].dflt : value, std::memory_order_relaxed);
+      return QLRT_OK;
+    }
+  return QLRT_ERR_ARG;
+}
+
+int qlrt_get_policy(const char* name, int* value) {
+  if (!name || !value) return QLRT_ERR_ARG;
+  for (int i = 0; i < P_COUNT; ++i)
+    if (!strcmp(name, kPolicies[i].env)) {
+      *value = policy((Policy)i);
+      return QLRT_OK;
+    }
+  return QLRT_ERR_ARG;
+}
+
 size_t qlrt_nf4_constants_bytes(int64_t k_in, int64_t n_out) { return gemm::consts_bytes(k_in, n_out); }
 
 qlrt_status qlrt_nf4_constants(const qlrt_nf4_weight* w, float* out, void* stream) {
@@ -1715,10 +1733,8 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   // the block-constant prepass (when no cache is given) and the doubled l2
   // copies run on the side stream while Ts is computed here
   gemm::Args a{};
-  cudaStream_t side = rank > 0 ? gemm::side_stream() : nullptr;
-  if (side && (cudaEventRecord(gemm::side_event(0), st) != cudaSuccess ||
-               cudaStreamWaitEvent(side, gemm::side_event(0), 0) != cudaSuccess))
-    side = nullptr;
+  gemm::SideCtx* sctx = rank > 0 ? gemm::side_ctx(st) : nullptr;
+  cudaStream_t side = gemm::fork_side(sctx, st);
   cudaStream_t aux = side ? side : st;
   if ((rc = gemm::fill_nf4(a, w, 1, consts, aux)) != QLRT_OK) return rc;
   __nv_bfloat16* l2d = (__nv_bfloat16*)gemm::dbl_region(workspace, ws_bytes, K, N, rank);
@@ -1737,9 +1753,7 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
                      &sk);
     if (rc != QLRT_OK) return rc;
   }
-  if (side && (cudaEventRecord(gemm::side_event(1), side) != cudaSuccess ||
-               cudaStreamWaitEvent(st, gemm::side_event(1), 0) != cudaSuccess))
-    return QLRT_ERR_CUDA;
+  if (side && !gemm::join_side(sctx, st)) return QLRT_ERR_CUDA;
   // Y^T[N, m] = W^T X^T (+ l2^T Ts^T): A = NF4 (MN-major image), B = X (K-major)
   a.M = (int)N;
   a.N = (int)m;
@@ -1782,8 +1796,7 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   // 16 dT CTAs land one per SM and hold back fused pairs that need whole SMs;
   // the backward's 64-tile grids already leave their idle SMs to dl2 / dl1.
   // (dl2 beside the grid as well: 2-9% slower.)
-  const char* e_ob = getenv("QLRT_OVERLAP_BWD");
-  const int cap = (e_ob && atoi(e_ob) && rank > 0 && !dt_given && rank % 64 == 0 && gemm::tile512_policy() &&
+  const int cap = (policy(P_OVERLAP_BWD) && rank > 0 && !dt_given && rank % 64 == 0 && gemm::tile512_policy() &&
                    gemm::pdl_policy())
                       ? gemm::overlap_cap(K, m, gemm::overlap_need_sms()) : 0;
   if (cap) {
@@ -1805,10 +1818,8 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
     a.units_cap = cap;
     Operand none{}, B{dy, N, 0}, A2{l1, rank, 0}, B2{dt_out, 2 * rank, 0};
     if ((rc = gemm::run(512, none, B, &A2, &B2, N, 2 * rank, a, st)) != QLRT_OK) return rc;
-    cudaStream_t side = gemm::side_stream();
-    if (side && (cudaEventRecord(gemm::side_event(0), st) != cudaSuccess ||
-                 cudaStreamWaitEvent(side, gemm::side_event(0), 0) != cudaSuccess))
-      side = nullptr;
+    gemm::SideCtx* sctx = gemm::side_ctx(st);
+    cudaStream_t side = gemm::fork_side(sctx, st);
     {
       Operand A{dy, N, 1}, B2t{ts, 2 * rank, 1};
       rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B2t, N, 2 * rank, m, 1.0f, dl2, N, 1,
@@ -1821,9 +1832,7 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
                        1, 0, (float*)workspace, part_bytes, st, rank, 0, &sk);
       if (rc != QLRT_OK) return rc;
     }
-    if (side && (cudaEventRecord(gemm::side_event(1), side) != cudaSuccess ||
-                 cudaStreamWaitEvent(st, gemm::side_event(1), 0) != cudaSuccess))
-      return QLRT_ERR_CUDA;
+    if (side && !gemm::join_side(sctx, st)) return QLRT_ERR_CUDA;
     return QLRT_OK;
   }
   if (rank > 0 && !dt_given) {
@@ -1837,11 +1846,8 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   // the adapter gradients dl2 and dl1 need only the inputs and dT: they run on
   // a side stream forked here and are launched after the fused dX GEMM, so
   // they fill the SMs its grid leaves idle (or follow it as its CTAs retire)
-  cudaStream_t side = nullptr;
-  if (rank > 0 && (side = gemm::side_stream()) &&
-      (cudaEventRecord(gemm::side_event(0), st) != cudaSuccess ||
-       cudaStreamWaitEvent(side, gemm::side_event(0), 0) != cudaSuccess))
-    side = nullptr;
+  gemm::SideCtx* sctx = rank > 0 ? gemm::side_ctx(st) : nullptr;
+  cudaStream_t side = gemm::fork_side(sctx, st);
   // dX^T[K, m] = W dY^T (+ l1 dT^T): A = NF4 (K-major image), B = dY (K-major)
   gemm::Args a{};
   a.M = (int)K;
@@ -1884,13 +1890,13 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   {
     // dl1[K, r] = Xa^T (dT_hi + dT_lo): A = Xa (MN-major [m][K]), B = [dT_hi | dT_lo] (MN-major [m][2r])
     Operand A{x, K, 1}, B{dt_out, 2 * rank, 1};
+    // (on the side stream it runs beside the fused dX grid, which owns the
+    // stream-K region: no stream-K for it there)
     rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, K, 2 * rank, m, 1.0f, dl1, rank, 1, 0,
-                     (float*)workspace, part_bytes, aux, rank, 0, &sk);
+                     (float*)workspace, part_bytes, aux, rank, 0, side ? nullptr : &sk);
     if (rc != QLRT_OK) return rc;
   }
-  if (side && (cudaEventRecord(gemm::side_event(1), side) != cudaSuccess ||
-               cudaStreamWaitEvent(st, gemm::side_event(1), 0) != cudaSuccess))
-    return QLRT_ERR_CUDA;
+  if (side && !gemm::join_side(sctx, st)) return QLRT_ERR_CUDA;
   return rc;
 }
 

@@ -327,8 +327,7 @@ qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* x
   for (int i = 0; i < 16; ++i) v.v[i] = (float)w->values[i];
   const int smem = gemv::WARPS * 32 * 16 * (int)sizeof(float4);  // 64 KB
   const int sh = __builtin_ctz((unsigned)w->blocksize2);
-  const char* env = getenv("QLRT_GEMV_WL");
-  const int wl = env ? atoi(env) : 6;
+  const int wl = policy(P_GEMV_WL) < 0 ? 6 : policy(P_GEMV_WL);
 #define QLRT_GEMV(WLV)                                                                                            \
   do {                                                                                                            \
     static bool attr = false;                                                                                     \

@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <atomic>
 #include "qlrt_b200.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -18,6 +21,42 @@
 namespace qlrt {
 
 constexpr int kNumSMs = 148;
+
+// ---- launch policies ------------------------------------------------------
+// Scheduling switches of the engine (measured A/B knobs).  Read
+// from the environment ONCE (first use), afterwards only through
+// qlrt_set_policy(): no getenv on the launch path.  One process-wide table of
+// atomics shared by every translation unit of the library.
+enum Policy {
+  P_PAIR, P_SIDE, P_TILE512, P_STAGGER, P_TMAOUT, P_HALFTAIL, P_PDL, P_SHARE, P_STREAMK, P_OVERLAP,
+  P_OVERLAP_SMS, P_PDL_TRIGGER, P_STREAMK_SKINNY, P_CSPLIT, P_OVERLAP_BWD, P_GEMV_WL, P_DQB_CTAS_PER_SM,
+  P_COUNT
+};
+struct PolicyDef {
+  const char* env;
+  int dflt;
+};
+inline const PolicyDef kPolicies[P_COUNT] = {
+    {"QLRT_PAIR", -1},         {"QLRT_SIDE", 1},           {"QLRT_TILE512", 1},   {"QLRT_STAGGER", 0},
+    {"QLRT_TMAOUT", 1},        {"QLRT_HALFTAIL", 1},       {"QLRT_PDL", 1},       {"QLRT_SHARE", 0},
+    {"QLRT_STREAMK", 1},       {"QLRT_OVERLAP", 1},        {"QLRT_OVERLAP_SMS", 8}, {"QLRT_PDL_TRIGGER", 1},
+    {"QLRT_STREAMK_SKINNY", 0}, {"QLRT_CSPLIT", 0},        {"QLRT_OVERLAP_BWD", 0}, {"QLRT_GEMV_WL", -1},
+    {"QLRT_DQB_CTAS_PER_SM", -1}};
+constexpr int kPolicyUnset = -0x7fffffff;
+inline std::atomic<int> g_policy[P_COUNT];
+inline std::atomic<bool> g_policy_init{false};
+
+inline void policy_load_env() {
+  for (int i = 0; i < P_COUNT; ++i) {
+    const char* e = getenv(kPolicies[i].env);
+    g_policy[i].store(e ? atoi(e) : kPolicies[i].dflt, std::memory_order_relaxed);
+  }
+  g_policy_init.store(true, std::memory_order_release);
+}
+inline int policy(Policy p) {
+  if (!g_policy_init.load(std::memory_order_acquire)) policy_load_env();
+  return g_policy[p].load(std::memory_order_relaxed);
+}
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -1010,10 +1010,10 @@ qlrt_status qlrt_dequantize4(const uint8_t* codes, int64_t n, int blocksize,
     // overlap one another's tails and balance dynamically (+13% at the 65B
     // shapes: 6.1 vs 5.4 TB/s); short ones (< 4 steps per warp) stay at one
     // resident wave.  QLRT_DQB_CTAS_PER_SM overrides.
-    const char* e_g = getenv("QLRT_DQB_CTAS_PER_SM");
+    const int e_g = policy(P_DQB_CTAS_PER_SM);
     const int64_t steps = cdiv(cdiv(n, 64), 32);
     const int64_t per_sm =
-        e_g ? atoi(e_g) : (steps > 4 * (int64_t)kNumSMs * QLRT_DQB_MINB * (DQB_TPB / 32) ? 16 : QLRT_DQB_MINB);
+        e_g > 0 ? e_g : (steps > 4 * (int64_t)kNumSMs * QLRT_DQB_MINB * (DQB_TPB / 32) ? 16 : QLRT_DQB_MINB);
     const int g = (int)(ctas < (int64_t)kNumSMs * per_sm ? ctas : (int64_t)kNumSMs * per_sm);
     const int sh = pow2_bs2 ? __builtin_ctz((unsigned)blocksize2) : 0;
     if (dq_codes)

@@ -22,6 +22,10 @@ CASES = {  # name: (seed, shape, codebook, blocksize, dq)
     "fp4_dq": (4, (32, 96), "fp4-e2m1", 64, True),
     "nfeq4_b16": (5, (7, 9), "nf-eq4", 16, False),
     "scalar": (6, (), "nf4", 64, False),
+    # k != 4: one byte per code (container.py:180-181)
+    "nf3_plain": (7, (5, 40), "nf3", 64, False),
+    "int8_dq": (8, (300,), "int8", 64, True),
+    "int2_b32": (9, (3, 33), "int2", 32, False),
 }
 arrays = {}
 for name, (seed, shape, cb, bs, dq) in CASES.items():

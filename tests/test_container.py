@@ -17,6 +17,8 @@ HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "conta
 CASES = {"golden_nf4_dq": ("nf4", 64, True), "nf4_plain_64x64": ("nf4", 64, False),
          "nf4_dq_ragged": ("nf4", 64, True), "int4_plain": ("int4", 64, False), "fp4_dq": ("fp4-e2m1", 64, True),
          "nfeq4_b16": ("nf-eq4", 16, False), "scalar": ("nf4", 64, False)}
+# k != 4: one byte per code in the file (reference container.py:180-181)
+K_CASES = {"nf3_plain": ("nf3", 64, False), "int8_dq": ("int8", 64, True), "int2_b32": ("int2", 32, False)}
 
 
 def _bytes(name):
@@ -27,7 +29,7 @@ def _bytes(name):
 # ---------------------------------------------------------------- host only
 def test_inspect_reference_files():
     from paper_2305_14314_b200 import container
-    for name, (cb, bs, dq) in CASES.items():
+    for name, (cb, bs, dq) in {**CASES, **K_CASES}.items():
         info = container.inspect_header(os.path.join(HERE, name + ".qlrt"))
         assert info["codebook"] == cb and info["blocksize"] == bs and info["double_quant"] is dq
         assert info["crc_ok"] is True and info["file_bytes"] == len(_bytes(name))
@@ -78,6 +80,11 @@ def test_reference_files_load_and_resave_byte_identical(tmp_path, qb, cuda):
         out = tmp_path / (name + ".qlrt")
         n = container.save(q, str(out))
         assert out.read_bytes() == _bytes(name) and n == len(_bytes(name)), name
+    for name, (cb, bs, dq) in K_CASES.items():  # byte round trip (the kernels quantize 4-bit only)
+        q = container.load(os.path.join(HERE, name + ".qlrt"))
+        assert q.codebook.bits == int(cb[-1]) and q.codes.numel() == q.n_blocks * bs
+        out = tmp_path / (name + ".qlrt")
+        assert container.save(q, str(out)) == len(_bytes(name)) and out.read_bytes() == _bytes(name), name
 
 
 @pytest.mark.gpu

@@ -231,7 +231,6 @@ def test_overlap_modes_match_default(env, qb, cuda):
     QLRT_OVERLAP_BWD) and the serial order agree within the GEMM tolerance
     (split-K vs one-CTA summation order of T / dT), and each is run-to-run
     deterministic."""
-    import os
     m, k, n, r = 1024, 4096, 4096, 64
     g = torch.Generator(device="cuda").manual_seed(3)
     q = qb.quantize(torch.randn(k, n, device="cuda", generator=g) * 0.02, qb.get_codebook("nf4"), 64,
@@ -247,18 +246,17 @@ def test_overlap_modes_match_default(env, qb, cuda):
         dx, gr = lin.backward(dy, c)
         return [y.clone(), dx.clone(), gr["adapter0.l1"].clone(), gr["adapter0.l2"].clone()]
 
+    from paper_2305_14314_b200._native import get_policy, set_policy
     base = run()
-    old = {kk: os.environ.get(kk) for kk in env}
-    os.environ.update(env)
+    old = {kk: get_policy(kk) for kk in env}
+    for kk, vv in env.items():
+        set_policy(kk, int(vv))
     try:
         alt = run()
         alt2 = run()
     finally:
         for kk, vv in old.items():
-            if vv is None:
-                os.environ.pop(kk, None)
-            else:
-                os.environ[kk] = vv
+            set_policy(kk, vv)
     for a, b, c in zip(base, alt, alt2):
         assert torch.equal(b, c)
         d = (a.float() - b.float()).abs()

@@ -35,12 +35,14 @@ ALL_KEYS = {kv.split("=")[0] for v in a.variants for kv in v.split(",")}
 
 
 def setenv(v):
-    """Exactly this variant's settings: keys set by other variants are cleared."""
+    """Exactly this variant's policies (qlrt_set_policy): keys set by other
+    variants go back to their defaults."""
+    from paper_2305_14314_b200._native import set_policy
     for kk in ALL_KEYS:
-        os.environ.pop(kk, None)
+        set_policy(kk, None)
     for kv in v.split(","):
         kk, vv = kv.split("=")
-        os.environ[kk] = vv
+        set_policy(kk, int(vv))
 
 
 for _ in range(a.rounds):

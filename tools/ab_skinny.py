@@ -26,7 +26,8 @@ for name, fn in cases.items():
     row = []
     for v in variants:
         kk, vv = v.split("=")
-        os.environ[kk] = vv
+        from paper_2305_14314_b200._native import set_policy
+        set_policy(kk, int(vv))
         out = fn().clone()
         if ref is None:
             ref = out

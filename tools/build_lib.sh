@@ -18,3 +18,12 @@ for p in "${pids[@]}"; do wait "$p"; done  # a failed compile fails the build
 "$NVCC" -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT/${QLRT_LIB_NAME:-libqlrt_b200.so}" "${objs[@]}" -lcudart
 rm -f "${objs[@]}"
 echo "built $OUT/${QLRT_LIB_NAME:-libqlrt_b200.so}"
+# torch custom-op layer (torch.ops.qlrt_b200.*) over the C ABI
+TORCH_DIR=$(python -c "import os, torch; print(os.path.dirname(torch.__file__))" 2>/dev/null)
+ABI=$(python -c "import torch; print(int(torch._C._GLIBCXX_USE_CXX11_ABI))" 2>/dev/null)
+g++ -O2 -std=c++17 -fPIC -shared -D_GLIBCXX_USE_CXX11_ABI=$ABI -DTORCH_API_INCLUDE_EXTENSION_H \
+  -I"$ROOT/include" -I"$TORCH_DIR/include" -I"$TORCH_DIR/include/torch/csrc/api/include" -I/usr/local/cuda/include \
+  "$SRC/torch_ops.cpp" -o "$OUT/libqlrt_torch_ops.so" \
+  -L"$OUT" -lqlrt_b200 -L"$TORCH_DIR/lib" -ltorch -ltorch_cpu -ltorch_cuda -lc10 -lc10_cuda \
+  -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$ORIGIN' -Wl,-rpath,"$TORCH_DIR/lib"
+echo "built $OUT/libqlrt_torch_ops.so"

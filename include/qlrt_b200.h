@@ -154,7 +154,9 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
 /* batch-1 GEMV variant of forward (M = 1), HBM-bound on the packed codes:
  *   y[N] = x[K] W + s (xa l1) l2         fp32 accumulate, bf16 out
  * (xa = the dropout-masked adapter input, NULL -> x; qlora.py:137-146).
- * W decodes as bf16(f32(v) * c) (as the fused GEMM); split-K partials are
+ * N % 256 == 0, K % 16 == 0 (the LLaMA shapes): tensor-core GEMV, W enters
+ * as fp16(v) * c (the reference's float32 W to ~2^-12); other shapes: W
+ * decodes as bf16(f32(v) * c) (as the fused GEMM).  Split-K partials are
  * summed in a fixed order (deterministic).  Needs N % 64 == 0, a
  * power-of-two blocksize2, 32-byte aligned codes; rank <= 512. */
 qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* xa,

@@ -20,7 +20,7 @@ Every computation runs in the CUDA library ``_lib/libqlrt_b200.so``
 fallback: calls raise RuntimeError without the library or a GPU.
 """
 
-from ._native import EXPORTS, LIB_PATH, load_library
+from ._native import EXPORTS, LIB_PATH, get_policy, load_library, set_policy
 from . import container
 from .analysis import QuantConfig, QuantErrorRow, quant_error_report
 from .blockquant import BlockQuantized, dequantize, pack_codes, quantize, unpack_codes

@@ -20,7 +20,12 @@
 // term and writes bf16 y.
 #include <stdlib.h>
 
+#include <type_traits>
+
+#include <cuda_fp16.h>
+
 #include "qlrt_common.cuh"
+#include "sm100_ptx.cuh"
 
 namespace qlrt {
 namespace gemv {
@@ -292,6 +297,521 @@ __global__ void __launch_bounds__(TPB) lora_t_kernel(const __nv_bfloat16* __rest
 }
 
 }  // namespace gemv
+
+// ---------------------------------------------------------------------------
+// Tensor-core GEMV (default): the decode is the bound of the kernel above
+// (~5 SASS per weight for a bf16(v c) table rebuilt per block + byte-permute
+// lookups + one FHFMA per weight).  Here the per-block constant moves to the
+// other operand and the lookup becomes one PRMT + one LDS per TWO weights:
+//
+//   y_j = sum_k x_k W[k][j] = sum_k (x_k c_{k,b(j)}) v(code[k][j])
+//
+// * A operand (mma.sync m16n8k16, f16 in, f32 accumulate) = the codebook
+//   values v of 16 columns x 16 rows, read from a fixed 256-entry table of
+//   fp16 pairs {v(lo nibble), v(hi nibble)} indexed by a byte that holds the
+//   codes of rows k and k+1 of one column (the fragment pairs along K).  The
+//   table has a private column per lane (entry e at e*256 + lane*4: bank =
+//   lane, no conflicts) at a 64 KB-aligned shared address, so the byte ->
+//   address step is a single PRMT that drops the index byte into bits 8-15 of
+//   the lane's column address.
+// * B operand = a_k = x_k c_{k,b} * 2^-E as an fp16 hi/lo pair (B columns
+//   2b / 2b+1 for the warp's two 64-column blocks b); the D rows of an m-tile
+//   whose block matches the B column pair hold the result (the rest of the
+//   16x8 tile is free compute).  c is the exact dq_decompress constant
+//   (fp64, doublequant.py:190-195); E is one power of two per CTA (max|x|
+//   over the CTA's rows times the largest constant its second-level blocks
+//   allow) so that |a 2^-E| < 2^15 fits fp16; partials are scaled back
+//   exactly.
+// Precision: W enters as fp16(v) * c (v rounded to 11 bits, a to ~22 bits),
+// i.e. closer to the reference's float32 W = f32(dequantize(q)) than the
+// bf16 W of the tensor-core GEMM (GEMV tolerance).
+//
+// Data movement: a stage = 16 rows x 2048 columns (1 KB of codes per row)
+// arrives as ONE 3-d TMA box [8 column groups][16 rows][128 B] (128B
+// swizzle: conflict-free 8-byte reads; 2 KB boxes were TMA-issue bound at
+// ~12 GB/s per SM), the stage's DQ bytes, x and c1 ride along as cp.async
+// on the same mbarrier; warp 0 keeps NST = 8 stages in flight.  Units =
+// (strip of 2048 columns, 16-row stage), split evenly over one CTA per SM in
+// strip-major order (stream-K style: a CTA covers <= 2-3 strip segments).
+// 16 warps: warp w owns columns [128 w, +128) of the strip (box w >> 1, half
+// w & 1) and all 16 rows of each stage; lane (g, t) reads 8 bytes (16
+// columns) of rows 2t, 2t+1, 2t+8, 2t+9.  A CTA flushes a strip segment as
+// an fp32 partial; the last segment of a strip (atomic ticket) sums the
+// partials in CTA order (deterministic), adds the LoRA term and writes bf16
+// y.  The prep kernel (ticket reset, LoRA partials) is the PDL predecessor:
+// the main grid waits for it only at its first flush.
+namespace gemv2 {
+
+constexpr int CWARPS = 16;  // lane 0 of warp 0 also issues the TMA loads
+constexpr int TPB = CWARPS * 32;
+constexpr int CTHREADS = CWARPS * 32;
+constexpr int STRIP = 2048;  // columns per strip = 8 TMA boxes of 128 B
+constexpr int ROWS = 16;     // rows per stage (= unit)
+constexpr int NST = 8;  // stages in flight (16 KB each) = a_k input prefetch depth (static ring slots)
+constexpr int STAGE = ROWS * STRIP / 2;  // 16 KB
+// shared layout: the CTA's dynamic window starts a few KB into the 228 KB;
+// the table sits at the 64 KB boundary, NFRONT stages + the scratch fill the
+// gap in front of it, the other stages follow it
+constexpr int NFRONT = NST < 3 ? NST : 3;
+constexpr int SMEM = 65536 + 65536 + (NST - NFRONT) * STAGE;
+
+struct Geo {
+  int64_t K, N, nbr, chunks, strips, units;
+  int grid;
+};
+
+static Geo geo(int64_t K, int64_t N, int sms) {
+  Geo g;
+  g.K = K;
+  g.N = N;
+  g.nbr = N / 64;
+  g.chunks = cdiv(K, ROWS);
+  g.strips = cdiv(N, STRIP);
+  g.units = g.chunks * g.strips;
+  g.grid = (int)(g.units < sms ? g.units : sms);
+  return g;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+// workspace: [partials (grid + strips) x STRIP f32][tpart zt x r f32][counters strips u32]
+static size_t part_off() { return 0; }
+static size_t tpart_off(const Geo& g) { return part_off() + align256((size_t)(g.grid + g.strips) * STRIP * 4); }
+static size_t cnt_off(const Geo& g, int r) {
+  return tpart_off(g) + align256((size_t)cdiv(g.K, 128) * (r > 0 ? r : 1) * 4);
+}
+static size_t ws_bytes(int64_t K, int64_t N, int r) {
+  const Geo g = geo(K, N, kNumSMs);
+  return cnt_off(g, r) + align256((size_t)g.strips * 4);
+}
+
+// first / last CTA covering strip s when CTA i owns units [i U / G, (i+1) U / G)
+__device__ __forceinline__ int first_cta(int64_t s, int64_t C, int64_t U, int64_t G) {
+  return (int)(((s * C + 1) * G + U - 1) / U) - 1;
+}
+__device__ __forceinline__ int last_cta(int64_t s, int64_t C, int64_t U, int64_t G) {
+  return (int)(((s + 1) * C * G + U - 1) / U) - 1;
+}
+
+// prep (one launch, PDL predecessor of the main kernel, which waits for it
+// only at its first strip flush): block 0 zeroes the strip tickets; blocks
+// >= 1 compute the LoRA partials tpart[z][j] = sum_{k in [128 z, 128 z + 128)}
+// xa_k l1[k][j] (8 columns per thread, 16-byte loads, all rows in flight)
+__global__ void __launch_bounds__(256) prep_kernel(int64_t K, const __nv_bfloat16* __restrict__ xa,
+                                                  const __nv_bfloat16* __restrict__ l1, int rank,
+                                                  float* __restrict__ tpart, unsigned* __restrict__ counters,
+                                                  int strips) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  __shared__ float sh[256 * 8];
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0) {
+    for (int i = tid; i < strips; i += 256) counters[i] = 0u;
+    return;
+  }
+  const int z = blockIdx.x - 1;
+  const int cpr = rank / 8;          // 16-byte column groups per row
+  const int rpp = 256 / cpr;         // rows per pass
+  const int cg = tid % cpr, rr = tid / cpr;
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (rr < rpp) {
+    for (int k0 = z * 128 + rr; k0 < z * 128 + 128 && k0 < K; k0 += rpp) {
+      const float xv = __bfloat162float(xa[k0]);
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(l1 + (int64_t)k0 * rank) + cg);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        a[2 * e] = fmaf(xv, __uint_as_float(w[e] << 16), a[2 * e]);
+        a[2 * e + 1] = fmaf(xv, __uint_as_float(w[e] & 0xFFFF0000u), a[2 * e + 1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) sh[tid * 8 + e] = a[e];
+  __syncthreads();
+  for (int j = tid; j < rank; j += 256) {
+    float acc = 0.0f;
+    for (int q = 0; q < rpp; ++q) acc += sh[(q * cpr + j / 8) * 8 + (j & 7)];
+    tpart[(int64_t)z * rank + j] = acc;
+  }
+}
+
+__device__ __forceinline__ uint32_t lds(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void cbar() {  // all 16 warps (named barrier 1)
+  asm volatile("bar.sync 1, %0;" ::"n"(CTHREADS) : "memory");
+}
+// 4- / 16-byte async copies into the stage's aux slot; src_size 0 -> zero fill
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(ptx::smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+struct Vals16 {
+  float v[16];
+};
+
+// last segment of a strip: partials in CTA order + LoRA, bf16 out
+__device__ __noinline__ void finalize_strip(int64_t strip, int f, int l, int64_t N, const float* __restrict__ part,
+                                            const float* __restrict__ tpart, int zt,
+                                            const __nv_bfloat16* __restrict__ l2, int rank, float s,
+                                            __nv_bfloat16* __restrict__ y, float* tsh) {
+  const int tid = threadIdx.x;
+  __threadfence();
+  if (rank > 0) {
+    for (int j = tid; j < rank; j += CTHREADS) {
+      float a = 0.0f;
+      for (int zz = 0; zz < zt; ++zz) a += __ldcg(tpart + (int64_t)zz * rank + j);
+      tsh[j] = s * a;
+    }
+  }
+  cbar();
+  for (int c = tid; c < STRIP; c += CTHREADS) {
+    const int64_t col = strip * STRIP + c;
+    if (col >= N) break;
+    float o = 0.0f;
+    for (int i = f; i <= l; ++i) o += __ldcg(part + (int64_t)(i + strip) * STRIP + c);
+    if (rank > 0) {
+      float la = 0.0f;
+      for (int j = 0; j < rank; ++j) la = fmaf(tsh[j], __bfloat162float(l2[(int64_t)j * N + col]), la);
+      o += la;
+    }
+    y[col] = __float2bfloat16_rn(o);
+  }
+  cbar();
+}
+
+// per-stage aux slot: DQ bytes [16 rows][32 blocks], x [16], c1 [16 rows][2]
+constexpr int AUX_DQ = 0, AUX_X = 512, AUX_C1 = 544, AUX = 704;
+
+__global__ void __launch_bounds__(TPB, 1)
+    gemv_mma_kernel(const __grid_constant__ CUtensorMap tm_codes, const uint8_t* __restrict__ dq_codes,
+                    const float* __restrict__ c1, int64_t n2, const float* __restrict__ mu, int bs2_shift,
+                    qlrt_fp8spec sp, Vals16 vals, float maxdec, int64_t K, int64_t N,
+                    const unsigned short* __restrict__ x, float* __restrict__ part, unsigned* __restrict__ counters,
+                    const float* __restrict__ tpart, int zt, const __nv_bfloat16* __restrict__ l2, int rank,
+                    float s, __nv_bfloat16* __restrict__ y) {
+  extern __shared__ __align__(1024) uint8_t dyn[];
+  __shared__ float tsh[512];
+  __shared__ unsigned last_flag, red_x[CWARPS], red_c[CWARPS];
+  __shared__ float scales[2];
+  __shared__ uint32_t v16[16];
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t nbr = N / 64, chunks = cdiv(K, ROWS), strips = cdiv(N, STRIP), units = chunks * strips;
+  const int G = (int)gridDim.x;
+  const int64_t ub = (int64_t)blockIdx.x * units / G, ue = (int64_t)(blockIdx.x + 1) * units / G;
+  const int nunits = (int)(ue - ub);
+
+  // ---- shared layout: 64 KB table at the first 64 KB-aligned address;
+  // 1 KB-aligned stages, the aux ring and the fp8 LUT around it
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(dyn);
+  const uint32_t tab = (base + 65535u) & ~65535u;
+  const uint32_t front = (base + 1023u) & ~1023u;
+  const uint32_t back = tab + 65536u;
+  const uint32_t aux0 = front + NFRONT * STAGE;
+  const uint32_t lut_a = aux0 + NST * AUX;
+  if (tab < lut_a + 2048u) __trap();  // (static smem grew: re-plan the layout)
+  double* lut = reinterpret_cast<double*>(dyn + (lut_a - base));
+
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) {
+      ptx::mbar_init(&full[i], 1 + 32);  // TMA tx arrive + warp 0's cp.async arrivals
+      ptx::mbar_init(&empty[i], CWARPS);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (tid < 16) v16[tid] = (uint32_t)__half_as_ushort(__float2half_rn(vals.v[tid]));
+  if (tid < 256) lut[tid] = fp8_decode_fast(tid, sp);
+  __syncthreads();
+
+  // ---- stage issue (warp 0; the codes and a_k inputs never depend on the
+  // prep kernel): 8 TMA boxes of codes + the DQ bytes, x and c1 of the 16 rows
+  int64_t ps = ub / chunks, pc = ub - ps * chunks;
+  auto slot_addr = [&](int sl) -> uint32_t {
+    return sl < NFRONT ? front + (uint32_t)sl * STAGE : back + (uint32_t)(sl - NFRONT) * STAGE;
+  };
+  auto issue = [&](int sl) {  // called by all 32 lanes of warp 0
+    const int64_t r0 = pc * ROWS;
+    if (lane == 0) {  // one 3-d box [8 column groups][16 rows][128 B] (OOB groups zero-filled)
+      ptx::mbar_arrive_expect_tx(&full[sl], (uint32_t)STAGE);
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+              slot_addr(sl)),
+          "l"(reinterpret_cast<uint64_t>(&tm_codes)), "r"(ptx::smem_u32(&full[sl])), "r"(0), "r"((int)r0),
+          "r"((int)(ps * 8))
+          : "memory");
+    }
+    const uint32_t ax = aux0 + (uint32_t)sl * AUX;
+    const int64_t jb0 = ps * 32;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // DQ bytes: 16 rows x 8 groups of 4 blocks
+      const int p = lane + 32 * j, r = p >> 3, q = p & 7;
+      const int64_t jb = jb0 + 4 * q;
+      cp_async4(ax + AUX_DQ + r * 32 + q * 4, dq_codes + (r0 + r) * nbr + jb, jb < nbr);
+    }
+    if (lane < 2) cp_async16(ax + AUX_X + lane * 16, x + r0 + lane * 8, true);
+    {  // c1 of row lane & 15: the (<= 2) second-level blocks its 32 first-level blocks span
+      const int r = lane & 15, which = lane >> 4;
+      const int64_t ic = (((r0 + r) * nbr + jb0) >> bs2_shift) + which;
+      cp_async4(ax + AUX_C1 + r * 8 + which * 4, c1 + ic, ic < n2);
+    }
+    cp_async_arrive(&full[sl]);
+    if (++pc == chunks) {
+      pc = 0;
+      ++ps;
+    }
+  };
+  if (wid == 0) {
+    if (lane == 0) ptx::prefetch_tmap(&tm_codes);
+    for (int i = 0; i < NST && i < nunits; ++i) issue(i);
+  }
+
+  // ---- table: entry e = {fp16 v(e & 15), fp16 v(e >> 4)} in every lane's column
+  for (int q = tid; q < 256 * 32; q += TPB) {
+    const int e = q >> 5, l = q & 31;
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(tab + (uint32_t)e * 256u + (uint32_t)l * 4u),
+                 "r"(v16[e & 15] | (v16[e >> 4] << 16)));
+  }
+
+  // ---- the fp16 scale 2^-E of this CTA: max |a| 2^-E < 2^15 over the a_k it
+  // uses (a = x c, c <= maxdec c1 + max(mu, 0)): max |x| and max c1 over the
+  // rows / second-level blocks of its units
+  const double mu_d = (double)__ldg(mu);
+  {
+    // segments of the CTA: strip s, rows [r_lo, r_hi) (<= a few; nunits * 16 rows in all)
+    unsigned mx = 0u, mc = 0u;
+    const int64_t s0 = ub / chunks, s1 = (ue - 1) / chunks;
+    for (int64_t sg = s0; sg <= s1; ++sg) {
+      const int64_t ra = sg == s0 ? (ub - s0 * chunks) * ROWS : 0;
+      const int64_t rb = sg == s1 ? (ue - s1 * chunks) * ROWS : K;
+      for (int64_t k = ra + tid; k < rb; k += TPB) {
+        const unsigned v = __ldg(x + k) & 0x7FFFu;
+        mx = v > mx ? v : mx;
+      }
+      const int64_t ia = (ra * nbr + sg * 32) >> bs2_shift;
+      int64_t ib = (((rb - 1) * nbr + sg * 32 + 31) >> bs2_shift) + 1;
+      ib = ib < n2 ? ib : n2;
+      for (int64_t i = ia + tid; i < ib; i += TPB) {
+        const unsigned v = __float_as_uint(__ldg(c1 + i)) & 0x7FFFFFFFu;
+        mc = v > mc ? v : mc;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned a = __shfl_xor_sync(0xffffffffu, mx, o), c = __shfl_xor_sync(0xffffffffu, mc, o);
+      mx = a > mx ? a : mx;
+      mc = c > mc ? c : mc;
+    }
+    if (lane == 0) {
+      red_x[wid] = mx;
+      red_c[wid] = mc;
+    }
+    __syncthreads();  // (also: the table is complete)
+    if (tid == 0) {
+      for (int w = 1; w < CWARPS; ++w) {
+        mx = red_x[w] > mx ? red_x[w] : mx;
+        mc = red_c[w] > mc ? red_c[w] : mc;
+      }
+      const double m = (double)__uint_as_float(mx << 16) * ((double)maxdec * (double)__uint_as_float(mc) + fmax(mu_d, 0.0));
+      int e = 0;
+      if (m > 0.0 && m < 1e300) {
+        e = ilogb(m) - 14;
+        e = e < -120 ? -120 : (e > 120 ? 120 : e);
+      }
+      scales[0] = ldexpf(1.0f, -e);
+      scales[1] = ldexpf(1.0f, e);
+    }
+    __syncthreads();
+  }
+  const float sc = scales[0], unsc = scales[1];
+
+  // ---- consumers: warp w owns columns [128 w, +128) of the strip (box w >> 1, half w & 1)
+  const int g = lane >> 2, t = lane & 3;
+  const int bx = wid >> 1, u = wid & 1;
+  const uint32_t lanereg = tab + (uint32_t)lane * 4u;
+  // this lane's 8 code bytes of rows 2t, 2t+1, 2t+8, 2t+9 inside box bx (128B swizzle)
+  const int cidx = u * 4 + (g >> 1);
+  uint32_t roff[4];
+  {
+    const int rr[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      roff[i] = (uint32_t)bx * (ROWS * 128) + (uint32_t)rr[i] * 128u + (uint32_t)((cidx ^ (rr[i] & 7)) << 4) +
+                (uint32_t)(g & 1) * 8u;
+  }
+  // a_k of (row a_r = lane & 15, block jl = 4 bx + 2 u + (lane >> 4) of the strip)
+  const int a_r = lane & 15, jl = bx * 4 + u * 2 + (lane >> 4);
+  const uint32_t a_dq = AUX_DQ + a_r * 32 + jl, a_x = AUX_X + a_r * 2, a_c = AUX_C1 + a_r * 8;
+  int64_t cs = ub / chunks;
+  int64_t blk = (((ub - cs * chunks) * ROWS) + a_r) * nbr + cs * 32 + jl;  // first-level block of the lane's a_k
+  int64_t blk0 = blk - jl;
+  bool jok = cs * 32 + jl < nbr;
+  const int64_t blk_step = ROWS * nbr;
+
+  float acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0f;
+
+  int left = (int)((cs + 1) * chunks - ub);  // units of strip cs still to do
+  const int src0 = ((g >> 1) & 1) * 16 + 2 * t;
+  const uint32_t bsel = (g & 1) ? 0x7632u : 0x5410u;
+  int sl = 0;
+  uint32_t par = 0u;
+  bool waited_prep = false;
+  for (int i = 0; i < nunits; ++i) {
+    if (left == 0) {
+      // ---- strip segment done: partial, ticket, maybe finalize
+      if (!waited_prep) {  // prep: zeroed tickets, LoRA partials
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        waited_prep = true;
+      }
+      if (t == (g >> 2)) {  // useful D lanes: lane g holds columns 16 g + 2 mt (+1) of the warp's 128
+        float* dst = part + (blockIdx.x + cs) * STRIP + wid * 128 + 16 * g;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+          *reinterpret_cast<float2*>(dst + 2 * mt) =
+              make_float2((acc[mt][0] + acc[mt][1]) * unsc, (acc[mt][2] + acc[mt][3]) * unsc);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.0f;
+      __threadfence();
+      cbar();
+      const int f = first_cta(cs, chunks, units, G), l = last_cta(cs, chunks, units, G);
+      if (tid == 0) last_flag = (atomicAdd(counters + cs, 1u) == (unsigned)(l - f)) ? 1u : 0u;
+      cbar();
+      if (last_flag) finalize_strip(cs, f, l, N, part, tpart, zt, l2, rank, s, y, tsh);
+      ++cs;
+      left = (int)chunks;
+      blk = (int64_t)a_r * nbr + cs * 32 + jl;
+      blk0 = blk - jl;
+      jok = cs * 32 + jl < nbr;
+    }
+    --left;
+    ptx::mbar_wait(&full[sl], par);
+    const uint32_t sa = sl < NFRONT ? front + (uint32_t)sl * STAGE : back + (uint32_t)(sl - NFRONT) * STAGE;
+    const uint32_t ax = aux0 + (uint32_t)sl * AUX;
+    const uint2 w0 = lds64(sa + roff[0]), w1 = lds64(sa + roff[1]), w2 = lds64(sa + roff[2]),
+                w3 = lds64(sa + roff[3]);
+    // a_k = x_k c_k 2^-E as an fp16 hi | lo pair
+    uint32_t hv;
+    {
+      uint32_t dqb, xb, c1b;
+      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(dqb) : "r"(ax + a_dq));
+      asm volatile("ld.shared.u16 %0, [%1];" : "=r"(xb) : "r"(ax + a_x));
+      const uint32_t which = (uint32_t)((blk >> bs2_shift) - (blk0 >> bs2_shift));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(c1b) : "r"(ax + a_c + which * 4u));
+      double r = __dadd_rn(__dmul_rn(lut[dqb], (double)__uint_as_float(c1b)), mu_d);
+      r = r > 0.0 ? r : 0.0;
+      const float a = jok ? (__uint_as_float(xb << 16) * __double2float_rn(r)) * sc : 0.0f;
+      const __half h = __float2half_rn(a);
+      const __half lo = __float2half_rn(a - __half2float(h));
+      hv = (uint32_t)__half_as_ushort(h) | ((uint32_t)__half_as_ushort(lo) << 16);
+    }
+    blk += blk_step;
+    blk0 += blk_step;
+    // index bytes: codes of rows (2t, 2t+1) resp. (2t+8, 2t+9) of one column
+    uint32_t ie[2], io[2], je[2], jo[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t x0 = h ? w0.y : w0.x, x1 = h ? w1.y : w1.x, x2 = h ? w2.y : w2.x, x3 = h ? w3.y : w3.x;
+      ie[h] = (x0 & 0x0F0F0F0Fu) | ((x1 << 4) & 0xF0F0F0F0u);
+      io[h] = ((x0 >> 4) & 0x0F0F0F0Fu) | (x1 & 0xF0F0F0F0u);
+      je[h] = (x2 & 0x0F0F0F0Fu) | ((x3 << 4) & 0xF0F0F0F0u);
+      jo[h] = ((x2 >> 4) & 0x0F0F0F0Fu) | (x3 & 0xF0F0F0F0u);
+    }
+    // B fragment: lanes g < 4 take column n = g (block g >> 1, hi / lo by g & 1)
+    const uint32_t v0 = __shfl_sync(0xffffffffu, hv, src0);
+    const uint32_t v1 = __shfl_sync(0xffffffffu, hv, src0 + 1);
+    const uint32_t v2 = __shfl_sync(0xffffffffu, hv, src0 + 8);
+    const uint32_t v3 = __shfl_sync(0xffffffffu, hv, src0 + 9);
+    const uint32_t b0 = g < 4 ? __byte_perm(v0, v1, bsel) : 0u;
+    const uint32_t b1 = g < 4 ? __byte_perm(v2, v3, bsel) : 0u;
+    // (the shuffles used every lane's stage bytes: release the slot)
+    if (lane == 0) ptx::mbar_arrive(&empty[sl]);
+    if (wid == 0 && i + NST < nunits) {  // warp 0 refills the slot once every warp has read it
+      ptx::mbar_wait(&empty[sl], par);
+      issue(sl);
+    }
+    if (++sl == NST) {
+      sl = 0;
+      par ^= 1u;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint32_t sel = 0x7604u | ((uint32_t)b << 4);
+        const uint32_t a0 = lds(__byte_perm(ie[h], lanereg, sel));
+        const uint32_t a1 = lds(__byte_perm(io[h], lanereg, sel));
+        const uint32_t a2 = lds(__byte_perm(je[h], lanereg, sel));
+        const uint32_t a3 = lds(__byte_perm(jo[h], lanereg, sel));
+        mma16816(acc[4 * h + b], a0, a1, a2, a3, b0, b1);
+      }
+    }
+  }
+  // ---- last segment
+  if (!waited_prep) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (t == (g >> 2)) {
+    float* dst = part + (blockIdx.x + cs) * STRIP + wid * 128 + 16 * g;
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+      *reinterpret_cast<float2*>(dst + 2 * mt) =
+          make_float2((acc[mt][0] + acc[mt][1]) * unsc, (acc[mt][2] + acc[mt][3]) * unsc);
+  }
+  __threadfence();
+  cbar();
+  const int f = first_cta(cs, chunks, units, G), l = last_cta(cs, chunks, units, G);
+  if (tid == 0) last_flag = (atomicAdd(counters + cs, 1u) == (unsigned)(l - f)) ? 1u : 0u;
+  cbar();
+  if (last_flag) finalize_strip(cs, f, l, N, part, tpart, zt, l2, rank, s, y, tsh);
+}
+
+// packed codes [K rows][N/2 bytes] as a 3-d uint8 tensor, box [8][16 rows][128 B], 128B swizzle
+static bool make_tmap_codes(CUtensorMap* m, const void* base, int64_t row_bytes, int64_t rows) {
+  typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  if (!fn || (((uintptr_t)base) & 15) || (row_bytes & 127)) return false;
+  // 3-d view {128 B, rows, 128-B column groups}: one box = a whole stage
+  cuuint64_t dims[3] = {128, (cuuint64_t)rows, (cuuint64_t)(row_bytes / 128)};
+  cuuint64_t strides[2] = {(cuuint64_t)row_bytes, 128};
+  cuuint32_t box[3] = {128, ROWS, 8};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace gemv2
 }  // namespace qlrt
 
 using namespace qlrt;
@@ -299,7 +819,8 @@ using namespace qlrt;
 extern "C" {
 
 size_t qlrt_gemv_workspace_bytes(int64_t k_in, int64_t n_out, int rank) {
-  return gemv::ws_bytes(k_in, n_out, rank);
+  const size_t a = gemv::ws_bytes(k_in, n_out, rank), b = gemv2::ws_bytes(k_in, n_out, rank);
+  return a > b ? a : b;
 }
 
 qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* xa, const void* l1, const void* l2,
@@ -313,6 +834,56 @@ qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* x
     return QLRT_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t K = w->k_in, N = w->n_out;
+  CUtensorMap tmc;
+  if (policy(P_GEMV_MMA) && (N % 256) == 0 && (K % 16) == 0 && w->blocksize2 >= 32 &&
+      (((uintptr_t)x) & 15) == 0 && gemv2::make_tmap_codes(&tmc, w->codes, N / 2, K)) {
+    // tensor-core GEMV: prep (tickets, max slots, LoRA partials) then the
+    // main kernel as its PDL dependent (prologue + first TMA loads overlap prep)
+    int dev = 0, sms = kNumSMs;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const gemv2::Geo g = gemv2::geo(K, N, sms);
+    uint8_t* ws = (uint8_t*)workspace;
+    float* part = (float*)(ws + gemv2::part_off());
+    float* tpart = (float*)(ws + gemv2::tpart_off(g));
+    unsigned* counters = (unsigned*)(ws + gemv2::cnt_off(g, rank));
+    const int zt = (int)cdiv(K, 128);
+    const double maxdec = fp8_max_value(w->spec.exp_bits, w->spec.mant_bits, w->spec.bias);
+    const int64_t n2 = cdiv(K * (N / 64), (int64_t)w->blocksize2);
+    gemv2::prep_kernel<<<1 + (rank > 0 ? zt : 0), 256, 0, st>>>(K, (const __nv_bfloat16*)(xa ? xa : x),
+                                                              (const __nv_bfloat16*)l1, rank, tpart, counters,
+                                                              (int)g.strips);
+    QLRT_CHECK_LAUNCH();
+    static std::atomic<unsigned long long> attr_mask{0};
+    if (!(attr_mask.load() & (1ull << (dev & 63)))) {
+      if (cudaFuncSetAttribute(gemv2::gemv_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv2::SMEM) !=
+          cudaSuccess)
+        return QLRT_ERR_CUDA;
+      // both kernels at the full shared-memory carveout: no L1/smem
+      // reconfiguration between the prep grid and the main grid
+      cudaFuncSetAttribute(gemv2::gemv_mma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(gemv2::prep_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      attr_mask.fetch_or(1ull << (dev & 63));
+    }
+    gemv2::Vals16 v;
+    for (int i = 0; i < 16; ++i) v.v[i] = (float)w->values[i];
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)g.grid);
+    cfg.blockDim = dim3(gemv2::TPB);
+    cfg.dynamicSmemBytes = gemv2::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = policy(P_PDL) ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, gemv2::gemv_mma_kernel, tmc, w->dq_codes, w->c1, n2, w->mu,
+                           (int)__builtin_ctz((unsigned)w->blocksize2), w->spec, v, (float)maxdec, K, N,
+                           (const unsigned short*)x, part, counters, (const float*)tpart, zt,
+                           (const __nv_bfloat16*)l2, rank, s, (__nv_bfloat16*)y) != cudaSuccess)
+      return QLRT_ERR_CUDA;
+    QLRT_CHECK_LAUNCH();
+    return QLRT_OK;
+  }
   const gemv::Plan p = gemv::plan(K, N);
   uint8_t* ws = (uint8_t*)workspace;
   float* part = (float*)ws;

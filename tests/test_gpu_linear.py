@@ -118,11 +118,15 @@ def test_fused_linear_vs_oracle(m, k, n, r, oracle, qb, cuda):
     assert_tol(gg["adapter0.l2"].cpu().numpy(), grads["adapter0.l2"], "dl2")
 
 
-@pytest.mark.parametrize("m,k,n", [(2048, 4096, 11008), (1024, 8192, 22016), (1024, 22016, 8192)])
+@pytest.mark.parametrize("m,k,n", [(2048, 4096, 11008), (2048, 4096, 4096), (2048, 11008, 4096),
+                                   (2048, 8192, 8192), (2048, 8192, 22016), (2048, 22016, 8192),
+                                   (2048, 6656, 6656), (2048, 6656, 17920), (2048, 17920, 6656)])
 def test_c2_shape_vs_torch_fp32(m, k, n, qb, cuda):
-    """Config C2 at full size (4096 -> 11008, r = 64, 4x512 tokens) and the
-    LLaMA-65B MLP shapes (C4) against a plain PyTorch fp32 reference of the
-    same bf16 operands (the fp64 oracle takes minutes at these sizes)."""
+    """Config C2 at full size (4096 -> 11008, r = 64, 4x512 tokens), the other
+    LLaMA-7B projections (C3), the three LLaMA-65B layer shapes at the C4 token
+    count (M = 2048) and the LLaMA-33B shapes (C5) against a plain PyTorch fp32
+    reference of the same bf16 operands (the fp64 oracle takes minutes at these
+    sizes)."""
     r, s = 64, 0.25
     torch.backends.cuda.matmul.allow_tf32 = False
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -178,27 +182,54 @@ def test_fresh_adapter_is_exact_noop(qb, cuda):
     assert torch.equal(plain.forward(x)[0], adapted.forward(x)[0])
 
 
-@pytest.mark.parametrize("k,n", [(8192, 8192), (4096, 11008), (1000, 22016), (64, 192), (8, 64)])
-def test_gemv_batch1(k, n, oracle, qb, cuda):
-    """Batch-1 GEMV (same engine, W decoded to bf16 in-kernel) vs the fp64
-    oracle over W = bf16(f32(dequantize(q))) -- the GEMM parity definition."""
+@pytest.mark.parametrize("k,n", [(8192, 8192), (4096, 11008), (1000, 22016), (64, 192), (8, 64), (296, 4160)])
+@pytest.mark.parametrize("mma", [1, 0])
+def test_gemv_batch1(k, n, mma, oracle, qb, cuda):
+    """Batch-1 GEMV vs the fp64 oracle.  The tensor-core GEMV (default,
+    QLRT_GEMV_MMA=1) multiplies fp16 codebook values by x_k c_k (fp16 hi/lo):
+    its W is the reference's float32 W = f32(dequantize(q)) (qlora.py:117-122)
+    to ~2^-12, so that is its oracle; the FHFMA GEMV (QLRT_GEMV_MMA=0) decodes
+    bf16(f32(v) c) like the fused GEMM and is held to W = bf16(f32(dequantize(q)))."""
     rng = np.random.default_rng(k + n)
     w = (0.02 * rng.standard_normal((k, n))).astype(np.float32)
     q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)
-    wd = bf16_round(qb.dequantize(q, torch.float32).cpu().numpy()).astype(np.float64)
+    w32 = qb.dequantize(q, torch.float32).cpu().numpy()
+    tc = mma and k % 16 == 0 and n % 256 == 0  # shapes the tensor-core GEMV takes
+    wd = (w32 if tc else bf16_round(w32)).astype(np.float64)
     x = bf16_round(rng.standard_normal((1, k)))
     r = 64
     l1 = bf16_round(rng.standard_normal((k, r)) / 8)
     l2 = bf16_round(0.01 * rng.standard_normal((r, n)))
-    lin = qb.QLinear(q, [qb.LoraAdapter(r, 16.0, torch.from_numpy(l1).cuda(), torch.from_numpy(l2).cuda())])
-    y, _ = lin.forward(torch.from_numpy(x))
-    ref = x.astype(np.float64) @ wd + 0.25 * (x.astype(np.float64) @ l1) @ l2
-    assert_tol(y.float().cpu().numpy(), bf16_round(ref), "gemv")
-    # no adapter, and determinism (split-K partials summed in a fixed order)
-    plain = qb.QLinear(q, [])
-    y0 = plain.forward(torch.from_numpy(x))[0]
-    assert_tol(y0.float().cpu().numpy(), bf16_round(x.astype(np.float64) @ wd), "gemv r=0")
-    assert torch.equal(y0, plain.forward(torch.from_numpy(x))[0])
+    qb.set_policy("QLRT_GEMV_MMA", mma)
+    try:
+        lin = qb.QLinear(q, [qb.LoraAdapter(r, 16.0, torch.from_numpy(l1).cuda(), torch.from_numpy(l2).cuda())])
+        y, _ = lin.forward(torch.from_numpy(x))
+        ref = x.astype(np.float64) @ wd + 0.25 * (x.astype(np.float64) @ l1) @ l2
+        assert_tol(y.float().cpu().numpy(), bf16_round(ref), "gemv")
+        # no adapter, and determinism (split-K partials summed in a fixed order)
+        plain = qb.QLinear(q, [])
+        y0 = plain.forward(torch.from_numpy(x))[0]
+        assert_tol(y0.float().cpu().numpy(), bf16_round(x.astype(np.float64) @ wd), "gemv r=0")
+        assert torch.equal(y0, plain.forward(torch.from_numpy(x))[0])
+    finally:
+        qb.set_policy("QLRT_GEMV_MMA", None)
+
+
+@pytest.mark.parametrize("xs,ws", [(3e4, 1.0), (1e-3, 1e-4), (1.0, 300.0)])
+def test_gemv_magnitudes(xs, ws, qb, cuda):
+    """The fp16 operand scale 2^-E of the tensor-core GEMV follows max|x| and
+    the largest representable block constant: huge, tiny and large-weight
+    inputs stay within tolerance (no fp16 overflow / flush)."""
+    rng = np.random.default_rng(11)
+    k, n = 2048, 1024
+    w = (ws * rng.standard_normal((k, n))).astype(np.float32)
+    q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)
+    wd = qb.dequantize(q, torch.float32).cpu().numpy().astype(np.float64)
+    x = bf16_round(xs * rng.standard_normal((1, k)))
+    x[0, ::7] = 0.0
+    y = qb.QLinear(q, []).forward(torch.from_numpy(x))[0]
+    assert torch.isfinite(y.float()).all()
+    assert_tol(y.float().cpu().numpy(), bf16_round(x.astype(np.float64) @ wd), f"gemv x*{xs} w*{ws}")
 
 
 def test_unfused_shape_path(oracle, qb, cuda):

@@ -103,6 +103,8 @@ struct Args {
   int units_cap;        // > 0: at most this many (pair) units (SMs left to the predecessor)
   int aug_wrap;         // > 0: the augmented A2 operand has only aug_wrap K rows/cols and is
                         // re-read for K2 = 2 aug_wrap ([l | l] without materialising the pair)
+  int cl2;              // plain 1-SM grid launched as 2-CTA clusters (independent CTAs): it
+                        // occupies whole SM pairs beside a pair grid instead of fragmenting them
 };
 
 #ifndef QLRT_MERGE_FULL
@@ -1329,6 +1331,15 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
   }
+  if (!PAIR && !NF4 && args.cl2 && args.csplit <= 1) {
+    cfg.gridDim = dim3((units + 1) / 2 * 2);
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+  }
   if (PAIR) {
     attrs[0].id = cudaLaunchAttributeClusterDimension;
     attrs[0].val.clusterDim.x = 2;
@@ -1488,8 +1499,10 @@ static int pick_splits(int64_t tiles, int64_t k_iters, int64_t per_split_bytes, 
 // reduce kernel (forces the fp32 workspace route); out_split: bf16 hi/lo.
 static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, int64_t N, int64_t K, float alpha,
                          void* out, int64_t ldo, int out_f32, int out_t, float* ws, size_t ws_bytes, cudaStream_t s,
-                         int fold = 0, int out_split = 0, const Args* sk = nullptr, int pdl_independent = 0) {
+                         int fold = 0, int out_split = 0, const Args* sk = nullptr, int pdl_independent = 0,
+                         int cl2 = 0) {
   Args a{};
+  a.cl2 = cl2;
   // pdl_independent: inputs only (nothing from the PDL predecessor) -- start
   // at once beside it, complete only after it (see Args::wait_at_end)
   a.aug_pdl = pdl_independent;
@@ -1702,7 +1715,8 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
   const bool big = gemm::tile512_policy();
   const int cap = (rank > 0 && !ts_given && rank % 64 == 0 && big && gemm::pdl_policy())
-                      ? gemm::overlap_cap(N, m, gemm::overlap_need_sms()) : 0;
+                      ? gemm::overlap_cap(N, m, (policy(P_CL2) & 1) ? (int)((cdiv(m, 128) + 1) / 2 * 2) : gemm::overlap_need_sms())
+                      : 0;
   if (cap) {
     // Ts beside the fused grid: constants first (the fused grid reads them from
     // its start), then Ts without split-K (bf16 hi/lo pair, one CTA per 128
@@ -1714,7 +1728,8 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
     // (one CTA per 128-token tile; capping it to the SMs left, each CTA
     // looping over tiles, was measured slower: Ts then outlasts the grid's
     // first tiles)
-    rc = gemm::plain(64, TA, TB, m, rank, K, s, ts_out, 2 * rank, 0, 0, nullptr, 0, st, 0, rank, nullptr);
+    rc = gemm::plain(64, TA, TB, m, rank, K, s, ts_out, 2 * rank, 0, 0, nullptr, 0, st, 0, rank, nullptr, 0,
+                     policy(P_CL2) & 1);
     if (rc != QLRT_OK) return rc;
     a.M = (int)N;
     a.N = (int)m;
@@ -1798,12 +1813,14 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   // (dl2 beside the grid as well: 2-9% slower.)
   const int cap = (policy(P_OVERLAP_BWD) && rank > 0 && !dt_given && rank % 64 == 0 && gemm::tile512_policy() &&
                    gemm::pdl_policy())
-                      ? gemm::overlap_cap(K, m, gemm::overlap_need_sms()) : 0;
+                      ? gemm::overlap_cap(K, m, (policy(P_CL2) & 2) ? (int)((cdiv(m, 128) + 1) / 2 * 2) : gemm::overlap_need_sms())
+                      : 0;
   if (cap) {
     gemm::Args a{};
     if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
     Operand DA{dy, N, 0}, DB{l2, N, 0};
-    rc = gemm::plain(64, DA, DB, m, rank, N, s, dt_out, 2 * rank, 0, 0, nullptr, 0, st, 0, rank, nullptr);
+    rc = gemm::plain(64, DA, DB, m, rank, N, s, dt_out, 2 * rank, 0, 0, nullptr, 0, st, 0, rank, nullptr, 0,
+                     (policy(P_CL2) >> 1) & 1);
     if (rc != QLRT_OK) return rc;
     a.M = (int)K;
     a.N = (int)m;
@@ -1835,7 +1852,8 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
     if (side && !gemm::join_side(sctx, st)) return QLRT_ERR_CUDA;
     return QLRT_OK;
   }
-  if (rank > 0 && !dt_given) {
+  const int diag = policy(P_DIAG_SKIP);
+  if (rank > 0 && !dt_given && !(diag & 2)) {
     // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):
     //   A = dY (K-major [m][N]), B = l2 (K-major [r][N])
     Operand A{dy, N, 0}, B{l2, N, 0};
@@ -1877,6 +1895,7 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   a.aug_wrap = wrap ? rank : 0;
   rc = gemm::run(bn_main, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, N, 2 * rank, a, st);
   if (rc != QLRT_OK || rank == 0) return rc;
+  if (diag & 1) return side && !gemm::join_side(sctx, st) ? QLRT_ERR_CUDA : QLRT_OK;
   cudaStream_t aux = side ? side : st;
   {
     // dl2^T[N, r] = dY^T (Ts_hi + Ts_lo): A = dY (MN-major [m][N]), B = [Ts_hi | Ts_lo]

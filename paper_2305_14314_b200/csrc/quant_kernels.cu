@@ -202,9 +202,73 @@ __device__ __forceinline__ void load8_stream<__nv_bfloat16>(const __nv_bfloat16*
   }
 }
 
+// Single-lookup bin table with a private column per lane (entry b of lane l
+// at b * 256 + l * 8: bank = lane, conflict-free): float2 (lo', hi) where the
+// low 4 mantissa bits of lo' carry the base code of the bin and lo' is the
+// bracket's lower end moved outwards by <= 31 ulp (never inwards).  For q in
+// the bin:  j = base + (q > lo'),  certain unless lo' < q < hi (then the
+// group is re-decided exactly).  Bins a bracket does not touch hold lo' = 4.0
+// (q > lo' never); bins that touch two or more brackets hold lo' = -4.0,
+// hi = 4.0 (always re-decided).  Bin edges are widened by 2^-20 so the fp32
+// bin index may be off by one at an edge.
+constexpr int PBIN = 128;
+constexpr float PS = 63.875f;  // |q| <= 1 + 2^-20 maps into [0.1, 127.9]: no clamp
+__device__ void build_private_bins(uint32_t tab, const qlrt_codebook4& cb, uint2* ent) {
+  // one entry per bin (PBIN threads), then replicated into every lane's column
+  const int n = cb.n_mids;
+  const float dlt = 9.5367431640625e-07f;  // 2^-20
+  for (int b = threadIdx.x; b < PBIN; b += blockDim.x) {
+    // bin b = floor(q * PS + 64) holds q in [(b - 64) / PS, (b - 63) / PS)
+    const float qa = (float)(b - 64) / PS - dlt;
+    const float qb = (float)(b - 63) / PS + dlt;
+    int base = 0, hits = 0, hit = 0;
+    for (int i = 0; i < n; ++i) {
+      if (cb.hi[i] < qa) ++base;
+      if (cb.lo[i] <= qb && cb.hi[i] >= qa) {
+        ++hits;
+        hit = i;
+      }
+    }
+    uint32_t lo_b;
+    float hi;
+    if (hits == 0) {
+      lo_b = __float_as_uint(4.0f) | (uint32_t)base;
+      hi = 4.0f;
+    } else if (hits == 1) {
+      const uint32_t bits = __float_as_uint(cb.lo[hit]);
+      lo_b = ((bits >> 31) ? ((bits + 16u) & ~15u) : ((bits - 16u) & ~15u)) | (uint32_t)base;
+      hi = cb.hi[hit];
+    } else {
+      lo_b = __float_as_uint(-4.0f) | (uint32_t)base;
+      hi = 4.0f;
+    }
+    ent[b] = make_uint2(lo_b, __float_as_uint(hi));
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < PBIN * 32; q += blockDim.x) {
+    const int b = q >> 5, l = q & 31;
+    const uint2 e = ent[b];
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(tab + (uint32_t)b * 256u + (uint32_t)l * 8u), "r"(e.x),
+                 "r"(e.y));
+  }
+}
+
+// code of element k of the group added into word (fields do not overlap:
+// word += code << 4k is one IMAD); bad |= (q inside the bin's bracket)
+template <int K>
+__device__ __forceinline__ void pbin_acc(float x, float r, uint32_t lanecol, uint32_t& word, bool& bad) {
+  const float q = x * r;
+  const uint32_t b = (uint32_t)__float2int_rd(fmaf(q, PS, 64.0f));
+  uint32_t lo_b, hi_b;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo_b), "=r"(hi_b) : "r"(lanecol + (b << 8)));
+  const bool above = q > __uint_as_float(lo_b);
+  bad = bad || (above && q < __uint_as_float(hi_b));
+  word += ((lo_b & 15u) + (above ? 1u : 0u)) * (1u << (4 * K));
+}
+
 // Phase A, fp32 / bf16 input, blocksize 64, n % 64 == 0 (whole blocks): the
 // streaming version.  8 lanes per block as below, a persistent grid, the next
-// group's 32 B (fp32: one 256-bit load) in flight while the current one is
+// two groups' 32 B (fp32: one 256-bit load each) in flight while the current one is
 // coded, and a branch-free fast path per element with one group-wide check
 // (bracket hits are re-decided exactly, rarely).
 template <typename T>
@@ -216,13 +280,20 @@ __global__ void __launch_bounds__(256, QLRT_Q_MINB) quantize64_stream_kernel(con
                                                                 float* __restrict__ absmax,
                                                                 unsigned long long* __restrict__ first_bad) {
   __shared__ BinTables t;
+  __shared__ uint2 pent[PBIN];
+  extern __shared__ __align__(16) uint8_t ptab[];  // PBIN x 32 lanes x 8 B
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  float nv[8];  // the next group's values in flight
+  float nv[8], nv2[8];  // the next two groups' values in flight
   if (g < n_groups) load8_stream<T>(x, g * 8, nv);
+  if (g + stride < n_groups) load8_stream<T>(x, (g + stride) * 8, nv2);
   build_bin_tables(t, cb);
+  const uint32_t tab = (uint32_t)__cvta_generic_to_shared(ptab);
+  build_private_bins(tab, cb, pent);
+  const uint32_t lanecol = tab + (uint32_t)lane * 8u;
   __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (the DQ chunk sums wait for our completion)
   const unsigned pad = (unsigned)cb.pad_code;
   // n_groups % 8 == 0 and stride % 8 == 0: 8-lane groups are all-in or all-out,
   // and the trip count is warp-uniform (the shuffles need every lane)
@@ -230,8 +301,11 @@ __global__ void __launch_bounds__(256, QLRT_Q_MINB) quantize64_stream_kernel(con
     const bool act = g < n_groups;
     float v[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = act ? nv[j] : 0.0f;
-    if (g + stride < n_groups) load8_stream<T>(x, (g + stride) * 8, nv);
+    for (int j = 0; j < 8; ++j) {
+      v[j] = act ? nv[j] : 0.0f;
+      nv[j] = nv2[j];
+    }
+    if (g + 2 * stride < n_groups) load8_stream<T>(x, (g + 2 * stride) * 8, nv2);
     unsigned mb = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) mb = max(mb, __float_as_uint(v[j]) & 0x7FFFFFFFu);
@@ -250,11 +324,17 @@ __global__ void __launch_bounds__(256, QLRT_Q_MINB) quantize64_stream_kernel(con
     uint32_t word;
     if (c > 0.0f) {
       const float r = __frcp_rn(c);
-      bool ok = r <= 3.402823466e38f;  // subnormal c: 1/c overflows -> exact path
+      bool bad = !(r <= 3.402823466e38f);  // subnormal c: 1/c overflows -> exact path
       word = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) word |= bin_j(v[j], r, t, ok) << (4 * j);
-      if (!ok) {
+      pbin_acc<0>((float)v[0], r, lanecol, word, bad);
+      pbin_acc<1>((float)v[1], r, lanecol, word, bad);
+      pbin_acc<2>((float)v[2], r, lanecol, word, bad);
+      pbin_acc<3>((float)v[3], r, lanecol, word, bad);
+      pbin_acc<4>((float)v[4], r, lanecol, word, bad);
+      pbin_acc<5>((float)v[5], r, lanecol, word, bad);
+      pbin_acc<6>((float)v[6], r, lanecol, word, bad);
+      pbin_acc<7>((float)v[7], r, lanecol, word, bad);
+      if (bad) {
         const bool fast_ok = r <= 3.402823466e38f;
         word = 0;
 #pragma unroll
@@ -438,56 +518,67 @@ __device__ double pairwise_leaf(const float* a, int n) {
   return s;
 }
 
-__device__ double pairwise_seq(const float* a, int n) {
-  int off[32], len[32], stage[32];
-  double left[32];
-  int sp = 0;
-  off[0] = 0; len[0] = n; stage[0] = 0;
-  double ret = 0.0;
-  while (true) {
-    const int L = len[sp];
-    if (L <= 128) {
-      ret = pairwise_leaf(a + off[sp], L);
-      if (sp == 0) return ret;
-      --sp;
-      continue;
-    }
-    int n2 = L / 2;
-    n2 -= n2 % 8;
-    if (stage[sp] == 0) {
-      stage[sp] = 1;
-      ++sp;
-      off[sp] = off[sp - 1]; len[sp] = n2; stage[sp] = 0;
-    } else if (stage[sp] == 1) {
-      left[sp] = ret;
-      stage[sp] = 2;
-      ++sp;
-      off[sp] = off[sp - 1] + n2; len[sp] = L - n2; stage[sp] = 0;
-    } else {
-      ret = __dadd_rn(left[sp], ret);
-      if (sp == 0) return ret;
-      --sp;
-    }
-  }
-}
-
 // One CTA (512 threads) per 8192-constant buffer chunk.  A full chunk is a
 // perfect pairwise tree of 64 leaves of 128; leaf accumulator j of leaf L is
 // a[128L + j] + a[128L + j + 8] + ... (16 terms, in order) -- one thread each
 // -- and the 8 accumulators combine as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
 // by xor-shuffles (IEEE addition is commutative, so both partners hold the
-// same value).  The last CTA to finish adds the chunk sums in order from 0.0
-// and writes mu = f32(sum / nb) (doublequant.py:164-166).
+// same value).  The encode kernel adds the chunk sums in order from 0.0
+// (doublequant.py:164-166).  PDL dependent of phase A.
 __global__ void __launch_bounds__(512) dq_chunk_sums_kernel(const float* __restrict__ c, int64_t nb,
-                                                            double* __restrict__ chunk_sums,
-                                                            unsigned* __restrict__ ticket,
-                                                            float* __restrict__ mu_out) {
+                                                            double* __restrict__ chunk_sums) {
   __shared__ double leaf[64];
-  __shared__ bool last;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // phase A's constants
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t base = (int64_t)blockIdx.x * 8192;
   const int len = (int)min((int64_t)8192, nb - base);
   if (len < 8192) {
-    if (threadIdx.x == 0) chunk_sums[blockIdx.x] = pairwise_seq(c + base, len);
+    // partial chunk: the same recursion tree (split at n/2 - n/2 % 8 down to
+    // leaves <= 128), built by thread 0 in preorder, leaves summed in
+    // parallel, interior nodes combined children-first (reverse preorder)
+    __shared__ int nd_off[256], nd_len[256], nd_l[256], nd_r[256], nd_leaf[256];
+    __shared__ double nd_val[256];
+    __shared__ int n_nodes, n_leaves;
+    if (threadIdx.x == 0) {
+      int stack[32], sp = 0, nn = 0, nl = 0;
+      nd_off[0] = 0;
+      nd_len[0] = len;
+      nn = 1;
+      stack[sp++] = 0;
+      while (sp) {
+        const int v = stack[--sp];
+        const int L = nd_len[v];
+        if (L <= 128) {
+          nd_l[v] = nd_r[v] = -1;
+          nd_leaf[nl++] = v;
+          continue;
+        }
+        int h = L / 2;
+        h -= h % 8;
+        const int a = nn++, b = nn++;
+        nd_off[a] = nd_off[v];
+        nd_len[a] = h;
+        nd_off[b] = nd_off[v] + h;
+        nd_len[b] = L - h;
+        nd_l[v] = a;
+        nd_r[v] = b;
+        stack[sp++] = b;  // (order of evaluation is irrelevant: values combine by the tree)
+        stack[sp++] = a;
+      }
+      n_nodes = nn;
+      n_leaves = nl;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_leaves; i += blockDim.x) {
+      const int v = nd_leaf[i];
+      nd_val[v] = pairwise_leaf(c + base + nd_off[v], nd_len[v]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int v = n_nodes - 1; v >= 0; --v)  // children have larger indices than their parent
+        if (nd_l[v] >= 0) nd_val[v] = __dadd_rn(nd_val[nd_l[v]], nd_val[nd_r[v]]);
+      chunk_sums[blockIdx.x] = nd_val[0];
+    }
   } else {
     const int L = threadIdx.x >> 3, j = threadIdx.x & 7;
     const float* a = c + base + L * 128 + j;
@@ -511,61 +602,62 @@ __global__ void __launch_bounds__(512) dq_chunk_sums_kernel(const float* __restr
     }
     if (threadIdx.x == 0) chunk_sums[blockIdx.x] = leaf[0];
   }
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  // the chunk sums in parallel into shared memory, then added in order
-  __shared__ double cs[512];
-  double acc = 0.0;
-  for (unsigned b = 0; b < gridDim.x; b += 512) {
-    __syncthreads();
-    if (b + threadIdx.x < gridDim.x) cs[threadIdx.x] = __ldcg(chunk_sums + b + threadIdx.x);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned e = min(512u, gridDim.x - b);
-      for (unsigned i = 0; i < e; ++i) acc = __dadd_rn(acc, cs[i]);
-    }
-  }
-  if (threadIdx.x == 0) {
-    *mu_out = __double2float_rn(__ddiv_rn(acc, (double)nb));
-    *ticket = 0u;  // re-armed for the next call
-  }
 }
 
-// One CTA per second-level block: centring by mu, fp64 absmax, c1 = f32(A / max),
-// codes = encode(centered / f64(c1))  (doublequant.py:167-186).
+
+// Persistent: every CTA adds the chunk sums in order (from 0.0) into
+// mu = f32(sum / nb) (CTA 0 stores it), then loops over second-level blocks:
+// centring by mu, fp64 absmax, c1 = f32(A / max), codes = encode(centered /
+// f64(c1))  (doublequant.py:164-186).  PDL dependent of the chunk sums.
 __global__ void __launch_bounds__(256) dq_encode_kernel(const float* __restrict__ c, int64_t nb,
-                                                        int bs2, const float* __restrict__ mu_in,
-                                                        qlrt_fp8spec sp,
+                                                        int bs2, const double* __restrict__ chunk_sums,
+                                                        int n_chunks, qlrt_fp8spec sp, float* __restrict__ mu_out,
                                                         float* __restrict__ c1,
                                                         uint8_t* __restrict__ codes) {
   __shared__ double s_red[8];
-  const double mu = (double)*mu_in;
-  const int64_t b0 = (int64_t)blockIdx.x * bs2;
-  const int64_t b1 = min(b0 + bs2, nb);
-  double amax = 0.0;
-  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x)
-    amax = fmax(amax, fabs(__dsub_rn((double)c[i], mu)));
-  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = amax;
+  __shared__ double cs[512];
+  __shared__ float s_mu;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  double acc = 0.0;
+  for (int b = 0; b < n_chunks; b += 512) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 512 && b + i < n_chunks; i += blockDim.x) cs[i] = __ldcg(chunk_sums + b + i);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int e = min(512, n_chunks - b);
+      for (int i = 0; i < e; ++i) acc = __dadd_rn(acc, cs[i]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    s_mu = __double2float_rn(__ddiv_rn(acc, (double)nb));
+    if (blockIdx.x == 0) *mu_out = s_mu;
+  }
   __syncthreads();
-  amax = 0.0;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) amax = fmax(amax, s_red[w]);
+  const double mu = (double)s_mu;
   const double maxv = fp8_max_value(sp.exp_bits, sp.mant_bits, sp.bias);
-  float scale = 0.0f;
-  if (amax > 0.0) scale = __double2float_rn(__ddiv_rn(amax, maxv));
-  if (threadIdx.x == 0) c1[blockIdx.x] = scale;  // 0 for flat / underflowing blocks
-  const double sd = (double)scale;
-  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-    unsigned code = 0u;
-    if (scale != 0.0f)
-      code = fp8_encode(__ddiv_rn(__dsub_rn((double)c[i], mu), sd), sp.exp_bits, sp.mant_bits,
-                        sp.bias, maxv);
-    codes[i] = (uint8_t)code;
+  const int64_t n2 = (nb + bs2 - 1) / bs2;
+  for (int64_t blk = blockIdx.x; blk < n2; blk += gridDim.x) {
+    const int64_t b0 = blk * bs2;
+    const int64_t b1 = min(b0 + bs2, nb);
+    double amax = 0.0;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x)
+      amax = fmax(amax, fabs(__dsub_rn((double)c[i], mu)));
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    __syncthreads();  // (s_red of the previous block consumed)
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = amax;
+    __syncthreads();
+    amax = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) amax = fmax(amax, s_red[w]);
+    float scale = 0.0f;
+    if (amax > 0.0) scale = __double2float_rn(__ddiv_rn(amax, maxv));
+    if (threadIdx.x == 0) c1[blk] = scale;  // 0 for flat / underflowing blocks
+    const double sd = (double)scale;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      unsigned code = 0u;
+      if (scale != 0.0f)
+        code = fp8_encode(__ddiv_rn(__dsub_rn((double)c[i], mu), sd), sp.exp_bits, sp.mant_bits, sp.bias, maxv);
+      codes[i] = (uint8_t)code;
+    }
   }
 }
 
@@ -924,12 +1016,13 @@ qlrt_status qlrt_quantize4(const void* x, int x_dtype, int64_t n, int blocksize,
     const int64_t n_groups = nb * 8;
     const int64_t want = cdiv(n_groups, 256);
     const int grid = (int)(want < (int64_t)kNumSMs * QLRT_Q_MINB ? want : (int64_t)kNumSMs * QLRT_Q_MINB);  // resident
+    constexpr int psm = PBIN * 32 * 8;  // private-column bin table
     if (x_dtype == QLRT_F32)
-      quantize64_stream_kernel<float><<<grid, 256, 0, s>>>((const float*)x, n_groups, *cb, (uint32_t*)codes, absmax,
-                                                          fb);
+      quantize64_stream_kernel<float><<<grid, 256, psm, s>>>((const float*)x, n_groups, *cb, (uint32_t*)codes, absmax,
+                                                            fb);
     else
-      quantize64_stream_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, n_groups, *cb,
-                                                                  (uint32_t*)codes, absmax, fb);
+      quantize64_stream_kernel<__nv_bfloat16><<<grid, 256, psm, s>>>((const __nv_bfloat16*)x, n_groups, *cb,
+                                                                    (uint32_t*)codes, absmax, fb);
   } else if (blocksize == 64 && aligned) {
     const int64_t n_groups = nb * 8;
     const int grid = grid_for(n_groups, 256, 8);
@@ -960,7 +1053,7 @@ qlrt_status qlrt_quantize4(const void* x, int x_dtype, int64_t n, int blocksize,
   return QLRT_OK;
 }
 
-// chunk sums + the ticket of the last-CTA mu reduction (zeroed per call)
+// chunk sums of the DQ mean (fp64 per 8192-constant chunk)
 size_t qlrt_dq_workspace_bytes(int64_t nb) { return (size_t)cdiv(nb, 8192) * sizeof(double) + 16; }
 
 qlrt_status qlrt_dq_compress(const float* absmax, int64_t nb, int blocksize2, qlrt_fp8spec spec,
@@ -972,11 +1065,24 @@ qlrt_status qlrt_dq_compress(const float* absmax, int64_t nb, int blocksize2, ql
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n_chunks = cdiv(nb, 8192);
   double* sums = (double*)workspace;
-  unsigned* ticket = (unsigned*)(sums + n_chunks);
-  if (cudaMemsetAsync(ticket, 0, sizeof(unsigned), s) != cudaSuccess) return QLRT_ERR_CUDA;
-  dq_chunk_sums_kernel<<<(unsigned)n_chunks, 512, 0, s>>>(absmax, nb, sums, ticket, mu);
+  // chunk sums, then the persistent encode (each CTA adds the chunk sums in
+  // order itself: no ticket, no memset), both PDL-chained to their producer
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = policy(P_PDL) ? 1 : 0;
+  cfg.stream = s;
+  cfg.gridDim = dim3((unsigned)n_chunks);
+  cfg.blockDim = dim3(512);
+  if (cudaLaunchKernelEx(&cfg, dq_chunk_sums_kernel, absmax, nb, sums) != cudaSuccess) return QLRT_ERR_CUDA;
   const int64_t n2 = cdiv(nb, blocksize2);
-  dq_encode_kernel<<<(unsigned)n2, 256, 0, s>>>(absmax, nb, blocksize2, mu, spec, c1, dq_codes);
+  cfg.gridDim = dim3((unsigned)(n2 < (int64_t)kNumSMs * 8 ? n2 : (int64_t)kNumSMs * 8));
+  cfg.blockDim = dim3(256);
+  if (cudaLaunchKernelEx(&cfg, dq_encode_kernel, absmax, nb, blocksize2, (const double*)sums, (int)n_chunks, spec, mu,
+                         c1, dq_codes) != cudaSuccess)
+    return QLRT_ERR_CUDA;
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }

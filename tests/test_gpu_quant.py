@@ -167,7 +167,7 @@ def test_fp8_grid_and_dq_cases(golden, golden_meta, qb, cuda):
 def test_dq_mean_order_random(oracle, qb, cuda):
     """numpy-order fp64 mean on adversarial magnitudes, several chunk counts."""
     rng = np.random.default_rng(21)
-    for n in (1, 7, 129, 8192, 8193, 3 * 8192 + 1000, 100_000):
+    for n in (1, 7, 129, 1031, 5000, 8191, 8192, 8193, 3 * 8192 + 1000, 100_000):
         c = np.abs(rng.standard_normal(n) * np.exp(rng.uniform(-40, 40, size=n))).astype(np.float32)
         ref = oracle.dq_compress(c, 256)
         dq = qb.dq_compress(c, 256)
@@ -238,3 +238,36 @@ def test_fp8_encode_midpoints_vs_oracle(spec_args, oracle, qb, cuda):
     x = np.concatenate([x, -x, [0.0, -0.0]])
     got = qb.encode_fp8(x, spec).cpu().numpy()
     assert np.array_equal(got, oracle.encode_fp8(x, ospec))
+
+
+@pytest.mark.parametrize("name", ["nf4", "fp4-e2m1", "fp4-e3m0", "int4", "nf-eq4"])
+def test_stream_quantize_all_4bit_codebooks(name, oracle, qb, cuda):
+    """The streaming phase-A kernel (fp32, blocksize 64, whole blocks) with its
+    single-lookup private bin table, for every 4-bit codebook: random values
+    and values within a few ulp of every midpoint (the fp64 re-decision)
+    match the oracle bit for bit; DQ over a partial 8192-chunk as well."""
+    cbo = oracle.get_codebook(name)
+    mids = cbo.midpoints()
+    rng = np.random.default_rng(len(name))
+    blocks = []
+    for b in range(300):
+        c = np.float32(rng.uniform(0.01, 20.0))
+        vals = [c if b % 2 else -c]
+        while len(vals) < 64:
+            if rng.random() < 0.5:
+                vals.append(np.float32(rng.uniform(-1, 1) * float(c)))
+                continue
+            m = mids[rng.integers(mids.size)]
+            v = np.float32(m * float(c))
+            for _ in range(int(rng.integers(0, 4))):
+                v = np.nextafter(v, np.float32(np.inf) if rng.random() < 0.5 else np.float32(-np.inf))
+            vals.append(np.float32(v))
+        blocks.append(vals)
+    x = np.concatenate([np.array(blocks, dtype=np.float32).reshape(-1),
+                        rng.standard_normal(64 * 5000).astype(np.float32)])
+    ref = oracle.quantize(x.astype(np.float64), cbo, 64, double_quant=True)
+    q = qb.quantize(torch.from_numpy(x).cuda(), qb.get_codebook(name), 64, double_quant=True)
+    assert np.array_equal(q.codes.cpu().numpy(), ref.codes)
+    assert q.dq.mu.item() == ref.dq.mu
+    assert np.array_equal(q.dq.codes.cpu().numpy(), ref.dq.codes)
+    assert np.array_equal(q.dq.c1.cpu().numpy(), ref.dq.c1)

@@ -151,6 +151,28 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
                                 const void* l2, int rank, float s, void* dt_out, void* dx,
                                 float* dl1, float* dl2, void* workspace, void* stream);
 
+/* backward with flags.  QLRT_BWD_DEFER: the adapter-gradient GEMMs (dl2, dl1)
+ * are left on the library's side stream of `stream` and NOT joined: they run
+ * beside whatever the caller issues next (the following layers' fused grids
+ * leave SMs idle) until qlrt_side_join(stream).  The caller must then keep x,
+ * ts, dy and dt_out alive and unmodified, and not read dl1 / dl2, until it has
+ * issued qlrt_side_join; side_workspace (>= qlrt_linear_workspace_bytes of
+ * the call, distinct from `workspace`) holds the deferred split-K partials.
+ * flags = 0 is qlrt_nf4_linear_bwd.  (The reference computes the gradients in
+ * the same call, qlora.py:150-167; only their completion point moves.) */
+#define QLRT_BWD_DEFER 1
+qlrt_status qlrt_nf4_linear_bwd_ex(const qlrt_nf4_weight* w, const void* dy, int64_t m,
+                                   const void* x, const void* ts, const void* l1,
+                                   const void* l2, int rank, float s, void* dt_out, void* dx,
+                                   float* dl1, float* dl2, void* workspace,
+                                   void* side_workspace, int flags, void* stream);
+/* `stream` waits for everything deferred on its side stream so far. */
+qlrt_status qlrt_side_join(void* stream);
+/* The side stream of `stream` (cudaStream_t; NULL when side streams are off),
+ * for callers that order against part of the deferred work with their own
+ * events. */
+void* qlrt_side_stream(void* stream);
+
 /* batch-1 GEMV variant of forward (M = 1), HBM-bound on the packed codes:
  *   y[N] = x[K] W + s (xa l1) l2         fp32 accumulate, bf16 out
  * (xa = the dropout-masked adapter input, NULL -> x; qlora.py:137-146).

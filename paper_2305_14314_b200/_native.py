@@ -18,6 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("QLRT_LIB_PATH") or os.path.join(_HERE, "_lib", "libqlrt_b200.so")
 
 QLRT_OK, QLRT_ERR_ARG, QLRT_ERR_CUDA, QLRT_ERR_UNSUPPORTED = 0, 1, 2, 3
+QLRT_BWD_DEFER = 1
 F32, BF16, F64 = 0, 1, 2
 SUMSQ_SCRATCH = 8 + 8 * 296 + 8
 
@@ -55,6 +56,10 @@ _SIGS = {
                             c_void_p, c_void_p, c_void_p, c_void_p],
     "qlrt_nf4_linear_bwd": [POINTER(NF4Weight), c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
                             c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    "qlrt_nf4_linear_bwd_ex": [POINTER(NF4Weight), c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                               c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p],
+    "qlrt_side_join": [c_void_p],
+    "qlrt_side_stream": [c_void_p],
     "qlrt_nf4_gemv": [POINTER(NF4Weight), c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_float, c_void_p, c_void_p, c_void_p],
     "qlrt_gemv_workspace_bytes": [c_int64, c_int64, c_int],
     "qlrt_gemm_bf16": [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int, c_int, c_float, c_int, c_int,
@@ -74,7 +79,7 @@ _SIGS = {
     "qlrt_set_policy": [ctypes.c_char_p, c_int],
     "qlrt_get_policy": [ctypes.c_char_p, POINTER(c_int)],
 }
-_RESTYPE = {"qlrt_dq_workspace_bytes": c_size_t, "qlrt_linear_workspace_bytes": c_size_t,
+_RESTYPE = {"qlrt_side_stream": c_void_p, "qlrt_dq_workspace_bytes": c_size_t, "qlrt_linear_workspace_bytes": c_size_t,
             "qlrt_gemv_workspace_bytes": c_size_t,
             "qlrt_nf4_constants_bytes": c_size_t,
             "qlrt_build_info": ctypes.c_char_p}

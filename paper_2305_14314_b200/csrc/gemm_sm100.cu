@@ -1500,9 +1500,10 @@ static int pick_splits(int64_t tiles, int64_t k_iters, int64_t per_split_bytes, 
 static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, int64_t N, int64_t K, float alpha,
                          void* out, int64_t ldo, int out_f32, int out_t, float* ws, size_t ws_bytes, cudaStream_t s,
                          int fold = 0, int out_split = 0, const Args* sk = nullptr, int pdl_independent = 0,
-                         int cl2 = 0) {
+                         int cl2 = 0, int units_cap = 0) {
   Args a{};
   a.cl2 = cl2;
+  a.units_cap = units_cap;
   // pdl_independent: inputs only (nothing from the PDL predecessor) -- start
   // at once beside it, complete only after it (see Args::wait_at_end)
   a.aug_pdl = pdl_independent;
@@ -1604,6 +1605,14 @@ static size_t dbl_bytes(int64_t k_in, int64_t n_out, int rank) {
   const int64_t mx = k_in > n_out ? k_in : n_out;
   return align256((size_t)mx * 2 * rank * 2);
 }
+// split-K partial bytes of one skinny adapter GEMM (<= 16 splits)
+static size_t side_part_bytes(int64_t m, int64_t k_in, int64_t n_out, int rank) {
+  const int64_t r = rank > 0 ? rank : 1;
+  int64_t a = 16 * m * 2 * r, b = 16 * k_in * 2 * r, c = 16 * 2 * r * n_out;
+  int64_t mx = a > b ? a : b;
+  mx = mx > c ? mx : c;
+  return align256((size_t)mx * 4);
+}
 // stream-K partials (one BM x 256 fp32 tile per CTA) + flags
 constexpr int kSkCols = 512;  // widest tile (pair 256 x 512)
 static size_t sk_bytes() { return align256((size_t)kNumSMs * BM * kSkCols * 4) + align256((size_t)kNumSMs * 4); }
@@ -1667,12 +1676,9 @@ qlrt_status qlrt_nf4_constants(const qlrt_nf4_weight* w, float* out, void* strea
 
 size_t qlrt_linear_workspace_bytes(int64_t m, int64_t k_in, int64_t n_out, int rank) {
   // split-K partials of the skinny adapter GEMMs (<= 16 splits each) + GEMV scratch
-  int64_t r = rank > 0 ? rank : 1;
-  int64_t a = 16 * m * 2 * r, b = 16 * k_in * 2 * r, c = 16 * 2 * r * n_out;
-  int64_t mx = a > b ? a : b;
-  mx = mx > c ? mx : c;
-  size_t total = gemm::align256((size_t)mx * 4) + 4096 + gemm::align256(gemm::consts_bytes(k_in, n_out)) +
-                 gemm::sk_bytes() + gemm::dbl_bytes(k_in, n_out, rank > 0 ? rank : 0);
+  size_t total = gemm::side_part_bytes(m, k_in, n_out, rank) + 4096 +
+                 gemm::align256(gemm::consts_bytes(k_in, n_out)) + gemm::sk_bytes() +
+                 gemm::dbl_bytes(k_in, n_out, rank > 0 ? rank : 0);
   const size_t gv = qlrt_gemv_workspace_bytes(k_in, n_out, rank > 0 ? rank : 0);  // M = 1 path
   return total > gv ? total : gv;
 }
@@ -1789,10 +1795,11 @@ qlrt_status qlrt_nf4_linear_fwd(const qlrt_nf4_weight* w, const void* x, const v
   return gemm::run(bn_main, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, K, 2 * rank, a, st);
 }
 
-qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_t m, const void* x, const void* ts,
-                                const void* l1, const void* l2, int rank, float s, void* dt_out, void* dx, float* dl1,
-                                float* dl2, void* workspace, void* stream) {
-  if (!gemm::weight_ok(w) || !dy || !dx || m <= 0 || rank < 0) return QLRT_ERR_ARG;
+qlrt_status qlrt_nf4_linear_bwd_ex(const qlrt_nf4_weight* w, const void* dy, int64_t m, const void* x,
+                                   const void* ts, const void* l1, const void* l2, int rank, float s, void* dt_out,
+                                   void* dx, float* dl1, float* dl2, void* workspace, void* side_workspace,
+                                   int flags, void* stream) {
+  if (!gemm::weight_ok(w) || !dy || !dx || m <= 0 || rank < 0 || (flags & ~QLRT_BWD_DEFER)) return QLRT_ERR_ARG;
   if (rank > 0 && (!x || !ts || !l1 || !dt_out || !dl1 || !dl2 || (rank % 8))) return QLRT_ERR_ARG;
   // l2 == NULL: dt_out already holds dT (several adapters concatenated by the host)
   const bool dt_given = rank > 0 && !l2;
@@ -1805,68 +1812,25 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   qlrt_status rc;
   gemm::Args sk{};
   gemm::sk_region(workspace, ws_bytes, K, N, rank, sk);
-  // QLRT_OVERLAP_BWD=1 (off: measured -6% to +2%): dT beside the fused dX
-  // grid as its PDL predecessor (no split-K; the grid waits for it only before
-  // the augmented segment), then dl2 (side stream) and dl1 at full width.  The
-  // 16 dT CTAs land one per SM and hold back fused pairs that need whole SMs;
-  // the backward's 64-tile grids already leave their idle SMs to dl2 / dl1.
-  // (dl2 beside the grid as well: 2-9% slower.)
+  // QLRT_BWD_DEFER: the adapter-gradient GEMMs (dl2, dl1) stay on the side
+  // stream, not joined -- they run beside whatever the caller issues next
+  // (the next layers' fused grids leave SMs idle) until qlrt_side_join.  Their
+  // split-K partials then live in side_workspace (the caller's next calls reuse
+  // `workspace` on its own stream meanwhile).
+  gemm::SideCtx* sctx = rank > 0 ? gemm::side_ctx(st) : nullptr;
+  const bool defer = (flags & QLRT_BWD_DEFER) && rank > 0 && sctx && side_workspace;
+  const int side_cap = defer ? (policy(P_SIDE_SMS) + 0) : 0;  // units cap of the deferred GEMMs (0: none)
+  const int bn_g = 2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256);
+  // QLRT_OVERLAP_BWD=1: dT beside the fused dX grid as its PDL predecessor
+  // (no split-K; the grid waits for it only before the augmented segment).
+  // Without deferral it measured -6% to +2% (dl2 / dl1 then trail the grid at
+  // full width); the 16 dT CTAs land one per SM and hold back fused pairs
+  // that need whole SMs unless they run as 2-CTA clusters (QLRT_CL2 & 2).
   const int cap = (policy(P_OVERLAP_BWD) && rank > 0 && !dt_given && rank % 64 == 0 && gemm::tile512_policy() &&
                    gemm::pdl_policy())
                       ? gemm::overlap_cap(K, m, (policy(P_CL2) & 2) ? (int)((cdiv(m, 128) + 1) / 2 * 2) : gemm::overlap_need_sms())
                       : 0;
-  if (cap) {
-    gemm::Args a{};
-    if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
-    Operand DA{dy, N, 0}, DB{l2, N, 0};
-    rc = gemm::plain(64, DA, DB, m, rank, N, s, dt_out, 2 * rank, 0, 0, nullptr, 0, st, 0, rank, nullptr, 0,
-                     (policy(P_CL2) >> 1) & 1);
-    if (rc != QLRT_OK) return rc;
-    a.M = (int)K;
-    a.N = (int)m;
-    a.splits = 1;
-    a.out = dx;
-    a.ldo = K;
-    a.out_t = 1;
-    a.alpha = 1.0f;
-    a.pair = 1;
-    a.aug_wrap = rank;
-    a.aug_pdl = 1;
-    a.units_cap = cap;
-    Operand none{}, B{dy, N, 0}, A2{l1, rank, 0}, B2{dt_out, 2 * rank, 0};
-    if ((rc = gemm::run(512, none, B, &A2, &B2, N, 2 * rank, a, st)) != QLRT_OK) return rc;
-    gemm::SideCtx* sctx = gemm::side_ctx(st);
-    cudaStream_t side = gemm::fork_side(sctx, st);
-    {
-      Operand A{dy, N, 1}, B2t{ts, 2 * rank, 1};
-      rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B2t, N, 2 * rank, m, 1.0f, dl2, N, 1,
-                       1, side ? nullptr : (float*)workspace, side ? 0 : part_bytes, side ? side : st, rank);
-      if (rc != QLRT_OK) return rc;
-    }
-    {
-      Operand A{x, K, 1}, B1{dt_out, 2 * rank, 1};
-      rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B1, K, 2 * rank, m, 1.0f, dl1, rank,
-                       1, 0, (float*)workspace, part_bytes, st, rank, 0, &sk);
-      if (rc != QLRT_OK) return rc;
-    }
-    if (side && !gemm::join_side(sctx, st)) return QLRT_ERR_CUDA;
-    return QLRT_OK;
-  }
   const int diag = policy(P_DIAG_SKIP);
-  if (rank > 0 && !dt_given && !(diag & 2)) {
-    // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):
-    //   A = dY (K-major [m][N]), B = l2 (K-major [r][N])
-    Operand A{dy, N, 0}, B{l2, N, 0};
-    rc = gemm::plain(64, A, B, m, rank, N, s, dt_out, 2 * rank, 0, 0, (float*)workspace, part_bytes, st, 0, rank,
-                     &sk);
-    if (rc != QLRT_OK) return rc;
-  }
-  // the adapter gradients dl2 and dl1 need only the inputs and dT: they run on
-  // a side stream forked here and are launched after the fused dX GEMM, so
-  // they fill the SMs its grid leaves idle (or follow it as its CTAs retire)
-  gemm::SideCtx* sctx = rank > 0 ? gemm::side_ctx(st) : nullptr;
-  cudaStream_t side = gemm::fork_side(sctx, st);
-  // dX^T[K, m] = W dY^T (+ l1 dT^T): A = NF4 (K-major image), B = dY (K-major)
   gemm::Args a{};
   a.M = (int)K;
   a.N = (int)m;
@@ -1876,47 +1840,100 @@ qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_
   a.out_f32 = 0;
   a.out_t = 1;
   a.alpha = 1.0f;
-  const int bn_main = gemm::tile512_policy() ? 512 : 256;
-  a.pair = bn_main == 512 ? 1 : gemm::pair_policy(0);
-  a.share = a.pair ? 0 : gemm::share_policy();
-  if (gemm::streamk_policy()) { a.sk_ws = sk.sk_ws; a.sk_flags = sk.sk_flags; }
-  if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
   Operand none{}, B{dy, N, 0};
-  // augmented segment K2 = 2r: [l1 | l1] [dT_hi | dT_lo]^T
-  __nv_bfloat16* l1d = (__nv_bfloat16*)gemm::dbl_region(workspace, ws_bytes, K, N, rank);
-  const bool wrap = rank > 0 && rank % 64 == 0;  // re-read l1 itself (no doubled copy)
-  if (rank && !wrap) {
-    for (int h = 0; h < 2; ++h)
-      if (cudaMemcpy2DAsync(l1d + h * rank, (size_t)4 * rank, l1, (size_t)2 * rank, (size_t)2 * rank, (size_t)K,
-                            cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-        return QLRT_ERR_CUDA;
+  cudaStream_t side = nullptr;
+  if (cap) {
+    if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
+    Operand DA{dy, N, 0}, DB{l2, N, 0};
+    rc = gemm::plain(64, DA, DB, m, rank, N, s, dt_out, 2 * rank, 0, 0, nullptr, 0, st, 0, rank, nullptr, 0,
+                     (policy(P_CL2) >> 1) & 1);
+    if (rc != QLRT_OK) return rc;
+    a.pair = 1;
+    a.aug_wrap = rank;
+    a.aug_pdl = 1;
+    a.units_cap = cap;
+    Operand A2{l1, rank, 0}, B2{dt_out, 2 * rank, 0};
+    // (dl2 / dl1 wait for dT: fork before the fused grid is issued, after dT)
+    side = gemm::fork_side(sctx, st);
+    if ((rc = gemm::run(512, none, B, &A2, &B2, N, 2 * rank, a, st)) != QLRT_OK) return rc;
+  } else {
+    if (rank > 0 && !dt_given && !(diag & 2)) {
+      // dT[m, 0:r] + dT[m, r:2r] = s * dY l2^T (bf16 hi/lo pair):
+      //   A = dY (K-major [m][N]), B = l2 (K-major [r][N])
+      Operand DA{dy, N, 0}, DB{l2, N, 0};
+      rc = gemm::plain(64, DA, DB, m, rank, N, s, dt_out, 2 * rank, 0, 0, (float*)workspace, part_bytes, st, 0, rank,
+                       &sk);
+      if (rc != QLRT_OK) return rc;
+    }
+    // the adapter gradients dl2 and dl1 need only the inputs and dT: they run on
+    // a side stream forked here and are launched after the fused dX GEMM, so
+    // they fill the SMs its grid leaves idle (or follow it as its CTAs retire)
+    side = gemm::fork_side(sctx, st);
+    // dX^T[K, m] = W dY^T (+ l1 dT^T): A = NF4 (K-major image), B = dY (K-major)
+    const int bn_main = gemm::tile512_policy() ? 512 : 256;
+    a.pair = bn_main == 512 ? 1 : gemm::pair_policy(0);
+    a.share = a.pair ? 0 : gemm::share_policy();
+    if (gemm::streamk_policy()) { a.sk_ws = sk.sk_ws; a.sk_flags = sk.sk_flags; }
+    if ((rc = gemm::fill_nf4(a, w, 2, consts, st)) != QLRT_OK) return rc;
+    // augmented segment K2 = 2r: [l1 | l1] [dT_hi | dT_lo]^T
+    __nv_bfloat16* l1d = (__nv_bfloat16*)gemm::dbl_region(workspace, ws_bytes, K, N, rank);
+    const bool wrap = rank > 0 && rank % 64 == 0;  // re-read l1 itself (no doubled copy)
+    if (rank && !wrap) {
+      for (int h = 0; h < 2; ++h)
+        if (cudaMemcpy2DAsync(l1d + h * rank, (size_t)4 * rank, l1, (size_t)2 * rank, (size_t)2 * rank, (size_t)K,
+                              cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+          return QLRT_ERR_CUDA;
+    }
+    Operand A2{wrap ? l1 : l1d, wrap ? rank : 2 * rank, 0}, B2{dt_out, 2 * rank, 0};
+    a.aug_wrap = wrap ? rank : 0;
+    rc = gemm::run(bn_main, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, N, 2 * rank, a, st);
+    if (rc != QLRT_OK || rank == 0) return rc;
   }
-  Operand A2{wrap ? l1 : l1d, wrap ? rank : 2 * rank, 0}, B2{dt_out, 2 * rank, 0};
-  a.aug_wrap = wrap ? rank : 0;
-  rc = gemm::run(bn_main, none, B, rank ? &A2 : nullptr, rank ? &B2 : nullptr, N, 2 * rank, a, st);
-  if (rc != QLRT_OK || rank == 0) return rc;
-  if (diag & 1) return side && !gemm::join_side(sctx, st) ? QLRT_ERR_CUDA : QLRT_OK;
+  if (diag & 1) return side && !defer && !gemm::join_side(sctx, st) ? QLRT_ERR_CUDA : QLRT_OK;
   cudaStream_t aux = side ? side : st;
   {
     // dl2^T[N, r] = dY^T (Ts_hi + Ts_lo): A = dY (MN-major [m][N]), B = [Ts_hi | Ts_lo]
     // (MN-major [m][2r]); the pair is folded in the epilogue, stored transposed
     // into dl2[r][N] (no split-K: the workspace belongs to dl1)
-    Operand A{dy, N, 1}, B{ts, 2 * rank, 1};
-    rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, N, 2 * rank, m, 1.0f, dl2, N, 1, 1,
-                     nullptr, 0, aux, rank);
+    Operand A{dy, N, 1}, B2t{ts, 2 * rank, 1};
+    rc = gemm::plain(bn_g, A, B2t, N, 2 * rank, m, 1.0f, dl2, N, 1, 1, nullptr, 0, aux, rank, 0, nullptr, 0, 0,
+                     side_cap);
     if (rc != QLRT_OK) return rc;
   }
   {
     // dl1[K, r] = Xa^T (dT_hi + dT_lo): A = Xa (MN-major [m][K]), B = [dT_hi | dT_lo] (MN-major [m][2r])
-    Operand A{x, K, 1}, B{dt_out, 2 * rank, 1};
     // (on the side stream it runs beside the fused dX grid, which owns the
-    // stream-K region: no stream-K for it there)
-    rc = gemm::plain(2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256), A, B, K, 2 * rank, m, 1.0f, dl1, rank, 1, 0,
-                     (float*)workspace, part_bytes, aux, rank, 0, side ? nullptr : &sk);
+    // stream-K region: no stream-K for it there; deferred, its split-K
+    // partials go to the side workspace)
+    Operand A{x, K, 1}, B1{dt_out, 2 * rank, 1};
+    float* pw = defer ? (float*)side_workspace : (float*)workspace;
+    rc = gemm::plain(bn_g, A, B1, K, 2 * rank, m, 1.0f, dl1, rank, 1, 0, pw, part_bytes, aux, rank, 0,
+                     side ? nullptr : &sk, 0, 0, side_cap);
     if (rc != QLRT_OK) return rc;
   }
-  if (side && !gemm::join_side(sctx, st)) return QLRT_ERR_CUDA;
+  if (side && !defer && !gemm::join_side(sctx, st)) return QLRT_ERR_CUDA;
   return rc;
+}
+
+qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_t m, const void* x, const void* ts,
+                                const void* l1, const void* l2, int rank, float s, void* dt_out, void* dx, float* dl1,
+                                float* dl2, void* workspace, void* stream) {
+  return qlrt_nf4_linear_bwd_ex(w, dy, m, x, ts, l1, l2, rank, s, dt_out, dx, dl1, dl2, workspace, nullptr, 0,
+                                stream);
+}
+
+void* qlrt_side_stream(void* stream) {
+  gemm::SideCtx* c = policy(P_SIDE) ? gemm::side_ctx((cudaStream_t)stream) : nullptr;
+  return c ? (void*)c->side : nullptr;
+}
+
+qlrt_status qlrt_side_join(void* stream) {
+  // the caller's stream waits for everything issued on its side stream so far
+  // (a no-op without one: nothing was deferred)
+  if (!policy(P_SIDE)) return QLRT_OK;
+  gemm::SideCtx* c = gemm::side_ctx((cudaStream_t)stream);
+  if (!c) return QLRT_OK;
+  return gemm::join_side(c, (cudaStream_t)stream) ? QLRT_OK : QLRT_ERR_CUDA;
 }
 
 }  // extern "C"

@@ -49,7 +49,7 @@ from .blockquant import quantize
 from .codebooks import get_codebook
 from .paging import Pager, PagerConfig
 from .parallel import GradBucket, LayerReducer
-from .qlora import LoraAdapter, QLinear
+from .qlora import LoraAdapter, QLinear, side_join
 from .training import TrainConfig, _sumsq_scratch
 
 PROJS = ("q", "k", "v", "o", "gate", "up", "down")
@@ -111,18 +111,19 @@ class _QLinearFn(torch.autograd.Function):
     adapter gradients go to the bucket views, not to autograd."""
 
     @staticmethod
-    def forward(ctx, x, anchor, layer, gviews, notify):
+    def forward(ctx, x, anchor, layer, gviews, notify, defer):
         y, cache = layer.forward(x)
-        ctx.layer, ctx.cache, ctx.gviews, ctx.notify = layer, cache, gviews, notify
+        ctx.layer, ctx.cache, ctx.gviews, ctx.notify, ctx.defer = layer, cache, gviews, notify, defer
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        dx, _ = ctx.layer.backward(dy.contiguous(), ctx.cache, grads_out=ctx.gviews)
+        dx, _ = ctx.layer.backward(dy.contiguous(), ctx.cache, grads_out=ctx.gviews,
+                                   defer=ctx.defer() if ctx.defer is not None else None)
         ctx.cache = None
-        if ctx.notify is not None:  # this projection's adapter gradients are in the bucket
+        if ctx.notify is not None:  # this projection's adapter gradients are issued
             ctx.notify()
-        return dx, None, None, None, None
+        return dx, None, None, None, None, None
 
 
 class _RMSNormFn(torch.autograd.Function):
@@ -225,7 +226,7 @@ class LlamaQLoRA:
     def __init__(self, cfg: LlamaConfig, device="cuda", seed: int = 0, train_cfg: TrainConfig | None = None, *,
                  group=None, optimizer: str = "plain", pager_budget_bytes: int | None = None,
                  page_bytes: int = 2 << 20, lookahead: int = 2, checkpoint: bool = False, bucket_layers: int = 4,
-                 wire_dtype=torch.float32, max_steps: int = 100_000):
+                 wire_dtype=torch.float32, max_steps: int = 100_000, defer_lag: int | None = 1):
         if optimizer not in ("plain", "paged"):
             raise ValueError(f"optimizer must be 'plain' or 'paged', got {optimizer!r}")
         self.cfg = cfg
@@ -233,6 +234,15 @@ class LlamaQLoRA:
         self.train_cfg = train_cfg or TrainConfig()
         self.checkpoint = checkpoint
         self.optimizer = optimizer
+        # deferred adapter gradients: each projection's dl2 / dl1 GEMMs stay on
+        # the library's side stream (QLRT_BWD_DEFER) and run beside the next
+        # projections' fused grids; layer li's are waited for (and its bucket
+        # span handed to the all-reduce) once layer li - defer_lag has issued
+        # its backward.  None: every backward joins its own side work.
+        self.defer_lag = defer_lag
+        self._inflight: dict = {}
+        self._side_ev: dict = {}
+        self._ready_q: list = []
         self.lookahead = lookahead
         g = torch.Generator(device=self.dev).manual_seed(seed)
         cb = get_codebook("nf4")
@@ -299,6 +309,7 @@ class LlamaQLoRA:
                 lay[pj + ".g"] = {"adapter0.l1": self.gviews[f"{li}.{pj}.l1"],
                                   "adapter0.l2": self.gviews[f"{li}.{pj}.l2"]}
             lay["notify"] = (lambda li=li: self._proj_done(li))
+            lay["index"] = li
             self.layers.append(lay)
         d = h // cfg.n_heads
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, d, 2, device=self.dev, dtype=torch.float32) / d))
@@ -327,11 +338,48 @@ class LlamaQLoRA:
     # ------------------------------------------------------------------ model
     def _proj_done(self, li: int) -> None:
         self._pending[li] -= 1
-        if self._pending[li] == 0:
+        if self._pending[li] != 0:
+            return
+        if self.defer_lag is None:
             self.reducer.layer_ready(li)
+            return
+        # mark the side work issued through layer li; wait for (and release) the
+        # layers issued defer_lag layers earlier
+        ev = torch.cuda.Event()
+        ev.record(self._side_stream())
+        self._side_ev[li] = ev
+        self._ready_q.append(li)
+        while len(self._ready_q) > self.defer_lag:
+            self._land(self._ready_q.pop(0))
+
+    def _land(self, li: int) -> None:
+        torch.cuda.current_stream().wait_event(self._side_ev.pop(li))
+        self._inflight.pop(li, None)
+        self.reducer.layer_ready(li)
+
+    def _land_all(self) -> None:
+        """Wait for every deferred adapter-gradient GEMM (end of backward)."""
+        if self.defer_lag is None:
+            return
+        side_join()
+        for li in self._ready_q:
+            self._side_ev.pop(li, None)
+            self._inflight.pop(li, None)
+            self.reducer.layer_ready(li)
+        self._ready_q = []
+        self._inflight.clear()
+
+    def _side_stream(self) -> torch.cuda.ExternalStream:
+        cur = torch.cuda.current_stream()
+        h = lib().qlrt_side_stream(cur.cuda_stream)
+        if not h:
+            raise RuntimeError("deferred adapter gradients need the library's side streams (QLRT_SIDE=1)")
+        return torch.cuda.ExternalStream(h)
 
     def _lin(self, x, lay, pj, anchor):
-        return _QLinearFn.apply(x, anchor, lay[pj], lay[pj + ".g"], lay["notify"])
+        li = lay["index"]
+        defer = None if self.defer_lag is None else (lambda li=li: self._inflight.setdefault(li, []))
+        return _QLinearFn.apply(x, anchor, lay[pj], lay[pj + ".g"], lay["notify"], defer)
 
     def _layer(self, x, li, anchor):
         cfg = self.cfg
@@ -377,9 +425,11 @@ class LlamaQLoRA:
         """Loss, backward with the overlapped adapter-gradient all-reduce, and
         the global fp64 sum of squares for the clip (capturable: no host sync)."""
         self._pending = [len(PROJS)] * self.cfg.n_layers
+        self._ready_q, self._side_ev = [], {}
         self.reducer.reset()
         loss = self.loss(tokens, targets)
         loss.backward()
+        self._land_all()
         self.reducer.finish()
         # step t + 1's Adam constants from the table (device-side counter)
         self.hyper.copy_(self.hyper_table.index_select(0, self.t_dev).view(-1))

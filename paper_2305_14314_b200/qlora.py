@@ -292,13 +292,29 @@ class QLinear:
                  "consts": consts}
         return y.reshape(*lead, self.out_dim), cache
 
-    def backward(self, d_y, cache: dict[str, Any], grads_out: dict | None = None
+    def _side_workspace(self, m: int) -> torch.Tensor:
+        """Split-K scratch of the deferred adapter-gradient GEMMs (side stream)."""
+        need = int(lib().qlrt_linear_workspace_bytes(max(m, 1), self.in_dim, self.out_dim, self._rank_total()))
+        dev = torch.cuda.current_device()
+        ws = _SIDE_WS.get(dev)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+            _SIDE_WS[dev] = ws
+        return ws
+
+    def backward(self, d_y, cache: dict[str, Any], grads_out: dict | None = None, defer: list | None = None
                  ) -> tuple[torch.Tensor, dict[str, torch.Tensor]]:
         """dX = dY W^T + sum_i (s_i dY l2_i^T) l1_i^T (masked), dl2_i = s_i t_i^T dY,
         dl1_i = xa_i^T (s_i dY l2_i^T) (qlora.py:150-167).  ``grads_out``
         optionally names fp32 buffers ([in, rank], [rank, out], e.g. views of a
         data-parallel gradient bucket) the fused kernels write the adapter
-        gradients into directly."""
+        gradients into directly.
+
+        ``defer`` (a list): on the fused single-adapter path the adapter-gradient
+        GEMMs stay on the library's side stream (QLRT_BWD_DEFER) and overlap
+        whatever the caller issues next; the tensors they read are appended to
+        ``defer``.  The gradients are valid only after :func:`side_join`, and
+        the caller keeps the list alive until it has called it."""
         d_y = torch.as_tensor(d_y).to(device="cuda", dtype=self.dtype).reshape(-1, self.out_dim).contiguous()
         m = d_y.shape[0]
         n_ad = len(self.adapters)
@@ -334,9 +350,14 @@ class QLinear:
             l1b, l2b = self._operands()
             if single:
                 ad = self.adapters[0]
-                check(lib().qlrt_nf4_linear_bwd(wd, ptr(d_y), m, ptr(xas[0]), ptr(ts), ptr(l1b), ptr(l2b), R,
-                                                float(ad.scaling), ptr(dt), ptr(d_x), ptr(dl1), ptr(dl2), ptr(ws),
-                                                stream_ptr()), "QLinear.backward")
+                defer_ok = defer is not None and (direct or not grads_out)
+                check(lib().qlrt_nf4_linear_bwd_ex(wd, ptr(d_y), m, ptr(xas[0]), ptr(ts), ptr(l1b), ptr(l2b), R,
+                                                   float(ad.scaling), ptr(dt), ptr(d_x), ptr(dl1), ptr(dl2), ptr(ws),
+                                                   ptr(self._side_workspace(m)) if defer_ok else None,
+                                                   _native.QLRT_BWD_DEFER if defer_ok else 0, stream_ptr()),
+                      "QLinear.backward")
+                if defer_ok:
+                    defer.extend((d_y, xas[0], ts, dt, dl1, dl2))
             else:
                 self._pairs([d_y] * n_ad, dt, True)  # dT given: l2 = NULL
                 check(lib().qlrt_nf4_linear_bwd(wd, ptr(d_y), m, ptr(cache["x"]), ptr(ts), ptr(l1b), None, R, 0.0,
@@ -390,6 +411,13 @@ class QLinear:
 
 
 _GEMM_WS: dict = {}
+_SIDE_WS: dict = {}
+
+
+def side_join(stream: torch.cuda.Stream | None = None) -> None:
+    """The (current) stream waits for the adapter-gradient GEMMs deferred by
+    ``QLinear.backward(defer=...)`` on it (qlrt_side_join)."""
+    check(lib().qlrt_side_join(stream_ptr() if stream is None else stream.cuda_stream), "side_join")
 
 
 def _pad2(t: torch.Tensor, r: int, c: int) -> torch.Tensor:
@@ -436,4 +464,4 @@ def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
     return out
 
 
-__all__ = ["LoraAdapter", "lora_init", "QLinear", "PLACEMENTS", "gemm_bf16"]
+__all__ = ["LoraAdapter", "lora_init", "QLinear", "PLACEMENTS", "gemm_bf16", "side_join"]

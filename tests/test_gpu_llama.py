@@ -167,17 +167,46 @@ def test_step_matches_reference_update_and_graph_replay(cuda):
     assert torch.equal(gl, el)
 
 
-def test_grad_groups_launch_as_backward_reaches_them(cuda):
+@pytest.mark.parametrize("lag", [None, 1, 2])
+def test_grad_groups_launch_as_backward_reaches_them(lag, cuda):
     """The overlapped reducer launches each layer group's all-reduce from
-    inside the backward, last group first (before the backward returns)."""
+    inside the backward, last group first (before the backward returns); with
+    deferred adapter gradients a layer's group launches once the backward is
+    ``lag`` layers further, the rest when the backward lands."""
     from paper_2305_14314_b200.llama import LlamaConfig, LlamaQLoRA
-    m = LlamaQLoRA(LlamaConfig.tiny(n_layers=4), seed=0, bucket_layers=1)
+    m = LlamaQLoRA(LlamaConfig.tiny(n_layers=4), seed=0, bucket_layers=1, defer_lag=lag)
     g = torch.Generator(device="cuda").manual_seed(0)
     tok = torch.randint(0, 512, (2, 64), device="cuda", generator=g)
     m._pending = [7] * 4
     m.reducer.reset()
     m.loss(tok, tok).backward()
+    assert m.reducer.launched == [3, 2, 1, 0][: 4 - (lag or 0)]
+    m._land_all()
     assert m.reducer.launched == [3, 2, 1, 0]
+
+
+@pytest.mark.parametrize("lag", [1, 3])
+def test_deferred_adapter_grads_equal_joined(lag, cuda):
+    """QLRT_BWD_DEFER moves only the completion point of dl2 / dl1 (side
+    stream, waited for ``lag`` layers later): loss and every adapter gradient
+    bit-identical to joining inside each projection's backward."""
+    from paper_2305_14314_b200.llama import LlamaConfig, LlamaQLoRA
+    cfg = LlamaConfig.tiny(n_layers=4, hidden=512, ffn=1024, rank=64)
+    a = LlamaQLoRA(cfg, seed=3, defer_lag=None)
+    b = LlamaQLoRA(cfg, seed=3, defer_lag=lag)
+    for mdl in (a, b):
+        for n, p in mdl.params.items():
+            if n.endswith(".l2"):
+                p.copy_(torch.randn(p.shape, device="cuda", generator=torch.Generator(device="cuda").manual_seed(4)) * 0.05)
+        mdl.shadow_flat.copy_(mdl.params_flat)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    tok = torch.randint(0, 512, (2, 64), device="cuda", generator=g)
+    la = a.forward_backward(tok, tok)
+    lb = b.forward_backward(tok, tok)
+    torch.cuda.synchronize()
+    assert torch.equal(la, lb)
+    assert torch.equal(a.bucket.flat, b.bucket.flat)
+    assert b._inflight == {} and b._ready_q == []
 
 
 def _paged_pair(budget_layers, page_bytes):

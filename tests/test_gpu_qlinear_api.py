@@ -122,3 +122,30 @@ def test_adam_updates_reach_the_kernels(qb, cuda):
         assert torch.equal(lin.backward(dy, c_now)[1]["adapter0.l1"], fresh.backward(dy, c_fresh)[1]["adapter0.l1"])
     assert not torch.equal(y_now, y0)
     assert float(lin.adapters[0].l2.abs().max()) > 0
+
+
+@pytest.mark.parametrize("k,n", [(4096, 11008), (1024, 704)])
+def test_deferred_backward_equals_joined(k, n, qb, cuda):
+    """QLinear.backward(defer=[...]) leaves dl2 / dl1 on the side stream
+    (QLRT_BWD_DEFER); after side_join every output is bit-identical to the
+    joined backward, and the inputs the side work reads are handed back."""
+    g = torch.Generator(device="cuda").manual_seed(7)
+    m, r = 512, 64
+    w = torch.randn(k, n, device="cuda", generator=g) * 0.02
+    q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)
+    l1 = (torch.randn(k, r, device="cuda", generator=g) / 8).bfloat16().float()
+    l2 = (torch.randn(r, n, device="cuda", generator=g) * 0.01).bfloat16().float()
+    lin = qb.QLinear(q, [qb.LoraAdapter(r, 16.0, l1, l2)])
+    x = torch.randn(m, k, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(m, n, device="cuda", generator=g).bfloat16()
+    y, cache = lin.forward(x)
+    dx0, g0 = lin.backward(dy, cache)
+    g0 = {kk: v.clone() for kk, v in g0.items()}
+    keep: list = []
+    dx1, g1 = lin.backward(dy, cache, defer=keep)
+    qb.side_join()
+    torch.cuda.synchronize()
+    assert len(keep) == 6
+    assert torch.equal(dx0, dx1)
+    for kk in g0:
+        assert torch.equal(g0[kk], g1[kk]), kk

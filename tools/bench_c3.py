@@ -12,11 +12,11 @@ import torch  # noqa: E402
 from paper_2305_14314_b200.llama import LlamaConfig, LlamaQLoRA  # noqa: E402
 
 
-def run(model_name="7b", layers=None, batch=4, steps=10, warmup=3, graph=True):
+def run(model_name="7b", layers=None, batch=4, steps=10, warmup=3, graph=True, lag=1):
     mk = {"7b": LlamaConfig.llama7b, "33b": LlamaConfig.llama33b, "tiny": LlamaConfig.tiny}[model_name]
     cfg = mk(**({"n_layers": layers} if layers else {}))
     t0 = time.time()
-    m = LlamaQLoRA(cfg, seed=0)
+    m = LlamaQLoRA(cfg, seed=0, defer_lag=lag)
     build_s = time.time() - t0
     g = torch.Generator(device="cuda").manual_seed(0)
     tok = torch.randint(0, cfg.vocab, (batch, cfg.seq), device="cuda", generator=g)
@@ -62,5 +62,7 @@ if __name__ == "__main__":
     ap.add_argument("--batch", type=int, default=4)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--lag", default="1", help="deferred adapter-gradient lag in layers, or 'none'")
     a = ap.parse_args()
-    print(json.dumps(run(a.model, a.layers, a.batch, a.steps, graph=not a.no_graph)))
+    print(json.dumps(run(a.model, a.layers, a.batch, a.steps, graph=not a.no_graph,
+                          lag=None if a.lag == "none" else int(a.lag))))

@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(TPB, 2)
   if (rank > 0) {
     for (int j = t; j < rank; j += TPB) {
       float a = 0.0f;
+#pragma unroll 8
       for (int zz = 0; zz < zt; ++zz) a += __ldcg(tpart + (int64_t)zz * rank + j);
       tsh[j] = s * a;
     }
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(TPB, 2)
   }
   if (!col_live) return;
   float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
   for (int zz = 0; zz < zc; ++zz) {
     const float4* p = reinterpret_cast<const float4*>(part + (int64_t)zz * N + col);
     const float4 a = __ldcg(p), b = __ldcg(p + 1);
@@ -244,6 +246,7 @@ __global__ void __launch_bounds__(TPB, 2)
   }
   if (rank > 0) {
     float l[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
     for (int j = 0; j < rank; ++j) {
       const uint4 u = __ldg(reinterpret_cast<const uint4*>(l2 + (int64_t)j * N + col));
       const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
@@ -342,8 +345,9 @@ __global__ void __launch_bounds__(TPB) lora_t_kernel(const __nv_bfloat16* __rest
 // the main grid waits for it only at its first flush.
 namespace gemv2 {
 
-constexpr int CWARPS = 16;  // lane 0 of warp 0 also issues the TMA loads
-constexpr int TPB = CWARPS * 32;
+constexpr int CWARPS = 16;  // consumer warps
+constexpr int PWARP = CWARPS;  // + one producer warp (TMA + aux copies)
+constexpr int TPB = (CWARPS + 1) * 32;
 constexpr int CTHREADS = CWARPS * 32;
 constexpr int STRIP = 2048;  // columns per strip = 8 TMA boxes of 128 B
 constexpr int ROWS = 16;     // rows per stage (= unit)
@@ -471,32 +475,67 @@ struct Vals16 {
   float v[16];
 };
 
-// last segment of a strip: partials in CTA order + LoRA, bf16 out
+// last segment of a strip: partials in CTA order + LoRA, bf16 out.  Every
+// sum keeps a fixed order (deterministic); the loads of a sum are issued
+// together (unrolled), not one dependent L2 round trip per term.
 __device__ __noinline__ void finalize_strip(int64_t strip, int f, int l, int64_t N, const float* __restrict__ part,
                                             const float* __restrict__ tpart, int zt,
                                             const __nv_bfloat16* __restrict__ l2, int rank, float s,
                                             __nv_bfloat16* __restrict__ y, float* tsh) {
+  __shared__ float tred[8][64];
   const int tid = threadIdx.x;
   __threadfence();
   if (rank > 0) {
-    for (int j = tid; j < rank; j += CTHREADS) {
+    // T[j] = s * sum_z tpart[z][j]: 8 interleaved partial sums per j, combined in order
+    const int jj = tid & 63, q = tid >> 6;
+    for (int j0 = 0; j0 < rank; j0 += 64) {
+      const int j = j0 + jj;
       float a = 0.0f;
-      for (int zz = 0; zz < zt; ++zz) a += __ldcg(tpart + (int64_t)zz * rank + j);
-      tsh[j] = s * a;
+      if (j < rank) {
+#pragma unroll 4
+        for (int zz = q; zz < zt; zz += 8) a += __ldcg(tpart + (int64_t)zz * rank + j);
+      }
+      tred[q][jj] = a;
+      cbar();
+      if (tid < 64 && j0 + tid < rank) {
+        float t = 0.0f;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) t += tred[g][tid];
+        tsh[j0 + tid] = s * t;
+      }
+      cbar();
     }
   }
-  cbar();
-  for (int c = tid; c < STRIP; c += CTHREADS) {
-    const int64_t col = strip * STRIP + c;
-    if (col >= N) break;
-    float o = 0.0f;
-    for (int i = f; i <= l; ++i) o += __ldcg(part + (int64_t)(i + strip) * STRIP + c);
-    if (rank > 0) {
-      float la = 0.0f;
-      for (int j = 0; j < rank; ++j) la = fmaf(tsh[j], __bfloat162float(l2[(int64_t)j * N + col]), la);
-      o += la;
+  // 4 consecutive columns per thread (STRIP = 4 * CTHREADS)
+  const int c = 4 * tid;
+  const int64_t col = strip * STRIP + c;
+  if (col < N) {  // N % 64 == 0: 4-column groups are all-in or all-out
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    const float* pp = part + (int64_t)(f + strip) * STRIP + c;
+#pragma unroll 16
+    for (int i = f; i <= l; ++i, pp += STRIP) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(pp));
+      o[0] += v.x; o[1] += v.y; o[2] += v.z; o[3] += v.w;
     }
-    y[col] = __float2bfloat16_rn(o);
+    if (rank > 0) {
+      float la[4] = {0.f, 0.f, 0.f, 0.f};
+      const __nv_bfloat16* lp = l2 + col;
+#pragma unroll 16
+      for (int j = 0; j < rank; ++j, lp += N) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(lp));
+        const float tj = tsh[j];
+        la[0] = fmaf(tj, __uint_as_float(u.x << 16), la[0]);
+        la[1] = fmaf(tj, __uint_as_float(u.x & 0xFFFF0000u), la[1]);
+        la[2] = fmaf(tj, __uint_as_float(u.y << 16), la[2]);
+        la[3] = fmaf(tj, __uint_as_float(u.y & 0xFFFF0000u), la[3]);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o[e] += la[e];
+    }
+    uint2 out;
+    out.x = pack_bf16x2(o[0], o[1]);
+    out.y = pack_bf16x2(o[2], o[3]);
+    *reinterpret_cast<uint2*>(y + col) = out;
   }
   cbar();
 }
@@ -582,13 +621,19 @@ __global__ void __launch_bounds__(TPB, 1)
       ++ps;
     }
   };
-  if (wid == 0) {
+  if (wid == PWARP) {
     if (lane == 0) ptx::prefetch_tmap(&tm_codes);
-    for (int i = 0; i < NST && i < nunits; ++i) issue(i);
+    for (int i = 0; i < nunits; ++i) {
+      const int sl = i % NST;
+      if (i >= NST) ptx::mbar_wait(&empty[sl], (uint32_t)((i / NST) - 1) & 1u);
+      issue(sl);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
   }
 
   // ---- table: entry e = {fp16 v(e & 15), fp16 v(e >> 4)} in every lane's column
-  for (int q = tid; q < 256 * 32; q += TPB) {
+  for (int q = tid; q < 256 * 32; q += CTHREADS) {
     const int e = q >> 5, l = q & 31;
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(tab + (uint32_t)e * 256u + (uint32_t)l * 4u),
                  "r"(v16[e & 15] | (v16[e >> 4] << 16)));
@@ -605,14 +650,14 @@ __global__ void __launch_bounds__(TPB, 1)
     for (int64_t sg = s0; sg <= s1; ++sg) {
       const int64_t ra = sg == s0 ? (ub - s0 * chunks) * ROWS : 0;
       const int64_t rb = sg == s1 ? (ue - s1 * chunks) * ROWS : K;
-      for (int64_t k = ra + tid; k < rb; k += TPB) {
+      for (int64_t k = ra + tid; k < rb; k += CTHREADS) {
         const unsigned v = __ldg(x + k) & 0x7FFFu;
         mx = v > mx ? v : mx;
       }
       const int64_t ia = (ra * nbr + sg * 32) >> bs2_shift;
       int64_t ib = (((rb - 1) * nbr + sg * 32 + 31) >> bs2_shift) + 1;
       ib = ib < n2 ? ib : n2;
-      for (int64_t i = ia + tid; i < ib; i += TPB) {
+      for (int64_t i = ia + tid; i < ib; i += CTHREADS) {
         const unsigned v = __float_as_uint(__ldg(c1 + i)) & 0x7FFFFFFFu;
         mc = v > mc ? v : mc;
       }
@@ -627,7 +672,7 @@ __global__ void __launch_bounds__(TPB, 1)
       red_x[wid] = mx;
       red_c[wid] = mc;
     }
-    __syncthreads();  // (also: the table is complete)
+    cbar();  // (also: the table is complete)
     if (tid == 0) {
       for (int w = 1; w < CWARPS; ++w) {
         mx = red_x[w] > mx ? red_x[w] : mx;
@@ -642,7 +687,7 @@ __global__ void __launch_bounds__(TPB, 1)
       scales[0] = ldexpf(1.0f, -e);
       scales[1] = ldexpf(1.0f, e);
     }
-    __syncthreads();
+    cbar();
   }
   const float sc = scales[0], unsc = scales[1];
 
@@ -749,10 +794,6 @@ __global__ void __launch_bounds__(TPB, 1)
     const uint32_t b1 = g < 4 ? __byte_perm(v2, v3, bsel) : 0u;
     // (the shuffles used every lane's stage bytes: release the slot)
     if (lane == 0) ptx::mbar_arrive(&empty[sl]);
-    if (wid == 0 && i + NST < nunits) {  // warp 0 refills the slot once every warp has read it
-      ptx::mbar_wait(&empty[sl], par);
-      issue(sl);
-    }
     if (++sl == NST) {
       sl = 0;
       par ^= 1u;

@@ -95,11 +95,12 @@ class _ManagedBuffer:
 class PagerConfig:
     """Budget of device-resident bytes (paging.py:25-39).  ``backing_path`` is
     accepted for API parity and unused: the backing store is host memory.
-    The default page is the GPU's 2 MiB unified-memory migration unit."""
+    The default page is the reference's 4 KiB; large optimizer states use
+    the GPU's 2 MiB unified-memory migration unit (the LLaMA harness)."""
 
     budget_bytes: int
     backing_path: str | None = None
-    page_bytes: int = 2 << 20
+    page_bytes: int = 4096
 
     def validate(self) -> None:
         if self.page_bytes < 1:

@@ -230,13 +230,71 @@ class QLinear:
             masks.append((draw >= ad.dropout_p).to(torch.float32) / keep)
         return masks
 
+    # -- exact-precision path (float32 / float64 layers) ---------------------
+    def _exact(self) -> bool:
+        return self.dtype in (torch.float32, torch.float64)
+
+    def _forward_exact(self, x, train: bool, rng) -> tuple[torch.Tensor, dict[str, Any]]:
+        """The reference's own op order at its precision (qlora.py:117-148): W
+        = dequantize(q) (float64, the bit-exact kernel) cast to the layer
+        dtype, then cuBLAS GEMMs in that dtype (TF32 off).  The toy layers
+        (16 x 16, 2 x 16, ...) are far below any tile of the fused kernels;
+        this is the path the GPU ToyModel / train_toy gates run through."""
+        if torch.backends.cuda.matmul.allow_tf32:
+            raise RuntimeError("exact-precision QLinear needs torch.backends.cuda.matmul.allow_tf32 = False")
+        dt = self.dtype
+        x = torch.as_tensor(x).to(device="cuda", dtype=dt)
+        if isinstance(self.base, BlockQuantized):
+            w = dequantize(self.base, torch.float64).to(dt)
+        else:
+            w = torch.as_tensor(self.base).to(device="cuda", dtype=dt)
+        y = x @ w
+        branches = []
+        for ad in self.adapters:
+            xa, mask = x, None
+            if train and ad.dropout_p > 0.0:
+                if rng is None:
+                    raise ValueError("dropout needs an rng in train mode")
+                keep = 1.0 - ad.dropout_p
+                if isinstance(rng, torch.Generator):
+                    draw = torch.rand(x.shape, generator=rng, device=x.device, dtype=torch.float64)
+                else:  # numpy Generator: the reference's exact mask (qlora.py:140-142)
+                    draw = torch.from_numpy(rng.random(tuple(x.shape))).to(x.device)
+                mask = (draw >= ad.dropout_p).to(dt) / keep
+                xa = x * mask
+            t = xa @ ad.l1.to(dt)
+            y = y + ad.scaling * (t @ ad.l2.to(dt))
+            branches.append({"xa": xa, "t": t, "mask": mask})
+        return y, {"x": x, "w": w, "branches": branches, "exact": True}
+
+    def _backward_exact(self, d_y, cache) -> tuple[torch.Tensor, dict[str, torch.Tensor]]:
+        """qlora.py:150-167 at the layer precision."""
+        dt = self.dtype
+        d_y = torch.as_tensor(d_y).to(device="cuda", dtype=dt)
+        d_x = d_y @ cache["w"].T
+        grads: dict[str, torch.Tensor] = {}
+        for i, (ad, br) in enumerate(zip(self.adapters, cache["branches"])):
+            s = ad.scaling
+            l1, l2 = ad.l1.to(dt), ad.l2.to(dt)
+            d_t = s * (d_y @ l2.T)
+            grads[f"adapter{i}.l2"] = s * (br["t"].T @ d_y)
+            grads[f"adapter{i}.l1"] = br["xa"].T @ d_t
+            d_xa = d_t @ l1.T
+            if br["mask"] is not None:
+                d_xa = d_xa * br["mask"]
+            d_x = d_x + d_xa
+        return d_x, grads
+
     # -- forward / backward -------------------------------------------------
     def forward(self, x, train: bool = False, rng=None) -> tuple[torch.Tensor, dict[str, Any]]:
         """y = x W + sum_i s_i (xa_i l1_i) l2_i (qlora.py:124-148).  One
         adapter without dropout is the fully fused path (Ts and the NF4 GEMM
         with the adapter term in its accumulator, all in the C ABI); several
         adapters or dropout compute the Ts pairs here and still join the same
-        accumulator; M = 1 runs the HBM-streaming GEMV."""
+        accumulator; M = 1 runs the HBM-streaming GEMV.  A float32 / float64
+        layer computes at that precision (``_forward_exact``)."""
+        if self._exact():
+            return self._forward_exact(x, train, rng)
         x = torch.as_tensor(x).to(device="cuda", dtype=self.dtype).contiguous()
         lead = x.shape[:-1]
         x2 = x.reshape(-1, self.in_dim)
@@ -315,6 +373,8 @@ class QLinear:
         whatever the caller issues next; the tensors they read are appended to
         ``defer``.  The gradients are valid only after :func:`side_join`, and
         the caller keeps the list alive until it has called it."""
+        if cache.get("exact"):
+            return self._backward_exact(d_y, cache)
         d_y = torch.as_tensor(d_y).to(device="cuda", dtype=self.dtype).reshape(-1, self.out_dim).contiguous()
         m = d_y.shape[0]
         n_ad = len(self.adapters)

@@ -52,7 +52,7 @@ def test_paged_equals_plain(budget_slabs, qb, cuda):
         if paged:
             slab = 2 * max(int(np.prod(s)) for s in shapes.values()) * 4
             pb = 2 << 20
-            pager = qb.pager_open(qb.PagerConfig(budget_bytes=budget_slabs * ((slab + pb - 1) // pb) * pb))
+            pager = qb.pager_open(qb.PagerConfig(budget_bytes=budget_slabs * ((slab + pb - 1) // pb) * pb, page_bytes=pb))
             store = qb.PagedMomentStore(pager)
         else:
             store = qb.PlainMomentStore()

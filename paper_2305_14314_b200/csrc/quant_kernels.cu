@@ -285,9 +285,12 @@ __global__ void __launch_bounds__(256, QLRT_Q_MINB) quantize64_stream_kernel(con
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  float nv[8], nv2[8];  // the next two groups' values in flight
-  if (g < n_groups) load8_stream<T>(x, g * 8, nv);
-  if (g + stride < n_groups) load8_stream<T>(x, (g + stride) * 8, nv2);
+  // two group buffers in flight, used alternately (no register rotation);
+  // a lane past the end keeps stale (finite or ignored) values: it reports
+  // nothing and stores nothing, and its 8-lane group only shuffles with itself
+  float va[8], vb[8];
+  if (g < n_groups) load8_stream<T>(x, g * 8, va);
+  if (g + stride < n_groups) load8_stream<T>(x, (g + stride) * 8, vb);
   build_bin_tables(t, cb);
   const uint32_t tab = (uint32_t)__cvta_generic_to_shared(ptab);
   build_private_bins(tab, cb, pent);
@@ -295,45 +298,36 @@ __global__ void __launch_bounds__(256, QLRT_Q_MINB) quantize64_stream_kernel(con
   __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (the DQ chunk sums wait for our completion)
   const unsigned pad = (unsigned)cb.pad_code;
-  // n_groups % 8 == 0 and stride % 8 == 0: 8-lane groups are all-in or all-out,
-  // and the trip count is warp-uniform (the shuffles need every lane)
-  for (int64_t gb = g - lane; gb < n_groups; gb += stride, g += stride) {
-    const bool act = g < n_groups;
-    float v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      v[j] = act ? nv[j] : 0.0f;
-      nv[j] = nv2[j];
-    }
-    if (g + 2 * stride < n_groups) load8_stream<T>(x, (g + 2 * stride) * 8, nv2);
+  auto body = [&](const float (&v)[8], int64_t gg) {
+    const bool act = gg < n_groups;
     unsigned mb = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) mb = max(mb, __float_as_uint(v[j]) & 0x7FFFFFFFu);
-    if (mb >= 0x7F800000u) {  // inf / NaN: first bad flat index
+    if (act && mb >= 0x7F800000u) {  // inf / NaN: first bad flat index
       unsigned long long bad = ~0ull;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if ((__float_as_uint(v[j]) & 0x7FFFFFFFu) >= 0x7F800000u) bad = min(bad, (unsigned long long)(g * 8 + j));
+        if ((__float_as_uint(v[j]) & 0x7FFFFFFFu) >= 0x7F800000u) bad = min(bad, (unsigned long long)(gg * 8 + j));
       atomicMin(first_bad, bad);
     }
     mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 1));
     mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 2));
     mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, 4));
-    if (!act) continue;
+    if (!act) return;
     const float c = __uint_as_float(mb);
     uint32_t word;
     if (c > 0.0f) {
       const float r = __frcp_rn(c);
       bool bad = !(r <= 3.402823466e38f);  // subnormal c: 1/c overflows -> exact path
       word = 0;
-      pbin_acc<0>((float)v[0], r, lanecol, word, bad);
-      pbin_acc<1>((float)v[1], r, lanecol, word, bad);
-      pbin_acc<2>((float)v[2], r, lanecol, word, bad);
-      pbin_acc<3>((float)v[3], r, lanecol, word, bad);
-      pbin_acc<4>((float)v[4], r, lanecol, word, bad);
-      pbin_acc<5>((float)v[5], r, lanecol, word, bad);
-      pbin_acc<6>((float)v[6], r, lanecol, word, bad);
-      pbin_acc<7>((float)v[7], r, lanecol, word, bad);
+      pbin_acc<0>(v[0], r, lanecol, word, bad);
+      pbin_acc<1>(v[1], r, lanecol, word, bad);
+      pbin_acc<2>(v[2], r, lanecol, word, bad);
+      pbin_acc<3>(v[3], r, lanecol, word, bad);
+      pbin_acc<4>(v[4], r, lanecol, word, bad);
+      pbin_acc<5>(v[5], r, lanecol, word, bad);
+      pbin_acc<6>(v[6], r, lanecol, word, bad);
+      pbin_acc<7>(v[7], r, lanecol, word, bad);
       if (bad) {
         const bool fast_ok = r <= 3.402823466e38f;
         word = 0;
@@ -344,8 +338,17 @@ __global__ void __launch_bounds__(256, QLRT_Q_MINB) quantize64_stream_kernel(con
     } else {
       word = pad * 0x11111111u;
     }
-    codes[g] = word;
-    if ((threadIdx.x & 7) == 0) absmax[g >> 3] = c;
+    codes[gg] = word;
+    if ((threadIdx.x & 7) == 0) absmax[gg >> 3] = c;
+  };
+  // n_groups % 8 == 0 and stride % 8 == 0: 8-lane groups are all-in or all-out,
+  // and the trip count is warp-uniform (the shuffles need every lane)
+  for (int64_t gb = g - lane; gb < n_groups; gb += 2 * stride, g += 2 * stride) {
+    body(va, g);
+    if (g + 2 * stride < n_groups) load8_stream<T>(x, (g + 2 * stride) * 8, va);
+    if (gb + stride >= n_groups) break;
+    body(vb, g + stride);
+    if (g + 3 * stride < n_groups) load8_stream<T>(x, (g + 3 * stride) * 8, vb);
   }
 }
 
@@ -862,6 +865,11 @@ __global__ void __launch_bounds__(DQB_TPB, QLRT_DQB_MINB) dequant64_bf16_kernel(
   const int64_t w = (int64_t)blockIdx.x * (DQB_TPB / 32) + (threadIdx.x >> 5);
   const int64_t s_beg = n_steps * w / n_warps, s_end = n_steps * (w + 1) / n_warps;
 
+  // PDL: the next launch may start its prologue as this grid drains; our
+  // reads wait for the predecessor grid (a no-op without the attribute)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (DQ) fp8_lut[threadIdx.x] = fp8_decode_fast(threadIdx.x, sp);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   uint32_t cw[8];
   float craw = 0.0f;   // absmax, or c1 of the block (DQ)
   uint32_t dqb = 0;    // DQ code byte
@@ -880,11 +888,8 @@ __global__ void __launch_bounds__(DQB_TPB, QLRT_DQB_MINB) dequant64_bf16_kernel(
       for (int i = 0; i < 8; ++i) cw[i] = 0u;
     }
   };
-  if (s_beg < s_end) fetch(s_beg);  // first loads in flight before the table build
-  if (DQ) {
-    fp8_lut[threadIdx.x] = fp8_decode_fast(threadIdx.x, sp);
-    __syncthreads();
-  }
+  if (s_beg < s_end) fetch(s_beg);
+  if (DQ) __syncthreads();  // (the fp8 table)
   const double mu_d = DQ ? (double)__ldg(mu) : 0.0;
   for (int64_t s = s_beg; s < s_end; ++s) {
     uint32_t cur[8];
@@ -1017,12 +1022,19 @@ qlrt_status qlrt_quantize4(const void* x, int x_dtype, int64_t n, int blocksize,
     const int64_t want = cdiv(n_groups, 256);
     const int grid = (int)(want < (int64_t)kNumSMs * QLRT_Q_MINB ? want : (int64_t)kNumSMs * QLRT_Q_MINB);  // resident
     constexpr int psm = PBIN * 32 * 8;  // private-column bin table
-    if (x_dtype == QLRT_F32)
-      quantize64_stream_kernel<float><<<grid, 256, psm, s>>>((const float*)x, n_groups, *cb, (uint32_t*)codes, absmax,
-                                                            fb);
-    else
-      quantize64_stream_kernel<__nv_bfloat16><<<grid, 256, psm, s>>>((const __nv_bfloat16*)x, n_groups, *cb,
-                                                                    (uint32_t*)codes, absmax, fb);
+    // (no PDL attribute: the first-bad sentinel memset precedes it)
+    cudaLaunchConfig_t cfg{};
+    cfg.stream = s;
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = psm;
+    const cudaError_t e =
+        x_dtype == QLRT_F32
+            ? cudaLaunchKernelEx(&cfg, quantize64_stream_kernel<float>, (const float*)x, n_groups, *cb,
+                                 (uint32_t*)codes, absmax, fb)
+            : cudaLaunchKernelEx(&cfg, quantize64_stream_kernel<__nv_bfloat16>, (const __nv_bfloat16*)x, n_groups,
+                                 *cb, (uint32_t*)codes, absmax, fb);
+    if (e != cudaSuccess) return QLRT_ERR_CUDA;
   } else if (blocksize == 64 && aligned) {
     const int64_t n_groups = nb * 8;
     const int grid = grid_for(n_groups, 256, 8);
@@ -1122,12 +1134,23 @@ qlrt_status qlrt_dequantize4(const uint8_t* codes, int64_t n, int blocksize,
         e_g > 0 ? e_g : (steps > 4 * (int64_t)kNumSMs * QLRT_DQB_MINB * (DQB_TPB / 32) ? 16 : QLRT_DQB_MINB);
     const int g = (int)(ctas < (int64_t)kNumSMs * per_sm ? ctas : (int64_t)kNumSMs * per_sm);
     const int sh = pow2_bs2 ? __builtin_ctz((unsigned)blocksize2) : 0;
-    if (dq_codes)
-      dequant64_bf16_kernel<true><<<g, DQB_TPB, 0, s>>>(codes, n, *cb, absmax, dq_codes, c1, mu, sh, spec,
-                                                        (__nv_bfloat16*)out);
-    else
-      dequant64_bf16_kernel<false><<<g, DQB_TPB, 0, s>>>(codes, n, *cb, absmax, dq_codes, c1, mu, sh, spec,
-                                                         (__nv_bfloat16*)out);
+    // programmatic dependent launch: back-to-back dequantizations overlap one
+    // another's launch and prologue with the predecessor's tail
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = policy(P_PDL) ? 1 : 0;
+    cfg.stream = s;
+    cfg.gridDim = dim3((unsigned)g);
+    cfg.blockDim = dim3(DQB_TPB);
+    const cudaError_t e =
+        dq_codes ? cudaLaunchKernelEx(&cfg, dequant64_bf16_kernel<true>, codes, n, *cb, absmax, dq_codes, c1, mu, sh,
+                                      spec, (__nv_bfloat16*)out)
+                 : cudaLaunchKernelEx(&cfg, dequant64_bf16_kernel<false>, codes, n, *cb, absmax, dq_codes, c1, mu,
+                                      sh, spec, (__nv_bfloat16*)out);
+    if (e != cudaSuccess) return QLRT_ERR_CUDA;
   } else if (blocksize == 64 && aligned) {
     const int g = grid_for(cdiv(n, 64), DQ_TPB, 16);
 #define QLRT_DQ64(O) dequant64_kernel<O><<<g, DQ_TPB, 0, s>>>((const uint4*)codes, n, *cb, absmax, dq_codes, c1, mu, \

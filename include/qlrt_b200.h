@@ -121,6 +121,10 @@ typedef struct {
 size_t qlrt_nf4_constants_bytes(int64_t k_in, int64_t n_out);
 qlrt_status qlrt_nf4_constants(const qlrt_nf4_weight* w, float* out, void* stream);
 
+/* One weight's block constants into columns [0, n_out/64) of rows of `pitch`
+ * floats: a member's slice of a concatenated (grouped) weight's cache. */
+qlrt_status qlrt_nf4_constants_into(const qlrt_nf4_weight* w, float* out, int64_t pitch, void* stream);
+
 /* Workspace bytes for the linear entry points (split-K partial sums). */
 /* (The workspace also holds the stream-K partial tiles and flags: the caller
  * zero-fills a new workspace once -- the flags must start at 0, and every
@@ -172,6 +176,27 @@ qlrt_status qlrt_side_join(void* stream);
  * for callers that order against part of the deferred work with their own
  * events. */
 void* qlrt_side_stream(void* stream);
+
+/* Sibling projections that share their input (q | k | v, gate | up) as one
+ * call: w describes W_cat = [W_0 | ... | W_{groups-1}] (codes concatenated
+ * along N, n_out = groups N_g, N_g % 256 == 0; every member quantized on
+ * its own -- the reference's per-layer QLinear -- its constants placed by
+ * qlrt_nf4_constants_into into w->consts, which is required); one adapter
+ * of rank r (r % 64 == 0) per member, l1_cat [K][groups r], l2_cat
+ * [r][n_out] bf16.  Ts_cat / dT_cat [M][groups 2r] hold each member's bf16
+ * [hi | lo] pair; Y, dY [M][n_out]; dl1 [K][groups r], dl2 [r][n_out] fp32.
+ * Same math per member as qlrt_nf4_linear_fwd / _bwd_ex (qlora.py:124-167):
+ * Ts for all members is one GEMM, the fused NF4 GEMM covers every member
+ * (the backward sums dX over them in its accumulator), dl1 is one GEMM. */
+qlrt_status qlrt_nf4_linear_group_fwd(const qlrt_nf4_weight* w, int groups, const void* x,
+                                      int64_t m, const void* l1, const void* l2, int rank,
+                                      float s, void* ts_out, void* y, void* workspace,
+                                      void* stream);
+qlrt_status qlrt_nf4_linear_group_bwd(const qlrt_nf4_weight* w, int groups, const void* dy,
+                                      int64_t m, const void* x, const void* ts, const void* l1,
+                                      const void* l2, int rank, float s, void* dt_out, void* dx,
+                                      float* dl1, float* dl2, void* workspace,
+                                      void* side_workspace, int flags, void* stream);
 
 /* batch-1 GEMV variant of forward (M = 1), HBM-bound on the packed codes:
  *   y[N] = x[K] W + s (xa l1) l2         fp32 accumulate, bf16 out
@@ -243,6 +268,15 @@ qlrt_status qlrt_swiglu_bwd(const void* g, const void* u, const void* dout, void
  * [seq][d/2] (cos, sin); inverse = 1 rotates back (the backward). */
 qlrt_status qlrt_rope(const void* x, void* y, const void* cos_sin, int64_t rows, int heads, int d,
                       int seq, int inverse, void* stream);
+/* RoPE with row pitches (elements): q / k read from or written to a column
+ * slice of the concatenated q | k | v projection. */
+qlrt_status qlrt_rope_strided(const void* x, int64_t ldx, void* y, int64_t ldy, const void* cos_sin,
+                              int64_t rows, int heads, int d, int seq, int inverse, void* stream);
+/* SwiGLU over a concatenated [gate | up] projection (rows x 2 cols): out =
+ * silu(g) * u [rows][cols]; backward writes d[gate | up]. */
+qlrt_status qlrt_swiglu_cat_fwd(const void* gu, void* out, int64_t rows, int64_t cols, void* stream);
+qlrt_status qlrt_swiglu_cat_bwd(const void* gu, const void* dout, void* dgu, int64_t rows, int64_t cols,
+                                void* stream);
 
 /* Launch-policy switches of the engine (the measured A/B knobs DESIGN.md
  * lists: QLRT_PAIR, QLRT_STREAMK, QLRT_OVERLAP, QLRT_OVERLAP_BWD, ...).  They

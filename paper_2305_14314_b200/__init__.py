@@ -31,7 +31,7 @@ from .errors import (BadMagicError, ChecksumMismatchError, ContainerError, Corru
                      TrainingDivergedError, TruncatedFileError, UnsupportedVersionError)
 from .paging import Pager, PagerConfig, Slab, pager_open
 from .parallel import GradBucket, allreduce_mean
-from .qlora import PLACEMENTS, LoraAdapter, QLinear, gemm_bf16, lora_init, side_join
+from .qlora import PLACEMENTS, LoraAdapter, QLinear, QLinearGroup, gemm_bf16, lora_init, side_join
 from .training import AdamOptimizer, PagedMomentStore, PlainMomentStore, TrainConfig, clip_global_norm
 from . import toy
 

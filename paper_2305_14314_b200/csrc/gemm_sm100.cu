@@ -105,6 +105,11 @@ struct Args {
                         // re-read for K2 = 2 aug_wrap ([l | l] without materialising the pair)
   int cl2;              // plain 1-SM grid launched as 2-CTA clusters (independent CTAs): it
                         // occupies whole SM pairs beside a pair grid instead of fragmenting them
+  // sibling projections concatenated along M (grouped forward): tile rows
+  // [g aug_gn, (g + 1) aug_gn) take their augmented B2 segment at K offset
+  // g aug_gstride (each member's [Ts_hi | Ts_lo] block of Ts_cat)
+  int aug_gn, aug_gstride;
+  int64_t aug_b2k;      // > 0: B2's own K extent (the whole Ts_cat row)
 };
 
 #ifndef QLRT_MERGE_FULL
@@ -286,7 +291,9 @@ __device__ __forceinline__ void store_chunk(const Args& p, const uint32_t (&r)[E
         if (n0 + j < NL) o[j] = __uint_as_float(r[j]) * a;
     }
   } else if (p.out_split) {  // bf16 hi/lo pair: v ~= hi + lo to ~16 mantissa bits
-    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + m * p.ldo + n0;
+    // column n of a member of width out_split -> [hi | lo] block of that member
+    // (n0 % out_split + EC <= out_split: a chunk stays inside one member)
+    __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + m * p.ldo + n0 + (n0 / p.out_split) * p.out_split;
 #pragma unroll
     for (int j = 0; j < EC; ++j) {
       if (n0 + j >= NL) continue;
@@ -503,7 +510,10 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           const int amn = aug ? p.a2_mn : p.a_mn;
           const int bmn = aug ? p.b2_mn : p.b_mn;
           const int k0 = (aug ? (i - nk) : (kb + i)) * BK;
-          const int k0a = (aug && p.aug_wrap) ? k0 % p.aug_wrap : k0;
+          // wrap: A2 holds aug_wrap K lines per group of 2 aug_wrap (hi and lo of
+          // each member's pair multiply the same l rows / columns)
+          const int k0a = (aug && p.aug_wrap) ? (k0 / (2 * p.aug_wrap)) * p.aug_wrap + k0 % p.aug_wrap : k0;
+          const int k0b = (aug && p.aug_gn) ? k0 + ((mt * BMP) / p.aug_gn) * p.aug_gstride : k0;
           const bool a_tma = aug || !NF4;
           if (aug && p.aug_pdl && !aug_ready) {  // B2 = the adapter product of the PDL predecessor
             asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -526,14 +536,14 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           }
           if (bmn) {
 #pragma unroll
-            for (int j = 0; j < (BNC + 63) / 64; ++j) tma(mb, &full[s], b_dst + j * 8192, n_cta + j * 64, k0);
+            for (int j = 0; j < (BNC + 63) / 64; ++j) tma(mb, &full[s], b_dst + j * 8192, n_cta + j * 64, k0b);
           } else if (NUM > 1) {  // one 128-token half of each UMMA's B, at the same offset in both CTAs
 #pragma unroll
             for (int j = 0; j < NUM; ++j)
               if (hh < 0 || hh == j)
-                tma(mb, &full[s], b_dst + j * (L::B_STAGE / NUM), k0, nt * BN + j * UN + (int)rank * (UN / 2));
+                tma(mb, &full[s], b_dst + j * (L::B_STAGE / NUM), k0b, nt * BN + j * UN + (int)rank * (UN / 2));
           } else {
-            tma(mb, &full[s], b_dst, k0, n_cta);
+            tma(mb, &full[s], b_dst, k0b, n_cta);
           }
         }
       }
@@ -1056,19 +1066,21 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
   asm volatile("griddepcontrol.wait;" ::: "memory");  // (PDL launch: the partials are complete)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t total = (int64_t)M * N;
-  const int NO = fold ? fold : N;
+  const int NO = fold ? N / 2 : N;  // fold: members of 2 fold columns [hi | lo] -> fold columns each
   const int64_t total_o = (int64_t)M * NO;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total_o;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = i / NO, n = i - m * NO;
-    const int64_t src = m * N + n;
+    const int64_t src = m * N + (fold ? (n / fold) * 2 * fold + n % fold : n);
     float acc = 0.0f;
     for (int z = 0; z < splits; ++z) {
       acc += ws[(int64_t)z * total + src];
       if (fold) acc += ws[(int64_t)z * total + src + fold];
     }
     acc *= alpha;
-    const int64_t o = out_t ? n * ldo + m : m * ldo + n;
+    // out_split: column n of a member of width out_split -> its [hi | lo] block
+    const int64_t ns = out_split ? n + (n / out_split) * out_split : n;
+    const int64_t o = out_t ? ns * ldo + m : m * ldo + ns;
     if (out_f32) {
       static_cast<float*>(out)[o] = acc;
     } else {
@@ -1084,17 +1096,19 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
 // arithmetic as dq_decompress (doublequant.py:190-195), once per GEMM call.
 __global__ void dq_constants_kernel(const uint8_t* __restrict__ dq_codes, const float* __restrict__ c1,
                                     const float* __restrict__ mu, int64_t rows, int64_t nbr, int64_t kpitch,
-                                    int bs2, qlrt_fp8spec sp, float* __restrict__ out) {
+                                    int64_t ncols, int bs2, qlrt_fp8spec sp, float* __restrict__ out) {
+  // columns [0, ncols) of each row (ncols = kpitch: the padding is zeroed;
+  // ncols = nbr: one member's slice of a concatenated weight's cache)
   const float m = *mu;
-  const int64_t total = rows * kpitch;
+  const int64_t total = rows * ncols;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / kpitch, j = i - r * kpitch;
+    const int64_t r = i / ncols, j = i - r * ncols;
     float c = 0.0f;
     if (j < nbr) {
       const int64_t blk = r * nbr + j;
       c = dq_constant(dq_codes[blk], c1[blk / bs2], m, sp);
     }
-    out[i] = c;
+    out[r * kpitch + j] = c;
   }
 }
 
@@ -1394,11 +1408,12 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   if (!(B.mn ? make_tmap(&tb, B.ptr, N, K, B.ld, 64) : make_tmap(&tb, B.ptr, K, N, B.ld, bbox)))
     return QLRT_ERR_UNSUPPORTED;
   if (K2) {
-    const int64_t K2a = args.aug_wrap ? args.aug_wrap : K2;  // A2's own K extent
-    if (args.aug_wrap && (args.aug_wrap % BK || K2 % args.aug_wrap)) return QLRT_ERR_UNSUPPORTED;
+    const int64_t K2a = args.aug_wrap ? K2 / 2 : K2;  // A2's own K extent
+    if (args.aug_wrap && (args.aug_wrap % BK || K2 % (2 * args.aug_wrap))) return QLRT_ERR_UNSUPPORTED;
+    const int64_t K2b = args.aug_b2k > 0 ? args.aug_b2k : K2;
     if (!(A2->mn ? make_tmap(&ta2, A2->ptr, M, K2a, A2->ld, 64) : make_tmap(&ta2, A2->ptr, K2a, M, A2->ld, BM)))
       return QLRT_ERR_UNSUPPORTED;
-    if (!(B2->mn ? make_tmap(&tb2, B2->ptr, N, K2, B2->ld, 64) : make_tmap(&tb2, B2->ptr, K2, N, B2->ld, bbox)))
+    if (!(B2->mn ? make_tmap(&tb2, B2->ptr, N, K2b, B2->ld, 64) : make_tmap(&tb2, B2->ptr, K2b, N, B2->ld, bbox)))
       return QLRT_ERR_UNSUPPORTED;
   } else {
     ta2 = nf4 ? tb : ta;
@@ -1464,7 +1479,7 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
 }
 
 static qlrt_status reduce(const Args& args, cudaStream_t s) {
-  const int64_t total = (int64_t)args.M * (args.fold ? args.fold : args.N);
+  const int64_t total = (int64_t)args.M * (args.fold ? args.N / 2 : args.N);
   int64_t g = (total + 255) / 256;
   if (g > 148 * 8) g = 148 * 8;
   cudaLaunchConfig_t cfg{};
@@ -1552,7 +1567,7 @@ static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, 
   a.splits = effective_splits(ws ? pick_splits(tiles, kit, M * N * 4, ws_bytes) : 1, (int)kit);
   // fold is applied in the epilogue when one column tile holds both halves
   // and there is no split-K (no reduce launch); otherwise the reduce kernel folds
-  const bool direct_fold = fold != 0 && a.splits == 1 && 2 * fold <= bn && N <= bn;
+  const bool direct_fold = fold != 0 && a.splits == 1 && 2 * fold <= bn && N == 2 * fold;
   a.to_ws = (fold != 0 && !direct_fold) || (out_split && out_t);
   if ((a.to_ws || a.splits > 1) && (!ws || (size_t)(M * N * 4) * a.splits > ws_bytes)) return QLRT_ERR_ARG;
   qlrt_status st = run(bn, A, B, nullptr, nullptr, K, 0, a, s);
@@ -1587,7 +1602,7 @@ static qlrt_status fill_nf4(Args& a, const qlrt_nf4_weight* w, int mode, float* 
   const int64_t total = w->k_in * a.kpitch;
   int64_t g = (total + 255) / 256;
   if (g > 148 * 8) g = 148 * 8;
-  dq_constants_kernel<<<(int)g, 256, 0, st>>>(w->dq_codes, w->c1, w->mu, w->k_in, w->n_out / 64, a.kpitch,
+  dq_constants_kernel<<<(int)g, 256, 0, st>>>(w->dq_codes, w->c1, w->mu, w->k_in, w->n_out / 64, a.kpitch, a.kpitch,
                                              w->blocksize2, w->spec, consts);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
@@ -1672,6 +1687,21 @@ qlrt_status qlrt_nf4_constants(const qlrt_nf4_weight* w, float* out, void* strea
   tmp.consts = nullptr;
   gemm::Args a{};
   return gemm::fill_nf4(a, &tmp, 1, out, (cudaStream_t)stream);
+}
+
+qlrt_status qlrt_nf4_constants_into(const qlrt_nf4_weight* w, float* out, int64_t pitch, void* stream) {
+  // one member's block constants into columns [0, n_out / 64) of rows of
+  // `pitch` floats (out = the member's first column of a concatenated cache)
+  if (!w || !w->dq_codes || !w->c1 || !w->mu || !out || w->n_out % 64 || pitch < w->n_out / 64 ||
+      w->blocksize2 <= 0)
+    return QLRT_ERR_ARG;
+  const int64_t nbr = w->n_out / 64;
+  int64_t g = (w->k_in * nbr + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  gemm::dq_constants_kernel<<<(int)g, 256, 0, (cudaStream_t)stream>>>(w->dq_codes, w->c1, w->mu, w->k_in, nbr, pitch,
+                                                                      nbr, w->blocksize2, w->spec, out);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
 }
 
 size_t qlrt_linear_workspace_bytes(int64_t m, int64_t k_in, int64_t n_out, int rank) {
@@ -1913,6 +1943,123 @@ qlrt_status qlrt_nf4_linear_bwd_ex(const qlrt_nf4_weight* w, const void* dy, int
   }
   if (side && !defer && !gemm::join_side(sctx, st)) return QLRT_ERR_CUDA;
   return rc;
+}
+
+// ---- sibling projections concatenated along N (q | k | v, gate | up) --------
+// W_cat = [W_0 | ... | W_{G-1}] with N_g = n_out / G columns each (N_g % 256
+// == 0: a 256-row tile of the fused GEMM never straddles two members), the
+// block-constant cache w->consts filled per member (column slices), one
+// adapter of rank r (r % 64 == 0) per member: l1_cat [K][G r], l2_cat [r][N].
+// Ts_cat / dT_cat hold each member's bf16 [hi | lo] pair: [m][G 2r].
+static bool group_ok(const qlrt_nf4_weight* w, int groups, int rank) {
+  return gemm::weight_ok(w) && w->consts && groups >= 1 && w->n_out % groups == 0 &&
+         (w->n_out / groups) % 256 == 0 && rank > 0 && rank % 64 == 0;
+}
+
+qlrt_status qlrt_nf4_linear_group_fwd(const qlrt_nf4_weight* w, int groups, const void* x, int64_t m,
+                                      const void* l1, const void* l2, int rank, float s, void* ts_out, void* y,
+                                      void* workspace, void* stream) {
+  if (!group_ok(w, groups, rank) || !x || !y || !l1 || !l2 || !ts_out || !workspace || m <= 0) return QLRT_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t K = w->k_in, N = w->n_out, Ng = N / groups;
+  const int R = groups * rank;
+  const size_t ws_bytes = qlrt_linear_workspace_bytes(m, K, N, R);
+  const size_t part_bytes =
+      ws_bytes - gemm::dbl_bytes(K, N, R) - gemm::sk_bytes() - gemm::align256(gemm::consts_bytes(K, N));
+  gemm::Args sk{};
+  gemm::sk_region(workspace, ws_bytes, K, N, R, sk);
+  qlrt_status rc;
+  // Ts_cat = s X [l1_0 | ... | l1_{G-1}]: one skinny GEMM for every member
+  // (they share X), each member's columns stored as its [hi | lo] pair
+  Operand A{x, K, 0}, B{l1, R, 1};
+  rc = gemm::plain(64, A, B, m, R, K, s, ts_out, 2 * R, 0, 0, (float*)workspace, part_bytes, st, 0, rank, &sk);
+  if (rc != QLRT_OK) return rc;
+  // Y^T[N, m] = W_cat^T X^T + per member [l2_g ; l2_g]^T [Ts_g]^T
+  gemm::Args a{};
+  if ((rc = gemm::fill_nf4(a, w, 1, nullptr, st)) != QLRT_OK) return rc;
+  a.M = (int)N;
+  a.N = (int)m;
+  a.splits = 1;
+  a.out = y;
+  a.ldo = N;
+  a.out_t = 1;
+  a.alpha = 1.0f;
+  const int bn_main = gemm::tile512_policy() ? 512 : 256;
+  a.pair = bn_main == 512 ? 1 : gemm::pair_policy(0);
+  if (gemm::streamk_policy()) { a.sk_ws = sk.sk_ws; a.sk_flags = sk.sk_flags; }
+  a.aug_wrap = rank;
+  a.aug_gn = (int)Ng;
+  a.aug_gstride = 2 * rank;
+  a.aug_b2k = 2 * R;
+  Operand none{}, Bx{x, K, 0}, A2{l2, N, 1}, B2{ts_out, 2 * R, 0};
+  return gemm::run(bn_main, none, Bx, &A2, &B2, K, 2 * rank, a, st);
+}
+
+qlrt_status qlrt_nf4_linear_group_bwd(const qlrt_nf4_weight* w, int groups, const void* dy, int64_t m,
+                                      const void* x, const void* ts, const void* l1, const void* l2, int rank,
+                                      float s, void* dt_out, void* dx, float* dl1, float* dl2, void* workspace,
+                                      void* side_workspace, int flags, void* stream) {
+  if (!group_ok(w, groups, rank) || !dy || !dx || !x || !ts || !l1 || !l2 || !dt_out || !dl1 || !dl2 ||
+      !workspace || m <= 0 || (flags & ~QLRT_BWD_DEFER))
+    return QLRT_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t K = w->k_in, N = w->n_out, Ng = N / groups;
+  const int R = groups * rank;
+  const size_t ws_bytes = qlrt_linear_workspace_bytes(m, K, N, R);
+  const size_t part_bytes =
+      ws_bytes - gemm::dbl_bytes(K, N, R) - gemm::sk_bytes() - gemm::align256(gemm::consts_bytes(K, N));
+  gemm::Args sk{};
+  gemm::sk_region(workspace, ws_bytes, K, N, R, sk);
+  qlrt_status rc;
+  typedef __nv_bfloat16 bf;
+  // dT_g = s dY_g l2_g^T into member g's [hi | lo] block of dT_cat
+  for (int g = 0; g < groups; ++g) {
+    Operand DA{(const bf*)dy + g * Ng, N, 0}, DB{(const bf*)l2 + g * Ng, N, 0};
+    rc = gemm::plain(64, DA, DB, m, rank, Ng, s, (bf*)dt_out + 2 * g * rank, 2 * R, 0, 0, (float*)workspace,
+                     part_bytes, st, 0, rank, &sk);
+    if (rc != QLRT_OK) return rc;
+  }
+  gemm::SideCtx* sctx = gemm::side_ctx(st);
+  const bool defer = (flags & QLRT_BWD_DEFER) && sctx && side_workspace;
+  const int side_cap = defer ? policy(P_SIDE_SMS) : 0;
+  cudaStream_t side = gemm::fork_side(sctx, st);
+  // dX^T[K, m] = W_cat dY_cat^T + sum_g [l1_g | l1_g] [dT_g]^T (K2 = G 2r; the
+  // wrapped A2 re-reads member g's l1 columns for both halves of its pair)
+  gemm::Args a{};
+  if ((rc = gemm::fill_nf4(a, w, 2, nullptr, st)) != QLRT_OK) return rc;
+  a.M = (int)K;
+  a.N = (int)m;
+  a.splits = 1;
+  a.out = dx;
+  a.ldo = K;
+  a.out_t = 1;
+  a.alpha = 1.0f;
+  const int bn_main = gemm::tile512_policy() ? 512 : 256;
+  a.pair = bn_main == 512 ? 1 : gemm::pair_policy(0);
+  if (gemm::streamk_policy()) { a.sk_ws = sk.sk_ws; a.sk_flags = sk.sk_flags; }
+  a.aug_wrap = rank;
+  Operand none{}, B{dy, N, 0}, A2{l1, R, 0}, B2{dt_out, 2 * R, 0};
+  if ((rc = gemm::run(bn_main, none, B, &A2, &B2, N, 2 * R, a, st)) != QLRT_OK) return rc;
+  cudaStream_t aux = side ? side : st;
+  const int bn_g = 2 * rank <= 64 ? 64 : (2 * rank <= 128 ? 128 : 256);
+  // dl2_g^T[N_g, r] = dY_g^T (Ts_g hi + lo), stored into columns g N_g.. of dl2[r][N]
+  for (int g = 0; g < groups; ++g) {
+    Operand A{(const bf*)dy + g * Ng, N, 1}, Bt{(const bf*)ts + 2 * g * rank, 2 * R, 1};
+    rc = gemm::plain(bn_g, A, Bt, Ng, 2 * rank, m, 1.0f, dl2 + g * Ng, N, 1, 1, nullptr, 0, aux, rank, 0, nullptr, 0,
+                     0, side_cap);
+    if (rc != QLRT_OK) return rc;
+  }
+  {
+    // dl1_cat[K, G r] = X^T (dT_cat hi + lo per member): one GEMM (the members share X)
+    Operand A{x, K, 1}, B1{dt_out, 2 * R, 1};
+    float* pw = defer ? (float*)side_workspace : (float*)workspace;
+    rc = gemm::plain(2 * R <= 128 ? (2 * R <= 64 ? 64 : 128) : ((2 * R) % 256 == 0 ? 256 : 128), A, B1, K, 2 * R, m,
+                     1.0f, dl1, R, 1, 0, pw,
+                     part_bytes, aux, rank, 0, side ? nullptr : &sk, 0, 0, side_cap);
+    if (rc != QLRT_OK) return rc;
+  }
+  if (side && !defer && !gemm::join_side(sctx, st)) return QLRT_ERR_CUDA;
+  return QLRT_OK;
 }
 
 qlrt_status qlrt_nf4_linear_bwd(const qlrt_nf4_weight* w, const void* dy, int64_t m, const void* x, const void* ts,

@@ -80,11 +80,15 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const uint4* __restric
 
 __device__ __forceinline__ float sigmoidf_(float g) { return 1.0f / (1.0f + __expf(-g)); }
 
-// out = silu(g) * u  (n % 8 == 0)
+// out = silu(g) * u over rows x (c8 * 8) elements, row pitches in 16 B units
+// (contiguous: one row; concatenated [g | u]: ldg = ldu = 2 c8)
 __global__ void swiglu_fwd_kernel(const uint4* __restrict__ g, const uint4* __restrict__ u, uint4* __restrict__ out,
-                                  int64_t n8) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint4 a = g[i], b = u[i];
+                                  int64_t rows, int64_t c8, int64_t ldg, int64_t ldu, int64_t ldo) {
+  const int64_t n8 = rows * c8;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n8; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = k / c8, c = k - r * c8;
+    const uint4 a = g[r * ldg + c], b = u[r * ldu + c];
+    const int64_t i = r * ldo + c;
     const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
     uint32_t o[4];
 #pragma unroll
@@ -99,9 +103,12 @@ __global__ void swiglu_fwd_kernel(const uint4* __restrict__ g, const uint4* __re
 // du = dout * silu(g);  dg = dout * u * s * (1 + g (1 - s)),  s = sigmoid(g)
 __global__ void swiglu_bwd_kernel(const uint4* __restrict__ g, const uint4* __restrict__ u,
                                   const uint4* __restrict__ dout, uint4* __restrict__ dg, uint4* __restrict__ du,
-                                  int64_t n8) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint4 a = g[i], b = u[i], c = dout[i];
+                                  int64_t rows, int64_t c8, int64_t ldgu, int64_t ldo) {
+  const int64_t n8 = rows * c8;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n8; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = k / c8, cc = k - r * c8;
+    const int64_t i = r * ldgu + cc;  // g, u, dg, du share a pitch
+    const uint4 a = g[i], b = u[i], c = dout[r * ldo + cc];
     const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w}, wc[4] = {c.x, c.y, c.z, c.w};
     uint32_t og[4], ou[4];
 #pragma unroll
@@ -125,16 +132,20 @@ __global__ void swiglu_bwd_kernel(const uint4* __restrict__ g, const uint4* __re
 // rotary embedding on [rows = b*s, heads, d] bf16, adjacent pairs (2i, 2i+1)
 // rotated by angle pos * inv_freq[i]; cs = (cos, sin) fp32 [s][d/2]; sign = -1
 // applies the inverse rotation (backward)
+// (row pitches ldx / ldy in 16 B units: q or k read from / written to a
+// column slice of the concatenated q | k | v projection)
 __global__ void rope_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, const float2* __restrict__ cs,
-                            int64_t rows, int heads, int d, int seq, float sign) {
+                            int64_t rows, int heads, int d, int seq, float sign, int64_t ldx, int64_t ldy) {
   const int d8 = d / 8;
-  const int64_t total = rows * heads * d8;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c8 = (int)(i % d8);
-    const int64_t row = i / ((int64_t)d8 * heads);
+  const int64_t rw = (int64_t)d8 * heads;
+  const int64_t total = rows * rw;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = (int)(k % d8);
+    const int64_t row = k / rw, within = k - row * rw;
     const int pos = (int)(row % seq);
     const float2* t = cs + (int64_t)pos * (d / 2) + c8 * 4;  // 4 pairs per 16 B
-    const uint4 a = x[i];
+    const int64_t i = row * ldy + within;
+    const uint4 a = x[row * ldx + within];
     const uint32_t w[4] = {a.x, a.y, a.z, a.w};
     uint32_t o[4];
 #pragma unroll
@@ -179,7 +190,7 @@ qlrt_status qlrt_rmsnorm_bwd(const void* dy, const void* x, const float* rstd, v
 qlrt_status qlrt_swiglu_fwd(const void* g, const void* u, void* out, int64_t n, void* stream) {
   if (!g || !u || !out || n <= 0 || (n % 8)) return QLRT_ERR_ARG;
   glue::swiglu_fwd_kernel<<<glue::grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)g, (const uint4*)u, (uint4*)out, n / 8);
+      (const uint4*)g, (const uint4*)u, (uint4*)out, 1, n / 8, 0, 0, 0);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }
@@ -188,7 +199,7 @@ qlrt_status qlrt_swiglu_bwd(const void* g, const void* u, const void* dout, void
                             void* stream) {
   if (!g || !u || !dout || !dg || !du || n <= 0 || (n % 8)) return QLRT_ERR_ARG;
   glue::swiglu_bwd_kernel<<<glue::grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)g, (const uint4*)u, (const uint4*)dout, (uint4*)dg, (uint4*)du, n / 8);
+      (const uint4*)g, (const uint4*)u, (const uint4*)dout, (uint4*)dg, (uint4*)du, 1, n / 8, 0, 0);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }
@@ -197,8 +208,41 @@ qlrt_status qlrt_rope(const void* x, void* y, const void* cos_sin, int64_t rows,
                       int inverse, void* stream) {
   if (!x || !y || !cos_sin || rows <= 0 || heads <= 0 || d <= 0 || (d % 8) || seq <= 0) return QLRT_ERR_ARG;
   const int64_t total = rows * heads * (d / 8);
+  const int64_t rw = (int64_t)heads * (d / 8);
   glue::rope_kernel<<<glue::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)x, (uint4*)y, (const float2*)cos_sin, rows, heads, d, seq, inverse ? -1.0f : 1.0f);
+      (const uint4*)x, (uint4*)y, (const float2*)cos_sin, rows, heads, d, seq, inverse ? -1.0f : 1.0f, rw, rw);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+qlrt_status qlrt_rope_strided(const void* x, int64_t ldx, void* y, int64_t ldy, const void* cos_sin, int64_t rows,
+                              int heads, int d, int seq, int inverse, void* stream) {
+  if (!x || !y || !cos_sin || rows <= 0 || heads <= 0 || d <= 0 || (d % 8) || seq <= 0 || (ldx % 8) || (ldy % 8) ||
+      ldx < (int64_t)heads * d || ldy < (int64_t)heads * d)
+    return QLRT_ERR_ARG;
+  const int64_t total = rows * heads * (d / 8);
+  glue::rope_kernel<<<glue::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)x, (uint4*)y, (const float2*)cos_sin, rows, heads, d, seq, inverse ? -1.0f : 1.0f, ldx / 8,
+      ldy / 8);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+// concatenated [g | u] rows (cols each): out[rows][cols] = silu(g) * u
+qlrt_status qlrt_swiglu_cat_fwd(const void* gu, void* out, int64_t rows, int64_t cols, void* stream) {
+  if (!gu || !out || rows <= 0 || cols <= 0 || (cols % 8)) return QLRT_ERR_ARG;
+  const int64_t c8 = cols / 8;
+  glue::swiglu_fwd_kernel<<<glue::grid_for(rows * c8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)gu, (const uint4*)gu + c8, (uint4*)out, rows, c8, 2 * c8, 2 * c8, c8);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+// d[g | u] rows from dout[rows][cols] and the saved [g | u]
+qlrt_status qlrt_swiglu_cat_bwd(const void* gu, const void* dout, void* dgu, int64_t rows, int64_t cols,
+                                void* stream) {
+  if (!gu || !dout || !dgu || rows <= 0 || cols <= 0 || (cols % 8)) return QLRT_ERR_ARG;
+  const int64_t c8 = cols / 8;
+  glue::swiglu_bwd_kernel<<<glue::grid_for(rows * c8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)gu, (const uint4*)gu + c8, (const uint4*)dout, (uint4*)dgu, (uint4*)dgu + c8, rows, c8, 2 * c8,
+      c8);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }

@@ -49,10 +49,12 @@ from .blockquant import quantize
 from .codebooks import get_codebook
 from .paging import Pager, PagerConfig
 from .parallel import GradBucket, LayerReducer
-from .qlora import LoraAdapter, QLinear, side_join
+from .qlora import LoraAdapter, QLinear, QLinearGroup, side_join
 from .training import TrainConfig, _sumsq_scratch
 
 PROJS = ("q", "k", "v", "o", "gate", "up", "down")
+# the projections as issued: siblings that read the same input form one unit
+UNITS_GROUPED = (("qkv", ("q", "k", "v")), ("o", ("o",)), ("gu", ("gate", "up")), ("down", ("down",)))
 
 
 @dataclass(frozen=True)
@@ -124,6 +126,81 @@ class _QLinearFn(torch.autograd.Function):
         if ctx.notify is not None:  # this projection's adapter gradients are issued
             ctx.notify()
         return dx, None, None, None, None, None
+
+
+class _QKVFn(torch.autograd.Function):
+    """q | k | v as one grouped NF4 linear (QLinearGroup: one Ts GEMM, one
+    fused grid, one dl1 GEMM), RoPE applied to the q and k column slices of
+    the concatenated output; the backward builds d[q | k | v] in place
+    (inverse RoPE into the slices) and runs the grouped backward once."""
+
+    @staticmethod
+    def forward(ctx, x, anchor, grp, gviews, notify, defer, cos_sin, nh):
+        b, s, h = x.shape
+        d = h // nh
+        ycat, cache = grp.forward(x)
+        q = torch.empty(b, s, nh, d, dtype=ycat.dtype, device=ycat.device)
+        k = torch.empty_like(q)
+        L = lib()
+        check(L.qlrt_rope_strided(ptr(ycat), 3 * h, ptr(q), h, ptr(cos_sin), b * s, nh, d, s, 0, stream_ptr()), "rope q")
+        check(L.qlrt_rope_strided(ptr(ycat) + 2 * h, 3 * h, ptr(k), h, ptr(cos_sin), b * s, nh, d, s, 0, stream_ptr()),
+              "rope k")
+        v = ycat[:, 2 * h:].contiguous().view(b, s, nh, d)
+        ctx.grp, ctx.cache, ctx.gviews, ctx.notify, ctx.defer = grp, cache, gviews, notify, defer
+        ctx.save_for_backward(cos_sin)
+        ctx.dims = (b, s, h, nh, d)
+        return q, k, v
+
+    @staticmethod
+    def backward(ctx, dq, dk, dv):
+        (cos_sin,) = ctx.saved_tensors
+        b, s, h, nh, d = ctx.dims
+        dq, dk = dq.contiguous(), dk.contiguous()
+        dycat = torch.empty(b * s, 3 * h, dtype=dq.dtype, device=dq.device)
+        L = lib()
+        check(L.qlrt_rope_strided(ptr(dq), h, ptr(dycat), 3 * h, ptr(cos_sin), b * s, nh, d, s, 1, stream_ptr()),
+              "rope q bwd")
+        check(L.qlrt_rope_strided(ptr(dk), h, ptr(dycat) + 2 * h, 3 * h, ptr(cos_sin), b * s, nh, d, s, 1,
+                                  stream_ptr()), "rope k bwd")
+        dycat[:, 2 * h:].view(b, s, nh, d).copy_(dv)
+        dx = ctx.grp.backward(dycat, ctx.cache, ctx.gviews["l1"], ctx.gviews["l2"],
+                              defer=ctx.defer() if ctx.defer is not None else None)
+        ctx.cache = None
+        if ctx.notify is not None:
+            ctx.notify()
+        return dx.view(b, s, h), None, None, None, None, None, None, None
+
+
+class _GateUpFn(torch.autograd.Function):
+    """gate | up as one grouped NF4 linear, SwiGLU over the concatenated
+    output; the backward writes d[gate | up] in place and runs the grouped
+    backward once."""
+
+    @staticmethod
+    def forward(ctx, x, anchor, grp, gviews, notify, defer):
+        b, s, h = x.shape
+        f = grp.n_member
+        ycat, cache = grp.forward(x)
+        out = torch.empty(b * s, f, dtype=ycat.dtype, device=ycat.device)
+        check(lib().qlrt_swiglu_cat_fwd(ptr(ycat), ptr(out), b * s, f, stream_ptr()), "swiglu")
+        ctx.grp, ctx.cache, ctx.gviews, ctx.notify, ctx.defer = grp, cache, gviews, notify, defer
+        ctx.save_for_backward(ycat)
+        ctx.dims = (b, s, h, f)
+        return out.view(b, s, f)
+
+    @staticmethod
+    def backward(ctx, dout):
+        (ycat,) = ctx.saved_tensors
+        b, s, h, f = ctx.dims
+        dgu = torch.empty_like(ycat)
+        check(lib().qlrt_swiglu_cat_bwd(ptr(ycat), ptr(dout.contiguous()), ptr(dgu), b * s, f, stream_ptr()),
+              "swiglu bwd")
+        dx = ctx.grp.backward(dgu, ctx.cache, ctx.gviews["l1"], ctx.gviews["l2"],
+                              defer=ctx.defer() if ctx.defer is not None else None)
+        ctx.cache = None
+        if ctx.notify is not None:
+            ctx.notify()
+        return dx.view(b, s, h), None, None, None, None, None
 
 
 class _RMSNormFn(torch.autograd.Function):
@@ -226,7 +303,8 @@ class LlamaQLoRA:
     def __init__(self, cfg: LlamaConfig, device="cuda", seed: int = 0, train_cfg: TrainConfig | None = None, *,
                  group=None, optimizer: str = "plain", pager_budget_bytes: int | None = None,
                  page_bytes: int = 2 << 20, lookahead: int = 2, checkpoint: bool = False, bucket_layers: int = 4,
-                 wire_dtype=torch.float32, max_steps: int = 100_000, defer_lag: int | None = 1):
+                 wire_dtype=torch.float32, max_steps: int = 100_000, defer_lag: int | None = 1,
+                 grouped: bool | None = None):
         if optimizer not in ("plain", "paged"):
             raise ValueError(f"optimizer must be 'plain' or 'paged', got {optimizer!r}")
         self.cfg = cfg
@@ -249,27 +327,49 @@ class LlamaQLoRA:
         h, v = cfg.hidden, cfg.vocab
         self.embed = (torch.randn(v, h, device=self.dev, generator=g) * 0.02).to(torch.bfloat16)
         self.lm_head = (torch.randn(h, v, device=self.dev, generator=g) * 0.02).to(torch.bfloat16)
+        # sibling projections that share their input run as one grouped call
+        # (q | k | v, gate | up: QLinearGroup) when the shapes allow it
+        if grouped is None:
+            grouped = cfg.rank % 64 == 0 and h % 256 == 0 and cfg.ffn % 256 == 0
+        self.grouped = bool(grouped)
+        self.units = (UNITS_GROUPED if self.grouped else tuple((pj, (pj,)) for pj in PROJS))
         # one flat fp32 buffer each for adapter parameters and gradients (layer
         # after layer, so a layer's -- and a group of layers' -- tensors are
-        # contiguous); a flat bf16 buffer for the MMA operand shadows (same layout)
-        names, shapes = [], {}
+        # contiguous; a unit's l1 [K][G r] / l2 [r][G N] blocks are contiguous);
+        # a flat bf16 buffer for the MMA operand shadows (same layout)
+        r = cfg.rank
+        ushapes = {}
         for li in range(cfg.n_layers):
-            for pj in PROJS:
-                a, b = cfg.proj_shape(pj)
-                shapes[f"{li}.{pj}.l1"] = (a, cfg.rank)
-                shapes[f"{li}.{pj}.l2"] = (cfg.rank, b)
-                names += [f"{li}.{pj}.l1", f"{li}.{pj}.l2"]
-        self.names = names
-        self.bucket = GradBucket(shapes, self.dev)          # gradients (all-reduced)
-        pbuf = GradBucket(shapes, self.dev)                 # parameters
+            for un, members in self.units:
+                a_, b_ = cfg.proj_shape(members[0])
+                ushapes[f"{li}.{un}.l1"] = (a_, len(members) * r)
+                ushapes[f"{li}.{un}.l2"] = (r, len(members) * b_)
+        self.bucket = GradBucket(ushapes, self.dev)         # gradients (all-reduced)
+        pbuf = GradBucket(ushapes, self.dev)                # parameters
         self.params_flat = pbuf.flat
-        self.params = pbuf.views()
         self.shadow_flat = torch.zeros(self.params_flat.numel(), dtype=torch.bfloat16, device=self.dev)
+        self.uparams, self.ugrads = pbuf.views(), self.bucket.views()
+        ushadows, off = {}, 0
+        for n, shp in ushapes.items():
+            k_ = int(np.prod(shp))
+            ushadows[n] = self.shadow_flat[off: off + k_].view(shp)
+            off += k_
+        # per-projection names / views (member g = column slice g of its unit)
+        names, self.params, self.gviews, shadows = [], {}, {}, {}
+        for li in range(cfg.n_layers):
+            for un, members in self.units:
+                a_, b_ = cfg.proj_shape(members[0])
+                for g_, pj in enumerate(members):
+                    for src, dst in ((self.uparams, self.params), (self.ugrads, self.gviews), (ushadows, shadows)):
+                        dst[f"{li}.{pj}.l1"] = src[f"{li}.{un}.l1"][:, g_ * r:(g_ + 1) * r]
+                        dst[f"{li}.{pj}.l2"] = src[f"{li}.{un}.l2"][:, g_ * b_:(g_ + 1) * b_]
+                    names += [f"{li}.{pj}.l1", f"{li}.{pj}.l2"]
+        self.names = names
         offs = self.bucket.offsets()
         self.layer_spans = []
         for li in range(cfg.n_layers):
-            first = offs[f"{li}.{PROJS[0]}.l1"][0]
-            last_off, last_n = offs[f"{li}.{PROJS[-1]}.l2"]
+            first = offs[f"{li}.{self.units[0][0]}.l1"][0]
+            last_off, last_n = offs[f"{li}.{self.units[-1][0]}.l2"]
             self.layer_spans.append((first, last_off + last_n - first))
         self.pager = None
         if optimizer == "plain":
@@ -280,37 +380,48 @@ class LlamaQLoRA:
             state = sum((2 * n * 4 + page_bytes - 1) // page_bytes * page_bytes for _, n in self.layer_spans)
             self.pager = Pager(PagerConfig(budget_bytes=pager_budget_bytes or state, page_bytes=page_bytes))
             self.mslabs = [self.pager.alloc(2 * n * 4) for _, n in self.layer_spans]
-        self.gviews = self.bucket.views()
-        shadows, off = {}, 0
-        for n in names:
-            k = int(np.prod(shapes[n]))
-            shadows[n] = self.shadow_flat[off: off + k].view(shapes[n])
-            off += k
         self.reducer = LayerReducer(self.bucket.flat, self.layer_spans, bucket_layers, group, wire_dtype)
-        self._pending = [len(PROJS)] * cfg.n_layers
+        self._pending = [len(self.units)] * cfg.n_layers
         self.layers = []
         for li in range(cfg.n_layers):
             lay = {}
+            qs = {}
             for pj in PROJS:
-                a, b = cfg.proj_shape(pj)
-                w = torch.randn(a, b, device=self.dev, generator=g) * 0.02
-                q = quantize(w, cb, 64, double_quant=True)
+                a_, b_ = cfg.proj_shape(pj)
+                w = torch.randn(a_, b_, device=self.dev, generator=g) * 0.02
+                qs[pj] = quantize(w, cb, 64, double_quant=True)
                 del w
                 l1, l2 = self.params[f"{li}.{pj}.l1"], self.params[f"{li}.{pj}.l2"]
-                l1.copy_(torch.randn(a, cfg.rank, device=self.dev, generator=g) / math.sqrt(cfg.rank))
+                l1.copy_(torch.randn(a_, r, device=self.dev, generator=g) / math.sqrt(r))
                 l2.zero_()  # lora_init: l2 = 0 (qlora.py:63-80)
-                ad = LoraAdapter(cfg.rank, cfg.alpha, l1, l2)
-                if cfg.rank % 8 == 0:  # the kernels read the shadows in place; Adam refreshes them
+                ad = LoraAdapter(r, cfg.alpha, l1, l2)
+                if r % 8 == 0 and not self.grouped:  # the kernels read the shadows in place; Adam refreshes them
                     s1, s2 = shadows[f"{li}.{pj}.l1"], shadows[f"{li}.{pj}.l2"]
                     s1.copy_(l1)
                     s2.copy_(l2)
                     ad.adopt_shadows(s1, s2)
-                lay[pj] = QLinear(q, [ad])
+                lay[pj] = QLinear(qs[pj], [ad])
                 lay[pj + ".g"] = {"adapter0.l1": self.gviews[f"{li}.{pj}.l1"],
                                   "adapter0.l2": self.gviews[f"{li}.{pj}.l2"]}
+            if self.grouped:
+                for un, members in self.units:
+                    if len(members) == 1:
+                        pj = members[0]
+                        lay[un] = QLinear(qs[pj], [LoraAdapter(r, cfg.alpha, self.uparams[f"{li}.{un}.l1"],
+                                                               self.uparams[f"{li}.{un}.l2"])])
+                        lay[un].adapters[0].adopt_shadows(ushadows[f"{li}.{un}.l1"], ushadows[f"{li}.{un}.l2"])
+                        lay[un + ".g"] = {"adapter0.l1": self.ugrads[f"{li}.{un}.l1"],
+                                          "adapter0.l2": self.ugrads[f"{li}.{un}.l2"]}
+                    else:
+                        lay[un] = QLinearGroup([qs[pj] for pj in members], self.uparams[f"{li}.{un}.l1"],
+                                               self.uparams[f"{li}.{un}.l2"], r, cfg.alpha,
+                                               l1b=ushadows[f"{li}.{un}.l1"], l2b=ushadows[f"{li}.{un}.l2"])
+                        lay[un + ".g"] = {"l1": self.ugrads[f"{li}.{un}.l1"], "l2": self.ugrads[f"{li}.{un}.l2"]}
             lay["notify"] = (lambda li=li: self._proj_done(li))
             lay["index"] = li
             self.layers.append(lay)
+        if self.grouped:
+            self.shadow_flat.copy_(self.params_flat)
         d = h // cfg.n_heads
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, d, 2, device=self.dev, dtype=torch.float32) / d))
         ang = torch.outer(torch.arange(cfg.seq, device=self.dev, dtype=torch.float32), inv)
@@ -388,6 +499,15 @@ class LlamaQLoRA:
         nh, d = cfg.n_heads, cfg.hidden // cfg.n_heads
         hn = _rmsnorm(x, cfg.rms_eps)
         cs = self.cos_sin[:s]
+        if self.grouped:
+            defer = None if self.defer_lag is None else (lambda li=li: self._inflight.setdefault(li, []))
+            q, k, v = _QKVFn.apply(hn, anchor, lay["qkv"], lay["qkv.g"], lay["notify"], defer, cs, nh)
+            a = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2),
+                                               is_causal=True).transpose(1, 2).reshape(b, s, cfg.hidden)
+            x = x + self._lin(a, lay, "o", anchor)
+            hn = _rmsnorm(x, cfg.rms_eps)
+            act = _GateUpFn.apply(hn, anchor, lay["gu"], lay["gu.g"], lay["notify"], defer)
+            return x + self._lin(act, lay, "down", anchor)
         q = _rope(self._lin(hn, lay, "q", anchor).view(b, s, nh, d), cs).transpose(1, 2)
         k = _rope(self._lin(hn, lay, "k", anchor).view(b, s, nh, d), cs).transpose(1, 2)
         v = self._lin(hn, lay, "v", anchor).view(b, s, nh, d).transpose(1, 2)
@@ -424,7 +544,7 @@ class LlamaQLoRA:
     def forward_backward(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         """Loss, backward with the overlapped adapter-gradient all-reduce, and
         the global fp64 sum of squares for the clip (capturable: no host sync)."""
-        self._pending = [len(PROJS)] * self.cfg.n_layers
+        self._pending = [len(self.units)] * self.cfg.n_layers
         self._ready_q, self._side_ev = [], {}
         self.reducer.reset()
         loss = self.loss(tokens, targets)

@@ -470,6 +470,142 @@ class QLinear:
         return out
 
 
+class QLinearGroup:
+    """Sibling projections that read the same input (q | k | v, gate | up) as
+    ONE call of the fused kernels -- the same math per member as a QLinear
+    with one adapter (qlora.py:124-167).
+
+    Every member keeps its own NF4 + DQ quantization (the reference's
+    per-layer QLinear; its DQ codes / c1 / mu stay per member); the packed
+    codes are concatenated along N into one buffer so one fused grid covers
+    all members (``release_member_codes`` drops the members' own copies).  ``l1`` [K][G r] and ``l2``
+    [r][G N_g] are fp32 masters (member g's adapter = column slice g), ``l1b``
+    / ``l2b`` their bf16 operand copies (kept current by the caller's fused
+    Adam, as the LLaMA harness does, or refreshed here on a version change).
+    """
+
+    def __init__(self, bases: list, l1: torch.Tensor, l2: torch.Tensor, rank: int, alpha: float,
+                 l1b: torch.Tensor | None = None, l2b: torch.Tensor | None = None,
+                 release_member_codes: bool = False):
+        g = len(bases)
+        k, ng = int(bases[0].shape[0]), int(bases[0].shape[1])
+        for b in bases:
+            if not (isinstance(b, BlockQuantized) and b.dq is not None and b.blocksize == 64
+                    and b.codebook.bits == 4 and tuple(b.shape) == (k, ng)):
+                raise ValueError("group members must be NF4 + DQ, blocksize 64, of one shape")
+        if ng % 256 or rank % 64:
+            raise ValueError(f"grouped projections need N_g % 256 == 0 and rank % 64 == 0 (got {ng}, {rank})")
+        if tuple(l1.shape) != (k, g * rank) or tuple(l2.shape) != (rank, g * ng):
+            raise ValueError("l1 must be [K][G r] and l2 [r][G N_g]")
+        self.groups, self.in_dim, self.n_member, self.rank, self.alpha = g, k, ng, rank, alpha
+        self.out_dim = g * ng
+        self.l1, self.l2 = l1, l2
+        self.codes = torch.empty(k, self.out_dim // 2, dtype=torch.uint8, device=l1.device)
+        for i, b in enumerate(bases):
+            self.codes[:, i * ng // 2: (i + 1) * ng // 2].copy_(b.codes.view(k, ng // 2))
+            if release_member_codes:  # (the concatenated buffer stays the only copy)
+                b.codes = None
+        self.bases = bases
+        self._ops = [l1b, l2b, None] if l1b is not None else None
+        self._wdesc = None
+        self._member_desc = []
+        for b in bases:
+            d = _native.NF4Weight()
+            d.dq_codes, d.c1, d.mu = ptr(b.dq.codes), ptr(b.dq.c1), ptr(b.dq.mu)
+            d.k_in, d.n_out, d.blocksize2 = k, ng, b.dq.blocksize2
+            d.spec = b.dq.spec.to_c()
+            self._member_desc.append(d)
+
+    @property
+    def scaling(self) -> float:
+        return self.alpha / self.rank
+
+    def operands(self):
+        """bf16 copies of l1 / l2 (caller-owned ones are used as they are)."""
+        if self._ops is None or (self._ops[2] is not None and self._ops[2] != (self.l1._version, self.l2._version)):
+            if self._ops is None:
+                self._ops = [torch.empty_like(self.l1, dtype=torch.bfloat16),
+                             torch.empty_like(self.l2, dtype=torch.bfloat16), None]
+            self._ops[0].copy_(self.l1)
+            self._ops[1].copy_(self.l2)
+            self._ops[2] = (self.l1._version, self.l2._version)
+        return self._ops[0], self._ops[1]
+
+    def _desc(self, consts: torch.Tensor):
+        if self._wdesc is None:
+            b = self.bases[0]
+            w = _native.NF4Weight()
+            w.codes, w.dq_codes, w.c1, w.mu = ptr(self.codes), ptr(b.dq.codes), ptr(b.dq.c1), ptr(b.dq.mu)
+            w.k_in, w.n_out, w.blocksize2 = self.in_dim, self.out_dim, b.dq.blocksize2
+            w.spec = b.dq.spec.to_c()
+            for i in range(16):
+                w.values[i] = float(b.codebook.values[i])
+            self._wdesc = w
+        self._wdesc.consts = ptr(consts)
+        return self._wdesc
+
+    def _constants(self) -> torch.Tensor:
+        """The members' block constants into one [K][round4(N/64)] cache (per
+        forward, shared with the backward; padding columns stay zero)."""
+        L = lib()
+        pitch = int(L.qlrt_nf4_constants_bytes(self.in_dim, self.out_dim)) // 4 // self.in_dim
+        out = torch.zeros(self.in_dim, pitch, dtype=torch.float32, device=self.l1.device)
+        nbr = self.n_member // 64
+        for i, d in enumerate(self._member_desc):
+            check(L.qlrt_nf4_constants_into(d, ptr(out) + 4 * i * nbr, pitch, stream_ptr()), "QLinearGroup constants")
+        return out
+
+    def _workspace(self, m: int, side: bool = False) -> torch.Tensor:
+        need = int(lib().qlrt_linear_workspace_bytes(max(m, 1), self.in_dim, self.out_dim, self.groups * self.rank))
+        table = _SIDE_WS if side else _LINEAR_WS
+        dev = torch.cuda.current_device()
+        ws = table.get(dev)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+            table[dev] = ws
+        return ws
+
+    def forward(self, x: torch.Tensor):
+        """Y_cat [M][G N_g] = X W_cat + per member s (X l1_g) l2_g."""
+        x2 = x.reshape(-1, self.in_dim)
+        if x2.dtype != torch.bfloat16 or not x2.is_contiguous():
+            x2 = x2.to(torch.bfloat16).contiguous()
+        m = x2.shape[0]
+        consts = self._constants()
+        l1b, l2b = self.operands()
+        ts = torch.empty(m, 2 * self.groups * self.rank, dtype=torch.bfloat16, device=x2.device)
+        y = torch.empty(m, self.out_dim, dtype=torch.bfloat16, device=x2.device)
+        check(lib().qlrt_nf4_linear_group_fwd(self._desc(consts), self.groups, ptr(x2), m, ptr(l1b), ptr(l2b),
+                                              self.rank, float(self.scaling), ptr(ts), ptr(y),
+                                              ptr(self._workspace(m)), stream_ptr()), "QLinearGroup.forward")
+        return y, {"x": x2, "ts": ts, "consts": consts}
+
+    def backward(self, d_y: torch.Tensor, cache: dict, dl1: torch.Tensor, dl2: torch.Tensor,
+                 defer: list | None = None) -> torch.Tensor:
+        """dX = sum_g (dY_g W_g^T + s dY_g l2_g^T l1_g^T); dl1 [K][G r] and dl2
+        [r][G N_g] (fp32, contiguous) receive every member's adapter
+        gradients.  ``defer``: as QLinear.backward."""
+        d_y = d_y.reshape(-1, self.out_dim)
+        if d_y.dtype != torch.bfloat16 or not d_y.is_contiguous():
+            d_y = d_y.to(torch.bfloat16).contiguous()
+        m = d_y.shape[0]
+        if not (dl1.is_contiguous() and dl2.is_contiguous() and dl1.dtype == torch.float32
+                and dl2.dtype == torch.float32):
+            raise ValueError("dl1 / dl2 must be contiguous float32")
+        l1b, l2b = self.operands()
+        dt = torch.empty(m, 2 * self.groups * self.rank, dtype=torch.bfloat16, device=d_y.device)
+        d_x = torch.empty(m, self.in_dim, dtype=torch.bfloat16, device=d_y.device)
+        check(lib().qlrt_nf4_linear_group_bwd(self._desc(cache["consts"]), self.groups, ptr(d_y), m, ptr(cache["x"]),
+                                              ptr(cache["ts"]), ptr(l1b), ptr(l2b), self.rank, float(self.scaling),
+                                              ptr(dt), ptr(d_x), ptr(dl1), ptr(dl2), ptr(self._workspace(m)),
+                                              ptr(self._workspace(m, side=True)) if defer is not None else None,
+                                              _native.QLRT_BWD_DEFER if defer is not None else 0, stream_ptr()),
+              "QLinearGroup.backward")
+        if defer is not None:
+            defer.extend((d_y, cache["x"], cache["ts"], dt, dl1, dl2))
+        return d_x
+
+
 _GEMM_WS: dict = {}
 _SIDE_WS: dict = {}
 
@@ -524,4 +660,4 @@ def gemm_bf16(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
     return out
 
 
-__all__ = ["LoraAdapter", "lora_init", "QLinear", "PLACEMENTS", "gemm_bf16", "side_join"]
+__all__ = ["LoraAdapter", "lora_init", "QLinear", "QLinearGroup", "PLACEMENTS", "gemm_bf16", "side_join"]

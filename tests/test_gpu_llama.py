@@ -92,10 +92,10 @@ def test_glue_kernels_match_torch(cuda):
     assert (t.grad.float() - tr.grad).abs().max() <= 2e-2 * tr.grad.abs().max()
 
 
-def _tiny(seed=0):
+def _tiny(seed=0, cfg_kw=None, **model_kw):
     from paper_2305_14314_b200.llama import LlamaConfig, LlamaQLoRA
-    cfg = LlamaConfig.tiny()
-    m = LlamaQLoRA(cfg, seed=seed)
+    cfg = LlamaConfig.tiny(**(cfg_kw or {}))
+    m = LlamaQLoRA(cfg, seed=seed, **model_kw)
     # make the adapters live (lora_init leaves l2 = 0): nonzero l2, shadows refreshed
     g = torch.Generator(device="cuda").manual_seed(seed + 1)
     for n, p in m.params.items():
@@ -107,8 +107,13 @@ def _tiny(seed=0):
     return m, tok, tgt
 
 
-def test_adapter_grads_match_fp32_reference(cuda):
-    m, tok, tgt = _tiny()
+@pytest.mark.parametrize("grouped", [False, True])
+def test_adapter_grads_match_fp32_reference(grouped, cuda):
+    """Adapter gradients of the harness (per projection, or q | k | v and
+    gate | up as grouped calls) against fp32 autograd of the same decoder."""
+    kw = {} if not grouped else {"hidden": 512, "ffn": 1024, "rank": 64}
+    m, tok, tgt = _tiny(cfg_kw=kw)
+    assert m.grouped == grouped
     loss = m.loss(tok, tgt)
     loss.backward()
     torch.cuda.synchronize()
@@ -304,3 +309,26 @@ def test_dp_two_ranks_equal_one_rank_over_concatenated_batch(cuda, tmp_path):
     assert float(d.max() / one["grads"].abs().max()) <= 2e-2
     assert float(d.mean() / one["grads"].abs().mean()) <= 1e-2
     assert json.loads(r0["launched"]) == [1, 0]
+
+
+@pytest.mark.parametrize("lag", [None, 1])
+def test_grouped_projections_match_separate(lag, cuda):
+    """q | k | v and gate | up as grouped calls (QLinearGroup: shared-input
+    adapter GEMMs, one fused grid per group, in-place RoPE / SwiGLU on the
+    concatenated outputs) against the same model run projection by
+    projection: same loss and adapter gradients within the bf16 tolerance."""
+    kw = {"hidden": 512, "ffn": 1024, "rank": 64}
+    a, tok, tgt = _tiny(4, cfg_kw=kw, grouped=False, defer_lag=lag)
+    b, _, _ = _tiny(4, cfg_kw=kw, grouped=True, defer_lag=lag)
+    assert b.grouped and not a.grouped
+    la = a.forward_backward(tok, tgt)
+    lb = b.forward_backward(tok, tgt)
+    torch.cuda.synchronize()
+    assert abs(la.item() - lb.item()) <= 1e-3 * abs(la.item())
+    ga = torch.cat([a.gviews[n].flatten() for n in a.names]).double()
+    gb = torch.cat([b.gviews[n].flatten() for n in b.names]).double()
+    d = (ga - gb).abs()
+    # (two bf16 pipelines through two layers; each also meets the fp32 bound
+    # of test_adapter_grads_match_fp32_reference)
+    assert d.max() / ga.abs().max() <= 5e-2, float(d.max() / ga.abs().max())
+    assert d.mean() / ga.abs().mean() <= 2e-2, float(d.mean() / ga.abs().mean())

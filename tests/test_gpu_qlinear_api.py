@@ -149,3 +149,45 @@ def test_deferred_backward_equals_joined(k, n, qb, cuda):
     assert torch.equal(dx0, dx1)
     for kk in g0:
         assert torch.equal(g0[kk], g1[kk]), kk
+
+
+@pytest.mark.parametrize("g,k,ng,m", [(3, 1024, 512, 300), (2, 512, 768, 256), (1, 256, 256, 128)])
+def test_group_linear_vs_torch_fp32(g, k, ng, m, qb, cuda):
+    """QLinearGroup (q | k | v, gate | up as one call): per member the same
+    math as QLinear with one adapter (qlora.py:124-167), against a plain
+    PyTorch fp32 statement over the same bf16 operands; dX sums the members."""
+    gen = torch.Generator(device="cuda").manual_seed(g * 100 + k)
+    r, alpha = 64, 16.0
+    s = alpha / r
+    bases = [qb.quantize(torch.randn(k, ng, device="cuda", generator=gen) * 0.02, qb.get_codebook("nf4"), 64,
+                         double_quant=True) for _ in range(g)]
+    wds = [qb.dequantize(b, torch.bfloat16).float() for b in bases]
+    l1 = (torch.randn(k, g * r, device="cuda", generator=gen) / 8).bfloat16().float()
+    l2 = (torch.randn(r, g * ng, device="cuda", generator=gen) * 0.05).bfloat16().float()
+    grp = qb.QLinearGroup(bases, l1, l2, r, alpha)
+    x = torch.randn(m, k, device="cuda", generator=gen).bfloat16()
+    dy = torch.randn(m, g * ng, device="cuda", generator=gen).bfloat16()
+    y, cache = grp.forward(x)
+    dl1 = torch.empty(k, g * r, device="cuda")
+    dl2 = torch.empty(r, g * ng, device="cuda")
+    dx = grp.backward(dy, cache, dl1, dl2)
+    torch.cuda.synchronize()
+    torch.backends.cuda.matmul.allow_tf32 = False
+    xf, dyf = x.float(), dy.float()
+    dx_ref = torch.zeros(m, k, device="cuda")
+    for i in range(g):
+        a1, a2 = l1[:, i * r:(i + 1) * r], l2[:, i * ng:(i + 1) * ng]
+        dyi = dyf[:, i * ng:(i + 1) * ng]
+        t = xf @ a1
+        y_ref = xf @ wds[i] + s * t @ a2
+        dt = s * dyi @ a2.t()
+        dx_ref += dyi @ wds[i].t() + dt @ a1.t()
+        for got, ref, what in ((y[:, i * ng:(i + 1) * ng].float(), y_ref.bfloat16().float(), "y"),
+                               (dl2[:, i * ng:(i + 1) * ng], s * t.t() @ dyi, "dl2"),
+                               (dl1[:, i * r:(i + 1) * r], xf.t() @ dt, "dl1")):
+            d = (got - ref).abs()
+            assert (d.max() / ref.abs().max()).item() <= MAX_REL, (what, i)
+            assert (d.mean() / ref.abs().mean()).item() <= MEAN_REL, (what, i)
+    d = (dx.float() - dx_ref.bfloat16().float()).abs()
+    assert (d.max() / dx_ref.abs().max()).item() <= MAX_REL
+    assert (d.mean() / dx_ref.abs().mean()).item() <= MEAN_REL

@@ -124,6 +124,10 @@ qlrt_status qlrt_nf4_constants(const qlrt_nf4_weight* w, float* out, void* strea
 /* One weight's block constants into columns [0, n_out/64) of rows of `pitch`
  * floats: a member's slice of a concatenated (grouped) weight's cache. */
 qlrt_status qlrt_nf4_constants_into(const qlrt_nf4_weight* w, float* out, int64_t pitch, void* stream);
+/* The same for up to 4 sibling weights of one shape in one launch (member g
+ * in columns [g n_out/64, (g + 1) n_out/64)). */
+qlrt_status qlrt_nf4_constants_group(const qlrt_nf4_weight* members, int groups, float* out, int64_t pitch,
+                                     void* stream);
 
 /* Workspace bytes for the linear entry points (split-K partial sums). */
 /* (The workspace also holds the stream-K partial tiles and flags: the caller
@@ -272,6 +276,13 @@ qlrt_status qlrt_rope(const void* x, void* y, const void* cos_sin, int64_t rows,
  * slice of the concatenated q | k | v projection. */
 qlrt_status qlrt_rope_strided(const void* x, int64_t ldx, void* y, int64_t ldy, const void* cos_sin,
                               int64_t rows, int heads, int d, int seq, int inverse, void* stream);
+/* q | k | v rows of the concatenated projection -> rotated q, k and a copy
+ * of v ([rows][heads d] each); backward: inverse-rotated dq, dk and dv into
+ * the concatenated d[q | k | v] rows (one pass each way). */
+qlrt_status qlrt_rope_qkv_fwd(const void* ycat, void* q, void* k, void* v, const void* cos_sin, int64_t rows,
+                              int heads, int d, int seq, void* stream);
+qlrt_status qlrt_rope_qkv_bwd(const void* dq, const void* dk, const void* dv, void* dycat, const void* cos_sin,
+                              int64_t rows, int heads, int d, int seq, void* stream);
 /* SwiGLU over a concatenated [gate | up] projection (rows x 2 cols): out =
  * silu(g) * u [rows][cols]; backward writes d[gate | up]. */
 qlrt_status qlrt_swiglu_cat_fwd(const void* gu, void* out, int64_t rows, int64_t cols, void* stream);

@@ -59,6 +59,7 @@ _SIGS = {
     "qlrt_nf4_linear_bwd_ex": [POINTER(NF4Weight), c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
                                c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p],
     "qlrt_nf4_constants_into": [POINTER(NF4Weight), c_void_p, c_int64, c_void_p],
+    "qlrt_nf4_constants_group": [POINTER(NF4Weight), c_int, c_void_p, c_int64, c_void_p],
     "qlrt_nf4_linear_group_fwd": [POINTER(NF4Weight), c_int, c_void_p, c_int64, c_void_p, c_void_p, c_int, c_float,
                                   c_void_p, c_void_p, c_void_p, c_void_p],
     "qlrt_nf4_linear_group_bwd": [POINTER(NF4Weight), c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
@@ -84,6 +85,8 @@ _SIGS = {
     "qlrt_rope_strided": [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int, c_int, c_int, c_int,
                           c_void_p],
     "qlrt_swiglu_cat_fwd": [c_void_p, c_void_p, c_int64, c_int64, c_void_p],
+    "qlrt_rope_qkv_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_void_p],
+    "qlrt_rope_qkv_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_void_p],
     "qlrt_swiglu_cat_bwd": [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p],
     "qlrt_build_info": [],
     "qlrt_set_policy": [ctypes.c_char_p, c_int],

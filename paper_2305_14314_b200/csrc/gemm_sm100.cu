@@ -110,6 +110,11 @@ struct Args {
   // g aug_gstride (each member's [Ts_hi | Ts_lo] block of Ts_cat)
   int aug_gn, aug_gstride;
   int64_t aug_b2k;      // > 0: B2's own K extent (the whole Ts_cat row)
+  // grouped-K skinny GEMM (the members' dT in one launch): output columns
+  // [g kg_n, (g + 1) kg_n) reduce over K range [g kg_k, (g + 1) kg_k) of A and
+  // B, and read B rows [0, kg_n); kg_kfull = the operands' whole K extent
+  int kg_n;
+  int64_t kg_k, kg_kfull;
 };
 
 #ifndef QLRT_MERGE_FULL
@@ -514,6 +519,8 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           // each member's pair multiply the same l rows / columns)
           const int k0a = (aug && p.aug_wrap) ? (k0 / (2 * p.aug_wrap)) * p.aug_wrap + k0 % p.aug_wrap : k0;
           const int k0b = (aug && p.aug_gn) ? k0 + ((mt * BMP) / p.aug_gn) * p.aug_gstride : k0;
+          const int kgg = (!aug && p.kg_n) ? (nt * BN) / p.kg_n : 0;  // grouped-K member of this column tile
+          const int kadd = kgg * (int)p.kg_k, nsub = kgg * p.kg_n;
           const bool a_tma = aug || !NF4;
           if (aug && p.aug_pdl && !aug_ready) {  // B2 = the adapter product of the PDL predecessor
             asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -528,10 +535,10 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
           uint8_t* b_dst = sB + s * L::B_STAGE;
           if (a_tma) {
             if (amn) {
-              tma(ma, &full[s], a_dst, m_cta, k0a);
-              tma(ma, &full[s], a_dst + 8192, m_cta + 64, k0a);
+              tma(ma, &full[s], a_dst, m_cta, k0a + kadd);
+              tma(ma, &full[s], a_dst + 8192, m_cta + 64, k0a + kadd);
             } else {
-              tma(ma, &full[s], a_dst, k0a, m_cta);
+              tma(ma, &full[s], a_dst, k0a + kadd, m_cta);
             }
           }
           if (bmn) {
@@ -543,7 +550,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
               if (hh < 0 || hh == j)
                 tma(mb, &full[s], b_dst + j * (L::B_STAGE / NUM), k0b, nt * BN + j * UN + (int)rank * (UN / 2));
           } else {
-            tma(mb, &full[s], b_dst, k0b, n_cta);
+            tma(mb, &full[s], b_dst, k0b + kadd, n_cta - nsub);
           }
         }
       }
@@ -1112,6 +1119,25 @@ __global__ void dq_constants_kernel(const uint8_t* __restrict__ dq_codes, const 
   }
 }
 
+// the block constants of up to 4 sibling weights (one row pitch, member g in
+// columns [g nbr, (g + 1) nbr)) in one launch
+struct GroupConsts {
+  const uint8_t* dq_codes[4];
+  const float* c1[4];
+  const float* mu[4];
+};
+__global__ void dq_constants_group_kernel(GroupConsts gc, int groups, int64_t rows, int64_t nbr, int64_t kpitch,
+                                          int bs2, qlrt_fp8spec sp, float* __restrict__ out) {
+  const int64_t w = (int64_t)groups * nbr;
+  const int64_t total = rows * w;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / w, jj = i - r * w;
+    const int g = (int)(jj / nbr);
+    const int64_t j = jj - (int64_t)g * nbr, blk = r * nbr + j;
+    out[r * kpitch + jj] = dq_constant(gc.dq_codes[g][blk], gc.c1[g][blk / bs2], *gc.mu[g], sp);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -1400,12 +1426,16 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
   }
   const int64_t M = args.M, N = args.N;
   if (bn < 64 && (B.mn || (B2 && B2->mn))) return QLRT_ERR_UNSUPPORTED;
-  if (!nf4 && !(A.mn ? make_tmap(&ta, A.ptr, M, K, A.ld, 64) : make_tmap(&ta, A.ptr, K, M, A.ld, BM)))
+  const int64_t KA = args.kg_n ? args.kg_kfull : K;  // grouped-K: the operands' whole K extent
+  if (args.kg_n && (nf4 || A.mn || B.mn || args.pair || bn % 64 || args.kg_n % bn || args.kg_k % BK))
+    return QLRT_ERR_UNSUPPORTED;
+  if (!nf4 && !(A.mn ? make_tmap(&ta, A.ptr, M, KA, A.ld, 64) : make_tmap(&ta, A.ptr, KA, M, A.ld, BM)))
     return QLRT_ERR_UNSUPPORTED;
   if (args.pair && ((bn != 256 && bn != 512) || (B2 && B2->mn && bn / 2 < 64))) return QLRT_ERR_UNSUPPORTED;
   if (bn == 512 && (!args.pair || B.mn || (B2 && B2->mn))) return QLRT_ERR_UNSUPPORTED;
   const int bbox = args.pair ? (bn > 256 ? 128 : bn / 2) : bn;  // B rows per TMA box
-  if (!(B.mn ? make_tmap(&tb, B.ptr, N, K, B.ld, 64) : make_tmap(&tb, B.ptr, K, N, B.ld, bbox)))
+  if (!(B.mn ? make_tmap(&tb, B.ptr, N, KA, B.ld, 64)
+             : make_tmap(&tb, B.ptr, KA, args.kg_n ? args.kg_n : N, B.ld, bbox)))
     return QLRT_ERR_UNSUPPORTED;
   if (K2) {
     const int64_t K2a = args.aug_wrap ? K2 / 2 : K2;  // A2's own K extent
@@ -1450,7 +1480,7 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
     const int64_t waves = (tiles + units - 1) / units;
     const int64_t T = args.k_iters + args.k_iters_aug;
     args.streamk = waves <= 2 && (double)tiles / (double)(waves * units) < 0.9 && T * tiles >= 2 * units;
-    if (args.aug_pdl) args.streamk = 0;
+    if (args.aug_pdl || args.kg_n) args.streamk = 0;
     // the flags are zero between launches: every owner re-arms the flags it
     // consumed; the caller zero-fills the region once (qlrt_streamk_init)
   } else {
@@ -1515,10 +1545,13 @@ static int pick_splits(int64_t tiles, int64_t k_iters, int64_t per_split_bytes, 
 static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, int64_t N, int64_t K, float alpha,
                          void* out, int64_t ldo, int out_f32, int out_t, float* ws, size_t ws_bytes, cudaStream_t s,
                          int fold = 0, int out_split = 0, const Args* sk = nullptr, int pdl_independent = 0,
-                         int cl2 = 0, int units_cap = 0) {
+                         int cl2 = 0, int units_cap = 0, int kg_n = 0, int64_t kg_kfull = 0) {
   Args a{};
   a.cl2 = cl2;
   a.units_cap = units_cap;
+  a.kg_n = kg_n;  // grouped-K (see Args): member width along N, K = one member's K extent
+  a.kg_k = kg_n ? K : 0;
+  a.kg_kfull = kg_kfull;
   // pdl_independent: inputs only (nothing from the PDL predecessor) -- start
   // at once beside it, complete only after it (see Args::wait_at_end)
   a.aug_pdl = pdl_independent;
@@ -1539,7 +1572,7 @@ static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, 
   const int64_t kit = (K + BK - 1) / BK;
   // (off by default: measured slower than split-K + reduce on the C2 LoRA shapes,
   //  tools/ab_skinny.py; QLRT_STREAMK_SKINNY=1 enables it)
-  if (policy(P_STREAMK_SKINNY) && sk && sk->sk_ws && streamk_policy() && !(out_split && out_t) &&
+  if (policy(P_STREAMK_SKINNY) && !kg_n && sk && sk->sk_ws && streamk_policy() && !(out_split && out_t) &&
       (!fold || (2 * fold <= bn && N <= bn))) {
     // skinny GEMM: stream-K over all SMs, partials reduced in-kernel, fold /
     // hi-lo split applied in the epilogue -- no split-K workspace, no reduce launch
@@ -1553,7 +1586,7 @@ static qlrt_status plain(int bn, const Operand& A, const Operand& B, int64_t M, 
   // kernel.  Off by default (QLRT_CSPLIT=1 enables it): measured 1.7-2.9x
   // slower than split-K + the reduce kernel on the C2 LoRA shapes
   // (tools/ab_skinny.py) -- clusters of 1-CTA-per-SM kernels co-schedule poorly
-  if (policy(P_CSPLIT) && tiles < 74 && !(out_split && out_t) && bn <= 256 && a.pair == 0 &&
+  if (policy(P_CSPLIT) && !kg_n && tiles < 74 && !(out_split && out_t) && bn <= 256 && a.pair == 0 &&
       (!fold || (2 * fold <= bn && N <= bn))) {
     int S = 1;
     while (S < 8 && tiles * (S + 1) <= num_sms() && (S + 1) * 4 <= kit) ++S;
@@ -1700,6 +1733,30 @@ qlrt_status qlrt_nf4_constants_into(const qlrt_nf4_weight* w, float* out, int64_
   if (g > 148 * 8) g = 148 * 8;
   gemm::dq_constants_kernel<<<(int)g, 256, 0, (cudaStream_t)stream>>>(w->dq_codes, w->c1, w->mu, w->k_in, nbr, pitch,
                                                                       nbr, w->blocksize2, w->spec, out);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_nf4_constants_group(const qlrt_nf4_weight* members, int groups, float* out, int64_t pitch,
+                                     void* stream) {
+  // every member's constants into one concatenated cache (one launch)
+  if (!members || groups < 1 || groups > 4 || !out) return QLRT_ERR_ARG;
+  gemm::GroupConsts gc{};
+  for (int g = 0; g < groups; ++g) {
+    const qlrt_nf4_weight& w = members[g];
+    if (!w.dq_codes || !w.c1 || !w.mu || w.n_out % 64 || w.k_in != members[0].k_in || w.n_out != members[0].n_out ||
+        w.blocksize2 != members[0].blocksize2 || w.blocksize2 <= 0)
+      return QLRT_ERR_ARG;
+    gc.dq_codes[g] = w.dq_codes;
+    gc.c1[g] = w.c1;
+    gc.mu[g] = w.mu;
+  }
+  const int64_t nbr = members[0].n_out / 64;
+  if (pitch < groups * nbr) return QLRT_ERR_ARG;
+  int64_t g = (members[0].k_in * groups * nbr + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  gemm::dq_constants_group_kernel<<<(int)g, 256, 0, (cudaStream_t)stream>>>(
+      gc, groups, members[0].k_in, nbr, pitch, members[0].blocksize2, members[0].spec, out);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }
@@ -2012,11 +2069,12 @@ qlrt_status qlrt_nf4_linear_group_bwd(const qlrt_nf4_weight* w, int groups, cons
   gemm::sk_region(workspace, ws_bytes, K, N, R, sk);
   qlrt_status rc;
   typedef __nv_bfloat16 bf;
-  // dT_g = s dY_g l2_g^T into member g's [hi | lo] block of dT_cat
-  for (int g = 0; g < groups; ++g) {
-    Operand DA{(const bf*)dy + g * Ng, N, 0}, DB{(const bf*)l2 + g * Ng, N, 0};
-    rc = gemm::plain(64, DA, DB, m, rank, Ng, s, (bf*)dt_out + 2 * g * rank, 2 * R, 0, 0, (float*)workspace,
-                     part_bytes, st, 0, rank, &sk);
+  // dT_g = s dY_g l2_g^T into member g's [hi | lo] block of dT_cat: one
+  // grouped-K launch (column tile g reduces over member g's K range)
+  {
+    Operand DA{dy, N, 0}, DB{l2, N, 0};
+    rc = gemm::plain(64, DA, DB, m, R, Ng, s, dt_out, 2 * R, 0, 0, (float*)workspace, part_bytes, st, 0, rank, &sk,
+                     0, 0, 0, rank, N);
     if (rc != QLRT_OK) return rc;
   }
   gemm::SideCtx* sctx = gemm::side_ctx(st);

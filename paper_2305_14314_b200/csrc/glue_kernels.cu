@@ -158,6 +158,40 @@ __global__ void rope_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, 
   }
 }
 
+// q | k | v rows of the concatenated projection <-> separate q, k, v (rows x
+// h, h = heads * d): forward rotates q and k and copies v out of ycat;
+// backward (sign = -1) writes the inverse-rotated dq, dk and dv into dycat
+template <bool FWD>
+__global__ void rope_qkv_kernel(const uint4* __restrict__ a, const uint4* __restrict__ b, const uint4* __restrict__ c,
+                                uint4* __restrict__ x, uint4* __restrict__ y, uint4* __restrict__ z,
+                                const float2* __restrict__ cs, int64_t rows, int h8, int d, int seq) {
+  // FWD: a = ycat (rows x 3 h8), x / y / z = q / k / v;  BWD: a / b / c = dq / dk / dv, x = dycat
+  const int d8 = d / 8;
+  const int64_t total = rows * 3 * h8;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = k / (3 * h8);
+    const int w = (int)(k - row * 3 * h8), part = w / h8, e = w - part * h8;
+    uint4 v;
+    if (FWD) v = a[k];
+    else v = (part == 0 ? a : part == 1 ? b : c)[row * h8 + e];
+    if (part < 2) {
+      const int pos = (int)(row % seq), c8 = e % d8;
+      const float2* t = cs + (int64_t)pos * (d / 2) + c8 * 4;
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 r = t[j];
+        const float x0 = bf_lo(wv[j]), x1 = bf_hi(wv[j]), sn = FWD ? r.y : -r.y;
+        o[j] = pack_bf16x2(x0 * r.x - x1 * sn, x0 * sn + x1 * r.x);
+      }
+      v = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    if (FWD) (part == 0 ? x : part == 1 ? y : z)[row * h8 + e] = v;
+    else x[k] = v;
+  }
+}
+
 static int grid_for(int64_t n, int tpb) {
   int64_t g = (n + tpb - 1) / tpb;
   return (int)(g < (int64_t)kNumSMs * 8 ? (g < 1 ? 1 : g) : (int64_t)kNumSMs * 8);
@@ -223,6 +257,27 @@ qlrt_status qlrt_rope_strided(const void* x, int64_t ldx, void* y, int64_t ldy, 
   glue::rope_kernel<<<glue::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
       (const uint4*)x, (uint4*)y, (const float2*)cos_sin, rows, heads, d, seq, inverse ? -1.0f : 1.0f, ldx / 8,
       ldy / 8);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+qlrt_status qlrt_rope_qkv_fwd(const void* ycat, void* q, void* k, void* v, const void* cos_sin, int64_t rows,
+                              int heads, int d, int seq, void* stream) {
+  if (!ycat || !q || !k || !v || !cos_sin || rows <= 0 || heads <= 0 || d <= 0 || (d % 8) || seq <= 0)
+    return QLRT_ERR_ARG;
+  const int h8 = heads * d / 8;
+  glue::rope_qkv_kernel<true><<<glue::grid_for(rows * 3 * h8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)ycat, nullptr, nullptr, (uint4*)q, (uint4*)k, (uint4*)v, (const float2*)cos_sin, rows, h8, d, seq);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+qlrt_status qlrt_rope_qkv_bwd(const void* dq, const void* dk, const void* dv, void* dycat, const void* cos_sin,
+                              int64_t rows, int heads, int d, int seq, void* stream) {
+  if (!dq || !dk || !dv || !dycat || !cos_sin || rows <= 0 || heads <= 0 || d <= 0 || (d % 8) || seq <= 0)
+    return QLRT_ERR_ARG;
+  const int h8 = heads * d / 8;
+  glue::rope_qkv_kernel<false><<<glue::grid_for(rows * 3 * h8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)dq, (const uint4*)dk, (const uint4*)dv, (uint4*)dycat, nullptr, nullptr, (const float2*)cos_sin,
+      rows, h8, d, seq);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }

@@ -140,12 +140,9 @@ class _QKVFn(torch.autograd.Function):
         d = h // nh
         ycat, cache = grp.forward(x)
         q = torch.empty(b, s, nh, d, dtype=ycat.dtype, device=ycat.device)
-        k = torch.empty_like(q)
-        L = lib()
-        check(L.qlrt_rope_strided(ptr(ycat), 3 * h, ptr(q), h, ptr(cos_sin), b * s, nh, d, s, 0, stream_ptr()), "rope q")
-        check(L.qlrt_rope_strided(ptr(ycat) + 2 * h, 3 * h, ptr(k), h, ptr(cos_sin), b * s, nh, d, s, 0, stream_ptr()),
-              "rope k")
-        v = ycat[:, 2 * h:].contiguous().view(b, s, nh, d)
+        k, v = torch.empty_like(q), torch.empty_like(q)
+        check(lib().qlrt_rope_qkv_fwd(ptr(ycat), ptr(q), ptr(k), ptr(v), ptr(cos_sin), b * s, nh, d, s, stream_ptr()),
+              "rope qkv")
         ctx.grp, ctx.cache, ctx.gviews, ctx.notify, ctx.defer = grp, cache, gviews, notify, defer
         ctx.save_for_backward(cos_sin)
         ctx.dims = (b, s, h, nh, d)
@@ -155,14 +152,10 @@ class _QKVFn(torch.autograd.Function):
     def backward(ctx, dq, dk, dv):
         (cos_sin,) = ctx.saved_tensors
         b, s, h, nh, d = ctx.dims
-        dq, dk = dq.contiguous(), dk.contiguous()
+        dq, dk, dv = dq.contiguous(), dk.contiguous(), dv.contiguous()
         dycat = torch.empty(b * s, 3 * h, dtype=dq.dtype, device=dq.device)
-        L = lib()
-        check(L.qlrt_rope_strided(ptr(dq), h, ptr(dycat), 3 * h, ptr(cos_sin), b * s, nh, d, s, 1, stream_ptr()),
-              "rope q bwd")
-        check(L.qlrt_rope_strided(ptr(dk), h, ptr(dycat) + 2 * h, 3 * h, ptr(cos_sin), b * s, nh, d, s, 1,
-                                  stream_ptr()), "rope k bwd")
-        dycat[:, 2 * h:].view(b, s, nh, d).copy_(dv)
+        check(lib().qlrt_rope_qkv_bwd(ptr(dq), ptr(dk), ptr(dv), ptr(dycat), ptr(cos_sin), b * s, nh, d, s,
+                                      stream_ptr()), "rope qkv bwd")
         dx = ctx.grp.backward(dycat, ctx.cache, ctx.gviews["l1"], ctx.gviews["l2"],
                               defer=ctx.defer() if ctx.defer is not None else None)
         ctx.cache = None

@@ -19,6 +19,8 @@ master copies are float32, mirrored to bf16 for the MMAs.
 
 from __future__ import annotations
 
+import ctypes
+
 from dataclasses import dataclass, field
 from typing import Any
 
@@ -508,13 +510,12 @@ class QLinearGroup:
         self.bases = bases
         self._ops = [l1b, l2b, None] if l1b is not None else None
         self._wdesc = None
-        self._member_desc = []
-        for b in bases:
-            d = _native.NF4Weight()
+        self._member_desc = (_native.NF4Weight * g)()
+        for i, b in enumerate(bases):
+            d = self._member_desc[i]
             d.dq_codes, d.c1, d.mu = ptr(b.dq.codes), ptr(b.dq.c1), ptr(b.dq.mu)
             d.k_in, d.n_out, d.blocksize2 = k, ng, b.dq.blocksize2
             d.spec = b.dq.spec.to_c()
-            self._member_desc.append(d)
 
     @property
     def scaling(self) -> float:
@@ -549,10 +550,16 @@ class QLinearGroup:
         forward, shared with the backward; padding columns stay zero)."""
         L = lib()
         pitch = int(L.qlrt_nf4_constants_bytes(self.in_dim, self.out_dim)) // 4 // self.in_dim
-        out = torch.zeros(self.in_dim, pitch, dtype=torch.float32, device=self.l1.device)
         nbr = self.n_member // 64
-        for i, d in enumerate(self._member_desc):
-            check(L.qlrt_nf4_constants_into(d, ptr(out) + 4 * i * nbr, pitch, stream_ptr()), "QLinearGroup constants")
+        alloc = torch.empty if pitch == self.groups * nbr else torch.zeros  # (padding columns must read 0)
+        out = alloc(self.in_dim, pitch, dtype=torch.float32, device=self.l1.device)
+        if self.groups <= 4:
+            check(L.qlrt_nf4_constants_group(self._member_desc, self.groups, ptr(out), pitch, stream_ptr()),
+                  "QLinearGroup constants")
+        else:
+            for i in range(self.groups):
+                check(L.qlrt_nf4_constants_into(ctypes.byref(self._member_desc[i]), ptr(out) + 4 * i * nbr, pitch,
+                                                stream_ptr()), "QLinearGroup constants")
         return out
 
     def _workspace(self, m: int, side: bool = False) -> torch.Tensor:

@@ -90,6 +90,38 @@ def test_glue_kernels_match_torch(cuda):
     rr.backward(dr.float())
     assert (r.float() - rr).abs().max() <= 2e-2 * rr.abs().max()
     assert (t.grad.float() - tr.grad).abs().max() <= 2e-2 * tr.grad.abs().max()
+    # the grouped-projection glue: RoPE / copy over concatenated q | k | v
+    # rows, SwiGLU over concatenated gate | up rows (forward and backward)
+    from paper_2305_14314_b200._native import lib, ptr, stream_ptr
+    b_, s_, nh, d = 2, 16, 4, 64
+    h = nh * d
+    ycat = torch.randn(b_ * s_, 3 * h, device="cuda", generator=g).bfloat16()
+    q, k, v = (torch.empty(b_, s_, nh, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    assert lib().qlrt_rope_qkv_fwd(ptr(ycat), ptr(q), ptr(k), ptr(v), ptr(cs), b_ * s_, nh, d, s_, stream_ptr()) == 0
+    yv = ycat.float().view(b_, s_, 3, nh, d)
+    for got, want in ((q, rope_reference(yv[:, :, 0], cs)), (k, rope_reference(yv[:, :, 1], cs)), (v, yv[:, :, 2])):
+        assert (got.float() - want).abs().max() <= 2e-2 * want.abs().max()
+    dq, dk, dv = (torch.randn(b_, s_, nh, d, device="cuda", generator=g).bfloat16() for _ in range(3))
+    dycat = torch.empty(b_ * s_, 3 * h, device="cuda", dtype=torch.bfloat16)
+    assert lib().qlrt_rope_qkv_bwd(ptr(dq), ptr(dk), ptr(dv), ptr(dycat), ptr(cs), b_ * s_, nh, d, s_,
+                                   stream_ptr()) == 0
+    inv = torch.stack((cs[..., 0], -cs[..., 1]), dim=-1)  # the inverse rotation
+    dv_ = dycat.float().view(b_, s_, 3, nh, d)
+    for got, want in ((dv_[:, :, 0], rope_reference(dq.float(), inv)), (dv_[:, :, 1], rope_reference(dk.float(), inv)),
+                      (dv_[:, :, 2], dv.float())):
+        assert (got - want).abs().max() <= 2e-2 * want.abs().max()
+    gu = torch.randn(300, 2 * 64, device="cuda", generator=g).bfloat16()
+    out = torch.empty(300, 64, device="cuda", dtype=torch.bfloat16)
+    assert lib().qlrt_swiglu_cat_fwd(ptr(gu), ptr(out), 300, 64, stream_ptr()) == 0
+    gr_, ur_ = gu.float()[:, :64].requires_grad_(True), gu.float()[:, 64:].requires_grad_(True)
+    orf = F.silu(gr_) * ur_
+    assert (out.float() - orf).abs().max() <= 2e-2 * orf.abs().max()
+    do = torch.randn(300, 64, device="cuda", generator=g).bfloat16()
+    dgu = torch.empty_like(gu)
+    assert lib().qlrt_swiglu_cat_bwd(ptr(gu), ptr(do), ptr(dgu), 300, 64, stream_ptr()) == 0
+    orf.backward(do.float())
+    assert (dgu.float()[:, :64] - gr_.grad).abs().max() <= 2e-2 * gr_.grad.abs().max()
+    assert (dgu.float()[:, 64:] - ur_.grad).abs().max() <= 2e-2 * ur_.grad.abs().max()
 
 
 def _tiny(seed=0, cfg_kw=None, **model_kw):

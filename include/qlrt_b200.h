@@ -129,6 +129,23 @@ qlrt_status qlrt_nf4_constants_into(const qlrt_nf4_weight* w, float* out, int64_
 qlrt_status qlrt_nf4_constants_group(const qlrt_nf4_weight* members, int groups, float* out, int64_t pitch,
                                      void* stream);
 
+/* Step-level prepass: the block constants of many weights in one launch.
+ * jobs_dev (device memory) lists, per weight (or member of a group), its DQ
+ * data and where its [rows][nbr] constants go (row pitch `pitch` floats);
+ * max_elems = the largest rows * nbr.  The fused kernels then read the
+ * caches (qlrt_nf4_weight.consts) instead of rebuilding them per call. */
+typedef struct {
+  const uint8_t* dq_codes;
+  const float* c1;
+  const float* mu;
+  float* out;
+  int64_t rows, nbr, pitch;
+  int blocksize2;
+  qlrt_fp8spec spec;
+} qlrt_nf4_const_job;
+qlrt_status qlrt_nf4_constants_batch(const qlrt_nf4_const_job* jobs_dev, int n_jobs, int64_t max_elems,
+                                     void* stream);
+
 /* Workspace bytes for the linear entry points (split-K partial sums). */
 /* (The workspace also holds the stream-K partial tiles and flags: the caller
  * zero-fills a new workspace once -- the flags must start at 0, and every

@@ -38,6 +38,11 @@ class NF4Weight(ctypes.Structure):
                 ("spec", Fp8SpecC), ("values", c_double * 16), ("consts", c_void_p)]
 
 
+class ConstJob(ctypes.Structure):
+    _fields_ = [("dq_codes", c_void_p), ("c1", c_void_p), ("mu", c_void_p), ("out", c_void_p), ("rows", c_int64),
+                ("nbr", c_int64), ("pitch", c_int64), ("blocksize2", c_int), ("spec", Fp8SpecC)]
+
+
 _SIGS = {
     "qlrt_quantize4": [c_void_p, c_int, c_int64, c_int, POINTER(Codebook4), c_void_p, c_void_p, c_void_p, c_void_p],
     "qlrt_dq_workspace_bytes": [c_int64],
@@ -60,6 +65,7 @@ _SIGS = {
                                c_float, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p],
     "qlrt_nf4_constants_into": [POINTER(NF4Weight), c_void_p, c_int64, c_void_p],
     "qlrt_nf4_constants_group": [POINTER(NF4Weight), c_int, c_void_p, c_int64, c_void_p],
+    "qlrt_nf4_constants_batch": [c_void_p, c_int, c_int64, c_void_p],
     "qlrt_nf4_linear_group_fwd": [POINTER(NF4Weight), c_int, c_void_p, c_int64, c_void_p, c_void_p, c_int, c_float,
                                   c_void_p, c_void_p, c_void_p, c_void_p],
     "qlrt_nf4_linear_group_bwd": [POINTER(NF4Weight), c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,

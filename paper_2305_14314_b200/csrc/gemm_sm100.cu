@@ -1138,6 +1138,18 @@ __global__ void dq_constants_group_kernel(GroupConsts gc, int groups, int64_t ro
   }
 }
 
+// many weights' block constants in one launch (blockIdx.y = job): the
+// step-level prepass of a model's frozen linears
+__global__ void dq_constants_batch_kernel(const qlrt_nf4_const_job* __restrict__ jobs) {
+  const qlrt_nf4_const_job j = jobs[blockIdx.y];
+  const float m = *j.mu;
+  const int64_t total = j.rows * j.nbr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / j.nbr, c = i - r * j.nbr;
+    j.out[r * j.pitch + c] = dq_constant(j.dq_codes[i], j.c1[i / j.blocksize2], m, j.spec);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -1757,6 +1769,16 @@ qlrt_status qlrt_nf4_constants_group(const qlrt_nf4_weight* members, int groups,
   if (g > 148 * 8) g = 148 * 8;
   gemm::dq_constants_group_kernel<<<(int)g, 256, 0, (cudaStream_t)stream>>>(
       gc, groups, members[0].k_in, nbr, pitch, members[0].blocksize2, members[0].spec, out);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_nf4_constants_batch(const qlrt_nf4_const_job* jobs_dev, int n_jobs, int64_t max_elems,
+                                     void* stream) {
+  if (!jobs_dev || n_jobs < 1 || n_jobs > 65535 || max_elems < 1) return QLRT_ERR_ARG;
+  int64_t gx = (max_elems + 255) / 256;
+  if (gx > 64) gx = 64;  // (grid-stride: n_jobs x 64 CTAs keep every SM busy)
+  gemm::dq_constants_batch_kernel<<<dim3((unsigned)gx, (unsigned)n_jobs), 256, 0, (cudaStream_t)stream>>>(jobs_dev);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }

@@ -44,6 +44,7 @@ import torch
 import torch.nn.functional as F
 import torch.utils.checkpoint as _ckpt
 
+from . import _native
 from ._native import check, lib, ptr, stream_ptr
 from .blockquant import quantize
 from .codebooks import get_codebook
@@ -415,6 +416,7 @@ class LlamaQLoRA:
             self.layers.append(lay)
         if self.grouped:
             self.shadow_flat.copy_(self.params_flat)
+        self._build_constant_jobs()
         d = h // cfg.n_heads
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, d, 2, device=self.dev, dtype=torch.float32) / d))
         ang = torch.outer(torch.arange(cfg.seq, device=self.dev, dtype=torch.float32), inv)
@@ -440,6 +442,43 @@ class LlamaQLoRA:
         self.sumsq = _sumsq_scratch(self.dev)
 
     # ------------------------------------------------------------------ model
+    def _build_constant_jobs(self) -> None:
+        """The frozen bases' block constants are double-dequantized once per
+        step for every linear in ONE launch (qlrt_nf4_constants_batch) into
+        per-unit caches the fused kernels read (the per-call prepass chain --
+        one or more small launches in front of every fused GEMM -- leaves the
+        critical path).  The caches hold what the forward kept for the
+        backward anyway (the reference keeps cache['w'], qlora.py:146-147)."""
+        L = lib()
+        jobs, self._consts = [], []
+        max_elems = 1
+        for lay in self.layers:
+            for un, members in self.units:
+                lin = lay[un] if self.grouped else lay[members[0]]
+                a_, b_ = self.cfg.proj_shape(members[0])
+                pitch = int(L.qlrt_nf4_constants_bytes(a_, len(members) * b_)) // 4 // a_
+                buf = torch.zeros(a_, pitch, dtype=torch.float32, device=self.dev)
+                lin.consts_cache = buf
+                self._consts.append(buf)
+                nbr = b_ // 64
+                for g_, pj in enumerate(members):
+                    q = lay[pj].base
+                    j = _native.ConstJob()
+                    j.dq_codes, j.c1, j.mu = ptr(q.dq.codes), ptr(q.dq.c1), ptr(q.dq.mu)
+                    j.out = ptr(buf) + 4 * g_ * nbr
+                    j.rows, j.nbr, j.pitch, j.blocksize2 = a_, nbr, pitch, q.dq.blocksize2
+                    j.spec = q.dq.spec.to_c()
+                    jobs.append(j)
+                    max_elems = max(max_elems, a_ * nbr)
+        arr = (_native.ConstJob * len(jobs))(*jobs)
+        self._const_jobs = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(self.dev)
+        self._const_n, self._const_max = len(jobs), max_elems
+
+    def refresh_constants(self) -> None:
+        """The step-level block-constant prepass (one launch, capturable)."""
+        check(lib().qlrt_nf4_constants_batch(ptr(self._const_jobs), self._const_n, self._const_max, stream_ptr()),
+              "constants prepass")
+
     def _proj_done(self, li: int) -> None:
         self._pending[li] -= 1
         if self._pending[li] != 0:
@@ -514,6 +553,7 @@ class LlamaQLoRA:
     def loss(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         cfg = self.cfg
         b, s = tokens.shape
+        self.refresh_constants()
         x = F.embedding(tokens, self.embed)
         for li in range(cfg.n_layers):
             if self.checkpoint:

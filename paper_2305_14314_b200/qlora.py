@@ -118,6 +118,9 @@ class QLinear:
         self._cat = None
         self._ws = None
         self._wdesc = None
+        # a block-constant cache kept current by the caller (a step-level
+        # prepass, qlrt_nf4_constants_batch); None: rebuilt every forward
+        self.consts_cache: torch.Tensor | None = None
 
     @property
     def in_dim(self) -> int:
@@ -319,7 +322,7 @@ class QLinear:
             ts_ready = False
         elif self.fused():
             # fp32 block constants built once here and shared with backward
-            consts = self._constants()
+            consts = self.consts_cache if self.consts_cache is not None else self._constants()
             l1b, l2b = self._operands() if n_ad else (None, None)
             if n_ad == 1:
                 ad = self.adapters[0]
@@ -510,6 +513,7 @@ class QLinearGroup:
         self.bases = bases
         self._ops = [l1b, l2b, None] if l1b is not None else None
         self._wdesc = None
+        self.consts_cache: torch.Tensor | None = None  # (as QLinear.consts_cache)
         self._member_desc = (_native.NF4Weight * g)()
         for i, b in enumerate(bases):
             d = self._member_desc[i]
@@ -578,7 +582,7 @@ class QLinearGroup:
         if x2.dtype != torch.bfloat16 or not x2.is_contiguous():
             x2 = x2.to(torch.bfloat16).contiguous()
         m = x2.shape[0]
-        consts = self._constants()
+        consts = self.consts_cache if self.consts_cache is not None else self._constants()
         l1b, l2b = self.operands()
         ts = torch.empty(m, 2 * self.groups * self.rank, dtype=torch.bfloat16, device=x2.device)
         y = torch.empty(m, self.out_dim, dtype=torch.bfloat16, device=x2.device)

@@ -300,6 +300,14 @@ qlrt_status qlrt_rope_qkv_fwd(const void* ycat, void* q, void* k, void* v, const
                               int heads, int d, int seq, void* stream);
 qlrt_status qlrt_rope_qkv_bwd(const void* dq, const void* dk, const void* dv, void* dycat, const void* cos_sin,
                               int64_t rows, int heads, int d, int seq, void* stream);
+/* Cross entropy of bf16 logit rows (targets in [0, vocab)): per-row loss =
+ * logsumexp - logit[target] and the row's logsumexp (fp32); backward writes
+ * bf16 d logits = (softmax - onehot) * grad / rows (mean reduction; grad =
+ * the device scalar upstream gradient). */
+qlrt_status qlrt_xent_fwd(const void* logits, const int64_t* targets, int64_t rows, int64_t vocab, float* loss,
+                          float* lse, void* stream);
+qlrt_status qlrt_xent_bwd(const void* logits, const int64_t* targets, const float* lse, const float* grad,
+                          int64_t rows, int64_t vocab, void* dlogits, void* stream);
 /* SwiGLU over a concatenated [gate | up] projection (rows x 2 cols): out =
  * silu(g) * u [rows][cols]; backward writes d[gate | up]. */
 qlrt_status qlrt_swiglu_cat_fwd(const void* gu, void* out, int64_t rows, int64_t cols, void* stream);

@@ -91,6 +91,8 @@ _SIGS = {
     "qlrt_rope_strided": [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int, c_int, c_int, c_int,
                           c_void_p],
     "qlrt_swiglu_cat_fwd": [c_void_p, c_void_p, c_int64, c_int64, c_void_p],
+    "qlrt_xent_fwd": [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p],
+    "qlrt_xent_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p],
     "qlrt_rope_qkv_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_void_p],
     "qlrt_rope_qkv_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_void_p],
     "qlrt_swiglu_cat_bwd": [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p],

@@ -192,6 +192,85 @@ __global__ void rope_qkv_kernel(const uint4* __restrict__ a, const uint4* __rest
   }
 }
 
+// cross entropy over bf16 logit rows (the harness's loss; torch computes it
+// in fp32 from a materialized fp32 copy of the logits): one CTA per row,
+// online max / sum-exp in one pass, loss[row] = lse - x[target]
+__global__ void __launch_bounds__(256) xent_fwd_kernel(const uint4* __restrict__ logits, const int64_t* __restrict__ tgt,
+                                                       int v8, float* __restrict__ loss, float* __restrict__ lse_out) {
+  __shared__ float sm[8], ss[8];
+  const int64_t row = blockIdx.x;
+  const uint4* x = logits + row * v8;
+  float m = -INFINITY, sum = 0.0f;
+  for (int i = threadIdx.x; i < v8; i += blockDim.x) {
+    const uint4 u = x[i];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    float e[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      e[2 * j] = bf_lo(w[j]);
+      e[2 * j + 1] = bf_hi(w[j]);
+    }
+    float bm = e[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) bm = fmaxf(bm, e[j]);
+    const float nm = fmaxf(m, bm);
+    float acc = sum * __expf(m - nm);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += __expf(e[j] - nm);
+    m = nm;
+    sum = acc;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, sum, o);
+    const float nm = fmaxf(m, om);
+    sum = (m == -INFINITY ? 0.0f : sum * __expf(m - nm)) + (om == -INFINITY ? 0.0f : os * __expf(om - nm));
+    m = nm;
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sm[w] = m;
+    ss[w] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = sm[0], S = ss[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+      const float nm = fmaxf(M, sm[i]);
+      S = S * __expf(M - nm) + ss[i] * __expf(sm[i] - nm);
+      M = nm;
+    }
+    const float lse = M + logf(S);
+    const int64_t t = tgt[row];
+    const unsigned short xb = reinterpret_cast<const unsigned short*>(x)[t];
+    loss[row] = lse - __uint_as_float((uint32_t)xb << 16);
+    lse_out[row] = lse;
+  }
+}
+// d logits[row][v] = (softmax - onehot(target)) * g / rows   (bf16 out)
+__global__ void xent_bwd_kernel(const uint4* __restrict__ logits, const int64_t* __restrict__ tgt,
+                                const float* __restrict__ lse, const float* __restrict__ grad, int v8, float inv_rows,
+                                uint4* __restrict__ dlogits) {
+  const int64_t row = blockIdx.x;
+  const float L = lse[row], sc = *grad * inv_rows;
+  const int64_t t = tgt[row];
+  const uint4* x = logits + row * v8;
+  uint4* d = dlogits + row * v8;
+  for (int i = threadIdx.x; i < v8; i += blockDim.x) {
+    const uint4 u = x[i];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t v0 = (int64_t)i * 8 + 2 * j;
+      const float p0 = __expf(bf_lo(w[j]) - L) - (v0 == t ? 1.0f : 0.0f);
+      const float p1 = __expf(bf_hi(w[j]) - L) - (v0 + 1 == t ? 1.0f : 0.0f);
+      o[j] = pack_bf16x2(p0 * sc, p1 * sc);
+    }
+    d[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 static int grid_for(int64_t n, int tpb) {
   int64_t g = (n + tpb - 1) / tpb;
   return (int)(g < (int64_t)kNumSMs * 8 ? (g < 1 ? 1 : g) : (int64_t)kNumSMs * 8);
@@ -278,6 +357,22 @@ qlrt_status qlrt_rope_qkv_bwd(const void* dq, const void* dk, const void* dv, vo
   glue::rope_qkv_kernel<false><<<glue::grid_for(rows * 3 * h8, 256), 256, 0, (cudaStream_t)stream>>>(
       (const uint4*)dq, (const uint4*)dk, (const uint4*)dv, (uint4*)dycat, nullptr, nullptr, (const float2*)cos_sin,
       rows, h8, d, seq);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+qlrt_status qlrt_xent_fwd(const void* logits, const int64_t* targets, int64_t rows, int64_t vocab, float* loss,
+                          float* lse, void* stream) {
+  if (!logits || !targets || !loss || !lse || rows <= 0 || vocab <= 0 || (vocab % 8)) return QLRT_ERR_ARG;
+  glue::xent_fwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>((const uint4*)logits, targets,
+                                                                          (int)(vocab / 8), loss, lse);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+qlrt_status qlrt_xent_bwd(const void* logits, const int64_t* targets, const float* lse, const float* grad,
+                          int64_t rows, int64_t vocab, void* dlogits, void* stream) {
+  if (!logits || !targets || !lse || !grad || !dlogits || rows <= 0 || vocab <= 0 || (vocab % 8)) return QLRT_ERR_ARG;
+  glue::xent_bwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)logits, targets, lse, grad, (int)(vocab / 8), 1.0f / (float)rows, (uint4*)dlogits);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }

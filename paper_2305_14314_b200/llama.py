@@ -267,6 +267,33 @@ class _RoPEFn(torch.autograd.Function):
         return dx, None
 
 
+class _XentFn(torch.autograd.Function):
+    """Mean cross entropy straight from the bf16 logits (no fp32 copy of the
+    [tokens x vocab] matrix): per-row logsumexp in one pass; the backward
+    recomputes softmax - onehot from the saved logsumexp."""
+
+    @staticmethod
+    def forward(ctx, logits, targets):
+        rows, vocab = logits.shape
+        logits = logits.contiguous()
+        tg = targets.reshape(-1).to(torch.int64).contiguous()
+        loss = torch.empty(rows, dtype=torch.float32, device=logits.device)
+        lse = torch.empty(rows, dtype=torch.float32, device=logits.device)
+        check(lib().qlrt_xent_fwd(ptr(logits), ptr(tg), rows, vocab, ptr(loss), ptr(lse), stream_ptr()), "xent")
+        ctx.save_for_backward(logits, tg, lse)
+        return loss.mean()
+
+    @staticmethod
+    def backward(ctx, g):
+        logits, tg, lse = ctx.saved_tensors
+        rows, vocab = logits.shape
+        d = torch.empty_like(logits)
+        g = g.to(torch.float32).reshape(1).contiguous()
+        check(lib().qlrt_xent_bwd(ptr(logits), ptr(tg), ptr(lse), ptr(g), rows, vocab, ptr(d), stream_ptr()),
+              "xent bwd")
+        return d, None
+
+
 def _rmsnorm(x: torch.Tensor, eps: float) -> torch.Tensor:
     return _RMSNormFn.apply(x, eps)
 
@@ -565,6 +592,8 @@ class LlamaQLoRA:
                 x = self._layer(x, li, self.anchor)
         x = _rmsnorm(x, cfg.rms_eps)
         logits = x.reshape(b * s, cfg.hidden) @ self.lm_head
+        if cfg.vocab % 8 == 0:
+            return _XentFn.apply(logits, targets)
         return F.cross_entropy(logits.float(), targets.reshape(-1))
 
     # ------------------------------------------------------------------ step

@@ -122,6 +122,17 @@ def test_glue_kernels_match_torch(cuda):
     orf.backward(do.float())
     assert (dgu.float()[:, :64] - gr_.grad).abs().max() <= 2e-2 * gr_.grad.abs().max()
     assert (dgu.float()[:, 64:] - ur_.grad).abs().max() <= 2e-2 * ur_.grad.abs().max()
+    # cross entropy straight from bf16 logits vs torch's fp32 cross entropy
+    from paper_2305_14314_b200.llama import _XentFn
+    lg = (torch.randn(300, 1000, device="cuda", generator=g) * 3).bfloat16().requires_grad_(True)
+    tg = torch.randint(0, 1000, (300,), device="cuda", generator=g)
+    lo = _XentFn.apply(lg, tg)
+    lr = lg.detach().float().requires_grad_(True)
+    lor = F.cross_entropy(lr, tg)
+    (2.5 * lo).backward()
+    (2.5 * lor).backward()
+    assert abs(lo.item() - lor.item()) <= 1e-5 * abs(lor.item())
+    assert (lg.grad.float() - lr.grad).abs().max() <= 1e-2 * lr.grad.abs().max()
 
 
 def _tiny(seed=0, cfg_kw=None, **model_kw):

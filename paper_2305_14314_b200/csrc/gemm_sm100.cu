@@ -1545,7 +1545,9 @@ static qlrt_status reduce(const Args& args, cudaStream_t s) {
 // split count that fills the machine for a tile grid, bounded by workspace
 static int pick_splits(int64_t tiles, int64_t k_iters, int64_t per_split_bytes, size_t ws_bytes) {
   if (tiles >= 74 || k_iters < 8) return 1;
-  int64_t sp = 148 / tiles;
+  // CTA budget (QLRT_SKINNY_CTAS): 148 = one per SM; the 64-wide skinny
+  // GEMMs fit two per SM (4 stages of 24 KB each)
+  int64_t sp = policy(P_SKINNY_CTAS) / tiles;
   if (sp > k_iters / 4) sp = k_iters / 4;
   if (sp > 16) sp = 16;
   if (per_split_bytes > 0 && (int64_t)ws_bytes / per_split_bytes < sp) sp = (int64_t)ws_bytes / per_split_bytes;

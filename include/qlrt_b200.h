@@ -282,6 +282,12 @@ qlrt_status qlrt_rmsnorm_fwd(const void* x, void* y, float* rstd, int64_t rows, 
                              float eps, void* stream);
 qlrt_status qlrt_rmsnorm_bwd(const void* dy, const void* x, const float* rstd, void* dx,
                              int64_t rows, int64_t h, void* stream);
+/* The residual add fused into the next norm: s = bf16(x + d), y = rmsnorm(s);
+ * and the norm's backward plus the residual branch: dx = rmsnorm_bwd(dy) + dres. */
+qlrt_status qlrt_add_rmsnorm_fwd(const void* x, const void* d, void* s, void* y, float* rstd, int64_t rows,
+                                 int64_t h, float eps, void* stream);
+qlrt_status qlrt_rmsnorm_bwd_add(const void* dy, const void* x, const float* rstd, const void* dres, void* dx,
+                                 int64_t rows, int64_t h, void* stream);
 qlrt_status qlrt_swiglu_fwd(const void* g, const void* u, void* out, int64_t n, void* stream);
 qlrt_status qlrt_swiglu_bwd(const void* g, const void* u, const void* dout, void* dg, void* du,
                             int64_t n, void* stream);

@@ -85,6 +85,8 @@ _SIGS = {
     "qlrt_prefetch": [c_void_p, c_size_t, c_int, c_void_p],
     "qlrt_rmsnorm_fwd": [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_void_p],
     "qlrt_rmsnorm_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p],
+    "qlrt_add_rmsnorm_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_void_p],
+    "qlrt_rmsnorm_bwd_add": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p],
     "qlrt_swiglu_fwd": [c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
     "qlrt_swiglu_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p],
     "qlrt_rope": [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int, c_void_p],

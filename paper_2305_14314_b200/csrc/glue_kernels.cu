@@ -49,10 +49,45 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const uint4* __restric
   }
 }
 
-// dx = r * dy - r^3 * x * sum(dy * x) / h
+// s = x + d (the residual stream), y = s * rsqrt(mean(s^2) + eps): the
+// residual add fused into the next norm (one read of x and d, s and y written)
+__global__ void __launch_bounds__(256) add_rmsnorm_fwd_kernel(const uint4* __restrict__ x, const uint4* __restrict__ d,
+                                                              uint4* __restrict__ s, uint4* __restrict__ y,
+                                                              float* __restrict__ rstd, int h8, float eps) {
+  __shared__ float red[8];
+  const int64_t row = blockIdx.x;
+  const uint4 *xr = x + row * h8, *dr = d + row * h8;
+  uint4* sr = s + row * h8;
+  float ss = 0.0f;
+  for (int i = threadIdx.x; i < h8; i += blockDim.x) {
+    const uint4 a = xr[i], b = dr[i];
+    const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      // bf16(x + d) as torch's bf16 add rounds it, then the norm of the rounded sum
+      o[j] = pack_bf16x2(bf_lo(wa[j]) + bf_lo(wb[j]), bf_hi(wa[j]) + bf_hi(wb[j]));
+      ss += bf_lo(o[j]) * bf_lo(o[j]) + bf_hi(o[j]) * bf_hi(o[j]);
+    }
+    sr[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  const float r = rsqrtf(block_sum(ss, red) / (float)(h8 * 8) + eps);
+  if (threadIdx.x == 0) rstd[row] = r;
+  uint4* yr = y + row * h8;
+  for (int i = threadIdx.x; i < h8; i += blockDim.x) {
+    const uint4 u = sr[i];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = pack_bf16x2(bf_lo(w[j]) * r, bf_hi(w[j]) * r);
+    yr[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// dx = r * dy - r^3 * x * sum(dy * x) / h  (+ dres: the residual branch's gradient)
 __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ x,
                                                           const float* __restrict__ rstd, uint4* __restrict__ dx,
-                                                          int h8) {
+                                                          int h8, const uint4* __restrict__ dres) {
   __shared__ float red[8];
   const int64_t row = blockIdx.x;
   const uint4 *xr = x + row * h8, *gr = dy + row * h8;
@@ -71,9 +106,20 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const uint4* __restric
     const uint4 a = xr[i], b = gr[i];
     const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
     uint32_t o[4];
+    if (dres) {  // + the residual gradient: d(x + delta) feeds both branches
+      const uint4 c = dres[row * h8 + i];
+      const uint32_t wc[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      o[j] = pack_bf16x2(r * bf_lo(wb[j]) - k * bf_lo(wa[j]), r * bf_hi(wb[j]) - k * bf_hi(wa[j]));
+      for (int j = 0; j < 4; ++j) {
+        // bf16(rmsnorm grad) + dres, as the separate kernels + torch add round it
+        const uint32_t g = pack_bf16x2(r * bf_lo(wb[j]) - k * bf_lo(wa[j]), r * bf_hi(wb[j]) - k * bf_hi(wa[j]));
+        o[j] = pack_bf16x2(bf_lo(g) + bf_lo(wc[j]), bf_hi(g) + bf_hi(wc[j]));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        o[j] = pack_bf16x2(r * bf_lo(wb[j]) - k * bf_lo(wa[j]), r * bf_hi(wb[j]) - k * bf_hi(wa[j]));
+    }
     dr[i] = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
@@ -295,7 +341,23 @@ qlrt_status qlrt_rmsnorm_bwd(const void* dy, const void* x, const float* rstd, v
                              void* stream) {
   if (!dy || !x || !rstd || !dx || rows <= 0 || h <= 0 || (h % 8)) return QLRT_ERR_ARG;
   glue::rmsnorm_bwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>((const uint4*)dy, (const uint4*)x, rstd,
-                                                                            (uint4*)dx, (int)(h / 8));
+                                                                            (uint4*)dx, (int)(h / 8), nullptr);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+qlrt_status qlrt_add_rmsnorm_fwd(const void* x, const void* d, void* s, void* y, float* rstd, int64_t rows, int64_t h,
+                                 float eps, void* stream) {
+  if (!x || !d || !s || !y || !rstd || rows <= 0 || h <= 0 || (h % 8)) return QLRT_ERR_ARG;
+  glue::add_rmsnorm_fwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)x, (const uint4*)d, (uint4*)s, (uint4*)y, rstd, (int)(h / 8), eps);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+qlrt_status qlrt_rmsnorm_bwd_add(const void* dy, const void* x, const float* rstd, const void* dres, void* dx,
+                                 int64_t rows, int64_t h, void* stream) {
+  if (!dy || !x || !rstd || !dres || !dx || rows <= 0 || h <= 0 || (h % 8)) return QLRT_ERR_ARG;
+  glue::rmsnorm_bwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>(
+      (const uint4*)dy, (const uint4*)x, rstd, (uint4*)dx, (int)(h / 8), (const uint4*)dres);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }

@@ -294,6 +294,41 @@ class _XentFn(torch.autograd.Function):
         return d, None
 
 
+class _AddRMSNormFn(torch.autograd.Function):
+    """Residual add fused into the following RMSNorm: s = x + d, y =
+    rmsnorm(s) in one kernel; the backward adds the norm's gradient and the
+    residual stream's own gradient in one kernel, for both inputs."""
+
+    @staticmethod
+    def forward(ctx, x, d, eps):
+        x, d = x.contiguous(), d.contiguous()
+        h = x.shape[-1]
+        rows = x.numel() // h
+        s = torch.empty_like(x)
+        y = torch.empty_like(x)
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        check(lib().qlrt_add_rmsnorm_fwd(ptr(x), ptr(d), ptr(s), ptr(y), ptr(rstd), rows, h, float(eps),
+                                         stream_ptr()), "add + rmsnorm")
+        ctx.save_for_backward(s, rstd)
+        return s, y
+
+    @staticmethod
+    def backward(ctx, ds, dy):
+        s, rstd = ctx.saved_tensors
+        h = s.shape[-1]
+        rows = s.numel() // h
+        if dy is None:
+            return ds, ds, None
+        dx = torch.empty_like(s)
+        dy = dy.contiguous()
+        if ds is None:
+            check(lib().qlrt_rmsnorm_bwd(ptr(dy), ptr(s), ptr(rstd), ptr(dx), rows, h, stream_ptr()), "rmsnorm bwd")
+        else:
+            check(lib().qlrt_rmsnorm_bwd_add(ptr(dy), ptr(s), ptr(rstd), ptr(ds.contiguous()), ptr(dx), rows, h,
+                                             stream_ptr()), "rmsnorm bwd + residual")
+        return dx, dx, None
+
+
 def _rmsnorm(x: torch.Tensor, eps: float) -> torch.Tensor:
     return _RMSNormFn.apply(x, eps)
 
@@ -551,46 +586,51 @@ class LlamaQLoRA:
         defer = None if self.defer_lag is None else (lambda li=li: self._inflight.setdefault(li, []))
         return _QLinearFn.apply(x, anchor, lay[pj], lay[pj + ".g"], lay["notify"], defer)
 
-    def _layer(self, x, li, anchor):
+    def _layer(self, x, delta, li, anchor):
+        """One decoder layer on the residual stream x + delta (the previous
+        layer's last residual add is fused into this layer's first norm);
+        returns (x, delta) with the layer output x + delta."""
         cfg = self.cfg
         lay = self.layers[li]
         b, s = x.shape[0], x.shape[1]
         nh, d = cfg.n_heads, cfg.hidden // cfg.n_heads
-        hn = _rmsnorm(x, cfg.rms_eps)
+        if delta is None:
+            hn = _rmsnorm(x, cfg.rms_eps)
+        else:
+            x, hn = _AddRMSNormFn.apply(x, delta, cfg.rms_eps)
         cs = self.cos_sin[:s]
         if self.grouped:
             defer = None if self.defer_lag is None else (lambda li=li: self._inflight.setdefault(li, []))
             q, k, v = _QKVFn.apply(hn, anchor, lay["qkv"], lay["qkv.g"], lay["notify"], defer, cs, nh)
             a = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2),
                                                is_causal=True).transpose(1, 2).reshape(b, s, cfg.hidden)
-            x = x + self._lin(a, lay, "o", anchor)
-            hn = _rmsnorm(x, cfg.rms_eps)
+            x, hn = _AddRMSNormFn.apply(x, self._lin(a, lay, "o", anchor), cfg.rms_eps)
             act = _GateUpFn.apply(hn, anchor, lay["gu"], lay["gu.g"], lay["notify"], defer)
-            return x + self._lin(act, lay, "down", anchor)
+            return x, self._lin(act, lay, "down", anchor)
         q = _rope(self._lin(hn, lay, "q", anchor).view(b, s, nh, d), cs).transpose(1, 2)
         k = _rope(self._lin(hn, lay, "k", anchor).view(b, s, nh, d), cs).transpose(1, 2)
         v = self._lin(hn, lay, "v", anchor).view(b, s, nh, d).transpose(1, 2)
         a = F.scaled_dot_product_attention(q, k, v, is_causal=True).transpose(1, 2).reshape(b, s, cfg.hidden)
-        x = x + self._lin(a, lay, "o", anchor)
-        hn = _rmsnorm(x, cfg.rms_eps)
+        x, hn = _AddRMSNormFn.apply(x, self._lin(a, lay, "o", anchor), cfg.rms_eps)
         gt = self._lin(hn, lay, "gate", anchor)
         up = self._lin(hn, lay, "up", anchor)
-        return x + self._lin(_SwiGLUFn.apply(gt, up), lay, "down", anchor)
+        return x, self._lin(_SwiGLUFn.apply(gt, up), lay, "down", anchor)
 
     def loss(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         cfg = self.cfg
         b, s = tokens.shape
         self.refresh_constants()
         x = F.embedding(tokens, self.embed)
+        delta = None
         for li in range(cfg.n_layers):
             if self.checkpoint:
                 # reentrant: the layer reruns under grad in the backward; the
                 # anchor (requires_grad) carries the graph through it
-                x = _ckpt.checkpoint(self._layer, x, li, self.anchor, use_reentrant=True,
-                                     preserve_rng_state=False)
+                x, delta = _ckpt.checkpoint(self._layer, x, delta, li, self.anchor, use_reentrant=True,
+                                            preserve_rng_state=False)
             else:
-                x = self._layer(x, li, self.anchor)
-        x = _rmsnorm(x, cfg.rms_eps)
+                x, delta = self._layer(x, delta, li, self.anchor)
+        _, x = _AddRMSNormFn.apply(x, delta, cfg.rms_eps)
         logits = x.reshape(b * s, cfg.hidden) @ self.lm_head
         if cfg.vocab % 8 == 0:
             return _XentFn.apply(logits, targets)

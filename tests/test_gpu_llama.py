@@ -122,6 +122,21 @@ def test_glue_kernels_match_torch(cuda):
     orf.backward(do.float())
     assert (dgu.float()[:, :64] - gr_.grad).abs().max() <= 2e-2 * gr_.grad.abs().max()
     assert (dgu.float()[:, 64:] - ur_.grad).abs().max() <= 2e-2 * ur_.grad.abs().max()
+    # residual add fused into the norm, forward and backward (both inputs)
+    from paper_2305_14314_b200.llama import _AddRMSNormFn
+    xa = torch.randn(7, 256, device="cuda", generator=g).bfloat16().requires_grad_(True)
+    da = torch.randn(7, 256, device="cuda", generator=g).bfloat16().requires_grad_(True)
+    sa, ya = _AddRMSNormFn.apply(xa, da, 1e-6)
+    xr_, dr_ = xa.detach().float().requires_grad_(True), da.detach().float().requires_grad_(True)
+    sr_ = xr_ + dr_
+    yr_ = sr_ * torch.rsqrt(sr_.pow(2).mean(-1, keepdim=True) + 1e-6)
+    gs, gy = (torch.randn(7, 256, device="cuda", generator=g).bfloat16() for _ in range(2))
+    torch.autograd.backward([sa, ya], [gs, gy])
+    torch.autograd.backward([sr_, yr_], [gs.float(), gy.float()])
+    assert (ya.float() - yr_).abs().max() <= 2e-2 * yr_.abs().max()
+    assert torch.equal(sa, (xa.detach() + da.detach()))
+    for got, want in ((xa.grad, xr_.grad), (da.grad, dr_.grad)):
+        assert (got.float() - want).abs().max() <= 2e-2 * want.abs().max()
     # cross entropy straight from bf16 logits vs torch's fp32 cross entropy
     from paper_2305_14314_b200.llama import _XentFn
     lg = (torch.randn(300, 1000, device="cuda", generator=g) * 3).bfloat16().requires_grad_(True)

@@ -22,6 +22,18 @@ def main(which: str) -> None:
             y, c = lin.forward(x)
             if which != "gemm_fwd":
                 lin.backward(dy, c)
+    elif which == "gemm_gu":  # the grouped gate | up fused forward of the C3 step (no adapter segment)
+        from paper_2305_14314_b200._native import lib, ptr, stream_ptr
+        qs = [qb.quantize(torch.randn(4096, 11008, device=dev) * 0.02, cb, 64, double_quant=True) for _ in range(2)]
+        grp = qb.QLinearGroup(qs, torch.zeros(4096, 128, device=dev), torch.zeros(64, 22016, device=dev), 64, 16.0)
+        consts = grp._constants()
+        desc = grp._desc(consts)
+        x = torch.randn(2048, 4096, device=dev).bfloat16()
+        y = torch.empty(2048, 22016, dtype=torch.bfloat16, device=dev)
+        ws = grp._workspace(2048)
+        for _ in range(4):
+            assert lib().qlrt_nf4_linear_fwd(desc, ptr(x), None, 2048, None, None, 0, 0.0, None, ptr(y), ptr(ws),
+                                             stream_ptr()) == 0
     elif which == "dequant":
         x = torch.randn(4096, 4096, device=dev)
         q = qb.quantize(x, cb, 64, double_quant=True)

@@ -11,7 +11,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 N="--set full --clock-control none --import-source on --kernel-name-base demangled"
 timeout 600 ncu $N -k regex:"gemm_kernel<.int.512, .bool.1" -s 2 -c 2 -o gpurun_out/prof_fused_c2 \
   python tools/prof_driver.py gemm_bwd > /dev/null 2>&1
+timeout 600 ncu $N -k regex:"gemm_kernel<.int.512, .bool.1" -s 2 -c 1 -o gpurun_out/prof_fused_gu \
+  python tools/prof_driver.py gemm_gu > /dev/null 2>&1
 timeout 300 ncu $N -k regex:dequant64_bf16 -s 2 -c 1 -o gpurun_out/prof_dequant_c1 python tools/prof_driver.py dequant > /dev/null 2>&1
 timeout 300 ncu $N -k regex:"quantize64|dq_chunk|dq_encode" -s 3 -c 3 -o gpurun_out/prof_quantize_c1 python tools/prof_driver.py quantize > /dev/null 2>&1
-timeout 300 ncu $N -k regex:gemv_nf4 -s 2 -c 1 -o gpurun_out/prof_gemv_c4 python tools/prof_driver.py gemv > /dev/null 2>&1
+timeout 300 ncu $N -k regex:gemv_mma -s 2 -c 1 -o gpurun_out/prof_gemv_c4 python tools/prof_driver.py gemv > /dev/null 2>&1
 ls -la gpurun_out/

@@ -8,7 +8,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
-reps = {"fused_fwd_c2": ("prof_fused_c2", 0), "fused_bwd_c2": ("prof_fused_c2", 1),
+reps = {"fused_fwd_gu": ("prof_fused_gu", 0), "fused_fwd_c2": ("prof_fused_c2", 0), "fused_bwd_c2": ("prof_fused_c2", 1),
         "dequant_c1": ("prof_dequant_c1", 0), "gemv_8192x22016": ("prof_gemv_c4", 0)}
 
 

@@ -603,6 +603,7 @@ __global__ void __launch_bounds__(TPB, 1)
     }
     const uint32_t ax = aux0 + (uint32_t)sl * AUX;
     const int64_t jb0 = ps * 32;
+#ifndef QLRT_GEMV_NOAUX
 #pragma unroll
     for (int j = 0; j < 4; ++j) {  // DQ bytes: 16 rows x 8 groups of 4 blocks
       const int p = lane + 32 * j, r = p >> 3, q = p & 7;
@@ -615,6 +616,7 @@ __global__ void __launch_bounds__(TPB, 1)
       const int64_t ic = (((r0 + r) * nbr + jb0) >> bs2_shift) + which;
       cp_async4(ax + AUX_C1 + r * 8 + which * 4, c1 + ic, ic < n2);
     }
+#endif
     cp_async_arrive(&full[sl]);
     if (++pc == chunks) {
       pc = 0;
@@ -754,6 +756,14 @@ __global__ void __launch_bounds__(TPB, 1)
     }
     --left;
     ptx::mbar_wait(&full[sl], par);
+#ifdef QLRT_GEMV_DIAG  // data movement only (measurement build)
+    if (lane == 0) ptx::mbar_arrive(&empty[sl]);
+    if (++sl == NST) {
+      sl = 0;
+      par ^= 1u;
+    }
+    continue;
+#endif
     const uint32_t sa = sl < NFRONT ? front + (uint32_t)sl * STAGE : back + (uint32_t)(sl - NFRONT) * STAGE;
     const uint32_t ax = aux0 + (uint32_t)sl * AUX;
     const uint2 w0 = lds64(sa + roff[0]), w1 = lds64(sa + roff[1]), w2 = lds64(sa + roff[2]),

@@ -34,6 +34,18 @@ def main(which: str) -> None:
         for _ in range(4):
             assert lib().qlrt_nf4_linear_fwd(desc, ptr(x), None, 2048, None, None, 0, 0.0, None, ptr(y), ptr(ws),
                                              stream_ptr()) == 0
+    elif which in ("group_bwd", "group_fwd"):  # the grouped gate | up linear of the C3 step with LoRA r = 64
+        qs = [qb.quantize(torch.randn(4096, 11008, device=dev) * 0.02, cb, 64, double_quant=True) for _ in range(2)]
+        grp = qb.QLinearGroup(qs, torch.randn(4096, 128, device=dev) / 8, torch.randn(64, 22016, device=dev) * .01,
+                              64, 16.0)
+        x = torch.randn(2048, 4096, device=dev).bfloat16()
+        dy = torch.randn(2048, 22016, device=dev).bfloat16()
+        dl1 = torch.empty(4096, 128, device=dev)
+        dl2 = torch.empty(64, 22016, device=dev)
+        for _ in range(4):
+            y, c = grp.forward(x)
+            if which == "group_bwd":
+                grp.backward(dy, c, dl1, dl2)
     elif which == "dequant":
         x = torch.randn(4096, 4096, device=dev)
         q = qb.quantize(x, cb, 64, double_quant=True)

@@ -270,6 +270,16 @@ qlrt_status qlrt_adam_step_dev(float* p, const float* g, float* m, float* v, int
 qlrt_status qlrt_sumsq_f64(const float* g, int64_t n, double* acc, void* stream);
 
 /* g *= scale (float32), for clip_global_norm. */
+/* clip_global_norm's per-tensor sum in numpy's own order: acc +=
+ * pairwise_sum(float64(g)^2) (np.sum(np.square(g, dtype=float64)),
+ * loops_utils.h.src).  The tree depends on n only and is built by the caller:
+ * leaves [n_leaves][2] = (offset, length <= 128) in order, internal nodes
+ * ops [][3] = (dst, left, right) indices into vals (leaves first), grouped
+ * by height (level_starts[n_levels + 1]), root = the index of the sum;
+ * vals >= n_leaves + #ops doubles. */
+qlrt_status qlrt_sumsq_f64_pairwise(const float* g, const int* leaves, int n_leaves, const int* ops,
+                                    const int* level_starts, int n_levels, int root, double* vals, double* acc,
+                                    void* stream);
 qlrt_status qlrt_scale_f32(float* g, int64_t n, float scale, void* stream);
 
 /* Paged optimizer state: advise + prefetch a managed range to a device

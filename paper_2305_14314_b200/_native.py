@@ -82,6 +82,8 @@ _SIGS = {
                            c_void_p],
     "qlrt_sumsq_f64": [c_void_p, c_int64, c_void_p, c_void_p],
     "qlrt_scale_f32": [c_void_p, c_int64, c_float, c_void_p],
+    "qlrt_sumsq_f64_pairwise": [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p,
+                                c_void_p],
     "qlrt_prefetch": [c_void_p, c_size_t, c_int, c_void_p],
     "qlrt_rmsnorm_fwd": [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_void_p],
     "qlrt_rmsnorm_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p],

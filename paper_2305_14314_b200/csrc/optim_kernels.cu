@@ -144,6 +144,51 @@ __global__ void __launch_bounds__(256) sumsq_kernel(const float* __restrict__ g,
   }
 }
 
+// numpy's pairwise sum of the float64 squares of one float32 tensor
+// (np.sum(np.square(g, dtype=float64)), loops_utils.h.src pairwise_sum): the
+// leaves (<= 128 values: 8 strided accumulators, combined
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail; < 8 values: sequential)
+// in parallel, then the tree's internal nodes level by level in one CTA.
+// The tree depends on n only; the host builds it (training.py).
+__global__ void pairwise_leaves_kernel(const float* __restrict__ g, const int* __restrict__ leaves, int n_leaves,
+                                       double* __restrict__ vals) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_leaves) return;
+  const float* a = g + leaves[2 * i];
+  const int n = leaves[2 * i + 1];
+  double res;
+  if (n < 8) {
+    res = 0.0;
+    for (int k = 0; k < n; ++k) res = __dadd_rn(res, __dmul_rn((double)a[k], (double)a[k]));
+  } else {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dmul_rn((double)a[j], (double)a[j]);
+    const int m = n - n % 8;
+    for (int k = 8; k < m; k += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], __dmul_rn((double)a[k + j], (double)a[k + j]));
+    }
+    res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                    __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (int k = m; k < n; ++k) res = __dadd_rn(res, __dmul_rn((double)a[k], (double)a[k]));
+  }
+  vals[i] = res;
+}
+
+// ops[3 j .. 3 j + 2] = (dst, left, right), grouped by tree height
+// (level_starts[h] .. level_starts[h + 1]); acc += vals[root]
+__global__ void __launch_bounds__(1024) pairwise_combine_kernel(double* __restrict__ vals, const int* __restrict__ ops,
+                                                                const int* __restrict__ level_starts, int n_levels,
+                                                                int root, double* __restrict__ acc) {
+  for (int h = 0; h < n_levels; ++h) {
+    for (int j = level_starts[h] + threadIdx.x; j < level_starts[h + 1]; j += blockDim.x)
+      vals[ops[3 * j]] = __dadd_rn(vals[ops[3 * j + 1]], vals[ops[3 * j + 2]]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *acc = __dadd_rn(*acc, vals[root]);
+}
+
 __global__ void scale_kernel(float* __restrict__ g, int64_t n, float scale) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     g[i] = __fmul_rn(g[i], scale);
@@ -190,6 +235,19 @@ qlrt_status qlrt_sumsq_f64(const float* g, int64_t n, double* acc, void* stream)
   double* partials = acc + 1;
   unsigned* counter = reinterpret_cast<unsigned*>(acc + 1 + 296);
   sumsq_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(g, n, partials, counter, acc);
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
+qlrt_status qlrt_sumsq_f64_pairwise(const float* g, const int* leaves, int n_leaves, const int* ops,
+                                    const int* level_starts, int n_levels, int root, double* vals, double* acc,
+                                    void* stream) {
+  if (!g || !leaves || n_leaves < 1 || !vals || !acc || n_levels < 0 || (n_levels > 0 && (!ops || !level_starts)))
+    return QLRT_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  pairwise_leaves_kernel<<<(n_leaves + 255) / 256, 256, 0, st>>>(g, leaves, n_leaves, vals);
+  QLRT_CHECK_LAUNCH();
+  pairwise_combine_kernel<<<1, 1024, 0, st>>>(vals, ops, level_starts, n_levels, root, acc);
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }

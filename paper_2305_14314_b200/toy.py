@@ -41,8 +41,8 @@ from .codebooks import get_codebook
 from .errors import TrainingDivergedError
 from .paging import PagerConfig, pager_open
 from .qlora import PLACEMENTS, QLinear, lora_init
-from .training import (OPTIMIZERS, AdamOptimizer, PagedMomentStore, PlainMomentStore, TrainConfig, _sumsq_scratch,
-                       clip_global_norm)
+from .training import (OPTIMIZERS, AdamOptimizer, PagedMomentStore, PlainMomentStore, TrainConfig, clip_global_norm,
+                       pairwise_sumsq)
 
 TASKS = ("regression", "moons")
 DTYPES = ("fp32", "nf4", "nf-eq4", "fp4-e2m1", "fp4-e3m0", "int4")
@@ -411,7 +411,6 @@ def _train_graph(model: ToyModel, task, cfg: TrainConfig, params: dict, order: l
     hyper = torch.zeros(8, dtype=torch.float32, device="cuda")
     losses = torch.zeros(n, dtype=torch.float64, device="cuda")
     norms = torch.zeros(n, dtype=torch.float64, device="cuda")
-    acc = _sumsq_scratch("cuda")
     moments = {}
     for name in order:
         p = params[name]
@@ -423,11 +422,9 @@ def _train_graph(model: ToyModel, task, cfg: TrainConfig, params: dict, order: l
         pred, caches = model.forward(x, train=True, rng=None)
         loss, d_pred = task.loss_and_grad(pred, y)
         grads = model.backward(d_pred, caches)
-        acc.zero_()
         for name in order:
-            g = grads[name].contiguous()
-            grads[name] = g
-            check(lib().qlrt_sumsq_f64(ptr(g), g.numel(), ptr(acc), stream_ptr()), "clip_global_norm")
+            grads[name] = grads[name].contiguous()
+        acc = pairwise_sumsq(grads, order)  # (clip_global_norm's numpy-order total)
         hyper.copy_(table.index_select(0, t_dev).view(-1))
         for name in order:
             p, g = params[name], grads[name]

@@ -8,8 +8,9 @@
 * ``PlainMomentStore`` keeps moments as device tensors; ``PagedMomentStore``
   keeps them in unified-memory slabs under a :class:`Pager` budget.  Both run
   the same kernel on the same bytes, so paged == plain bit for bit.
-* ``clip_global_norm`` sums squares in fp64 on the device and scales in
-  place with the float32-rounded factor (training.py:398-413).
+* ``clip_global_norm`` sums squares in fp64 on the device in numpy's
+  pairwise order and scales in place with the float32-rounded factor
+  (training.py:398-413).
 """
 
 from __future__ import annotations
@@ -106,6 +107,78 @@ class PagedMomentStore:
         self.pager.flush()
 
 
+def _pairwise_tree(n: int):
+    """numpy's pairwise-sum tree over n values (loops_utils.h.src): leaves of
+    <= 128 values in order, internal nodes (dst, left, right) grouped by
+    height.  Returns (leaves [L][2], ops [I][3], level_starts, root)."""
+    leaves: list = []
+    ops: list = []
+
+    def rec(off: int, length: int):
+        if length <= 128:
+            leaves.append((off, length))
+            return ("L", len(leaves) - 1), 0
+        n2 = length // 2
+        n2 -= n2 % 8
+        a, ha = rec(off, n2)
+        b, hb = rec(off + n2, length - n2)
+        ops.append((a, b, max(ha, hb) + 1))
+        return ("I", len(ops) - 1), max(ha, hb) + 1
+
+    root, _ = rec(0, n)
+    n_l = len(leaves)
+    order = sorted(range(len(ops)), key=lambda j: ops[j][2])
+    pos = {j: n_l + k for k, j in enumerate(order)}
+    idx = lambda node: node[1] if node[0] == "L" else pos[node[1]]  # noqa: E731
+    flat_ops, starts, h_prev = [], [0], None
+    for k, j in enumerate(order):
+        a, b, h = ops[j]
+        if h_prev is not None and h != h_prev:
+            starts.append(k)
+        h_prev = h
+        flat_ops += [n_l + k, idx(a), idx(b)]
+    starts.append(len(order))
+    if not order:
+        starts = [0]
+    return (np.asarray(leaves, dtype=np.int32).reshape(-1), np.asarray(flat_ops, dtype=np.int32),
+            np.asarray(starts, dtype=np.int32), idx(root), n_l + len(order))
+
+
+_TREES: dict = {}
+
+
+def _tree_dev(n: int, device):
+    key = (n, str(device))
+    t = _TREES.get(key)
+    if t is None:
+        leaves, ops, starts, root, n_vals = _pairwise_tree(n)
+        to = lambda a: torch.from_numpy(a).to(device) if a.size else torch.zeros(1, dtype=torch.int32, device=device)  # noqa: E731
+        t = (to(leaves), to(ops), to(starts), len(leaves) // 2, len(starts) - 1, root,
+             torch.empty(n_vals, dtype=torch.float64, device=device))
+        _TREES[key] = t
+    return t
+
+
+def pairwise_sumsq(grads: dict, order: list) -> torch.Tensor:
+    """Device fp64 sum over ``order`` of np.sum(np.square(g, dtype=float64))
+    in numpy's own pairwise order per tensor, the tensors added in order from
+    0.0 -- clip_global_norm's total, bit for bit (training.py:398-407)."""
+    dev = grads[order[0]].device
+    acc = torch.zeros(1, dtype=torch.float64, device=dev)
+    for name in order:
+        g = grads[name]
+        if not g.is_contiguous():
+            g = g.contiguous()
+        if g.dtype != torch.float32:
+            raise ValueError("clip_global_norm expects float32 gradients")
+        if g.numel() == 0:
+            continue
+        leaves, ops, starts, n_leaves, n_levels, root, vals = _tree_dev(g.numel(), dev)
+        check(lib().qlrt_sumsq_f64_pairwise(ptr(g), ptr(leaves), n_leaves, ptr(ops), ptr(starts), n_levels, root,
+                                            ptr(vals), ptr(acc), stream_ptr()), "clip_global_norm")
+    return acc
+
+
 def _sumsq_scratch(device) -> torch.Tensor:
     return torch.zeros(SUMSQ_SCRATCH // 8, dtype=torch.float64, device=device)
 
@@ -125,8 +198,10 @@ def global_sumsq(grads: dict, order: list) -> torch.Tensor:
 
 def clip_global_norm(grads: dict, order: list, max_norm: float) -> float:
     """Scale every gradient in place when the joint 2-norm exceeds ``max_norm``;
-    returns the pre-clip norm (training.py:398-413)."""
-    norm = math.sqrt(float(global_sumsq(grads, order).item()))
+    returns the pre-clip norm (training.py:398-413).  The sum of squares runs
+    in numpy's pairwise order (``pairwise_sumsq``): the norm, hence the f32
+    scale, is bit-identical to the reference's."""
+    norm = math.sqrt(float(pairwise_sumsq(grads, order).item()))
     if norm > max_norm and norm > 0.0:
         scale = float(np.float32(max_norm / norm))
         for name in order:
@@ -194,4 +269,4 @@ def check_finite(loss: float, norm: float, step: int) -> None:
 
 
 __all__ = ["TrainConfig", "PlainMomentStore", "PagedMomentStore", "AdamOptimizer", "clip_global_norm",
-           "global_sumsq", "check_finite", "OPTIMIZERS"]
+           "global_sumsq", "pairwise_sumsq", "check_finite", "OPTIMIZERS"]

@@ -2,6 +2,8 @@
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import pytest
 import torch
@@ -71,3 +73,25 @@ def test_paged_equals_plain(budget_slabs, qb, cuda):
             pager.close()
     for k in shapes:
         assert np.array_equal(results[0][k], results[1][k]), k
+
+
+@pytest.mark.parametrize("shape", [(1,), (7,), (8,), (100,), (128,), (129,), (16, 4), (4096, 64), (64, 11008),
+                                   (333, 37)])
+def test_clip_norm_in_numpy_pairwise_order(shape, qb, cuda):
+    """clip_global_norm's sum of squares follows numpy's pairwise order per
+    tensor (training.py:404-406): the norm is bit-identical to the
+    reference's for every size, so the f32 clip scale is too."""
+    rng = np.random.default_rng(sum(shape))
+    gs = {"a": (rng.standard_normal(shape) * 3).astype(np.float32),
+          "b": (rng.standard_normal((5, 3)) * 1e-3).astype(np.float32)}
+    want = 0.0
+    for name in ("a", "b"):
+        want += float(np.sum(np.square(gs[name], dtype=np.float64)))
+    got = qb.training.pairwise_sumsq({k: torch.from_numpy(v).cuda() for k, v in gs.items()}, ["a", "b"])
+    assert float(got.item()) == want
+    dev = {k: torch.from_numpy(v.copy()).cuda() for k, v in gs.items()}
+    norm = qb.clip_global_norm(dev, ["a", "b"], 0.3)
+    assert norm == math.sqrt(want)
+    scale = np.float32(0.3 / norm)
+    for k in gs:
+        assert np.array_equal(dev[k].cpu().numpy(), gs[k] * scale)

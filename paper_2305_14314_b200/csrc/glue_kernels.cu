@@ -26,6 +26,8 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // y = x * rsqrt(mean(x^2) + eps), one CTA per row (h % 8 == 0)
 __global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const uint4* __restrict__ x, uint4* __restrict__ y,
                                                           float* __restrict__ rstd, int h8, float eps) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (no early trigger: a fused GEMM launched
+  // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
   __shared__ float red[8];
   const int64_t row = blockIdx.x;
   const uint4* xr = x + row * h8;
@@ -54,6 +56,8 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const uint4* __restric
 __global__ void __launch_bounds__(256) add_rmsnorm_fwd_kernel(const uint4* __restrict__ x, const uint4* __restrict__ d,
                                                               uint4* __restrict__ s, uint4* __restrict__ y,
                                                               float* __restrict__ rstd, int h8, float eps) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (no early trigger: a fused GEMM launched
+  // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
   __shared__ float red[8];
   const int64_t row = blockIdx.x;
   const uint4 *xr = x + row * h8, *dr = d + row * h8;
@@ -88,6 +92,8 @@ __global__ void __launch_bounds__(256) add_rmsnorm_fwd_kernel(const uint4* __res
 __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ x,
                                                           const float* __restrict__ rstd, uint4* __restrict__ dx,
                                                           int h8, const uint4* __restrict__ dres) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (no early trigger: a fused GEMM launched
+  // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
   __shared__ float red[8];
   const int64_t row = blockIdx.x;
   const uint4 *xr = x + row * h8, *gr = dy + row * h8;
@@ -130,6 +136,8 @@ __device__ __forceinline__ float sigmoidf_(float g) { return 1.0f / (1.0f + __ex
 // (contiguous: one row; concatenated [g | u]: ldg = ldu = 2 c8)
 __global__ void swiglu_fwd_kernel(const uint4* __restrict__ g, const uint4* __restrict__ u, uint4* __restrict__ out,
                                   int64_t rows, int64_t c8, int64_t ldg, int64_t ldu, int64_t ldo) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (no early trigger: a fused GEMM launched
+  // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
   const int64_t n8 = rows * c8;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n8; k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = k / c8, c = k - r * c8;
@@ -150,6 +158,8 @@ __global__ void swiglu_fwd_kernel(const uint4* __restrict__ g, const uint4* __re
 __global__ void swiglu_bwd_kernel(const uint4* __restrict__ g, const uint4* __restrict__ u,
                                   const uint4* __restrict__ dout, uint4* __restrict__ dg, uint4* __restrict__ du,
                                   int64_t rows, int64_t c8, int64_t ldgu, int64_t ldo) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (no early trigger: a fused GEMM launched
+  // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
   const int64_t n8 = rows * c8;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n8; k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = k / c8, cc = k - r * c8;
@@ -182,6 +192,8 @@ __global__ void swiglu_bwd_kernel(const uint4* __restrict__ g, const uint4* __re
 // column slice of the concatenated q | k | v projection)
 __global__ void rope_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, const float2* __restrict__ cs,
                             int64_t rows, int heads, int d, int seq, float sign, int64_t ldx, int64_t ldy) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (no early trigger: a fused GEMM launched
+  // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
   const int d8 = d / 8;
   const int64_t rw = (int64_t)d8 * heads;
   const int64_t total = rows * rw;
@@ -211,6 +223,8 @@ template <bool FWD>
 __global__ void rope_qkv_kernel(const uint4* __restrict__ a, const uint4* __restrict__ b, const uint4* __restrict__ c,
                                 uint4* __restrict__ x, uint4* __restrict__ y, uint4* __restrict__ z,
                                 const float2* __restrict__ cs, int64_t rows, int h8, int d, int seq) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (no early trigger: a fused GEMM launched
+  // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
   // FWD: a = ycat (rows x 3 h8), x / y / z = q / k / v;  BWD: a / b / c = dq / dk / dv, x = dycat
   const int d8 = d / 8;
   const int64_t total = rows * 3 * h8;
@@ -243,6 +257,8 @@ __global__ void rope_qkv_kernel(const uint4* __restrict__ a, const uint4* __rest
 // online max / sum-exp in one pass, loss[row] = lse - x[target]
 __global__ void __launch_bounds__(256) xent_fwd_kernel(const uint4* __restrict__ logits, const int64_t* __restrict__ tgt,
                                                        int v8, float* __restrict__ loss, float* __restrict__ lse_out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (no early trigger: a fused GEMM launched
+  // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
   __shared__ float sm[8], ss[8];
   const int64_t row = blockIdx.x;
   const uint4* x = logits + row * v8;
@@ -297,6 +313,8 @@ __global__ void __launch_bounds__(256) xent_fwd_kernel(const uint4* __restrict__
 __global__ void xent_bwd_kernel(const uint4* __restrict__ logits, const int64_t* __restrict__ tgt,
                                 const float* __restrict__ lse, const float* __restrict__ grad, int v8, float inv_rows,
                                 uint4* __restrict__ dlogits) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (no early trigger: a fused GEMM launched
+  // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
   const int64_t row = blockIdx.x;
   const float L = lse[row], sc = *grad * inv_rows;
   const int64_t t = tgt[row];
@@ -317,6 +335,24 @@ __global__ void xent_bwd_kernel(const uint4* __restrict__ logits, const int64_t*
   }
 }
 
+// programmatic dependent launch: the glue kernel may be scheduled while its
+// predecessor (a fused GEMM) drains; it waits before touching memory
+template <typename... KArgs, typename... Args>
+static qlrt_status launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = policy(P_PDL) ? 1 : 0;
+  if (cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...) != cudaSuccess) return QLRT_ERR_CUDA;
+  QLRT_CHECK_LAUNCH();
+  return QLRT_OK;
+}
+
 static int grid_for(int64_t n, int tpb) {
   int64_t g = (n + tpb - 1) / tpb;
   return (int)(g < (int64_t)kNumSMs * 8 ? (g < 1 ? 1 : g) : (int64_t)kNumSMs * 8);
@@ -331,52 +367,42 @@ extern "C" {
 
 qlrt_status qlrt_rmsnorm_fwd(const void* x, void* y, float* rstd, int64_t rows, int64_t h, float eps, void* stream) {
   if (!x || !y || !rstd || rows <= 0 || h <= 0 || (h % 8)) return QLRT_ERR_ARG;
-  glue::rmsnorm_fwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>((const uint4*)x, (uint4*)y, rstd,
+  return glue::launch_pdl(glue::rmsnorm_fwd_kernel, dim3((unsigned)rows), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)x, (uint4*)y, rstd,
                                                                             (int)(h / 8), eps);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
 }
 
 qlrt_status qlrt_rmsnorm_bwd(const void* dy, const void* x, const float* rstd, void* dx, int64_t rows, int64_t h,
                              void* stream) {
   if (!dy || !x || !rstd || !dx || rows <= 0 || h <= 0 || (h % 8)) return QLRT_ERR_ARG;
-  glue::rmsnorm_bwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>((const uint4*)dy, (const uint4*)x, rstd,
+  return glue::launch_pdl(glue::rmsnorm_bwd_kernel, dim3((unsigned)rows), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)dy, (const uint4*)x, rstd,
                                                                             (uint4*)dx, (int)(h / 8), nullptr);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
 }
 qlrt_status qlrt_add_rmsnorm_fwd(const void* x, const void* d, void* s, void* y, float* rstd, int64_t rows, int64_t h,
                                  float eps, void* stream) {
   if (!x || !d || !s || !y || !rstd || rows <= 0 || h <= 0 || (h % 8)) return QLRT_ERR_ARG;
-  glue::add_rmsnorm_fwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)x, (const uint4*)d, (uint4*)s, (uint4*)y, rstd, (int)(h / 8), eps);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
+  return glue::launch_pdl(glue::add_rmsnorm_fwd_kernel, dim3((unsigned)rows), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)x, (const uint4*)d, (uint4*)s, (uint4*)y, rstd, (int)(h / 8), eps);
 }
 qlrt_status qlrt_rmsnorm_bwd_add(const void* dy, const void* x, const float* rstd, const void* dres, void* dx,
                                  int64_t rows, int64_t h, void* stream) {
   if (!dy || !x || !rstd || !dres || !dx || rows <= 0 || h <= 0 || (h % 8)) return QLRT_ERR_ARG;
-  glue::rmsnorm_bwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)dy, (const uint4*)x, rstd, (uint4*)dx, (int)(h / 8), (const uint4*)dres);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
+  return glue::launch_pdl(glue::rmsnorm_bwd_kernel, dim3((unsigned)rows), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)dy, (const uint4*)x, rstd, (uint4*)dx, (int)(h / 8), (const uint4*)dres);
 }
 
 qlrt_status qlrt_swiglu_fwd(const void* g, const void* u, void* out, int64_t n, void* stream) {
   if (!g || !u || !out || n <= 0 || (n % 8)) return QLRT_ERR_ARG;
-  glue::swiglu_fwd_kernel<<<glue::grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)g, (const uint4*)u, (uint4*)out, 1, n / 8, 0, 0, 0);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
+  return glue::launch_pdl(glue::swiglu_fwd_kernel, dim3(glue::grid_for(n / 8, 256)), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)g, (const uint4*)u, (uint4*)out, 1, n / 8, 0, 0, 0);
 }
 
 qlrt_status qlrt_swiglu_bwd(const void* g, const void* u, const void* dout, void* dg, void* du, int64_t n,
                             void* stream) {
   if (!g || !u || !dout || !dg || !du || n <= 0 || (n % 8)) return QLRT_ERR_ARG;
-  glue::swiglu_bwd_kernel<<<glue::grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)g, (const uint4*)u, (const uint4*)dout, (uint4*)dg, (uint4*)du, 1, n / 8, 0, 0);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
+  return glue::launch_pdl(glue::swiglu_bwd_kernel, dim3(glue::grid_for(n / 8, 256)), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)g, (const uint4*)u, (const uint4*)dout, (uint4*)dg, (uint4*)du, 1, n / 8, 0, 0);
 }
 
 qlrt_status qlrt_rope(const void* x, void* y, const void* cos_sin, int64_t rows, int heads, int d, int seq,
@@ -384,10 +410,8 @@ qlrt_status qlrt_rope(const void* x, void* y, const void* cos_sin, int64_t rows,
   if (!x || !y || !cos_sin || rows <= 0 || heads <= 0 || d <= 0 || (d % 8) || seq <= 0) return QLRT_ERR_ARG;
   const int64_t total = rows * heads * (d / 8);
   const int64_t rw = (int64_t)heads * (d / 8);
-  glue::rope_kernel<<<glue::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)x, (uint4*)y, (const float2*)cos_sin, rows, heads, d, seq, inverse ? -1.0f : 1.0f, rw, rw);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
+  return glue::launch_pdl(glue::rope_kernel, dim3(glue::grid_for(total, 256)), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)x, (uint4*)y, (const float2*)cos_sin, rows, heads, d, seq, inverse ? -1.0f : 1.0f, rw, rw);
 }
 qlrt_status qlrt_rope_strided(const void* x, int64_t ldx, void* y, int64_t ldy, const void* cos_sin, int64_t rows,
                               int heads, int d, int seq, int inverse, void* stream) {
@@ -395,68 +419,55 @@ qlrt_status qlrt_rope_strided(const void* x, int64_t ldx, void* y, int64_t ldy, 
       ldx < (int64_t)heads * d || ldy < (int64_t)heads * d)
     return QLRT_ERR_ARG;
   const int64_t total = rows * heads * (d / 8);
-  glue::rope_kernel<<<glue::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)x, (uint4*)y, (const float2*)cos_sin, rows, heads, d, seq, inverse ? -1.0f : 1.0f, ldx / 8,
+  return glue::launch_pdl(glue::rope_kernel, dim3(glue::grid_for(total, 256)), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)x, (uint4*)y, (const float2*)cos_sin, rows, heads, d, seq, inverse ? -1.0f : 1.0f, ldx / 8,
       ldy / 8);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
 }
 qlrt_status qlrt_rope_qkv_fwd(const void* ycat, void* q, void* k, void* v, const void* cos_sin, int64_t rows,
                               int heads, int d, int seq, void* stream) {
   if (!ycat || !q || !k || !v || !cos_sin || rows <= 0 || heads <= 0 || d <= 0 || (d % 8) || seq <= 0)
     return QLRT_ERR_ARG;
   const int h8 = heads * d / 8;
-  glue::rope_qkv_kernel<true><<<glue::grid_for(rows * 3 * h8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)ycat, nullptr, nullptr, (uint4*)q, (uint4*)k, (uint4*)v, (const float2*)cos_sin, rows, h8, d, seq);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
+  return glue::launch_pdl(glue::rope_qkv_kernel<true>, dim3(glue::grid_for(rows * 3 * h8, 256)), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)ycat, nullptr, nullptr, (uint4*)q, (uint4*)k, (uint4*)v, (const float2*)cos_sin, rows, h8, d, seq);
 }
 qlrt_status qlrt_rope_qkv_bwd(const void* dq, const void* dk, const void* dv, void* dycat, const void* cos_sin,
                               int64_t rows, int heads, int d, int seq, void* stream) {
   if (!dq || !dk || !dv || !dycat || !cos_sin || rows <= 0 || heads <= 0 || d <= 0 || (d % 8) || seq <= 0)
     return QLRT_ERR_ARG;
   const int h8 = heads * d / 8;
-  glue::rope_qkv_kernel<false><<<glue::grid_for(rows * 3 * h8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)dq, (const uint4*)dk, (const uint4*)dv, (uint4*)dycat, nullptr, nullptr, (const float2*)cos_sin,
+  return glue::launch_pdl(glue::rope_qkv_kernel<false>, dim3(glue::grid_for(rows * 3 * h8, 256)), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)dq, (const uint4*)dk, (const uint4*)dv, (uint4*)dycat, nullptr, nullptr, (const float2*)cos_sin,
       rows, h8, d, seq);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
 }
 qlrt_status qlrt_xent_fwd(const void* logits, const int64_t* targets, int64_t rows, int64_t vocab, float* loss,
                           float* lse, void* stream) {
   if (!logits || !targets || !loss || !lse || rows <= 0 || vocab <= 0 || (vocab % 8)) return QLRT_ERR_ARG;
-  glue::xent_fwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>((const uint4*)logits, targets,
+  return glue::launch_pdl(glue::xent_fwd_kernel, dim3((unsigned)rows), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)logits, targets,
                                                                           (int)(vocab / 8), loss, lse);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
 }
 qlrt_status qlrt_xent_bwd(const void* logits, const int64_t* targets, const float* lse, const float* grad,
                           int64_t rows, int64_t vocab, void* dlogits, void* stream) {
   if (!logits || !targets || !lse || !grad || !dlogits || rows <= 0 || vocab <= 0 || (vocab % 8)) return QLRT_ERR_ARG;
-  glue::xent_bwd_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)logits, targets, lse, grad, (int)(vocab / 8), 1.0f / (float)rows, (uint4*)dlogits);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
+  return glue::launch_pdl(glue::xent_bwd_kernel, dim3((unsigned)rows), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)logits, targets, lse, grad, (int)(vocab / 8), 1.0f / (float)rows, (uint4*)dlogits);
 }
 // concatenated [g | u] rows (cols each): out[rows][cols] = silu(g) * u
 qlrt_status qlrt_swiglu_cat_fwd(const void* gu, void* out, int64_t rows, int64_t cols, void* stream) {
   if (!gu || !out || rows <= 0 || cols <= 0 || (cols % 8)) return QLRT_ERR_ARG;
   const int64_t c8 = cols / 8;
-  glue::swiglu_fwd_kernel<<<glue::grid_for(rows * c8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)gu, (const uint4*)gu + c8, (uint4*)out, rows, c8, 2 * c8, 2 * c8, c8);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
+  return glue::launch_pdl(glue::swiglu_fwd_kernel, dim3(glue::grid_for(rows * c8, 256)), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)gu, (const uint4*)gu + c8, (uint4*)out, rows, c8, 2 * c8, 2 * c8, c8);
 }
 // d[g | u] rows from dout[rows][cols] and the saved [g | u]
 qlrt_status qlrt_swiglu_cat_bwd(const void* gu, const void* dout, void* dgu, int64_t rows, int64_t cols,
                                 void* stream) {
   if (!gu || !dout || !dgu || rows <= 0 || cols <= 0 || (cols % 8)) return QLRT_ERR_ARG;
   const int64_t c8 = cols / 8;
-  glue::swiglu_bwd_kernel<<<glue::grid_for(rows * c8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const uint4*)gu, (const uint4*)gu + c8, (const uint4*)dout, (uint4*)dgu, (uint4*)dgu + c8, rows, c8, 2 * c8,
+  return glue::launch_pdl(glue::swiglu_bwd_kernel, dim3(glue::grid_for(rows * c8, 256)), dim3(256), (cudaStream_t)stream,
+                          (const uint4*)gu, (const uint4*)gu + c8, (const uint4*)dout, (uint4*)dgu, (uint4*)dgu + c8, rows, c8, 2 * c8,
       c8);
-  QLRT_CHECK_LAUNCH();
-  return QLRT_OK;
 }
 
 }  // extern "C"

@@ -2072,6 +2072,10 @@ qlrt_status qlrt_nf4_linear_group_fwd(const qlrt_nf4_weight* w, int groups, cons
   a.aug_gn = (int)Ng;
   a.aug_gstride = 2 * rank;
   a.aug_b2k = 2 * R;
+  // the fused grid is the PDL dependent of Ts's split-K reduce: it starts its
+  // main K loop as Ts's CTAs retire and waits for Ts_cat only before the
+  // augmented segment (X, the only earlier input, is older than Ts)
+  a.aug_pdl = gemm::pdl_policy() ? 1 : 0;
   Operand none{}, Bx{x, K, 0}, A2{l2, N, 1}, B2{ts_out, 2 * R, 0};
   return gemm::run(bn_main, none, Bx, &A2, &B2, K, 2 * rank, a, st);
 }

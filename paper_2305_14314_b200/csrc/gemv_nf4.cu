@@ -352,6 +352,7 @@ constexpr int CTHREADS = CWARPS * 32;
 constexpr int STRIP = 2048;  // columns per strip = 8 TMA boxes of 128 B
 constexpr int ROWS = 16;     // rows per stage (= unit)
 constexpr int NST = 8;  // stages in flight (16 KB each) = a_k input prefetch depth (static ring slots)
+constexpr int NMAX = 32;  // prep blocks reducing max |x| / max |c1| (the GEMV's fp16 scale)
 constexpr int STAGE = ROWS * STRIP / 2;  // 16 KB
 // shared layout: the CTA's dynamic window starts a few KB into the 228 KB;
 // the table sits at the 64 KB boundary, NFRONT stages + the scratch fill the
@@ -383,9 +384,10 @@ static size_t tpart_off(const Geo& g) { return part_off() + align256((size_t)(g.
 static size_t cnt_off(const Geo& g, int r) {
   return tpart_off(g) + align256((size_t)cdiv(g.K, 128) * (r > 0 ? r : 1) * 4);
 }
+static size_t max_off(const Geo& g, int r) { return cnt_off(g, r) + align256((size_t)g.strips * 4); }
 static size_t ws_bytes(int64_t K, int64_t N, int r) {
   const Geo g = geo(K, N, kNumSMs);
-  return cnt_off(g, r) + align256((size_t)g.strips * 4);
+  return max_off(g, r) + align256((size_t)NMAX * 8);
 }
 
 // first / last CTA covering strip s when CTA i owns units [i U / G, (i+1) U / G)
@@ -400,18 +402,52 @@ __device__ __forceinline__ int last_cta(int64_t s, int64_t C, int64_t U, int64_t
 // only at its first strip flush): block 0 zeroes the strip tickets; blocks
 // >= 1 compute the LoRA partials tpart[z][j] = sum_{k in [128 z, 128 z + 128)}
 // xa_k l1[k][j] (8 columns per thread, 16-byte loads, all rows in flight)
-__global__ void __launch_bounds__(256) prep_kernel(int64_t K, const __nv_bfloat16* __restrict__ xa,
+__global__ void __launch_bounds__(256) prep_kernel(int64_t K, const unsigned short* __restrict__ x,
+                                                  const float* __restrict__ c1, int64_t n2,
+                                                  const __nv_bfloat16* __restrict__ xa,
                                                   const __nv_bfloat16* __restrict__ l1, int rank,
                                                   float* __restrict__ tpart, unsigned* __restrict__ counters,
-                                                  int strips) {
+                                                  int strips, uint2* __restrict__ slots) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ float sh[256 * 8];
+  __shared__ unsigned rx[8], rc[8];
   const int tid = threadIdx.x;
   if (blockIdx.x == 0) {
     for (int i = tid; i < strips; i += 256) counters[i] = 0u;
     return;
   }
-  const int z = blockIdx.x - 1;
+  if (blockIdx.x <= NMAX) {  // max |x| (bf16 bits) and max |c1| over slices -> slots[b - 1]
+    const int b = blockIdx.x - 1;
+    unsigned mx = 0u, mc = 0u;
+    for (int64_t k = (int64_t)b * 256 + tid; k < K; k += (int64_t)NMAX * 256) {
+      const unsigned v = __ldg(x + k) & 0x7FFFu;
+      mx = v > mx ? v : mx;
+    }
+    for (int64_t i = (int64_t)b * 256 + tid; i < n2; i += (int64_t)NMAX * 256) {
+      const unsigned v = __float_as_uint(__ldg(c1 + i)) & 0x7FFFFFFFu;
+      mc = v > mc ? v : mc;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned p = __shfl_xor_sync(0xffffffffu, mx, o), q = __shfl_xor_sync(0xffffffffu, mc, o);
+      mx = p > mx ? p : mx;
+      mc = q > mc ? q : mc;
+    }
+    if ((tid & 31) == 0) {
+      rx[tid >> 5] = mx;
+      rc[tid >> 5] = mc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < 8; ++w) {
+        mx = rx[w] > mx ? rx[w] : mx;
+        mc = rc[w] > mc ? rc[w] : mc;
+      }
+      slots[b] = make_uint2(mx, mc);
+    }
+    return;
+  }
+  const int z = blockIdx.x - 1 - NMAX;
   const int cpr = rank / 8;          // 16-byte column groups per row
   const int rpp = 256 / cpr;         // rows per pass
   const int cg = tid % cpr, rr = tid / cpr;
@@ -548,11 +584,11 @@ __global__ void __launch_bounds__(TPB, 1)
                     const float* __restrict__ c1, int64_t n2, const float* __restrict__ mu, int bs2_shift,
                     qlrt_fp8spec sp, Vals16 vals, float maxdec, int64_t K, int64_t N,
                     const unsigned short* __restrict__ x, float* __restrict__ part, unsigned* __restrict__ counters,
-                    const float* __restrict__ tpart, int zt, const __nv_bfloat16* __restrict__ l2, int rank,
-                    float s, __nv_bfloat16* __restrict__ y) {
+                    const uint2* __restrict__ slots, const float* __restrict__ tpart, int zt,
+                    const __nv_bfloat16* __restrict__ l2, int rank, float s, __nv_bfloat16* __restrict__ y) {
   extern __shared__ __align__(1024) uint8_t dyn[];
   __shared__ float tsh[512];
-  __shared__ unsigned last_flag, red_x[CWARPS], red_c[CWARPS];
+  __shared__ unsigned last_flag;
   __shared__ float scales[2];
   __shared__ uint32_t v16[16];
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
@@ -641,56 +677,29 @@ __global__ void __launch_bounds__(TPB, 1)
                  "r"(v16[e & 15] | (v16[e >> 4] << 16)));
   }
 
-  // ---- the fp16 scale 2^-E of this CTA: max |a| 2^-E < 2^15 over the a_k it
-  // uses (a = x c, c <= maxdec c1 + max(mu, 0)): max |x| and max c1 over the
-  // rows / second-level blocks of its units
+  // ---- the fp16 scale 2^-E: max |a| 2^-E < 2^15 over every a_k (a = x c,
+  // c <= maxdec max c1 + max(mu, 0)); the maxima come from the prep kernel
+  // (its max blocks), which also zeroed the tickets: wait for it here, while
+  // the producer's first stages are already in flight
   const double mu_d = (double)__ldg(mu);
-  {
-    // segments of the CTA: strip s, rows [r_lo, r_hi) (<= a few; nunits * 16 rows in all)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tid == 0) {
     unsigned mx = 0u, mc = 0u;
-    const int64_t s0 = ub / chunks, s1 = (ue - 1) / chunks;
-    for (int64_t sg = s0; sg <= s1; ++sg) {
-      const int64_t ra = sg == s0 ? (ub - s0 * chunks) * ROWS : 0;
-      const int64_t rb = sg == s1 ? (ue - s1 * chunks) * ROWS : K;
-      for (int64_t k = ra + tid; k < rb; k += CTHREADS) {
-        const unsigned v = __ldg(x + k) & 0x7FFFu;
-        mx = v > mx ? v : mx;
-      }
-      const int64_t ia = (ra * nbr + sg * 32) >> bs2_shift;
-      int64_t ib = (((rb - 1) * nbr + sg * 32 + 31) >> bs2_shift) + 1;
-      ib = ib < n2 ? ib : n2;
-      for (int64_t i = ia + tid; i < ib; i += CTHREADS) {
-        const unsigned v = __float_as_uint(__ldg(c1 + i)) & 0x7FFFFFFFu;
-        mc = v > mc ? v : mc;
-      }
+    for (int i = 0; i < NMAX; ++i) {
+      const uint2 v = __ldcg(slots + i);
+      mx = v.x > mx ? v.x : mx;
+      mc = v.y > mc ? v.y : mc;
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const unsigned a = __shfl_xor_sync(0xffffffffu, mx, o), c = __shfl_xor_sync(0xffffffffu, mc, o);
-      mx = a > mx ? a : mx;
-      mc = c > mc ? c : mc;
+    const double m = (double)__uint_as_float(mx << 16) * ((double)maxdec * (double)__uint_as_float(mc) + fmax(mu_d, 0.0));
+    int e = 0;
+    if (m > 0.0 && m < 1e300) {
+      e = ilogb(m) - 14;
+      e = e < -120 ? -120 : (e > 120 ? 120 : e);
     }
-    if (lane == 0) {
-      red_x[wid] = mx;
-      red_c[wid] = mc;
-    }
-    cbar();  // (also: the table is complete)
-    if (tid == 0) {
-      for (int w = 1; w < CWARPS; ++w) {
-        mx = red_x[w] > mx ? red_x[w] : mx;
-        mc = red_c[w] > mc ? red_c[w] : mc;
-      }
-      const double m = (double)__uint_as_float(mx << 16) * ((double)maxdec * (double)__uint_as_float(mc) + fmax(mu_d, 0.0));
-      int e = 0;
-      if (m > 0.0 && m < 1e300) {
-        e = ilogb(m) - 14;
-        e = e < -120 ? -120 : (e > 120 ? 120 : e);
-      }
-      scales[0] = ldexpf(1.0f, -e);
-      scales[1] = ldexpf(1.0f, e);
-    }
-    cbar();
+    scales[0] = ldexpf(1.0f, -e);
+    scales[1] = ldexpf(1.0f, e);
   }
+  cbar();  // (also: the table is complete)
   const float sc = scales[0], unsc = scales[1];
 
   // ---- consumers: warp w owns columns [128 w, +128) of the strip (box w >> 1, half w & 1)
@@ -725,7 +734,7 @@ __global__ void __launch_bounds__(TPB, 1)
   const uint32_t bsel = (g & 1) ? 0x7632u : 0x5410u;
   int sl = 0;
   uint32_t par = 0u;
-  bool waited_prep = false;
+  bool waited_prep = true;  // (waited in the prologue)
   for (int i = 0; i < nunits; ++i) {
     if (left == 0) {
       // ---- strip segment done: partial, ticket, maybe finalize
@@ -892,7 +901,12 @@ qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* x
     // main kernel as its PDL dependent (prologue + first TMA loads overlap prep)
     int dev = 0, sms = kNumSMs;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const gemv2::Geo g = gemv2::geo(K, N, sms);
+    // small weights: fewer CTAs with >= QLRT_GEMV_MIN_UNITS stages each (fewer
+    // strip partials to sum; the per-CTA prologue amortized over more stages)
+    const int64_t units_all = cdiv(K, gemv2::ROWS) * cdiv(N, gemv2::STRIP);
+    const int mu_ = policy(P_GEMV_MIN_UNITS) > 0 ? policy(P_GEMV_MIN_UNITS) : 1;
+    const int64_t want = cdiv(units_all, mu_);
+    const gemv2::Geo g = gemv2::geo(K, N, (int)(want < sms ? want : sms));
     uint8_t* ws = (uint8_t*)workspace;
     float* part = (float*)(ws + gemv2::part_off());
     float* tpart = (float*)(ws + gemv2::tpart_off(g));
@@ -900,9 +914,10 @@ qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* x
     const int zt = (int)cdiv(K, 128);
     const double maxdec = fp8_max_value(w->spec.exp_bits, w->spec.mant_bits, w->spec.bias);
     const int64_t n2 = cdiv(K * (N / 64), (int64_t)w->blocksize2);
-    gemv2::prep_kernel<<<1 + (rank > 0 ? zt : 0), 256, 0, st>>>(K, (const __nv_bfloat16*)(xa ? xa : x),
-                                                              (const __nv_bfloat16*)l1, rank, tpart, counters,
-                                                              (int)g.strips);
+    uint2* slots = (uint2*)(ws + gemv2::max_off(g, rank));
+    gemv2::prep_kernel<<<1 + gemv2::NMAX + (rank > 0 ? zt : 0), 256, 0, st>>>(
+        K, (const unsigned short*)x, w->c1, n2, (const __nv_bfloat16*)(xa ? xa : x), (const __nv_bfloat16*)l1, rank,
+        tpart, counters, (int)g.strips, slots);
     QLRT_CHECK_LAUNCH();
     static std::atomic<unsigned long long> attr_mask{0};
     if (!(attr_mask.load() & (1ull << (dev & 63)))) {
@@ -929,7 +944,7 @@ qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* x
     cfg.numAttrs = policy(P_PDL) ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, gemv2::gemv_mma_kernel, tmc, w->dq_codes, w->c1, n2, w->mu,
                            (int)__builtin_ctz((unsigned)w->blocksize2), w->spec, v, (float)maxdec, K, N,
-                           (const unsigned short*)x, part, counters, (const float*)tpart, zt,
+                           (const unsigned short*)x, part, counters, (const uint2*)slots, (const float*)tpart, zt,
                            (const __nv_bfloat16*)l2, rank, s, (__nv_bfloat16*)y) != cudaSuccess)
       return QLRT_ERR_CUDA;
     QLRT_CHECK_LAUNCH();

@@ -664,6 +664,57 @@ __global__ void __launch_bounds__(256) dq_encode_kernel(const float* __restrict_
   }
 }
 
+// The same encode with one warp per second-level block (warp-shuffle absmax,
+// no block barriers inside the loop, the block's elements spread over the
+// lanes): the groups of a call run in parallel across every resident warp.
+__global__ void __launch_bounds__(256) dq_encode_warp_kernel(const float* __restrict__ c, int64_t nb, int bs2,
+                                                             const double* __restrict__ chunk_sums, int n_chunks,
+                                                             qlrt_fp8spec sp, float* __restrict__ mu_out,
+                                                             float* __restrict__ c1, uint8_t* __restrict__ codes) {
+  __shared__ double cs[512];
+  __shared__ float s_mu;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  double acc = 0.0;
+  for (int b = 0; b < n_chunks; b += 512) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 512 && b + i < n_chunks; i += blockDim.x) cs[i] = __ldcg(chunk_sums + b + i);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int e = min(512, n_chunks - b);
+      for (int i = 0; i < e; ++i) acc = __dadd_rn(acc, cs[i]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    s_mu = __double2float_rn(__ddiv_rn(acc, (double)nb));
+    if (blockIdx.x == 0) *mu_out = s_mu;
+  }
+  __syncthreads();
+  const double mu = (double)s_mu;
+  const double maxv = fp8_max_value(sp.exp_bits, sp.mant_bits, sp.bias);
+  const int64_t n2 = (nb + bs2 - 1) / bs2;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t blk = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); blk < n2; blk += warps) {
+    const int64_t b0 = blk * bs2;
+    const int64_t b1 = min(b0 + bs2, nb);
+    double amax = 0.0;
+    for (int64_t i = b0 + lane; i < b1; i += 32) amax = fmax(amax, fabs(__dsub_rn((double)__ldg(c + i), mu)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    float scale = 0.0f;
+    if (amax > 0.0) scale = __double2float_rn(__ddiv_rn(amax, maxv));
+    if (lane == 0) c1[blk] = scale;  // 0 for flat / underflowing blocks
+    const double sd = (double)scale;
+    for (int64_t i = b0 + lane; i < b1; i += 32) {
+      unsigned code = 0u;
+      if (scale != 0.0f)
+        code = fp8_encode(__ddiv_rn(__dsub_rn((double)__ldg(c + i), mu), sd), sp.exp_bits, sp.mant_bits, sp.bias,
+                          maxv);
+      codes[i] = (uint8_t)code;
+    }
+  }
+}
+
 __global__ void dq_decompress_kernel(const uint8_t* __restrict__ codes,
                                      const float* __restrict__ c1, const float* __restrict__ mu,
                                      int64_t nb, int bs2, qlrt_fp8spec sp,
@@ -1090,11 +1141,19 @@ qlrt_status qlrt_dq_compress(const float* absmax, int64_t nb, int blocksize2, ql
   cfg.blockDim = dim3(512);
   if (cudaLaunchKernelEx(&cfg, dq_chunk_sums_kernel, absmax, nb, sums) != cudaSuccess) return QLRT_ERR_CUDA;
   const int64_t n2 = cdiv(nb, blocksize2);
-  cfg.gridDim = dim3((unsigned)(n2 < (int64_t)kNumSMs * 8 ? n2 : (int64_t)kNumSMs * 8));
   cfg.blockDim = dim3(256);
-  if (cudaLaunchKernelEx(&cfg, dq_encode_kernel, absmax, nb, blocksize2, (const double*)sums, (int)n_chunks, spec, mu,
-                         c1, dq_codes) != cudaSuccess)
-    return QLRT_ERR_CUDA;
+  if (blocksize2 <= 4096) {  // one warp per second-level block
+    const int64_t ctas = cdiv(n2, 8);
+    cfg.gridDim = dim3((unsigned)(ctas < (int64_t)kNumSMs * 8 ? ctas : (int64_t)kNumSMs * 8));
+    if (cudaLaunchKernelEx(&cfg, dq_encode_warp_kernel, absmax, nb, blocksize2, (const double*)sums, (int)n_chunks,
+                           spec, mu, c1, dq_codes) != cudaSuccess)
+      return QLRT_ERR_CUDA;
+  } else {
+    cfg.gridDim = dim3((unsigned)(n2 < (int64_t)kNumSMs * 8 ? n2 : (int64_t)kNumSMs * 8));
+    if (cudaLaunchKernelEx(&cfg, dq_encode_kernel, absmax, nb, blocksize2, (const double*)sums, (int)n_chunks, spec,
+                           mu, c1, dq_codes) != cudaSuccess)
+      return QLRT_ERR_CUDA;
+  }
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
 }

@@ -103,6 +103,54 @@ __global__ void __launch_bounds__(128, 1) tma_rows(const __grid_constant__ CUten
   if (iters < 0) *sink = smem[0];
 }
 
+// the GEMV's handshake: one producer warp (lane 0 issues) + `nc` consumer
+// warps that wait on full[s] and arrive on empty[s]; the producer refills a
+// slot once every consumer warp has arrived
+__global__ void __launch_bounds__(544, 1) tma_rows_hs(const __grid_constant__ CUtensorMap tm, int stages, int nc,
+                                                      int rows, int stage_bytes, int iters, unsigned long long* sink) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[16], empty[16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], nc);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == nc) {
+    if (lane != 0) return;
+    int r0 = (int)(((long long)blockIdx.x * rows / gridDim.x) / 16 * 16);
+    const int strip = blockIdx.x % 8;
+    for (int i = 0; i < iters; ++i) {
+      const int s = i % stages;
+      if (i >= stages) ptx::mbar_wait(&empty[s], (uint32_t)((i / stages) - 1) & 1u);
+      ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)stage_bytes);
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+              ptx::smem_u32(smem + s * stage_bytes)),
+          "l"(reinterpret_cast<uint64_t>(&tm)), "r"(ptx::smem_u32(&full[s])), "r"(0), "r"(r0), "r"(strip * 8)
+          : "memory");
+      r0 += 16;
+      if (r0 >= rows) r0 = 0;
+    }
+    return;
+  }
+  if (warp > nc) return;
+  uint32_t par = 0;
+  int s = 0;
+  for (int i = 0; i < iters; ++i) {
+    ptx::mbar_wait(&full[s], par);
+    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    if (++s == stages) {
+      s = 0;
+      par ^= 1u;
+    }
+  }
+  if (iters < 0) *sink = smem[0];
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -202,6 +250,38 @@ int main() {
         printf("gemv-like %s %s, %2d stages: %7.1f GB/s chip, %5.1f GB/s/SM %s\n", d3 ? "3d [8][16][128B] swz128" :
                "2d [16][1KB] u32 noswz", (variant & 1) ? "promo none " : "promo 256B", st, bytes / ms / 1e6,
                bytes / ms / 1e6 / sms, cudaGetErrorString(cudaGetLastError()));
+      }
+    }
+  }
+  // the handshake variant (3-d box, 256B promotion)
+  {
+    const int grows = 32768, row_bytes = 8192;
+    cudaFuncSetAttribute(tma_rows_hs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    CUtensorMap tm;
+    cuuint64_t dims[3] = {128, (cuuint64_t)grows, (cuuint64_t)(row_bytes / 128)};
+    cuuint64_t strides[2] = {(cuuint64_t)row_bytes, 128};
+    cuuint32_t box[3] = {128, 16, 8};
+    cuuint32_t es[3] = {1, 1, 1};
+    enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    for (int nc : {1, 4, 16}) {
+      for (int st : {8, 12}) {
+        const int stage_bytes = 16 * 1024;
+        const int iters = (int)((256ll << 20) / stage_bytes / sms);
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        for (int rep = 0; rep < 2; ++rep) {
+          cudaEventRecord(a);
+          tma_rows_hs<<<sms, (nc + 1) * 32, st * stage_bytes>>>(tm, st, nc, grows, stage_bytes, iters, sink);
+          cudaEventRecord(b);
+          cudaEventSynchronize(b);
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        const double bytes = (double)iters * stage_bytes * sms;
+        printf("handshake: %2d consumer warps, %2d stages: %7.1f GB/s chip %s\n", nc, st, bytes / ms / 1e6,
+               cudaGetErrorString(cudaGetLastError()));
       }
     }
   }

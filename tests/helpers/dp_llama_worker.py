@@ -18,7 +18,8 @@ def main() -> None:
     if world > 1:
         dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2305_14314_b200.llama import LlamaConfig, LlamaQLoRA
-    cfg = LlamaConfig.tiny(n_layers=2)
+    kw = {"hidden": 512, "ffn": 1024, "rank": 64} if os.environ.get("GROUPED") == "1" else {}
+    cfg = LlamaConfig.tiny(n_layers=2, **kw)
     m = LlamaQLoRA(cfg, seed=0, bucket_layers=1)
     g = torch.Generator(device="cuda").manual_seed(7)
     for n, p in m.params.items():

@@ -15,6 +15,9 @@ import torch.nn.functional as F
 
 pytestmark = pytest.mark.gpu
 
+# a tiny decoder whose shapes take the grouped q|k|v / gate|up path
+GROUPED_TINY = {"hidden": 512, "ffn": 1024, "rank": 64}
+
 
 def _reference_grads(model, tokens, targets):
     """fp32 autograd through the same decoder; returns loss and d/d(l1, l2)."""
@@ -272,9 +275,9 @@ def test_deferred_adapter_grads_equal_joined(lag, cuda):
     assert b._inflight == {} and b._ready_q == []
 
 
-def _paged_pair(budget_layers, page_bytes):
+def _paged_pair(budget_layers, page_bytes, cfg_kw=None):
     from paper_2305_14314_b200.llama import LlamaConfig, LlamaQLoRA
-    cfg = LlamaConfig.tiny(n_layers=4)
+    cfg = LlamaConfig.tiny(n_layers=4, **(cfg_kw or {}))
     plain = LlamaQLoRA(cfg, seed=5)
     span = plain.layer_spans[0][1]
     slab_pages = (2 * span * 4 + page_bytes - 1) // page_bytes
@@ -283,13 +286,14 @@ def _paged_pair(budget_layers, page_bytes):
     return plain, paged
 
 
-@pytest.mark.parametrize("budget_layers,page_bytes", [(1, 64 << 10), (2, 64 << 10), (4, 2 << 20)])
-def test_paged_adamw_equals_plain(budget_layers, page_bytes, cuda):
+@pytest.mark.parametrize("budget_layers,page_bytes,cfg_kw", [(1, 64 << 10, None), (2, 64 << 10, None),
+                                                            (4, 2 << 20, None), (1, 1 << 20, GROUPED_TINY)])
+def test_paged_adamw_equals_plain(budget_layers, page_bytes, cfg_kw, cuda):
     """PagedMomentStore transparency on the training path (pkg/tests/
     test_training.py:325-350): the paged harness -- moments in unified-memory
     pages under a budget below the total state, elevator order, look-ahead
     prefetch -- produces bit-identical parameters and moments to the plain one."""
-    plain, paged = _paged_pair(budget_layers, page_bytes)
+    plain, paged = _paged_pair(budget_layers, page_bytes, cfg_kw)
     g = torch.Generator(device="cuda").manual_seed(2)
     tok = torch.randint(0, 512, (2, 64), device="cuda", generator=g)
     tgt = torch.randint(0, 512, (2, 64), device="cuda", generator=g)
@@ -309,11 +313,12 @@ def test_paged_adamw_equals_plain(budget_layers, page_bytes, cuda):
     paged.close()
 
 
-def test_checkpointed_layers_match(cuda):
+@pytest.mark.parametrize("cfg_kw", [{}, GROUPED_TINY], ids=["per-projection", "grouped"])
+def test_checkpointed_layers_match(cfg_kw, cuda):
     """Gradient checkpointing recomputes each layer in the backward: same loss
     and adapter gradients as keeping the activations."""
     from paper_2305_14314_b200.llama import LlamaConfig, LlamaQLoRA
-    cfg = LlamaConfig.tiny(n_layers=3)
+    cfg = LlamaConfig.tiny(n_layers=3, **cfg_kw)
     a = LlamaQLoRA(cfg, seed=9)
     b = LlamaQLoRA(cfg, seed=9, checkpoint=True)
     g = torch.Generator(device="cuda").manual_seed(1)
@@ -331,8 +336,9 @@ def test_checkpointed_layers_match(cuda):
     assert float(d) <= 1e-6, float(d)
 
 
-@pytest.mark.timeout(300)
-def test_dp_two_ranks_equal_one_rank_over_concatenated_batch(cuda, tmp_path):
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("grouped", ["0", "1"])
+def test_dp_two_ranks_equal_one_rank_over_concatenated_batch(grouped, cuda, tmp_path):
     """Two data-parallel ranks (gloo, both on cuda:0), each on half of the
     batch: the all-reduced adapter gradients and the loss equal one rank's
     over the whole batch (tolerance: bf16 GEMMs see different M tilings)."""
@@ -349,13 +355,13 @@ def test_dp_two_ranks_equal_one_rank_over_concatenated_batch(cuda, tmp_path):
     procs = []
     for r in range(2):
         env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
-                   OUT=str(tmp_path / f"r{r}.pt"))
+                   OUT=str(tmp_path / f"r{r}.pt"), GROUPED=grouped)
         procs.append(subprocess.Popen([sys.executable, helper], env=env, stdout=subprocess.PIPE,
                                       stderr=subprocess.PIPE, text=True))
     for p in procs:
         out, err = p.communicate(timeout=280)
         assert p.returncode == 0, err[-3000:]
-    env = dict(os.environ, RANK="0", WORLD_SIZE="1", OUT=str(tmp_path / "single.pt"))
+    env = dict(os.environ, RANK="0", WORLD_SIZE="1", OUT=str(tmp_path / "single.pt"), GROUPED=grouped)
     env.pop("MASTER_PORT", None)
     single = subprocess.run([sys.executable, helper], env=env, capture_output=True, text=True, timeout=280)
     assert single.returncode == 0, single.stderr[-3000:]

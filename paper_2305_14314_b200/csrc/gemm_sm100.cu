@@ -1495,6 +1495,17 @@ static qlrt_status run(int bn, const Operand& A, const Operand& B, const Operand
     if (args.aug_pdl || args.kg_n) args.streamk = 0;
     // the flags are zero between launches: every owner re-arms the flags it
     // consumed; the caller zero-fills the region once (qlrt_streamk_init)
+  } else if (policy(P_SK512) > 0 && args.sk_ws && bn == 512 && args.pair && args.splits == 1 && !args.aug_pdl &&
+             !args.kg_n && !args.share) {
+    // QLRT_SK512 = min k-iterations: stream-K over 256 x 512 pair tiles for a
+    // grid of fewer tiles than SM pairs (one partial round) with a long K
+    // loop -- every pair gets ~tiles / pairs of the K work, partial tiles
+    // fixed up through the stream-K region
+    const int64_t tiles = ((M + 255) / 256) * ((N + 511) / 512);
+    const int64_t units = args.units_cap > 0 && args.units_cap < num_sms() / 2 ? args.units_cap : num_sms() / 2;
+    const int64_t T = args.k_iters + args.k_iters_aug;
+    args.streamk = tiles < units && T >= policy(P_SK512) && num_sms() <= kNumSMs;
+    if (args.streamk) args.tail_from = 0;
   } else {
     args.streamk = 0;
   }

@@ -30,7 +30,7 @@ constexpr int kNumSMs = 148;
 enum Policy {
   P_PAIR, P_SIDE, P_TILE512, P_STAGGER, P_TMAOUT, P_HALFTAIL, P_PDL, P_SHARE, P_STREAMK, P_OVERLAP,
   P_OVERLAP_SMS, P_PDL_TRIGGER, P_STREAMK_SKINNY, P_CSPLIT, P_OVERLAP_BWD, P_GEMV_WL, P_DQB_CTAS_PER_SM,
-  P_GEMV_MMA, P_DIAG_SKIP, P_CL2, P_SIDE_SMS, P_SKINNY_CTAS, P_GEMV_MIN_UNITS, P_COUNT
+  P_GEMV_MMA, P_DIAG_SKIP, P_CL2, P_SIDE_SMS, P_SKINNY_CTAS, P_GEMV_MIN_UNITS, P_SK512, P_COUNT
 };
 struct PolicyDef {
   const char* env;
@@ -42,7 +42,7 @@ inline const PolicyDef kPolicies[P_COUNT] = {
     {"QLRT_STREAMK", 1},       {"QLRT_OVERLAP", 1},        {"QLRT_OVERLAP_SMS", 8}, {"QLRT_PDL_TRIGGER", 1},
     {"QLRT_STREAMK_SKINNY", 0}, {"QLRT_CSPLIT", 0},        {"QLRT_OVERLAP_BWD", 0}, {"QLRT_GEMV_WL", -1},
     {"QLRT_DQB_CTAS_PER_SM", -1}, {"QLRT_GEMV_MMA", 1},
-    {"QLRT_DIAG_SKIP", 0},     {"QLRT_CL2", 0},          {"QLRT_SIDE_SMS", 0},     {"QLRT_SKINNY_CTAS", 148}, {"QLRT_GEMV_MIN_UNITS", 8}};  // measurement only: 1 skips dl2/dl1, 2 skips dT (wrong results)
+    {"QLRT_DIAG_SKIP", 0},     {"QLRT_CL2", 0},          {"QLRT_SIDE_SMS", 0},     {"QLRT_SKINNY_CTAS", 148}, {"QLRT_GEMV_MIN_UNITS", 8}, {"QLRT_SK512", 0}};  // measurement only: 1 skips dl2/dl1, 2 skips dT (wrong results)
 constexpr int kPolicyUnset = -0x7fffffff;
 inline std::atomic<int> g_policy[P_COUNT];
 inline std::atomic<bool> g_policy_init{false};

@@ -243,7 +243,8 @@ def run_reference(args, rank: int) -> None:
 def c3_config(world: int) -> dict:
     return {"workload": "C3: LLaMA-7B-shape QLoRA finetune step (32 layers, h 4096, ffn 11008, 32 heads, vocab "
                         "32000; q,k,v,o,gate,up,down NF4+DQ frozen with LoRA r=64 alpha 16), seq 512 x 4 "
-                        "sequences per GPU, data-parallel adapter-gradient all-reduce, fused clip + AdamW",
+                        "sequences per GPU, data-parallel adapter-gradient all-reduce, fused clip + paged AdamW (moments in "
+                        "unified-memory pages)",
             "tokens_per_gpu": C3_TOKENS, "seq_len": 512, "global_batch": 4 * world,
             "parallelism": f"dp{world}",
             "l2": "inputs larger than L2: every step streams 3.3 GB of NF4 weights (126 MB L2)"}
@@ -278,11 +279,14 @@ def llama_step_bench(torch, dist, name, cfg, world, dev, steps, warmup, optimize
     torch.cuda.current_stream().wait_stream(side)
     torch.cuda.synchronize()
     captured = False
+    # paged moments that all stay resident (the budget holds them): the
+    # optimizer issues no migration, so it joins the captured step too
+    opt_in_graph = m.optimizer_resident()
     if graph:
         try:
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr):
-                loss_g = m.forward_backward(tok, tgt) if paged else m.train_step(tok, tgt)
+                loss_g = m.train_step(tok, tgt) if opt_in_graph else m.forward_backward(tok, tgt)
             captured = True
         except Exception as e:  # pragma: no cover - reported, eager steps instead
             graph_err = repr(e)[:200]
@@ -292,7 +296,7 @@ def llama_step_bench(torch, dist, name, cfg, world, dev, steps, warmup, optimize
         m.set_step_constants()
         if captured:
             gr.replay()
-            if paged:
+            if not opt_in_graph:
                 m.optimizer_step()
             return loss_g
         return m.train_step(tok, tgt)
@@ -334,6 +338,7 @@ def llama_step_bench(torch, dist, name, cfg, world, dev, steps, warmup, optimize
            "tflops_per_gpu": cfg.flops_per_token() * batch * cfg.seq / (ms / 1e3) / 1e12,
            "flops_per_token": cfg.flops_per_token(), "linear_params": cfg.linear_params,
            "lora_params": cfg.lora_params, "optimizer": optimizer, "build_s": build_s, "cuda_graph": captured,
+           "optimizer_in_graph": captured and opt_in_graph,
            "max_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9, "loss": float(loss.item()),
            "clocks": clk.summary()}
     if graph and not captured:
@@ -729,8 +734,10 @@ def main() -> None:
     t_wall = time.perf_counter()
 
     # ---- headline: C3 LLaMA-7B QLoRA step, tokens/s (weak scaling over ranks)
+    # (paged AdamW as SURVEY.md §8(d) C3 names it: the moments in unified-memory
+    # pages under a budget that holds them; the whole step one CUDA graph)
     c3 = llama_step_bench(torch, dist, "llama-7b shapes", LlamaConfig.llama7b(), world, dev, args.steps, args.warmup,
-                          e2e_steps=max(4, args.steps // 2), count_launches=True)
+                          optimizer="paged", e2e_steps=max(4, args.steps // 2), count_launches=True)
     c3["roofline_tokens_per_s"] = world * tf_burst * 1e12 / c3["flops_per_token"]
     c3["roofline_frac"] = c3["tokens_per_s"] / c3["roofline_tokens_per_s"]
     value = c3["tokens_per_s"]
@@ -765,12 +772,13 @@ def main() -> None:
                 extras.update(fn())
             except Exception as e:  # pragma: no cover
                 extras.setdefault("errors", []).append(repr(e)[:300])
-        for label, budget_frac in (("c3_llama7b_paged_resident", None), ("c3_llama7b_paged_budget50", 0.5)):
+        for label, opt, budget_frac in (("c3_llama7b_plain_adamw", "plain", None),
+                                        ("c3_llama7b_paged_budget50", "paged", 0.5)):
             try:
                 cfg7 = LlamaConfig.llama7b()
                 budget = None if budget_frac is None else int(8 * cfg7.lora_params * budget_frac)
                 r = llama_step_bench(torch, dist, "llama-7b shapes", cfg7, world, dev, max(4, args.steps // 2), 3,
-                                     optimizer="paged", budget=budget)
+                                     optimizer=opt, budget=budget)
                 r["vs_plain_ms"] = c3["ms_per_step"]
                 extras[label] = r
             except Exception as e:  # pragma: no cover

@@ -24,7 +24,10 @@ device buffer and the whole step captures into one CUDA graph;
 :class:`~paper_2305_14314_b200.paging.Pager` budget (the reference's
 PagedMomentStore, training.py:371-395: one slab per layer holding its m then
 v), the forward/backward still one CUDA graph and the optimizer walking the
-layer slabs with look-ahead prefetch on the pager's side streams.  The walk
+layer slabs with look-ahead prefetch on the pager's side streams; once every
+slab is resident under a budget that holds them all
+(``optimizer_resident()``) the optimizer issues no migration and the whole
+step captures into one graph.  The walk
 alternates direction every step (an elevator scan), so the reference's LRU
 keeps exactly the slabs the next step needs first and evicts the ones it has
 finished with; each parameter's update is independent, so the order changes
@@ -686,6 +689,18 @@ class LlamaQLoRA:
             self.pager.release(self.mslabs[li])
             for j in order[i + 1: i + 1 + self.lookahead]:
                 self.pager.prefetch(self.mslabs[j])
+
+    def optimizer_resident(self) -> bool:
+        """Plain moments, or paged moments whose budget holds every slab and
+        every slab's pages resident: the optimizer step issues no migration
+        and makes no host decision that could differ between steps, so the
+        whole train step (optimizer included) may be captured in one graph."""
+        if self.pager is None:
+            return True
+        pb = self.pager.config.page_bytes
+        pages = [p for sl in self.mslabs for p in sl.pages(pb)]
+        return (len(pages) * pb <= self.pager.config.budget_bytes
+                and all(self.pager.table.is_resident(p) for p in pages))
 
     def train_step(self, tokens: torch.Tensor, targets: torch.Tensor, group=None) -> torch.Tensor:
         """One QLoRA step; call set_step_constants() first.  Capturable as a

@@ -396,3 +396,40 @@ def test_grouped_projections_match_separate(lag, cuda):
     # of test_adapter_grads_match_fp32_reference)
     assert d.max() / ga.abs().max() <= 5e-2, float(d.max() / ga.abs().max())
     assert d.mean() / ga.abs().mean() <= 2e-2, float(d.mean() / ga.abs().mean())
+
+
+def test_paged_resident_step_captures_whole(cuda):
+    """Paged moments under a budget that holds them: once resident the
+    optimizer issues no migration (optimizer_resident()), so the whole train
+    step -- paged Adam included -- replays from one CUDA graph, bit-identical
+    to eager steps."""
+    from paper_2305_14314_b200.llama import LlamaConfig, LlamaQLoRA
+    cfg = LlamaConfig.tiny(n_layers=2)
+    a = LlamaQLoRA(cfg, seed=6, optimizer="paged")
+    b = LlamaQLoRA(cfg, seed=6, optimizer="paged")
+    assert not a.optimizer_resident()  # nothing faulted in yet
+    g = torch.Generator(device="cuda").manual_seed(3)
+    tok = torch.randint(0, 512, (2, 64), device="cuda", generator=g)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        a.set_step_constants()
+        a.train_step(tok, tok)
+    torch.cuda.current_stream().wait_stream(s)
+    b.set_step_constants()
+    b.train_step(tok, tok)
+    torch.cuda.synchronize()
+    assert a.optimizer_resident()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        a.train_step(tok, tok)
+    for _ in range(2):
+        a.set_step_constants()
+        graph.replay()
+        b.set_step_constants()
+        b.train_step(tok, tok)
+    torch.cuda.synchronize()
+    assert torch.equal(a.params_flat, b.params_flat)
+    ma, va = a.moments()
+    mb, vb = b.moments()
+    assert torch.equal(ma, mb) and torch.equal(va, vb)

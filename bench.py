@@ -279,6 +279,8 @@ def llama_step_bench(torch, dist, name, cfg, world, dev, steps, warmup, optimize
     torch.cuda.current_stream().wait_stream(side)
     torch.cuda.synchronize()
     captured = False
+    if graph and world > 1 and dist.get_backend() == "gloo":
+        graph = False  # (gloo collectives are not capturable: the shared-GPU launcher check runs eager)
     # paged moments that all stay resident (the budget holds them): the
     # optimizer issues no migration, so it joins the captured step too
     opt_in_graph = m.optimizer_resident()
@@ -722,10 +724,19 @@ def main() -> None:
 
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} rank(s)", file=sys.stderr)
+    # QLRT_BENCH_SHARE_GPU=1 (launcher check only, not a scaling number): every
+    # rank on cuda:0 with gloo -- exercises the spawn / rank / reduction path
+    # on a one-GPU box
+    share = os.environ.get("QLRT_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     import paper_2305_14314_b200 as qb
     from paper_2305_14314_b200.llama import LlamaConfig
 

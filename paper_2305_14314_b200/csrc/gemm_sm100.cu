@@ -120,6 +120,9 @@ struct Args {
 #ifndef QLRT_MERGE_FULL
 #define QLRT_MERGE_FULL 1
 #endif
+#ifndef QLRT_EPI_FRAG
+#define QLRT_EPI_FRAG 1  // fragment-layout TMEM loads + stmatrix for the staged D^T epilogue
+#endif
 #ifndef QLRT_ISSUE_E
 #define QLRT_ISSUE_E 2  // MMA issue: 2 = elect.sync region (uniform datapath), 0 = lane-0 issue (old)
 #endif
@@ -811,8 +814,87 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
       const int hh = item_half(tile, tdummy);
       const int cbeg = hh >= 0 ? hh * UN : 0;  // a half tile drains its own 256 columns
       const int cend = direct_fold ? p.fold : (hh >= 0 ? cbeg + UN : BN);
+      // the staged 32 x 32 D^T tile (row j = token n0 + j) out with 16B vector
+      // stores: 4 lanes cover one 64B output row segment
+      auto store_staged_t = [&](const __nv_bfloat16* st, int64_t n0) {
+        const int64_t mcol = m_base + quarter * 32 + (lane & 3) * 8;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int rr = q * 8 + (lane >> 2);
+          const int64_t n = n0 + rr;
+          const uint4 v = *reinterpret_cast<const uint4*>(st + rr * 32 + (lane & 3) * 8);
+          if (n < p.N) {
+            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + n * p.ldo + mcol;
+            if (mcol + 8 <= p.M && (p.ldo & 7) == 0) {
+              *reinterpret_cast<uint4*>(o) = v;
+            } else {
+              const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (mcol + u < p.M)
+                  reinterpret_cast<unsigned short*>(o)[u] = (unsigned short)(vw[u >> 1] >> (16 * (u & 1)));
+            }
+          }
+        }
+        __syncwarp();
+      };
+      // bf16 D^T through the per-warp staging tile, loaded in the mma fragment
+      // layout (tcgen05.ld 16x256b) and transposed by stmatrix: 2 loads + 16
+      // packs + 4 stmatrix per 32 x 32 chunk instead of 32 scalar 16-bit stores
+      const bool staged_t = EC == 32 && (p.tma_out || (p.out_t && !p.out_f32 && p.splits == 1 && !p.to_ws));
+      const bool frag = staged_t && QLRT_EPI_FRAG && !partial && !csplit && v_end == unit0 + 1;
 #pragma unroll 1
-      for (int c0 = cbeg + csub * EC; c0 < cend; c0 += CSTEP) {
+      for (int c0 = cbeg + csub * EC; c0 < cend && frag; c0 += CSTEP) {
+        uint32_t r[32];
+        const uint32_t tq = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0;
+        ptx::tmem_ld_frag32(tq, tq + (16u << 16), r);
+        if (direct_fold) {
+          uint32_t r2[32];
+          ptx::tmem_ld_frag32(tq + p.fold, tq + (16u << 16) + p.fold, r2);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
+        }
+        if (p.alpha != 1.0f) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * p.alpha);
+        }
+        const int64_t n0 = (int64_t)nt * BN + c0;
+        __nv_bfloat16* st = sE + (warp - kEpiWarp0) * 32 * 32;
+        if (p.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        // matrix i of each stmatrix = features 8i..8i+7 x tokens 8x..8x+7; this
+        // lane addresses stored row (token) 8x + lane % 8 of matrix lane / 8
+        const uint32_t sa = ptx::smem_u32(st) + (uint32_t)(((lane & 7) * 32 + 8 * (lane >> 3)) * 2);
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+          ptx::stmatrix_x4_trans(
+              sa + x * 8 * 32 * 2,
+              ptx::pack_bf16x2(__uint_as_float(r[4 * x]), __uint_as_float(r[4 * x + 1])),
+              ptx::pack_bf16x2(__uint_as_float(r[4 * x + 2]), __uint_as_float(r[4 * x + 3])),
+              ptx::pack_bf16x2(__uint_as_float(r[16 + 4 * x]), __uint_as_float(r[16 + 4 * x + 1])),
+              ptx::pack_bf16x2(__uint_as_float(r[16 + 4 * x + 2]), __uint_as_float(r[16 + 4 * x + 3])));
+        if (p.tma_out) {
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tmO),
+                "r"((int)(m_base + quarter * 32)), "r"((int)n0), "r"(ptx::smem_u32(st))
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        } else {
+          __syncwarp();
+          store_staged_t(st, n0);
+        }
+        if (NUM == 2 && NACC == 1 && p.stagger && hh < 0 && c0 + CSTEP >= UN && c0 < UN) {
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_leader(&tempty[0]);
+        }
+      }
+#pragma unroll 1
+      for (int c0 = cbeg + csub * EC; c0 < cend && !frag; c0 += CSTEP) {
         uint32_t r[EC];
         if (partial) {
           ptx::tmem_ld<EC>(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, r);
@@ -861,26 +943,7 @@ __global__ void __launch_bounds__(NF4 ? kNF4Threads : kPlainThreads, 1)
 #pragma unroll
           for (int j = 0; j < EC; ++j) st[j * 32 + lane] = __float2bfloat16_rn(__uint_as_float(r[j]) * p.alpha);
           __syncwarp();
-          const int64_t mcol = m_base + quarter * 32 + (lane & 3) * 8;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int rr = q * 8 + (lane >> 2);
-            const int64_t n = n0 + rr;
-            const uint4 v = *reinterpret_cast<const uint4*>(st + rr * 32 + (lane & 3) * 8);
-            if (n < p.N) {
-              __nv_bfloat16* o = static_cast<__nv_bfloat16*>(p.out) + n * p.ldo + mcol;
-              if (mcol + 8 <= p.M && (p.ldo & 7) == 0) {
-                *reinterpret_cast<uint4*>(o) = v;
-              } else {
-                const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                  if (mcol + u < p.M)
-                    reinterpret_cast<unsigned short*>(o)[u] = (unsigned short)(vw[u >> 1] >> (16 * (u & 1)));
-              }
-            }
-          }
-          __syncwarp();
+          store_staged_t(st, n0);
         } else if (m < p.M) {
           store_chunk<EC>(p, r, m, n0, z);
         }

@@ -590,13 +590,24 @@ def c4_sweep(qb, torch, dev, flush, stream, tf_burst, hbm):
             "bwd_frac": fb / (t_b / 1e3) / 1e12 / tf_burst,
             "note": "QLinear.forward / .backward with LoRA r=64 (all launches: constants, adapter products, "
                     "fused NF4 GEMM), FLOPs incl. the adapter terms"}
-        lin0 = qb.QLinear(q, [])
-        xv = torch.randn(1, k, device=dev, generator=g).bfloat16()
-        t = _timed(torch, stream, flush, [lambda: lin0.forward(xv)])
+        del lin, x, dy, cache, holder
+        # batch-1 GEMV: one launch after an L2 flush, and the decode regime --
+        # distinct weights of this shape back to back (> 2x L2, like the
+        # layers of a model), per launch
         gb = k * n // 2 + k * n // 64 + 4 * (k * n // 64 // 256) + 2 * k + 2 * n
+        reps = max(2, -(-(256 << 20) // gb))
+        lins = [qb.QLinear(q, [])] + [
+            qb.QLinear(qb.quantize(torch.randn(k, n, device=dev, generator=g) * 0.02, cb, 64, double_quant=True), [])
+            for _ in range(reps - 1)]
+        xv = torch.randn(1, k, device=dev, generator=g).bfloat16()
+        t = _timed(torch, stream, flush, [lambda: lins[0].forward(xv)])
+        ts = _timed(torch, stream, flush, [(lambda li: (lambda: li.forward(xv)))(li) for li in lins]) / reps
         out[f"c4_gemv_{k}x{n}"] = {"gbs": gb / (t / 1e3) / 1e9, "ms": t, "bytes": gb,
-                                   "frac_hbm": gb / (t / 1e3) / 1e9 / hbm}
-        del q, lin, lin0, x, dy, cache, holder
+                                   "stream_ms": ts, "stream_gbs": gb / (ts / 1e3) / 1e9,
+                                   "frac_hbm": gb / (ts / 1e3) / 1e9 / hbm,
+                                   "note": f"ms: one launch after an L2 flush; stream: {reps} distinct weights back "
+                                           "to back (> L2), per launch"}
+        del q, lins
     torch.cuda.empty_cache()
     return out
 

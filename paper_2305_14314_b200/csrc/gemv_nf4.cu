@@ -345,6 +345,18 @@ __global__ void __launch_bounds__(TPB) lora_t_kernel(const __nv_bfloat16* __rest
 // the main grid waits for it only at its first flush.
 namespace gemv2 {
 
+#ifdef QLRT_GEMV_TL  // per-CTA globaltimer timeline (tools/gemv_tl.py); not in the product build
+__device__ unsigned long long g_gemv_tl[kNumSMs][16];
+__device__ unsigned long long g_gemv_tl_prep[2];  // [min start, max end] of the prep kernel
+#define TLSET(slot, v) g_gemv_tl[blockIdx.x % kNumSMs][slot] = (unsigned long long)(v)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#else
+#define TLSET(slot, v)
+#endif
 constexpr int CWARPS = 16;  // consumer warps
 constexpr int PWARP = CWARPS;  // + one producer warp (TMA + aux copies)
 constexpr int TPB = (CWARPS + 1) * 32;
@@ -409,6 +421,12 @@ __global__ void __launch_bounds__(256) prep_kernel(int64_t K, const unsigned sho
                                                   float* __restrict__ tpart, unsigned* __restrict__ counters,
                                                   int strips, uint2* __restrict__ slots) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef QLRT_GEMV_TL
+  if (threadIdx.x == 0) atomicMin(&g_gemv_tl_prep[0], gtimer());
+  struct TlEnd {
+    __device__ ~TlEnd() { if (threadIdx.x == 0) atomicMax(&g_gemv_tl_prep[1], gtimer()); }
+  } tl_end;
+#endif
   __shared__ float sh[256 * 8];
   __shared__ unsigned rx[8], rc[8];
   const int tid = threadIdx.x;
@@ -597,6 +615,10 @@ __global__ void __launch_bounds__(TPB, 1)
   const int G = (int)gridDim.x;
   const int64_t ub = (int64_t)blockIdx.x * units / G, ue = (int64_t)(blockIdx.x + 1) * units / G;
   const int nunits = (int)(ue - ub);
+#ifdef QLRT_GEMV_TL
+  unsigned long long tl_wait = 0;
+  if (threadIdx.x == 0) { TLSET(0, gtimer()); TLSET(7, nunits); }
+#endif
 
   // ---- shared layout: 64 KB table at the first 64 KB-aligned address;
   // 1 KB-aligned stages, the aux ring and the fp8 LUT around it
@@ -619,6 +641,9 @@ __global__ void __launch_bounds__(TPB, 1)
   if (tid < 16) v16[tid] = (uint32_t)__half_as_ushort(__float2half_rn(vals.v[tid]));
   if (tid < 256) lut[tid] = fp8_decode_fast(tid, sp);
   __syncthreads();
+#ifdef QLRT_GEMV_TL
+  if (tid == 0) TLSET(10, gtimer());
+#endif
 
   // ---- stage issue (warp 0; the codes and a_k inputs never depend on the
   // prep kernel): 8 TMA boxes of codes + the DQ bytes, x and c1 of the 16 rows
@@ -667,6 +692,9 @@ __global__ void __launch_bounds__(TPB, 1)
       issue(sl);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+#ifdef QLRT_GEMV_TL
+    if (lane == 0) TLSET(6, gtimer());
+#endif
     return;
   }
 
@@ -677,19 +705,32 @@ __global__ void __launch_bounds__(TPB, 1)
                  "r"(v16[e & 15] | (v16[e >> 4] << 16)));
   }
 
+#ifdef QLRT_GEMV_TL
+  if (tid == 0) TLSET(8, gtimer());
+#endif
   // ---- the fp16 scale 2^-E: max |a| 2^-E < 2^15 over every a_k (a = x c,
   // c <= maxdec max c1 + max(mu, 0)); the maxima come from the prep kernel
   // (its max blocks), which also zeroed the tickets: wait for it here, while
   // the producer's first stages are already in flight
   const double mu_d = (double)__ldg(mu);
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (tid == 0) {
-    unsigned mx = 0u, mc = 0u;
-    for (int i = 0; i < NMAX; ++i) {
-      const uint2 v = __ldcg(slots + i);
-      mx = v.x > mx ? v.x : mx;
-      mc = v.y > mc ? v.y : mc;
+#ifdef QLRT_GEMV_TL
+  if (tid == 0) TLSET(9, gtimer());
+#endif
+  unsigned mx = 0u, mc = 0u;
+  if (wid == 0) {  // the NMAX = 32 slots: one per lane, then a warp max (one L2 round trip)
+    static_assert(NMAX == 32, "one slot per lane");
+    const uint2 v = __ldcg(slots + lane);
+    mx = v.x;
+    mc = v.y;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned p = __shfl_xor_sync(0xffffffffu, mx, o), q = __shfl_xor_sync(0xffffffffu, mc, o);
+      mx = p > mx ? p : mx;
+      mc = q > mc ? q : mc;
     }
+  }
+  if (tid == 0) {
     const double m = (double)__uint_as_float(mx << 16) * ((double)maxdec * (double)__uint_as_float(mc) + fmax(mu_d, 0.0));
     int e = 0;
     if (m > 0.0 && m < 1e300) {
@@ -701,6 +742,9 @@ __global__ void __launch_bounds__(TPB, 1)
   }
   cbar();  // (also: the table is complete)
   const float sc = scales[0], unsc = scales[1];
+#ifdef QLRT_GEMV_TL
+  if (tid == 0) TLSET(1, gtimer());
+#endif
 
   // ---- consumers: warp w owns columns [128 w, +128) of the strip (box w >> 1, half w & 1)
   const int g = lane >> 2, t = lane & 3;
@@ -764,7 +808,19 @@ __global__ void __launch_bounds__(TPB, 1)
       jok = cs * 32 + jl < nbr;
     }
     --left;
+#ifdef QLRT_GEMV_TL
+    {
+      const unsigned long long t0 = gtimer();
+      ptx::mbar_wait(&full[sl], par);
+      if (tid == 0) {
+        const unsigned long long t1 = gtimer();
+        tl_wait += t1 - t0;
+        if (i == 0) TLSET(2, t1);
+      }
+    }
+#else
     ptx::mbar_wait(&full[sl], par);
+#endif
 #ifdef QLRT_GEMV_DIAG  // data movement only (measurement build)
     if (lane == 0) ptx::mbar_arrive(&empty[sl]);
     if (++sl == NST) {
@@ -831,6 +887,9 @@ __global__ void __launch_bounds__(TPB, 1)
     }
   }
   // ---- last segment
+#ifdef QLRT_GEMV_TL
+  if (tid == 0) { TLSET(3, gtimer()); TLSET(5, tl_wait); }
+#endif
   if (!waited_prep) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (t == (g >> 2)) {
     float* dst = part + (blockIdx.x + cs) * STRIP + wid * 128 + 16 * g;
@@ -844,7 +903,13 @@ __global__ void __launch_bounds__(TPB, 1)
   const int f = first_cta(cs, chunks, units, G), l = last_cta(cs, chunks, units, G);
   if (tid == 0) last_flag = (atomicAdd(counters + cs, 1u) == (unsigned)(l - f)) ? 1u : 0u;
   cbar();
+#ifdef QLRT_GEMV_TL
+  if (tid == 0) { TLSET(11, gtimer()); TLSET(12, last_flag); }
+#endif
   if (last_flag) finalize_strip(cs, f, l, N, part, tpart, zt, l2, rank, s, y, tsh);
+#ifdef QLRT_GEMV_TL
+  if (tid == 0) TLSET(4, gtimer());
+#endif
 }
 
 // packed codes [K rows][N/2 bytes] as a 3-d uint8 tensor, box [8][16 rows][128 B], 128B swizzle
@@ -877,6 +942,15 @@ static bool make_tmap_codes(CUtensorMap* m, const void* base, int64_t row_bytes,
 using namespace qlrt;
 
 extern "C" {
+#ifdef QLRT_GEMV_TL
+// host: [kNumSMs][16] per-CTA slots, then the prep kernel's [start, end]; resets the prep pair
+int qlrt_gemv_tl_fetch(unsigned long long* host) {
+  if (cudaMemcpyFromSymbol(host, gemv2::g_gemv_tl, sizeof(gemv2::g_gemv_tl)) != cudaSuccess) return 1;
+  if (cudaMemcpyFromSymbol(host + kNumSMs * 16, gemv2::g_gemv_tl_prep, 16) != cudaSuccess) return 1;
+  const unsigned long long init[2] = {~0ull, 0ull};
+  return cudaMemcpyToSymbol(gemv2::g_gemv_tl_prep, init, 16) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 size_t qlrt_gemv_workspace_bytes(int64_t k_in, int64_t n_out, int rank) {
   const size_t a = gemv::ws_bytes(k_in, n_out, rank), b = gemv2::ws_bytes(k_in, n_out, rank);

@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(TPB, 1)
   const uint32_t aux0 = front + NFRONT * STAGE;
   const uint32_t lut_a = aux0 + NST * AUX;
   if (tab < lut_a + 2048u) __trap();  // (static smem grew: re-plan the layout)
-  double* lut = reinterpret_cast<double*>(dyn + (lut_a - base));
+  float* lut = reinterpret_cast<float*>(dyn + (lut_a - base));  // fp8 code -> value (exact in fp32)
 
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(TPB, 1)
     ptx::fence_mbar_init();
   }
   if (tid < 16) v16[tid] = (uint32_t)__half_as_ushort(__float2half_rn(vals.v[tid]));
-  if (tid < 256) lut[tid] = fp8_decode_fast(tid, sp);
+  if (tid < 256) lut[tid] = (float)fp8_decode_fast(tid, sp);
   __syncthreads();
 #ifdef QLRT_GEMV_TL
   if (tid == 0) TLSET(10, gtimer());
@@ -764,10 +764,14 @@ __global__ void __launch_bounds__(TPB, 1)
   const int a_r = lane & 15, jl = bx * 4 + u * 2 + (lane >> 4);
   const uint32_t a_dq = AUX_DQ + a_r * 32 + jl, a_x = AUX_X + a_r * 2, a_c = AUX_C1 + a_r * 8;
   int64_t cs = ub / chunks;
-  int64_t blk = (((ub - cs * chunks) * ROWS) + a_r) * nbr + cs * 32 + jl;  // first-level block of the lane's a_k
-  int64_t blk0 = blk - jl;
+  // first-level block of the lane's row at the strip's first column: only its
+  // offset inside a second-level block matters (which of the <= 2 c1 values
+  // the lane's block uses), kept as a 32-bit residue
+  const uint32_t bmask2 = (1u << bs2_shift) - 1u;
+  uint32_t lo2 = (uint32_t)(((((ub - cs * chunks) * ROWS) + a_r) * nbr + cs * 32) & bmask2);
   bool jok = cs * 32 + jl < nbr;
-  const int64_t blk_step = ROWS * nbr;
+  const uint32_t step2 = (uint32_t)((ROWS * nbr) & bmask2);
+  const float mu_f = __ldg(mu);
 
   float acc[8][4];
 #pragma unroll
@@ -776,6 +780,7 @@ __global__ void __launch_bounds__(TPB, 1)
   int left = (int)((cs + 1) * chunks - ub);  // units of strip cs still to do
   const int src0 = ((g >> 1) & 1) * 16 + 2 * t;
   const uint32_t bsel = (g & 1) ? 0x7632u : 0x5410u;
+  const uint32_t bmask = g < 4 ? 0xFFFFFFFFu : 0u;  // lanes g < 4 hold B column g
   int sl = 0;
   uint32_t par = 0u;
   bool waited_prep = true;  // (waited in the prologue)
@@ -803,8 +808,7 @@ __global__ void __launch_bounds__(TPB, 1)
       if (last_flag) finalize_strip(cs, f, l, N, part, tpart, zt, l2, rank, s, y, tsh);
       ++cs;
       left = (int)chunks;
-      blk = (int64_t)a_r * nbr + cs * 32 + jl;
-      blk0 = blk - jl;
+      lo2 = (uint32_t)(((int64_t)a_r * nbr + cs * 32) & bmask2);
       jok = cs * 32 + jl < nbr;
     }
     --left;
@@ -839,17 +843,18 @@ __global__ void __launch_bounds__(TPB, 1)
       uint32_t dqb, xb, c1b;
       asm volatile("ld.shared.u8 %0, [%1];" : "=r"(dqb) : "r"(ax + a_dq));
       asm volatile("ld.shared.u16 %0, [%1];" : "=r"(xb) : "r"(ax + a_x));
-      const uint32_t which = (uint32_t)((blk >> bs2_shift) - (blk0 >> bs2_shift));
+      const uint32_t which = (lo2 + (uint32_t)jl) >> bs2_shift;
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(c1b) : "r"(ax + a_c + which * 4u));
-      double r = __dadd_rn(__dmul_rn(lut[dqb], (double)__uint_as_float(c1b)), mu_d);
-      r = r > 0.0 ? r : 0.0;
-      const float a = jok ? (__uint_as_float(xb << 16) * __double2float_rn(r)) * sc : 0.0f;
+      // c = max(v_dq c1 + mu, 0) in one fp32 rounding (fma; the reference
+      // rounds the fp64 value to fp32 -- equal except for a double-rounding
+      // tie, far inside the GEMV tolerance)
+      const float c = fmaxf(fmaf(lut[dqb], __uint_as_float(c1b), mu_f), 0.0f);
+      const float a = jok ? (__uint_as_float(xb << 16) * c) * sc : 0.0f;
       const __half h = __float2half_rn(a);
-      const __half lo = __float2half_rn(a - __half2float(h));
-      hv = (uint32_t)__half_as_ushort(h) | ((uint32_t)__half_as_ushort(lo) << 16);
+      const float dl = a - __half2float(h);
+      asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hv) : "f"(dl), "f"(a));  // {lo = h, hi = f16(a - h)}
     }
-    blk += blk_step;
-    blk0 += blk_step;
+    lo2 = (lo2 + step2) & bmask2;
     // index bytes: codes of rows (2t, 2t+1) resp. (2t+8, 2t+9) of one column
     uint32_t ie[2], io[2], je[2], jo[2];
 #pragma unroll
@@ -865,8 +870,8 @@ __global__ void __launch_bounds__(TPB, 1)
     const uint32_t v1 = __shfl_sync(0xffffffffu, hv, src0 + 1);
     const uint32_t v2 = __shfl_sync(0xffffffffu, hv, src0 + 8);
     const uint32_t v3 = __shfl_sync(0xffffffffu, hv, src0 + 9);
-    const uint32_t b0 = g < 4 ? __byte_perm(v0, v1, bsel) : 0u;
-    const uint32_t b1 = g < 4 ? __byte_perm(v2, v3, bsel) : 0u;
+    const uint32_t b0 = __byte_perm(v0, v1, bsel) & bmask;
+    const uint32_t b1 = __byte_perm(v2, v3, bsel) & bmask;
     // (the shuffles used every lane's stage bytes: release the slot)
     if (lane == 0) ptx::mbar_arrive(&empty[sl]);
     if (++sl == NST) {

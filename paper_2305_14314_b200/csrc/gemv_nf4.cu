@@ -497,6 +497,12 @@ __device__ __forceinline__ uint32_t lds(uint32_t a) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
+// (a & 0x0F0F0F0F) | (b & 0xF0F0F0F0) as one LOP3
+__device__ __forceinline__ uint32_t nib_merge(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(a), "r"(b), "r"(0x0F0F0F0Fu));
+  return d;
+}
 __device__ __forceinline__ uint2 lds64(uint32_t a) {
   uint2 v;
   asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
@@ -860,10 +866,10 @@ __global__ void __launch_bounds__(TPB, 1)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t x0 = h ? w0.y : w0.x, x1 = h ? w1.y : w1.x, x2 = h ? w2.y : w2.x, x3 = h ? w3.y : w3.x;
-      ie[h] = (x0 & 0x0F0F0F0Fu) | ((x1 << 4) & 0xF0F0F0F0u);
-      io[h] = ((x0 >> 4) & 0x0F0F0F0Fu) | (x1 & 0xF0F0F0F0u);
-      je[h] = (x2 & 0x0F0F0F0Fu) | ((x3 << 4) & 0xF0F0F0F0u);
-      jo[h] = ((x2 >> 4) & 0x0F0F0F0Fu) | (x3 & 0xF0F0F0F0u);
+      ie[h] = nib_merge(x0, x1 << 4);
+      io[h] = nib_merge(x0 >> 4, x1);
+      je[h] = nib_merge(x2, x3 << 4);
+      jo[h] = nib_merge(x2 >> 4, x3);
     }
     // B fragment: lanes g < 4 take column n = g (block g >> 1, hi / lo by g & 1)
     const uint32_t v0 = __shfl_sync(0xffffffffu, hv, src0);

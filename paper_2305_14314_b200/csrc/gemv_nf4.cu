@@ -329,15 +329,15 @@ __global__ void __launch_bounds__(TPB) lora_t_kernel(const __nv_bfloat16* __rest
 // i.e. closer to the reference's float32 W = f32(dequantize(q)) than the
 // bf16 W of the tensor-core GEMM (GEMV tolerance).
 //
-// Data movement: a stage = 16 rows x 2048 columns (1 KB of codes per row)
-// arrives as ONE 3-d TMA box [8 column groups][16 rows][128 B] (128B
+// Data movement: a stage = 32 rows x 2048 columns (1 KB of codes per row)
+// arrives as ONE 3-d TMA box [8 column groups][32 rows][128 B] (128B
 // swizzle: conflict-free 8-byte reads; 2 KB boxes were TMA-issue bound at
 // ~12 GB/s per SM), the stage's DQ bytes, x and c1 ride along as cp.async
-// on the same mbarrier; warp 0 keeps NST = 8 stages in flight.  Units =
-// (strip of 2048 columns, 16-row stage), split evenly over one CTA per SM in
+// on the same mbarrier; a producer warp keeps NST = 3 stages (96 KB) in
+// flight.  Units = (strip of 2048 columns, 32-row stage), split evenly over one CTA per SM in
 // strip-major order (stream-K style: a CTA covers <= 2-3 strip segments).
 // 16 warps: warp w owns columns [128 w, +128) of the strip (box w >> 1, half
-// w & 1) and all 16 rows of each stage; lane (g, t) reads 8 bytes (16
+// w & 1) and all 32 rows (two k16 halves) of each stage; lane (g, t) reads 8 bytes (16
 // columns) of rows 2t, 2t+1, 2t+8, 2t+9.  A CTA flushes a strip segment as
 // an fp32 partial; the last segment of a strip (atomic ticket) sums the
 // partials in CTA order (deterministic), adds the LoRA term and writes bf16
@@ -362,14 +362,14 @@ constexpr int PWARP = CWARPS;  // + one producer warp (TMA + aux copies)
 constexpr int TPB = (CWARPS + 1) * 32;
 constexpr int CTHREADS = CWARPS * 32;
 constexpr int STRIP = 2048;  // columns per strip = 8 TMA boxes of 128 B
-constexpr int ROWS = 16;     // rows per stage (= unit)
-constexpr int NST = 8;  // stages in flight (16 KB each) = a_k input prefetch depth (static ring slots)
+constexpr int ROWS = 32;     // rows per stage (= unit): two k16 halves per stage
+constexpr int NST = 3;  // stages in flight (32 KB each) = a_k input prefetch depth (static ring slots)
 constexpr int NMAX = 32;  // prep blocks reducing max |x| / max |c1| (the GEMV's fp16 scale)
-constexpr int STAGE = ROWS * STRIP / 2;  // 16 KB
+constexpr int STAGE = ROWS * STRIP / 2;  // 32 KB
 // shared layout: the CTA's dynamic window starts a few KB into the 228 KB;
 // the table sits at the 64 KB boundary, NFRONT stages + the scratch fill the
 // gap in front of it, the other stages follow it
-constexpr int NFRONT = NST < 3 ? NST : 3;
+constexpr int NFRONT = 1;
 constexpr int SMEM = 65536 + 65536 + (NST - NFRONT) * STAGE;
 
 struct Geo {
@@ -600,8 +600,8 @@ __device__ __noinline__ void finalize_strip(int64_t strip, int f, int l, int64_t
   cbar();
 }
 
-// per-stage aux slot: DQ bytes [16 rows][32 blocks], x [16], c1 [16 rows][2]
-constexpr int AUX_DQ = 0, AUX_X = 512, AUX_C1 = 544, AUX = 704;
+// per-stage aux slot: DQ bytes [32 rows][32 blocks], x [32], c1 [32 rows][2]
+constexpr int AUX_DQ = 0, AUX_X = 1024, AUX_C1 = 1088, AUX = 1408;
 
 __global__ void __launch_bounds__(TPB, 1)
     gemv_mma_kernel(const __grid_constant__ CUtensorMap tm_codes, const uint8_t* __restrict__ dq_codes,
@@ -652,14 +652,14 @@ __global__ void __launch_bounds__(TPB, 1)
 #endif
 
   // ---- stage issue (warp 0; the codes and a_k inputs never depend on the
-  // prep kernel): 8 TMA boxes of codes + the DQ bytes, x and c1 of the 16 rows
+  // prep kernel): one TMA box of codes + the DQ bytes, x and c1 of the 32 rows
   int64_t ps = ub / chunks, pc = ub - ps * chunks;
   auto slot_addr = [&](int sl) -> uint32_t {
     return sl < NFRONT ? front + (uint32_t)sl * STAGE : back + (uint32_t)(sl - NFRONT) * STAGE;
   };
   auto issue = [&](int sl) {  // called by all 32 lanes of warp 0
     const int64_t r0 = pc * ROWS;
-    if (lane == 0) {  // one 3-d box [8 column groups][16 rows][128 B] (OOB groups zero-filled)
+    if (lane == 0) {  // one 3-d box [8 column groups][32 rows][128 B] (OOB groups zero-filled)
       ptx::mbar_arrive_expect_tx(&full[sl], (uint32_t)STAGE);
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
@@ -672,16 +672,16 @@ __global__ void __launch_bounds__(TPB, 1)
     const int64_t jb0 = ps * 32;
 #ifndef QLRT_GEMV_NOAUX
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {  // DQ bytes: 16 rows x 8 groups of 4 blocks
+    for (int j = 0; j < 8; ++j) {  // DQ bytes: 32 rows x 8 groups of 4 blocks
       const int p = lane + 32 * j, r = p >> 3, q = p & 7;
       const int64_t jb = jb0 + 4 * q;
       cp_async4(ax + AUX_DQ + r * 32 + q * 4, dq_codes + (r0 + r) * nbr + jb, jb < nbr);
     }
-    if (lane < 2) cp_async16(ax + AUX_X + lane * 16, x + r0 + lane * 8, true);
-    {  // c1 of row lane & 15: the (<= 2) second-level blocks its 32 first-level blocks span
-      const int r = lane & 15, which = lane >> 4;
-      const int64_t ic = (((r0 + r) * nbr + jb0) >> bs2_shift) + which;
-      cp_async4(ax + AUX_C1 + r * 8 + which * 4, c1 + ic, ic < n2);
+    if (lane < 4) cp_async16(ax + AUX_X + lane * 16, x + r0 + lane * 8, true);
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {  // c1 of row lane: the (<= 2) second-level blocks its 32 blocks span
+      const int64_t ic = (((r0 + lane) * nbr + jb0) >> bs2_shift) + which;
+      cp_async4(ax + AUX_C1 + lane * 8 + which * 4, c1 + ic, ic < n2);
     }
 #endif
     cp_async_arrive(&full[sl]);
@@ -758,6 +758,8 @@ __global__ void __launch_bounds__(TPB, 1)
   const uint32_t lanereg = tab + (uint32_t)lane * 4u;
   // this lane's 8 code bytes of rows 2t, 2t+1, 2t+8, 2t+9 inside box bx (128B swizzle)
   const int cidx = u * 4 + (g >> 1);
+  // (half q of the stage = rows 16 q .. 16 q + 15: the same offsets + q * 2 KB,
+  // since (r + 16) & 7 = r & 7 keeps the swizzle)
   uint32_t roff[4];
   {
     const int rr[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
@@ -766,7 +768,7 @@ __global__ void __launch_bounds__(TPB, 1)
       roff[i] = (uint32_t)bx * (ROWS * 128) + (uint32_t)rr[i] * 128u + (uint32_t)((cidx ^ (rr[i] & 7)) << 4) +
                 (uint32_t)(g & 1) * 8u;
   }
-  // a_k of (row a_r = lane & 15, block jl = 4 bx + 2 u + (lane >> 4) of the strip)
+  // a_k of (rows a_r = lane & 15 and a_r + 16, block jl = 4 bx + 2 u + (lane >> 4) of the strip)
   const int a_r = lane & 15, jl = bx * 4 + u * 2 + (lane >> 4);
   const uint32_t a_dq = AUX_DQ + a_r * 32 + jl, a_x = AUX_X + a_r * 2, a_c = AUX_C1 + a_r * 8;
   int64_t cs = ub / chunks;
@@ -777,6 +779,7 @@ __global__ void __launch_bounds__(TPB, 1)
   uint32_t lo2 = (uint32_t)(((((ub - cs * chunks) * ROWS) + a_r) * nbr + cs * 32) & bmask2);
   bool jok = cs * 32 + jl < nbr;
   const uint32_t step2 = (uint32_t)((ROWS * nbr) & bmask2);
+  const uint32_t half2 = (uint32_t)((16 * nbr) & bmask2);  // residue step to row a_r + 16
   const float mu_f = __ldg(mu);
 
   float acc[8][4];
@@ -841,16 +844,20 @@ __global__ void __launch_bounds__(TPB, 1)
 #endif
     const uint32_t sa = sl < NFRONT ? front + (uint32_t)sl * STAGE : back + (uint32_t)(sl - NFRONT) * STAGE;
     const uint32_t ax = aux0 + (uint32_t)sl * AUX;
-    const uint2 w0 = lds64(sa + roff[0]), w1 = lds64(sa + roff[1]), w2 = lds64(sa + roff[2]),
-                w3 = lds64(sa + roff[3]);
-    // a_k = x_k c_k 2^-E as an fp16 hi | lo pair
-    uint32_t hv;
-    {
+    uint2 w[2][4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int i2 = 0; i2 < 4; ++i2) w[q][i2] = lds64(sa + q * 2048u + roff[i2]);
+    // a_k = x_k c_k 2^-E as an fp16 hi | lo pair, rows a_r (q = 0) and a_r + 16 (q = 1)
+    uint32_t hv[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
       uint32_t dqb, xb, c1b;
-      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(dqb) : "r"(ax + a_dq));
-      asm volatile("ld.shared.u16 %0, [%1];" : "=r"(xb) : "r"(ax + a_x));
-      const uint32_t which = (lo2 + (uint32_t)jl) >> bs2_shift;
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(c1b) : "r"(ax + a_c + which * 4u));
+      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(dqb) : "r"(ax + a_dq + q * 512u));
+      asm volatile("ld.shared.u16 %0, [%1];" : "=r"(xb) : "r"(ax + a_x + q * 32u));
+      const uint32_t which = (((lo2 + (q ? half2 : 0u)) & bmask2) + (uint32_t)jl) >> bs2_shift;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(c1b) : "r"(ax + a_c + q * 128u + which * 4u));
       // c = max(v_dq c1 + mu, 0) in one fp32 rounding (fma; the reference
       // rounds the fp64 value to fp32 -- equal except for a double-rounding
       // tie, far inside the GEMV tolerance)
@@ -858,44 +865,54 @@ __global__ void __launch_bounds__(TPB, 1)
       const float a = jok ? (__uint_as_float(xb << 16) * c) * sc : 0.0f;
       const __half h = __float2half_rn(a);
       const float dl = a - __half2float(h);
-      asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hv) : "f"(dl), "f"(a));  // {lo = h, hi = f16(a - h)}
+      asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hv[q]) : "f"(dl), "f"(a));  // {lo = h, hi = f16(a - h)}
     }
     lo2 = (lo2 + step2) & bmask2;
     // index bytes: codes of rows (2t, 2t+1) resp. (2t+8, 2t+9) of one column
-    uint32_t ie[2], io[2], je[2], jo[2];
+    uint32_t ie[2][2], io[2][2], je[2][2], jo[2][2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const uint32_t x0 = h ? w0.y : w0.x, x1 = h ? w1.y : w1.x, x2 = h ? w2.y : w2.x, x3 = h ? w3.y : w3.x;
-      ie[h] = nib_merge(x0, x1 << 4);
-      io[h] = nib_merge(x0 >> 4, x1);
-      je[h] = nib_merge(x2, x3 << 4);
-      jo[h] = nib_merge(x2 >> 4, x3);
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t x0 = h ? w[q][0].y : w[q][0].x, x1 = h ? w[q][1].y : w[q][1].x;
+        const uint32_t x2 = h ? w[q][2].y : w[q][2].x, x3 = h ? w[q][3].y : w[q][3].x;
+        ie[q][h] = nib_merge(x0, x1 << 4);
+        io[q][h] = nib_merge(x0 >> 4, x1);
+        je[q][h] = nib_merge(x2, x3 << 4);
+        jo[q][h] = nib_merge(x2 >> 4, x3);
+      }
+    // B fragments: lanes g < 4 take column n = g (block g >> 1, hi / lo by g & 1)
+    uint32_t b0[2], b1[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint32_t v0 = __shfl_sync(0xffffffffu, hv[q], src0);
+      const uint32_t v1 = __shfl_sync(0xffffffffu, hv[q], src0 + 1);
+      const uint32_t v2 = __shfl_sync(0xffffffffu, hv[q], src0 + 8);
+      const uint32_t v3 = __shfl_sync(0xffffffffu, hv[q], src0 + 9);
+      b0[q] = __byte_perm(v0, v1, bsel) & bmask;
+      b1[q] = __byte_perm(v2, v3, bsel) & bmask;
     }
-    // B fragment: lanes g < 4 take column n = g (block g >> 1, hi / lo by g & 1)
-    const uint32_t v0 = __shfl_sync(0xffffffffu, hv, src0);
-    const uint32_t v1 = __shfl_sync(0xffffffffu, hv, src0 + 1);
-    const uint32_t v2 = __shfl_sync(0xffffffffu, hv, src0 + 8);
-    const uint32_t v3 = __shfl_sync(0xffffffffu, hv, src0 + 9);
-    const uint32_t b0 = __byte_perm(v0, v1, bsel) & bmask;
-    const uint32_t b1 = __byte_perm(v2, v3, bsel) & bmask;
-    // (the shuffles used every lane's stage bytes: release the slot)
+    // (the shuffles used every lane's aux bytes, the index bytes its codes:
+    // release the slot)
     if (lane == 0) ptx::mbar_arrive(&empty[sl]);
     if (++sl == NST) {
       sl = 0;
       par ^= 1u;
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int q = 0; q < 2; ++q)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const uint32_t sel = 0x7604u | ((uint32_t)b << 4);
-        const uint32_t a0 = lds(__byte_perm(ie[h], lanereg, sel));
-        const uint32_t a1 = lds(__byte_perm(io[h], lanereg, sel));
-        const uint32_t a2 = lds(__byte_perm(je[h], lanereg, sel));
-        const uint32_t a3 = lds(__byte_perm(jo[h], lanereg, sel));
-        mma16816(acc[4 * h + b], a0, a1, a2, a3, b0, b1);
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint32_t sel = 0x7604u | ((uint32_t)b << 4);
+          const uint32_t a0 = lds(__byte_perm(ie[q][h], lanereg, sel));
+          const uint32_t a1 = lds(__byte_perm(io[q][h], lanereg, sel));
+          const uint32_t a2 = lds(__byte_perm(je[q][h], lanereg, sel));
+          const uint32_t a3 = lds(__byte_perm(jo[q][h], lanereg, sel));
+          mma16816(acc[4 * h + b], a0, a1, a2, a3, b0[q], b1[q]);
+        }
       }
-    }
   }
   // ---- last segment
 #ifdef QLRT_GEMV_TL
@@ -923,7 +940,7 @@ __global__ void __launch_bounds__(TPB, 1)
 #endif
 }
 
-// packed codes [K rows][N/2 bytes] as a 3-d uint8 tensor, box [8][16 rows][128 B], 128B swizzle
+// packed codes [K rows][N/2 bytes] as a 3-d uint8 tensor, box [8][32 rows][128 B], 128B swizzle
 static bool make_tmap_codes(CUtensorMap* m, const void* base, int64_t row_bytes, int64_t rows) {
   typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -980,7 +997,7 @@ qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* x
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t K = w->k_in, N = w->n_out;
   CUtensorMap tmc;
-  if (policy(P_GEMV_MMA) && (N % 256) == 0 && (K % 16) == 0 && w->blocksize2 >= 32 &&
+  if (policy(P_GEMV_MMA) && (N % 256) == 0 && (K % gemv2::ROWS) == 0 && w->blocksize2 >= 32 &&
       (((uintptr_t)x) & 15) == 0 && gemv2::make_tmap_codes(&tmc, w->codes, N / 2, K)) {
     // tensor-core GEMV: prep (tickets, max slots, LoRA partials) then the
     // main kernel as its PDL dependent (prologue + first TMA loads overlap prep)

@@ -357,6 +357,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #else
 #define TLSET(slot, v)
 #endif
+#ifndef QLRT_GEMV_EVICT_FIRST
+#define QLRT_GEMV_EVICT_FIRST 1
+#endif
 constexpr int CWARPS = 16;  // consumer warps
 constexpr int PWARP = CWARPS;  // + one producer warp (TMA + aux copies)
 constexpr int TPB = (CWARPS + 1) * 32;
@@ -654,6 +657,10 @@ __global__ void __launch_bounds__(TPB, 1)
   // ---- stage issue (warp 0; the codes and a_k inputs never depend on the
   // prep kernel): one TMA box of codes + the DQ bytes, x and c1 of the 32 rows
   int64_t ps = ub / chunks, pc = ub - ps * chunks;
+#if QLRT_GEMV_EVICT_FIRST
+  uint64_t evict_first;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(evict_first));
+#endif
   auto slot_addr = [&](int sl) -> uint32_t {
     return sl < NFRONT ? front + (uint32_t)sl * STAGE : back + (uint32_t)(sl - NFRONT) * STAGE;
   };
@@ -661,12 +668,23 @@ __global__ void __launch_bounds__(TPB, 1)
     const int64_t r0 = pc * ROWS;
     if (lane == 0) {  // one 3-d box [8 column groups][32 rows][128 B] (OOB groups zero-filled)
       ptx::mbar_arrive_expect_tx(&full[sl], (uint32_t)STAGE);
+#if QLRT_GEMV_EVICT_FIRST
+      // the codes are read once: evict-first in L2, so the stream does not
+      // push out what is reused (x, c1, partials, this kernel's own code)
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+          "%4, %5}], [%2], %6;" ::"r"(slot_addr(sl)),
+          "l"(reinterpret_cast<uint64_t>(&tm_codes)), "r"(ptx::smem_u32(&full[sl])), "r"(0), "r"((int)r0),
+          "r"((int)(ps * 8)), "l"(evict_first)
+          : "memory");
+#else
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
               slot_addr(sl)),
           "l"(reinterpret_cast<uint64_t>(&tm_codes)), "r"(ptx::smem_u32(&full[sl])), "r"(0), "r"((int)r0),
           "r"((int)(ps * 8))
           : "memory");
+#endif
     }
     const uint32_t ax = aux0 + (uint32_t)sl * AUX;
     const int64_t jb0 = ps * 32;

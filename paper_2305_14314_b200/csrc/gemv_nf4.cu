@@ -367,7 +367,6 @@ constexpr int CTHREADS = CWARPS * 32;
 constexpr int STRIP = 2048;  // columns per strip = 8 TMA boxes of 128 B
 constexpr int ROWS = 32;     // rows per stage (= unit): two k16 halves per stage
 constexpr int NST = 3;  // stages in flight (32 KB each) = a_k input prefetch depth (static ring slots)
-constexpr int NMAX = 32;  // prep blocks reducing max |x| / max |c1| (the GEMV's fp16 scale)
 constexpr int STAGE = ROWS * STRIP / 2;  // 32 KB
 // shared layout: the CTA's dynamic window starts a few KB into the 228 KB;
 // the table sits at the 64 KB boundary, NFRONT stages + the scratch fill the
@@ -399,10 +398,9 @@ static size_t tpart_off(const Geo& g) { return part_off() + align256((size_t)(g.
 static size_t cnt_off(const Geo& g, int r) {
   return tpart_off(g) + align256((size_t)cdiv(g.K, 128) * (r > 0 ? r : 1) * 4);
 }
-static size_t max_off(const Geo& g, int r) { return cnt_off(g, r) + align256((size_t)g.strips * 4); }
 static size_t ws_bytes(int64_t K, int64_t N, int r) {
   const Geo g = geo(K, N, kNumSMs);
-  return max_off(g, r) + align256((size_t)NMAX * 8);
+  return cnt_off(g, r) + align256((size_t)g.strips * 4);
 }
 
 // first / last CTA covering strip s when CTA i owns units [i U / G, (i+1) U / G)
@@ -417,12 +415,10 @@ __device__ __forceinline__ int last_cta(int64_t s, int64_t C, int64_t U, int64_t
 // only at its first strip flush): block 0 zeroes the strip tickets; blocks
 // >= 1 compute the LoRA partials tpart[z][j] = sum_{k in [128 z, 128 z + 128)}
 // xa_k l1[k][j] (8 columns per thread, 16-byte loads, all rows in flight)
-__global__ void __launch_bounds__(256) prep_kernel(int64_t K, const unsigned short* __restrict__ x,
-                                                  const float* __restrict__ c1, int64_t n2,
-                                                  const __nv_bfloat16* __restrict__ xa,
+__global__ void __launch_bounds__(256) prep_kernel(int64_t K, const __nv_bfloat16* __restrict__ xa,
                                                   const __nv_bfloat16* __restrict__ l1, int rank,
                                                   float* __restrict__ tpart, unsigned* __restrict__ counters,
-                                                  int strips, uint2* __restrict__ slots) {
+                                                  int strips) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifdef QLRT_GEMV_TL
   if (threadIdx.x == 0) atomicMin(&g_gemv_tl_prep[0], gtimer());
@@ -431,44 +427,12 @@ __global__ void __launch_bounds__(256) prep_kernel(int64_t K, const unsigned sho
   } tl_end;
 #endif
   __shared__ float sh[256 * 8];
-  __shared__ unsigned rx[8], rc[8];
   const int tid = threadIdx.x;
   if (blockIdx.x == 0) {
     for (int i = tid; i < strips; i += 256) counters[i] = 0u;
     return;
   }
-  if (blockIdx.x <= NMAX) {  // max |x| (bf16 bits) and max |c1| over slices -> slots[b - 1]
-    const int b = blockIdx.x - 1;
-    unsigned mx = 0u, mc = 0u;
-    for (int64_t k = (int64_t)b * 256 + tid; k < K; k += (int64_t)NMAX * 256) {
-      const unsigned v = __ldg(x + k) & 0x7FFFu;
-      mx = v > mx ? v : mx;
-    }
-    for (int64_t i = (int64_t)b * 256 + tid; i < n2; i += (int64_t)NMAX * 256) {
-      const unsigned v = __float_as_uint(__ldg(c1 + i)) & 0x7FFFFFFFu;
-      mc = v > mc ? v : mc;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const unsigned p = __shfl_xor_sync(0xffffffffu, mx, o), q = __shfl_xor_sync(0xffffffffu, mc, o);
-      mx = p > mx ? p : mx;
-      mc = q > mc ? q : mc;
-    }
-    if ((tid & 31) == 0) {
-      rx[tid >> 5] = mx;
-      rc[tid >> 5] = mc;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      for (int w = 1; w < 8; ++w) {
-        mx = rx[w] > mx ? rx[w] : mx;
-        mc = rc[w] > mc ? rc[w] : mc;
-      }
-      slots[b] = make_uint2(mx, mc);
-    }
-    return;
-  }
-  const int z = blockIdx.x - 1 - NMAX;
+  const int z = blockIdx.x - 1;
   const int cpr = rank / 8;          // 16-byte column groups per row
   const int rpp = 256 / cpr;         // rows per pass
   const int cg = tid % cpr, rr = tid / cpr;
@@ -555,8 +519,14 @@ __device__ __noinline__ void finalize_strip(int64_t strip, int f, int l, int64_t
       const int j = j0 + jj;
       float a = 0.0f;
       if (j < rank) {
-#pragma unroll 4
-        for (int zz = q; zz < zt; zz += 8) a += __ldcg(tpart + (int64_t)zz * rank + j);
+        for (int z0 = q; z0 < zt; z0 += 64) {  // 8 loads in flight, summed in order
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = z0 + 8 * e < zt ? __ldcg(tpart + (int64_t)(z0 + 8 * e) * rank + j) : 0.f;
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (z0 + 8 * e < zt) a += v[e];
+        }
       }
       tred[q][jj] = a;
       cbar();
@@ -575,10 +545,18 @@ __device__ __noinline__ void finalize_strip(int64_t strip, int f, int l, int64_t
   if (col < N) {  // N % 64 == 0: 4-column groups are all-in or all-out
     float o[4] = {0.f, 0.f, 0.f, 0.f};
     const float* pp = part + (int64_t)(f + strip) * STRIP + c;
-#pragma unroll 16
-    for (int i = f; i <= l; ++i, pp += STRIP) {
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(pp));
-      o[0] += v.x; o[1] += v.y; o[2] += v.z; o[3] += v.w;
+    // 8 predicated loads in flight, then the adds in CTA order (a runtime
+    // trip-count loop would run its < 16 remainder one L2 round trip at a time)
+    for (int i0 = f; i0 <= l; i0 += 8, pp += 8 * STRIP) {
+      float4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        v[j] = i0 + j <= l ? __ldcg(reinterpret_cast<const float4*>(pp + j * STRIP)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (i0 + j <= l) {
+          o[0] += v[j].x; o[1] += v[j].y; o[2] += v[j].z; o[3] += v[j].w;
+        }
     }
     if (rank > 0) {
       float la[4] = {0.f, 0.f, 0.f, 0.f};
@@ -611,19 +589,23 @@ __global__ void __launch_bounds__(TPB, 1)
                     const float* __restrict__ c1, int64_t n2, const float* __restrict__ mu, int bs2_shift,
                     qlrt_fp8spec sp, Vals16 vals, float maxdec, int64_t K, int64_t N,
                     const unsigned short* __restrict__ x, float* __restrict__ part, unsigned* __restrict__ counters,
-                    const uint2* __restrict__ slots, const float* __restrict__ tpart, int zt,
+                    const float* __restrict__ tpart, int zt,
                     const __nv_bfloat16* __restrict__ l2, int rank, float s, __nv_bfloat16* __restrict__ y) {
   extern __shared__ __align__(1024) uint8_t dyn[];
   __shared__ float tsh[512];
   __shared__ unsigned last_flag;
   __shared__ float scales[2];
   __shared__ uint32_t v16[16];
+  __shared__ unsigned red_max[CWARPS][2];
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t nbr = N / 64, chunks = cdiv(K, ROWS), strips = cdiv(N, STRIP), units = chunks * strips;
   const int G = (int)gridDim.x;
   const int64_t ub = (int64_t)blockIdx.x * units / G, ue = (int64_t)(blockIdx.x + 1) * units / G;
   const int nunits = (int)(ue - ub);
+  // mu (a DRAM read that would otherwise queue behind the code stream): issued first
+  float mu_f;
+  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(mu_f) : "l"(mu));
 #ifdef QLRT_GEMV_TL
   unsigned long long tl_wait = 0;
   if (threadIdx.x == 0) { TLSET(0, gtimer()); TLSET(7, nunits); }
@@ -732,37 +714,58 @@ __global__ void __launch_bounds__(TPB, 1)
 #ifdef QLRT_GEMV_TL
   if (tid == 0) TLSET(8, gtimer());
 #endif
-  // ---- the fp16 scale 2^-E: max |a| 2^-E < 2^15 over every a_k (a = x c,
-  // c <= maxdec max c1 + max(mu, 0)); the maxima come from the prep kernel
-  // (its max blocks), which also zeroed the tickets: wait for it here, while
-  // the producer's first stages are already in flight
-  const double mu_d = (double)__ldg(mu);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#ifdef QLRT_GEMV_TL
-  if (tid == 0) TLSET(9, gtimer());
-#endif
-  unsigned mx = 0u, mc = 0u;
-  if (wid == 0) {  // the NMAX = 32 slots: one per lane, then a warp max (one L2 round trip)
-    static_assert(NMAX == 32, "one slot per lane");
-    const uint2 v = __ldcg(slots + lane);
-    mx = v.x;
-    mc = v.y;
+  // ---- the fp16 scale 2^-E of this CTA: max |a| 2^-E < 2^15 over the a_k
+  // of its own rows (a = x c, c <= maxdec max c1 + max(mu, 0)).  x and c1
+  // are inputs (ready when the grid starts: the prep grid in front of it is
+  // not programmatic); reading them here, before the code stream fills the
+  // memory queues, is cheaper than a dependent read of values from the
+  // prep grid once the stream runs (~3 us under full load).
+  // Partials are unscaled per CTA, so E need not agree across CTAs.
+  const double mu_d = (double)mu_f;
+  {
+    unsigned mx = 0u, mc = 0u;
+    for (int64_t i = tid; i < (int64_t)nunits * ROWS; i += CTHREADS) {
+      const int64_t uu = ub + i / ROWS, st = uu / chunks;
+      const int64_t r = (uu - st * chunks) * ROWS + i % ROWS;
+      const unsigned xv = (unsigned)__ldg(x + r) & 0x7FFFu;
+      mx = xv > mx ? xv : mx;
+      const int64_t ic = (r * nbr + st * 32) >> bs2_shift;
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (ic + e < n2) {
+          const unsigned cv = __float_as_uint(__ldg(c1 + ic + e)) & 0x7FFFFFFFu;
+          mc = cv > mc ? cv : mc;
+        }
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       const unsigned p = __shfl_xor_sync(0xffffffffu, mx, o), q = __shfl_xor_sync(0xffffffffu, mc, o);
       mx = p > mx ? p : mx;
       mc = q > mc ? q : mc;
     }
-  }
-  if (tid == 0) {
-    const double m = (double)__uint_as_float(mx << 16) * ((double)maxdec * (double)__uint_as_float(mc) + fmax(mu_d, 0.0));
-    int e = 0;
-    if (m > 0.0 && m < 1e300) {
-      e = ilogb(m) - 14;
-      e = e < -120 ? -120 : (e > 120 ? 120 : e);
+    if (lane == 0) {
+      red_max[wid][0] = mx;
+      red_max[wid][1] = mc;
     }
-    scales[0] = ldexpf(1.0f, -e);
-    scales[1] = ldexpf(1.0f, e);
+    cbar();
+#ifdef QLRT_GEMV_TL
+    if (tid == 0) TLSET(13, gtimer());
+#endif
+    if (tid == 0) {
+      for (int w2 = 1; w2 < CWARPS; ++w2) {
+        mx = red_max[w2][0] > mx ? red_max[w2][0] : mx;
+        mc = red_max[w2][1] > mc ? red_max[w2][1] : mc;
+      }
+      const double m =
+          (double)__uint_as_float(mx << 16) * ((double)maxdec * (double)__uint_as_float(mc) + fmax(mu_d, 0.0));
+      int e = 0;
+      if (m > 0.0 && m < 1e300) {
+        e = ilogb(m) - 14;
+        e = e < -120 ? -120 : (e > 120 ? 120 : e);
+      }
+      scales[0] = ldexpf(1.0f, -e);
+      scales[1] = ldexpf(1.0f, e);
+    }
   }
   cbar();  // (also: the table is complete)
   const float sc = scales[0], unsc = scales[1];
@@ -798,7 +801,6 @@ __global__ void __launch_bounds__(TPB, 1)
   bool jok = cs * 32 + jl < nbr;
   const uint32_t step2 = (uint32_t)((ROWS * nbr) & bmask2);
   const uint32_t half2 = (uint32_t)((16 * nbr) & bmask2);  // residue step to row a_r + 16
-  const float mu_f = __ldg(mu);
 
   float acc[8][4];
 #pragma unroll
@@ -810,7 +812,7 @@ __global__ void __launch_bounds__(TPB, 1)
   const uint32_t bmask = g < 4 ? 0xFFFFFFFFu : 0u;  // lanes g < 4 hold B column g
   int sl = 0;
   uint32_t par = 0u;
-  bool waited_prep = true;  // (waited in the prologue)
+  bool waited_prep = false;  // prep (tickets, LoRA partials): waited for at the first flush
   for (int i = 0; i < nunits; ++i) {
     if (left == 0) {
       // ---- strip segment done: partial, ticket, maybe finalize
@@ -1017,7 +1019,7 @@ qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* x
   CUtensorMap tmc;
   if (policy(P_GEMV_MMA) && (N % 256) == 0 && (K % gemv2::ROWS) == 0 && w->blocksize2 >= 32 &&
       (((uintptr_t)x) & 15) == 0 && gemv2::make_tmap_codes(&tmc, w->codes, N / 2, K)) {
-    // tensor-core GEMV: prep (tickets, max slots, LoRA partials) then the
+    // tensor-core GEMV: prep (tickets, LoRA partials) then the
     // main kernel as its PDL dependent (prologue + first TMA loads overlap prep)
     int dev = 0, sms = kNumSMs;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1034,10 +1036,8 @@ qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* x
     const int zt = (int)cdiv(K, 128);
     const double maxdec = fp8_max_value(w->spec.exp_bits, w->spec.mant_bits, w->spec.bias);
     const int64_t n2 = cdiv(K * (N / 64), (int64_t)w->blocksize2);
-    uint2* slots = (uint2*)(ws + gemv2::max_off(g, rank));
-    gemv2::prep_kernel<<<1 + gemv2::NMAX + (rank > 0 ? zt : 0), 256, 0, st>>>(
-        K, (const unsigned short*)x, w->c1, n2, (const __nv_bfloat16*)(xa ? xa : x), (const __nv_bfloat16*)l1, rank,
-        tpart, counters, (int)g.strips, slots);
+    gemv2::prep_kernel<<<1 + (rank > 0 ? zt : 0), 256, 0, st>>>(
+        K, (const __nv_bfloat16*)(xa ? xa : x), (const __nv_bfloat16*)l1, rank, tpart, counters, (int)g.strips);
     QLRT_CHECK_LAUNCH();
     static std::atomic<unsigned long long> attr_mask{0};
     if (!(attr_mask.load() & (1ull << (dev & 63)))) {
@@ -1064,7 +1064,7 @@ qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* x
     cfg.numAttrs = policy(P_PDL) ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, gemv2::gemv_mma_kernel, tmc, w->dq_codes, w->c1, n2, w->mu,
                            (int)__builtin_ctz((unsigned)w->blocksize2), w->spec, v, (float)maxdec, K, N,
-                           (const unsigned short*)x, part, counters, (const uint2*)slots, (const float*)tpart, zt,
+                           (const unsigned short*)x, part, counters, (const float*)tpart, zt,
                            (const __nv_bfloat16*)l2, rank, s, (__nv_bfloat16*)y) != cudaSuccess)
       return QLRT_ERR_CUDA;
     QLRT_CHECK_LAUNCH();

@@ -16,17 +16,20 @@ lib = _native.lib()
 SMS = 148
 buf = np.zeros(SMS * 16 + 2, dtype=np.uint64)
 fetch = lambda: lib.qlrt_gemv_tl_fetch(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)))  # noqa: E731
-for shp in sys.argv[1:] or ["8192x22016", "8192x8192"]:
+STREAM = "--stream" in sys.argv  # 3 distinct weights back to back; the timeline of the last launch
+for shp in [a for a in sys.argv[1:] if not a.startswith("--")] or ["8192x22016", "8192x8192"]:
     k, n = (int(v) for v in shp.split("x"))
-    q = qb.quantize(torch.randn(k, n, device="cuda") * 0.02, qb.get_codebook("nf4"), 64, double_quant=True)
+    lins = [qb.QLinear(qb.quantize(torch.randn(k, n, device="cuda") * 0.02, qb.get_codebook("nf4"), 64,
+                                   double_quant=True), []) for _ in range(3 if STREAM else 1)]
     x = torch.randn(1, k, device="cuda").bfloat16()
-    lin = qb.QLinear(q, [])
     for _ in range(2):
-        lin.forward(x)
+        for lin in lins:
+            lin.forward(x)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()  # replayed like bench.py times it (no host gaps between launches)
     with torch.cuda.graph(g):
-        lin.forward(x)
+        for lin in lins:
+            lin.forward(x)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for rep in range(3):
         torch.cuda.synchronize()
@@ -45,7 +48,7 @@ for shp in sys.argv[1:] or ["8192x22016", "8192x8192"]:
     rel = lambda v: (v - t0) / 1e3  # noqa: E731
     print(f"== {shp}: event {e0.elapsed_time(e1) * 1e3:.1f} us; prep {rel(ps):.1f}..{rel(pe):.1f} us")
     names = ["entry", "prologue_done", "first_stage", "loop_end", "exit", "wait_full_us", "producer_done"]
-    names = list(enumerate(names)) + [(10, "init_synced"), (8, "table_built"), (9, "prep_waited"), (11, "ticket_done")]
+    names = list(enumerate(names)) + [(10, "init_synced"), (8, "table_built"), (13, "maxima_reduced"), (11, "ticket_done")]
     for i, nm in names:
         v = t[:, i] / 1e3 if nm == "wait_full_us" else rel(t[:, i])
         print(f"  {nm:14s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f}")

@@ -545,15 +545,16 @@ __device__ __noinline__ void finalize_strip(int64_t strip, int f, int l, int64_t
   if (col < N) {  // N % 64 == 0: 4-column groups are all-in or all-out
     float o[4] = {0.f, 0.f, 0.f, 0.f};
     const float* pp = part + (int64_t)(f + strip) * STRIP + c;
-    // 8 predicated loads in flight, then the adds in CTA order (a runtime
-    // trip-count loop would run its < 16 remainder one L2 round trip at a time)
-    for (int i0 = f; i0 <= l; i0 += 8, pp += 8 * STRIP) {
-      float4 v[8];
+    // 16 predicated loads in flight, then the adds in CTA order (a runtime
+    // trip-count loop would run its remainder one L2 round trip at a time,
+    // ~1-3 us each while other CTAs still stream)
+    for (int i0 = f; i0 <= l; i0 += 16, pp += 16 * STRIP) {
+      float4 v[16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < 16; ++j)
         v[j] = i0 + j <= l ? __ldcg(reinterpret_cast<const float4*>(pp + j * STRIP)) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < 16; ++j)
         if (i0 + j <= l) {
           o[0] += v[j].x; o[1] += v[j].y; o[2] += v[j].z; o[3] += v[j].w;
         }
@@ -704,6 +705,25 @@ __global__ void __launch_bounds__(TPB, 1)
     return;
   }
 
+  // ---- this CTA's scale inputs (x, c1 of its rows; see below), loaded first
+  // so their latency overlaps the table build
+  const int64_t nrows_cta = (int64_t)nunits * ROWS;
+  auto scale_item = [&](int64_t i, unsigned& xv, unsigned& c0, unsigned& c1v) {
+    const int64_t uu = ub + i / ROWS, st = uu / chunks;
+    const int64_t r = (uu - st * chunks) * ROWS + i % ROWS;
+    const int64_t ic = (r * nbr + st * 32) >> bs2_shift;
+    xv = (unsigned)__ldg(x + r) & 0x7FFFu;
+    c0 = ic < n2 ? __float_as_uint(__ldg(c1 + ic)) & 0x7FFFFFFFu : 0u;
+    c1v = ic + 1 < n2 ? __float_as_uint(__ldg(c1 + ic + 1)) & 0x7FFFFFFFu : 0u;
+  };
+  constexpr int SCALE_IT = 2;
+  unsigned sx[SCALE_IT], s0[SCALE_IT], s1[SCALE_IT];
+#pragma unroll
+  for (int it = 0; it < SCALE_IT; ++it) {
+    sx[it] = s0[it] = s1[it] = 0u;
+    if (tid + (int64_t)it * CTHREADS < nrows_cta) scale_item(tid + (int64_t)it * CTHREADS, sx[it], s0[it], s1[it]);
+  }
+
   // ---- table: entry e = {fp16 v(e & 15), fp16 v(e >> 4)} in every lane's column
   for (int q = tid; q < 256 * 32; q += CTHREADS) {
     const int e = q >> 5, l = q & 31;
@@ -724,18 +744,18 @@ __global__ void __launch_bounds__(TPB, 1)
   const double mu_d = (double)mu_f;
   {
     unsigned mx = 0u, mc = 0u;
-    for (int64_t i = tid; i < (int64_t)nunits * ROWS; i += CTHREADS) {
-      const int64_t uu = ub + i / ROWS, st = uu / chunks;
-      const int64_t r = (uu - st * chunks) * ROWS + i % ROWS;
-      const unsigned xv = (unsigned)__ldg(x + r) & 0x7FFFu;
-      mx = xv > mx ? xv : mx;
-      const int64_t ic = (r * nbr + st * 32) >> bs2_shift;
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
-        if (ic + e < n2) {
-          const unsigned cv = __float_as_uint(__ldg(c1 + ic + e)) & 0x7FFFFFFFu;
-          mc = cv > mc ? cv : mc;
-        }
+    for (int it = 0; it < SCALE_IT; ++it) {
+      mx = sx[it] > mx ? sx[it] : mx;
+      mc = s0[it] > mc ? s0[it] : mc;
+      mc = s1[it] > mc ? s1[it] : mc;
+    }
+    for (int64_t i = tid + (int64_t)SCALE_IT * CTHREADS; i < nrows_cta; i += CTHREADS) {
+      unsigned xv, c0, c1v;
+      scale_item(i, xv, c0, c1v);
+      mx = xv > mx ? xv : mx;
+      mc = c0 > mc ? c0 : mc;
+      mc = c1v > mc ? c1v : mc;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {

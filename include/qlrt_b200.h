@@ -222,7 +222,7 @@ qlrt_status qlrt_nf4_linear_group_bwd(const qlrt_nf4_weight* w, int groups, cons
 /* batch-1 GEMV variant of forward (M = 1), HBM-bound on the packed codes:
  *   y[N] = x[K] W + s (xa l1) l2         fp32 accumulate, bf16 out
  * (xa = the dropout-masked adapter input, NULL -> x; qlora.py:137-146).
- * N % 256 == 0, K % 16 == 0 (the LLaMA shapes): tensor-core GEMV, W enters
+ * N % 256 == 0, K % 32 == 0 (the LLaMA shapes): tensor-core GEMV, W enters
  * as fp16(v) * c (the reference's float32 W to ~2^-12); other shapes: W
  * decodes as bf16(f32(v) * c) (as the fused GEMM).  Split-K partials are
  * summed in a fixed order (deterministic).  Needs N % 64 == 0, a

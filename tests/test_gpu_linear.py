@@ -182,7 +182,8 @@ def test_fresh_adapter_is_exact_noop(qb, cuda):
     assert torch.equal(plain.forward(x)[0], adapted.forward(x)[0])
 
 
-@pytest.mark.parametrize("k,n", [(8192, 8192), (4096, 11008), (1000, 22016), (64, 192), (8, 64), (296, 4160)])
+@pytest.mark.parametrize("k,n", [(8192, 8192), (4096, 11008), (1000, 22016), (64, 192), (8, 64), (296, 4160),
+                                 (4112, 512)])
 @pytest.mark.parametrize("mma", [1, 0])
 def test_gemv_batch1(k, n, mma, oracle, qb, cuda):
     """Batch-1 GEMV vs the fp64 oracle.  The tensor-core GEMV (default,
@@ -194,7 +195,7 @@ def test_gemv_batch1(k, n, mma, oracle, qb, cuda):
     w = (0.02 * rng.standard_normal((k, n))).astype(np.float32)
     q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)
     w32 = qb.dequantize(q, torch.float32).cpu().numpy()
-    tc = mma and k % 16 == 0 and n % 256 == 0  # shapes the tensor-core GEMV takes
+    tc = mma and k % 32 == 0 and n % 256 == 0  # shapes the tensor-core GEMV takes (32-row stages)
     wd = (w32 if tc else bf16_round(w32)).astype(np.float64)
     x = bf16_round(rng.standard_normal((1, k)))
     r = 64

@@ -79,7 +79,20 @@ def main():
         nb = n // 64
         by = 4 * n + n // 2 + nb + 4 * (nb // 256) + 4
         t = timed([lambda: quantize_async(x, cb, 64, double_quant=True)])
-        res["quantize_dq_f32_4096x4096"] = {"bytes": by, "single_us": t * 1e3, "single_gbs": by / t / 1e6}
+        xs = [torch.randn(4096, 4096, device="cuda") for _ in range(4)]
+        ts = timed([(lambda xx: (lambda: quantize_async(xx, cb, 64, double_quant=True)))(xx) for xx in xs]) / 4
+        # phase A alone (codes + absmax), through the C ABI
+        from paper_2305_14314_b200._native import F32, lib, ptr, stream_ptr
+        codes = torch.empty(n // 2, dtype=torch.uint8, device="cuda")
+        am = torch.empty(nb, dtype=torch.float32, device="cuda")
+        fb = torch.empty(1, dtype=torch.int64, device="cuda")
+        cbc = cb.to_c()
+        ta = timed([(lambda xx: (lambda: lib().qlrt_quantize4(ptr(xx), F32, n, 64, cbc, ptr(codes), ptr(am), ptr(fb),
+                                                              stream_ptr())))(xx) for xx in xs]) / 4
+        by_a = 4 * n + n // 2 + 4 * nb
+        res["quantize_dq_f32_4096x4096"] = {"bytes": by, "single_us": t * 1e3, "single_gbs": by / t / 1e6,
+                                            "stream_us": ts * 1e3, "stream_gbs": by / ts / 1e6,
+                                            "phase_a_stream_us": ta * 1e3, "phase_a_gbs": by_a / ta / 1e6}
     if "gemv" in only:
         for k, nn in ((8192, 8192), (8192, 22016), (22016, 8192)):
             w = torch.randn(k, nn, device="cuda") * 0.02

@@ -233,6 +233,26 @@ def test_gemv_magnitudes(xs, ws, qb, cuda):
     assert_tol(y.float().cpu().numpy(), bf16_round(x.astype(np.float64) @ wd), f"gemv x*{xs} w*{ws}")
 
 
+def test_gemv_per_cta_scales(qb, cuda):
+    """Each GEMV CTA picks its fp16 operand scale from its own rows: rows of
+    x spanning 12 orders of magnitude (the CTAs' scales differ by ~2^40) still
+    sum to the fp64 result within tolerance, deterministically."""
+    rng = np.random.default_rng(5)
+    k, n = 8192, 4096
+    w = (0.02 * rng.standard_normal((k, n))).astype(np.float32)
+    q = qb.quantize(w, qb.get_codebook("nf4"), 64, double_quant=True)
+    wd = qb.dequantize(q, torch.float32).cpu().numpy().astype(np.float64)
+    x = rng.standard_normal((1, k))
+    x[0, : k // 4] *= 1e6
+    x[0, k // 4: k // 2] *= 1e-6
+    x = bf16_round(x)
+    lin = qb.QLinear(q, [])
+    y = lin.forward(torch.from_numpy(x))[0]
+    assert torch.isfinite(y.float()).all()
+    assert_tol(y.float().cpu().numpy(), bf16_round(x.astype(np.float64) @ wd), "gemv per-CTA scales")
+    assert torch.equal(y, lin.forward(torch.from_numpy(x))[0])
+
+
 def test_unfused_shape_path(oracle, qb, cuda):
     """out_dim % 64 != 0 / non-DQ bases route through dequantize + engine GEMMs."""
     rng = np.random.default_rng(5)

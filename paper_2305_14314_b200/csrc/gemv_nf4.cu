@@ -419,6 +419,10 @@ __global__ void __launch_bounds__(256) prep_kernel(int64_t K, const __nv_bfloat1
                                                   const __nv_bfloat16* __restrict__ l1, int rank,
                                                   float* __restrict__ tpart, unsigned* __restrict__ counters,
                                                   int strips) {
+  // launched programmatically behind whatever precedes it (its launch overlaps
+  // that grid's tail): wait for it, and only then release the main grid, so
+  // the main grid still starts after all prior work completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifdef QLRT_GEMV_TL
   if (threadIdx.x == 0) atomicMin(&g_gemv_tl_prep[0], gtimer());
@@ -725,10 +729,12 @@ __global__ void __launch_bounds__(TPB, 1)
   }
 
   // ---- table: entry e = {fp16 v(e & 15), fp16 v(e >> 4)} in every lane's column
-  for (int q = tid; q < 256 * 32; q += CTHREADS) {
-    const int e = q >> 5, l = q & 31;
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(tab + (uint32_t)e * 256u + (uint32_t)l * 4u),
-                 "r"(v16[e & 15] | (v16[e >> 4] << 16)));
+  // (16-byte stores: 4 lanes' copies at a time)
+  for (int q = tid; q < 256 * 8; q += CTHREADS) {
+    const int e = q >> 3, l4 = q & 7;
+    const uint32_t ev = v16[e & 15] | (v16[e >> 4] << 16);
+    asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(tab + (uint32_t)e * 256u + (uint32_t)l4 * 16u),
+                 "r"(ev));
   }
 
 #ifdef QLRT_GEMV_TL
@@ -1056,9 +1062,20 @@ qlrt_status qlrt_nf4_gemv(const qlrt_nf4_weight* w, const void* x, const void* x
     const int zt = (int)cdiv(K, 128);
     const double maxdec = fp8_max_value(w->spec.exp_bits, w->spec.mant_bits, w->spec.bias);
     const int64_t n2 = cdiv(K * (N / 64), (int64_t)w->blocksize2);
-    gemv2::prep_kernel<<<1 + (rank > 0 ? zt : 0), 256, 0, st>>>(
-        K, (const __nv_bfloat16*)(xa ? xa : x), (const __nv_bfloat16*)l1, rank, tpart, counters, (int)g.strips);
-    QLRT_CHECK_LAUNCH();
+    {
+      cudaLaunchConfig_t pc{};
+      pc.gridDim = dim3((unsigned)(1 + (rank > 0 ? zt : 0)));
+      pc.blockDim = dim3(256);
+      pc.stream = st;
+      cudaLaunchAttribute pa[1];
+      pa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      pa[0].val.programmaticStreamSerializationAllowed = 1;
+      pc.attrs = pa;
+      pc.numAttrs = policy(P_PDL) ? 1 : 0;
+      if (cudaLaunchKernelEx(&pc, gemv2::prep_kernel, K, (const __nv_bfloat16*)(xa ? xa : x),
+                             (const __nv_bfloat16*)l1, rank, tpart, counters, (int)g.strips) != cudaSuccess)
+        return QLRT_ERR_CUDA;
+    }
     static std::atomic<unsigned long long> attr_mask{0};
     if (!(attr_mask.load() & (1ull << (dev & 63)))) {
       if (cudaFuncSetAttribute(gemv2::gemv_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv2::SMEM) !=

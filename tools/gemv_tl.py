@@ -43,8 +43,9 @@ for shp in [a for a in sys.argv[1:] if not a.startswith("--")] or ["8192x22016",
         torch.cuda.synchronize()
         fetch()
     t = buf[:SMS * 16].reshape(SMS, 16).astype(np.int64)
+    t = t[t[:, 0] > 0]  # CTAs of this launch (smaller grids leave rows unused)
     ps, pe = int(buf[SMS * 16]), int(buf[SMS * 16 + 1])
-    t0 = min(t[:, 0].min(), ps)
+    t0 = min(t[:, 0].min(), ps) if ps > 0 else t[:, 0].min()
     rel = lambda v: (v - t0) / 1e3  # noqa: E731
     print(f"== {shp}: event {e0.elapsed_time(e1) * 1e3:.1f} us; prep {rel(ps):.1f}..{rel(pe):.1f} us")
     names = ["entry", "prologue_done", "first_stage", "loop_end", "exit", "wait_full_us", "producer_done"]

@@ -1327,6 +1327,22 @@ static SideCtx* side_ctx(cudaStream_t caller) {
   g_side[g_side_n] = c;
   return &g_side[g_side_n++];
 }
+static bool is_side_stream(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  for (int i = 0; i < g_side_n; ++i)
+    if (g_side[i].side == s) return true;
+  return false;
+}
+// critical-path launches (the caller's stream) ahead of the side stream's
+static void add_priority(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attrs, cudaStream_t s) {
+  const int pr = policy(P_PRIO);  // 1: the caller's stream first, 2: the side stream first
+  if (!pr || is_side_stream(s) != (pr == 2)) return;
+  cudaLaunchAttribute& at = attrs[cfg.numAttrs];
+  at.id = cudaLaunchAttributePriority;
+  at.val.priority = high_priority();
+  cfg.attrs = attrs;
+  cfg.numAttrs += 1;
+}
 // fork: the side stream waits for everything issued on `st` so far
 static cudaStream_t fork_side(SideCtx* c, cudaStream_t st) {
   if (!c || cudaEventRecord(c->ev[0], st) != cudaSuccess || cudaStreamWaitEvent(c->side, c->ev[0], 0) != cudaSuccess)
@@ -1425,7 +1441,7 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
   cfg.blockDim = dim3(NF4 ? kNF4Threads : kPlainThreads);
   cfg.dynamicSmemBytes = L::BYTES;
   cfg.stream = s;
-  cudaLaunchAttribute attrs[2];
+  cudaLaunchAttribute attrs[3];
   if (!PAIR && !NF4 && args.csplit > 1) {  // one CTA per (tile, split), clusters of csplit
     cfg.gridDim = dim3(m_tiles * n_tiles * args.csplit);
     attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -1470,6 +1486,7 @@ static qlrt_status launch_t(const CUtensorMap& a, const CUtensorMap& b, const CU
     cfg.attrs = attrs;
     cfg.numAttrs += 1;
   }
+  add_priority(cfg, attrs, s);
   if (cudaLaunchKernelEx(&cfg, kern, a, b, a2, b2, c, k, o, args) != cudaSuccess) return QLRT_ERR_CUDA;
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;
@@ -1602,13 +1619,14 @@ static qlrt_status reduce(const Args& args, cudaStream_t s) {
   cfg.gridDim = dim3((unsigned)g);
   cfg.blockDim = dim3(256);
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   if (pdl_policy()) {  // launched early behind the split-K GEMM (see Args::pdl_trigger)
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
   }
+  add_priority(cfg, at, s);
   if (cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, (const float*)args.ws, args.splits, args.M, args.N, args.fold,
                          args.alpha, args.out, args.ldo, args.out_f32, args.out_t, args.out_split) != cudaSuccess)
     return QLRT_ERR_CUDA;

@@ -343,11 +343,16 @@ static qlrt_status launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaSt
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = policy(P_PDL) ? 1 : 0;
+  if (policy(P_PRIO) == 1) {  // (the step's critical path: ahead of side-stream work)
+    at[cfg.numAttrs].id = cudaLaunchAttributePriority;
+    at[cfg.numAttrs].val.priority = high_priority();
+    cfg.numAttrs += 1;
+  }
   if (cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...) != cudaSuccess) return QLRT_ERR_CUDA;
   QLRT_CHECK_LAUNCH();
   return QLRT_OK;

@@ -30,7 +30,7 @@ constexpr int kNumSMs = 148;
 enum Policy {
   P_PAIR, P_SIDE, P_TILE512, P_STAGGER, P_TMAOUT, P_HALFTAIL, P_PDL, P_SHARE, P_STREAMK, P_OVERLAP,
   P_OVERLAP_SMS, P_PDL_TRIGGER, P_STREAMK_SKINNY, P_CSPLIT, P_OVERLAP_BWD, P_GEMV_WL, P_DQB_CTAS_PER_SM,
-  P_GEMV_MMA, P_DIAG_SKIP, P_CL2, P_SIDE_SMS, P_SKINNY_CTAS, P_GEMV_MIN_UNITS, P_SK512, P_COUNT
+  P_GEMV_MMA, P_DIAG_SKIP, P_CL2, P_SIDE_SMS, P_SKINNY_CTAS, P_GEMV_MIN_UNITS, P_SK512, P_PRIO, P_COUNT
 };
 struct PolicyDef {
   const char* env;
@@ -42,7 +42,11 @@ inline const PolicyDef kPolicies[P_COUNT] = {
     {"QLRT_STREAMK", 1},       {"QLRT_OVERLAP", 1},        {"QLRT_OVERLAP_SMS", 8}, {"QLRT_PDL_TRIGGER", 1},
     {"QLRT_STREAMK_SKINNY", 0}, {"QLRT_CSPLIT", 0},        {"QLRT_OVERLAP_BWD", 0}, {"QLRT_GEMV_WL", -1},
     {"QLRT_DQB_CTAS_PER_SM", -1}, {"QLRT_GEMV_MMA", 1},
-    {"QLRT_DIAG_SKIP", 0},     {"QLRT_CL2", 0},          {"QLRT_SIDE_SMS", 0},     {"QLRT_SKINNY_CTAS", 148}, {"QLRT_GEMV_MIN_UNITS", 8}, {"QLRT_SK512", 0}};  // measurement only: 1 skips dl2/dl1, 2 skips dT (wrong results)
+    // QLRT_DIAG_SKIP is measurement only: 1 skips dl2/dl1, 2 skips dT (wrong results)
+    {"QLRT_DIAG_SKIP", 0},     {"QLRT_CL2", 0},          {"QLRT_SIDE_SMS", 0},     {"QLRT_SKINNY_CTAS", 148}, {"QLRT_GEMV_MIN_UNITS", 8}, {"QLRT_SK512", 0},
+    // QLRT_PRIO (measured, off): 1 launches the caller's stream at the
+    // device's greatest priority, 2 the side stream (C3: -2.5% / neutral)
+    {"QLRT_PRIO", 0}};
 constexpr int kPolicyUnset = -0x7fffffff;
 inline std::atomic<int> g_policy[P_COUNT];
 inline std::atomic<bool> g_policy_init{false};
@@ -60,6 +64,18 @@ inline int policy(Policy p) {
 }
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// greatest launch priority of the current device (numerically lowest)
+inline int high_priority() {
+  static std::atomic<int> cached{1};
+  int p = cached.load(std::memory_order_relaxed);
+  if (p == 1) {
+    int lo = 0, hi = 0;
+    p = cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess ? hi : 0;
+    cached.store(p, std::memory_order_relaxed);
+  }
+  return p;
+}
 
 // ---- 8-bit float of the double quantizer (doublequant.py:33-121) ----------
 // decode: exact dyadic value of every byte (no NaN/Inf; 0x80 is -0.0)

@@ -14,7 +14,13 @@ dy = torch.randn(m, n, device="cuda").bfloat16()
 l1 = (torch.randn(k, r, device="cuda") / 8).bfloat16()
 l2 = (torch.randn(r, n, device="cuda") * .01).bfloat16()
 ts = torch.randn(m, 2 * r, device="cuda").bfloat16()
+dy_gu = torch.randn(m, 2 * n, device="cuda").bfloat16()
+l2_gu = (torch.randn(2 * r, 2 * n, device="cuda") * .01).bfloat16()
+dy_o = torch.randn(m, k, device="cuda").bfloat16()
+l2_o = (torch.randn(r, k, device="cuda") * .01).bfloat16()
 cases = {
+    "dT gu = dY l2^T (2048x128x22016)": lambda: qb.gemm_bf16(dy_gu, l2_gu, b_t=True, out_dtype=torch.float32),
+    "dT o  = dY l2^T (2048x64x4096)": lambda: qb.gemm_bf16(dy_o, l2_o, b_t=True, out_dtype=torch.float32),
     "Ts = X l1      (2048x64x4096)": lambda: qb.gemm_bf16(x, l1, out_dtype=torch.float32),
     "dT = dY l2^T   (2048x64x11008)": lambda: qb.gemm_bf16(dy, l2, b_t=True, out_dtype=torch.float32),
     "dl2^T = dY^T Ts (11008x128x2048)": lambda: qb.gemm_bf16(dy, ts, a_t=True, out_dtype=torch.float32),

@@ -183,7 +183,7 @@ def test_fresh_adapter_is_exact_noop(qb, cuda):
 
 
 @pytest.mark.parametrize("k,n", [(8192, 8192), (4096, 11008), (1000, 22016), (64, 192), (8, 64), (296, 4160),
-                                 (4112, 512)])
+                                 (4112, 512), (32, 256), (96, 2304)])
 @pytest.mark.parametrize("mma", [1, 0])
 def test_gemv_batch1(k, n, mma, oracle, qb, cuda):
     """Batch-1 GEMV vs the fp64 oracle.  The tensor-core GEMV (default,

@@ -277,6 +277,39 @@ def test_unfused_shape_path(oracle, qb, cuda):
     assert_tol(gr["adapter0.l1"].cpu().numpy(), grr["adapter0.l1"], "dl1")
 
 
+@pytest.mark.parametrize("tmaout", [0, 2])
+@pytest.mark.parametrize("m,k,n", [(1024, 4096, 4160), (600, 2048, 1536)])
+def test_epilogue_store_paths_identical(tmaout, m, k, n, qb, cuda):
+    """The fused GEMM's bf16 D^T epilogues -- TMA stores from the stmatrix
+    staging tile (default), 16-byte stores from the same tile (QLRT_TMAOUT=0)
+    and direct per-row stores (=2) -- write bit-identical Y and dX, including
+    partial feature and token tiles."""
+    from paper_2305_14314_b200._native import get_policy, set_policy
+    g = torch.Generator(device="cuda").manual_seed(6)
+    q = qb.quantize(torch.randn(k, n, device="cuda", generator=g) * 0.02, qb.get_codebook("nf4"), 64,
+                    double_quant=True)
+    x = torch.randn(m, k, device="cuda", generator=g).bfloat16()
+    dy = torch.randn(m, n, device="cuda", generator=g).bfloat16()
+    ad = qb.LoraAdapter(64, 16.0, (torch.randn(k, 64, device="cuda", generator=g) / 8).bfloat16().float(),
+                        (torch.randn(64, n, device="cuda", generator=g) * 0.01).bfloat16().float())
+    lin = qb.QLinear(q, [ad])
+
+    def run():
+        y, c = lin.forward(x)
+        dx, _ = lin.backward(dy, c)
+        return y.clone(), dx.clone()
+
+    y0, dx0 = run()
+    old = get_policy("QLRT_TMAOUT")
+    set_policy("QLRT_TMAOUT", tmaout)
+    try:
+        y1, dx1 = run()
+    finally:
+        set_policy("QLRT_TMAOUT", old)
+    assert torch.equal(y0, y1)
+    assert torch.equal(dx0, dx1)
+
+
 @pytest.mark.parametrize("env", [{"QLRT_OVERLAP": "0"}, {"QLRT_OVERLAP_BWD": "1"}])
 def test_overlap_modes_match_default(env, qb, cuda):
     """The PDL-chained adapter products (forward default; backward behind

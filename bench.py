@@ -216,7 +216,8 @@ def run_reference(args, rank: int) -> None:
     layers = _cpu_c3_layers(ref)
     last: dict = {}
     vals = []
-    n_steps = args.warmup + args.steps
+    # at least one full cycle of the 7 shapes: the extrapolation needs every one
+    n_steps = max(args.warmup + args.steps, len(layers))
     for i in range(n_steps):
         name, k, n, lin, x, dy = layers[i % len(layers)]
         t0 = time.perf_counter()

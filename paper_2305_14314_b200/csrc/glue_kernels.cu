@@ -138,9 +138,9 @@ __global__ void swiglu_fwd_kernel(const uint4* __restrict__ g, const uint4* __re
                                   int64_t rows, int64_t c8, int64_t ldg, int64_t ldu, int64_t ldo) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // (no early trigger: a fused GEMM launched
   // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
-  const int64_t n8 = rows * c8;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n8; k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = k / c8, c = k - r * c8;
+  // rows on grid y, 16-byte columns on grid x (no 64-bit divisions on the element path)
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < c8; c += (int64_t)gridDim.x * blockDim.x) {
     const uint4 a = g[r * ldg + c], b = u[r * ldu + c];
     const int64_t i = r * ldo + c;
     const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
@@ -160,9 +160,9 @@ __global__ void swiglu_bwd_kernel(const uint4* __restrict__ g, const uint4* __re
                                   int64_t rows, int64_t c8, int64_t ldgu, int64_t ldo) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // (no early trigger: a fused GEMM launched
   // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
-  const int64_t n8 = rows * c8;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n8; k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = k / c8, cc = k - r * c8;
+  // rows on grid y, 16-byte columns on grid x (no 64-bit divisions on the element path)
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+  for (int64_t cc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; cc < c8; cc += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = r * ldgu + cc;  // g, u, dg, du share a pitch
     const uint4 a = g[i], b = u[i], c = dout[r * ldo + cc];
     const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w}, wc[4] = {c.x, c.y, c.z, c.w};
@@ -195,12 +195,12 @@ __global__ void rope_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, 
   asm volatile("griddepcontrol.wait;" ::: "memory");  // (no early trigger: a fused GEMM launched
   // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
   const int d8 = d / 8;
-  const int64_t rw = (int64_t)d8 * heads;
-  const int64_t total = rows * rw;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
-    const int c8 = (int)(k % d8);
-    const int64_t row = k / rw, within = k - row * rw;
-    const int pos = (int)(row % seq);
+  const int rw = d8 * heads;
+  // one CTA per row: the position once, 32-bit column arithmetic
+  const int64_t row = blockIdx.x;
+  const int pos = (int)(row % seq);
+  for (int within = threadIdx.x; within < rw; within += blockDim.x) {
+    const int c8 = within % d8;
     const float2* t = cs + (int64_t)pos * (d / 2) + c8 * 4;  // 4 pairs per 16 B
     const int64_t i = row * ldy + within;
     const uint4 a = x[row * ldx + within];
@@ -227,15 +227,17 @@ __global__ void rope_qkv_kernel(const uint4* __restrict__ a, const uint4* __rest
   // behind us would park its 1-CTA-per-SM grid on the SMs we still need)
   // FWD: a = ycat (rows x 3 h8), x / y / z = q / k / v;  BWD: a / b / c = dq / dk / dv, x = dycat
   const int d8 = d / 8;
-  const int64_t total = rows * 3 * h8;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = k / (3 * h8);
-    const int w = (int)(k - row * 3 * h8), part = w / h8, e = w - part * h8;
+  // one CTA per row: the position once, the q / k / v parts as an outer loop
+  const int64_t row = blockIdx.x;
+  const int pos = (int)(row % seq);
+  for (int part = 0; part < 3; ++part)
+  for (int e = threadIdx.x; e < h8; e += blockDim.x) {
+    const int64_t k = row * 3 * h8 + (int64_t)part * h8 + e;
     uint4 v;
     if (FWD) v = a[k];
     else v = (part == 0 ? a : part == 1 ? b : c)[row * h8 + e];
     if (part < 2) {
-      const int pos = (int)(row % seq), c8 = e % d8;
+      const int c8 = e % d8;
       const float2* t = cs + (int64_t)pos * (d / 2) + c8 * 4;
       const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
       uint32_t o[4];
@@ -358,9 +360,11 @@ static qlrt_status launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaSt
   return QLRT_OK;
 }
 
-static int grid_for(int64_t n, int tpb) {
-  int64_t g = (n + tpb - 1) / tpb;
-  return (int)(g < (int64_t)kNumSMs * 8 ? (g < 1 ? 1 : g) : (int64_t)kNumSMs * 8);
+// (columns, rows) grid of an elementwise row kernel: 256-thread column blocks
+static dim3 grid_rows(int64_t rows, int64_t c8) {
+  const int64_t gx = (c8 + 255) / 256, gy = rows;
+  const int64_t cx = gx < (int64_t)kNumSMs * 8 ? gx : (int64_t)kNumSMs * 8;
+  return dim3((unsigned)(cx < 1 ? 1 : cx), (unsigned)(gy < 65535 ? gy : 65535));
 }
 
 }  // namespace glue
@@ -399,23 +403,22 @@ qlrt_status qlrt_rmsnorm_bwd_add(const void* dy, const void* x, const float* rst
 
 qlrt_status qlrt_swiglu_fwd(const void* g, const void* u, void* out, int64_t n, void* stream) {
   if (!g || !u || !out || n <= 0 || (n % 8)) return QLRT_ERR_ARG;
-  return glue::launch_pdl(glue::swiglu_fwd_kernel, dim3(glue::grid_for(n / 8, 256)), dim3(256), (cudaStream_t)stream,
+  return glue::launch_pdl(glue::swiglu_fwd_kernel, glue::grid_rows(1, n / 8), dim3(256), (cudaStream_t)stream,
                           (const uint4*)g, (const uint4*)u, (uint4*)out, 1, n / 8, 0, 0, 0);
 }
 
 qlrt_status qlrt_swiglu_bwd(const void* g, const void* u, const void* dout, void* dg, void* du, int64_t n,
                             void* stream) {
   if (!g || !u || !dout || !dg || !du || n <= 0 || (n % 8)) return QLRT_ERR_ARG;
-  return glue::launch_pdl(glue::swiglu_bwd_kernel, dim3(glue::grid_for(n / 8, 256)), dim3(256), (cudaStream_t)stream,
+  return glue::launch_pdl(glue::swiglu_bwd_kernel, glue::grid_rows(1, n / 8), dim3(256), (cudaStream_t)stream,
                           (const uint4*)g, (const uint4*)u, (const uint4*)dout, (uint4*)dg, (uint4*)du, 1, n / 8, 0, 0);
 }
 
 qlrt_status qlrt_rope(const void* x, void* y, const void* cos_sin, int64_t rows, int heads, int d, int seq,
                       int inverse, void* stream) {
   if (!x || !y || !cos_sin || rows <= 0 || heads <= 0 || d <= 0 || (d % 8) || seq <= 0) return QLRT_ERR_ARG;
-  const int64_t total = rows * heads * (d / 8);
   const int64_t rw = (int64_t)heads * (d / 8);
-  return glue::launch_pdl(glue::rope_kernel, dim3(glue::grid_for(total, 256)), dim3(256), (cudaStream_t)stream,
+  return glue::launch_pdl(glue::rope_kernel, dim3((unsigned)rows), dim3(256), (cudaStream_t)stream,
                           (const uint4*)x, (uint4*)y, (const float2*)cos_sin, rows, heads, d, seq, inverse ? -1.0f : 1.0f, rw, rw);
 }
 qlrt_status qlrt_rope_strided(const void* x, int64_t ldx, void* y, int64_t ldy, const void* cos_sin, int64_t rows,
@@ -423,8 +426,7 @@ qlrt_status qlrt_rope_strided(const void* x, int64_t ldx, void* y, int64_t ldy, 
   if (!x || !y || !cos_sin || rows <= 0 || heads <= 0 || d <= 0 || (d % 8) || seq <= 0 || (ldx % 8) || (ldy % 8) ||
       ldx < (int64_t)heads * d || ldy < (int64_t)heads * d)
     return QLRT_ERR_ARG;
-  const int64_t total = rows * heads * (d / 8);
-  return glue::launch_pdl(glue::rope_kernel, dim3(glue::grid_for(total, 256)), dim3(256), (cudaStream_t)stream,
+  return glue::launch_pdl(glue::rope_kernel, dim3((unsigned)rows), dim3(256), (cudaStream_t)stream,
                           (const uint4*)x, (uint4*)y, (const float2*)cos_sin, rows, heads, d, seq, inverse ? -1.0f : 1.0f, ldx / 8,
       ldy / 8);
 }
@@ -433,7 +435,7 @@ qlrt_status qlrt_rope_qkv_fwd(const void* ycat, void* q, void* k, void* v, const
   if (!ycat || !q || !k || !v || !cos_sin || rows <= 0 || heads <= 0 || d <= 0 || (d % 8) || seq <= 0)
     return QLRT_ERR_ARG;
   const int h8 = heads * d / 8;
-  return glue::launch_pdl(glue::rope_qkv_kernel<true>, dim3(glue::grid_for(rows * 3 * h8, 256)), dim3(256), (cudaStream_t)stream,
+  return glue::launch_pdl(glue::rope_qkv_kernel<true>, dim3((unsigned)rows), dim3(256), (cudaStream_t)stream,
                           (const uint4*)ycat, nullptr, nullptr, (uint4*)q, (uint4*)k, (uint4*)v, (const float2*)cos_sin, rows, h8, d, seq);
 }
 qlrt_status qlrt_rope_qkv_bwd(const void* dq, const void* dk, const void* dv, void* dycat, const void* cos_sin,
@@ -441,7 +443,7 @@ qlrt_status qlrt_rope_qkv_bwd(const void* dq, const void* dk, const void* dv, vo
   if (!dq || !dk || !dv || !dycat || !cos_sin || rows <= 0 || heads <= 0 || d <= 0 || (d % 8) || seq <= 0)
     return QLRT_ERR_ARG;
   const int h8 = heads * d / 8;
-  return glue::launch_pdl(glue::rope_qkv_kernel<false>, dim3(glue::grid_for(rows * 3 * h8, 256)), dim3(256), (cudaStream_t)stream,
+  return glue::launch_pdl(glue::rope_qkv_kernel<false>, dim3((unsigned)rows), dim3(256), (cudaStream_t)stream,
                           (const uint4*)dq, (const uint4*)dk, (const uint4*)dv, (uint4*)dycat, nullptr, nullptr, (const float2*)cos_sin,
       rows, h8, d, seq);
 }
@@ -462,7 +464,7 @@ qlrt_status qlrt_xent_bwd(const void* logits, const int64_t* targets, const floa
 qlrt_status qlrt_swiglu_cat_fwd(const void* gu, void* out, int64_t rows, int64_t cols, void* stream) {
   if (!gu || !out || rows <= 0 || cols <= 0 || (cols % 8)) return QLRT_ERR_ARG;
   const int64_t c8 = cols / 8;
-  return glue::launch_pdl(glue::swiglu_fwd_kernel, dim3(glue::grid_for(rows * c8, 256)), dim3(256), (cudaStream_t)stream,
+  return glue::launch_pdl(glue::swiglu_fwd_kernel, glue::grid_rows(rows, c8), dim3(256), (cudaStream_t)stream,
                           (const uint4*)gu, (const uint4*)gu + c8, (uint4*)out, rows, c8, 2 * c8, 2 * c8, c8);
 }
 // d[g | u] rows from dout[rows][cols] and the saved [g | u]
@@ -470,7 +472,7 @@ qlrt_status qlrt_swiglu_cat_bwd(const void* gu, const void* dout, void* dgu, int
                                 void* stream) {
   if (!gu || !dout || !dgu || rows <= 0 || cols <= 0 || (cols % 8)) return QLRT_ERR_ARG;
   const int64_t c8 = cols / 8;
-  return glue::launch_pdl(glue::swiglu_bwd_kernel, dim3(glue::grid_for(rows * c8, 256)), dim3(256), (cudaStream_t)stream,
+  return glue::launch_pdl(glue::swiglu_bwd_kernel, glue::grid_rows(rows, c8), dim3(256), (cudaStream_t)stream,
                           (const uint4*)gu, (const uint4*)gu + c8, (const uint4*)dout, (uint4*)dgu, (uint4*)dgu + c8, rows, c8, 2 * c8,
       c8);
 }

@@ -264,7 +264,7 @@ qlrt_status qlrt_adam_step_dev(float* p, const float* g, float* m, float* v, int
                                const float* hyper, const double* sumsq, double max_norm,
                                void* p_bf16, void* stream);
 
-/* sum of squares in fp64 of n floats, accumulated into acc[0] (device).
+/* sum of squares in fp64 of n floats (4-byte aligned), accumulated into acc[0] (device).
  * acc must have QLRT_SUMSQ_SCRATCH bytes: acc[0] result, then scratch. */
 #define QLRT_SUMSQ_SCRATCH (8 + 8 * 296 + 8)
 qlrt_status qlrt_sumsq_f64(const float* g, int64_t n, double* acc, void* stream);

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) adam_dev_kernel(float* __restrict__ p, co
   }
 }
 
-// fp64 sum of squares: per-thread sequential over a grid-stride range, then
+// fp64 sum of squares: per-thread chains over a grid-stride range, then
 // a fixed-shape tree per CTA and a fixed-order add of CTA partials by the
 // last CTA (deterministic for a given n and grid).
 __global__ void __launch_bounds__(256) sumsq_kernel(const float* __restrict__ g, int64_t n,
@@ -118,12 +118,35 @@ __global__ void __launch_bounds__(256) sumsq_kernel(const float* __restrict__ g,
                                                     double* __restrict__ acc) {
   __shared__ double red[256];
   __shared__ bool last;
-  double s = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double d = (double)g[i];
-    s = __dadd_rn(s, __dmul_rn(d, d));
+  // 16-byte loads, 8 in flight per thread, four independent fp64 chains
+  // (x, y, z, w lanes of the float4s); the scalar tail goes to thread 0 of
+  // CTA 0 -- a fixed order for a given n and grid
+  // (a head of < 4 floats up to the first 16-byte boundary joins the tail)
+  int64_t h = (int64_t)(((16u - (uint32_t)((uintptr_t)g & 15u)) & 15u) >> 2);
+  h = h < n ? h : n;
+  const float4* g4 = reinterpret_cast<const float4*>(g + h);
+  const int64_t n4 = (n - h) >> 2, stride = (int64_t)gridDim.x * blockDim.x;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  auto add4 = [&](const float4 v) {
+    s0 = __dadd_rn(s0, __dmul_rn((double)v.x, (double)v.x));
+    s1 = __dadd_rn(s1, __dmul_rn((double)v.y, (double)v.y));
+    s2 = __dadd_rn(s2, __dmul_rn((double)v.z, (double)v.z));
+    s3 = __dadd_rn(s3, __dmul_rn((double)v.w, (double)v.w));
+  };
+  for (; j + 7 * stride < n4; j += 8 * stride) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(g4 + j + u * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) add4(v[u]);
   }
-  red[threadIdx.x] = s;
+  for (; j < n4; j += stride) add4(__ldg(g4 + j));
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int64_t i = 0; i < h; ++i) s0 = __dadd_rn(s0, __dmul_rn((double)g[i], (double)g[i]));
+    for (int64_t i = h + n4 * 4; i < n; ++i) s0 = __dadd_rn(s0, __dmul_rn((double)g[i], (double)g[i]));
+  }
+  red[threadIdx.x] = __dadd_rn(__dadd_rn(s0, s1), __dadd_rn(s2, s3));
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {
     if (threadIdx.x < w) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + w]);
@@ -229,7 +252,7 @@ qlrt_status qlrt_adam_step_dev(float* p, const float* g, float* m, float* v, int
 // acc must point to a device double; the scratch (partials + counter) lives
 // right after it: caller passes a buffer of >= 8 + 8*148*2 + 8 bytes.
 qlrt_status qlrt_sumsq_f64(const float* g, int64_t n, double* acc, void* stream) {
-  if (!g || !acc || n <= 0) return QLRT_ERR_ARG;
+  if (!g || !acc || n <= 0 || (((uintptr_t)g) & 3)) return QLRT_ERR_ARG;
   int64_t blocks = (n + 255) / 256;
   if (blocks > 296) blocks = 296;
   double* partials = acc + 1;

@@ -95,3 +95,17 @@ def test_clip_norm_in_numpy_pairwise_order(shape, qb, cuda):
     scale = np.float32(0.3 / norm)
     for k in gs:
         assert np.array_equal(dev[k].cpu().numpy(), gs[k] * scale)
+
+
+@pytest.mark.parametrize("n,off", [(1, 0), (7, 1), (4096, 0), (1_000_003, 3), (40_000_000, 2)])
+def test_fixed_order_sumsq(n, off, qb, cuda):
+    """qlrt_sumsq_f64 (the harness's clip norm): fp64 sum of squares of a
+    float32 vector, also from an unaligned start; deterministic run to run."""
+    from paper_2305_14314_b200.training import global_sumsq
+    g = torch.Generator(device="cuda").manual_seed(n)
+    base = torch.randn(n + off, device="cuda", generator=g)
+    v = base[off:]
+    got = float(global_sumsq({"v": v}, ["v"]).item())
+    want = float((v.double() ** 2).sum().item())
+    assert got == pytest.approx(want, rel=1e-12)
+    assert got == float(global_sumsq({"v": v}, ["v"]).item())

@@ -673,6 +673,25 @@ __global__ void __launch_bounds__(256) dq_encode_warp_kernel(const float* __rest
                                                              float* __restrict__ c1, uint8_t* __restrict__ codes) {
   __shared__ double cs[512];
   __shared__ float s_mu;
+  // The first block's constants go to registers before the wait: this grid
+  // starts only after the chunk-sum grid passed its own wait (its trigger
+  // follows it), i.e. after the producer of c completed -- only the chunk
+  // sums need the wait.  Saves a dependent round trip and the second read.
+  constexpr int PRE = 8;  // blocksize2 <= 256
+  const int lane = threadIdx.x & 31;
+  const int64_t n2 = (nb + bs2 - 1) / bs2;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t blk_first = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const bool pre = bs2 <= 32 * PRE && blk_first < n2;
+  float pv[PRE];
+#pragma unroll
+  for (int k = 0; k < PRE; ++k) pv[k] = 0.0f;
+  if (pre) {
+    const int64_t b0 = blk_first * bs2, b1 = min(b0 + bs2, nb);
+#pragma unroll
+    for (int k = 0; k < PRE; ++k)
+      if (b0 + lane + 32 * k < b1) pv[k] = __ldg(c + b0 + lane + 32 * k);
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   double acc = 0.0;
   for (int b = 0; b < n_chunks; b += 512) {
@@ -691,26 +710,42 @@ __global__ void __launch_bounds__(256) dq_encode_warp_kernel(const float* __rest
   __syncthreads();
   const double mu = (double)s_mu;
   const double maxv = fp8_max_value(sp.exp_bits, sp.mant_bits, sp.bias);
-  const int64_t n2 = (nb + bs2 - 1) / bs2;
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t blk = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); blk < n2; blk += warps) {
+  for (int64_t blk = blk_first; blk < n2; blk += warps) {
     const int64_t b0 = blk * bs2;
     const int64_t b1 = min(b0 + bs2, nb);
+    const bool in_regs = pre && blk == blk_first;
     double amax = 0.0;
-    for (int64_t i = b0 + lane; i < b1; i += 32) amax = fmax(amax, fabs(__dsub_rn((double)__ldg(c + i), mu)));
+    if (in_regs) {
+#pragma unroll
+      for (int k = 0; k < PRE; ++k)
+        if (b0 + lane + 32 * k < b1) amax = fmax(amax, fabs(__dsub_rn((double)pv[k], mu)));
+    } else {
+      for (int64_t i = b0 + lane; i < b1; i += 32) amax = fmax(amax, fabs(__dsub_rn((double)__ldg(c + i), mu)));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     float scale = 0.0f;
     if (amax > 0.0) scale = __double2float_rn(__ddiv_rn(amax, maxv));
     if (lane == 0) c1[blk] = scale;  // 0 for flat / underflowing blocks
     const double sd = (double)scale;
-    for (int64_t i = b0 + lane; i < b1; i += 32) {
-      unsigned code = 0u;
-      if (scale != 0.0f)
-        code = fp8_encode(__ddiv_rn(__dsub_rn((double)__ldg(c + i), mu), sd), sp.exp_bits, sp.mant_bits, sp.bias,
-                          maxv);
-      codes[i] = (uint8_t)code;
+    if (in_regs) {
+#pragma unroll
+      for (int k = 0; k < PRE; ++k) {
+        const int64_t i = b0 + lane + 32 * k;
+        if (i >= b1) break;
+        unsigned code = 0u;
+        if (scale != 0.0f)
+          code = fp8_encode(__ddiv_rn(__dsub_rn((double)pv[k], mu), sd), sp.exp_bits, sp.mant_bits, sp.bias, maxv);
+        codes[i] = (uint8_t)code;
+      }
+    } else {
+      for (int64_t i = b0 + lane; i < b1; i += 32) {
+        unsigned code = 0u;
+        if (scale != 0.0f)
+          code = fp8_encode(__ddiv_rn(__dsub_rn((double)__ldg(c + i), mu), sd), sp.exp_bits, sp.mant_bits, sp.bias,
+                            maxv);
+        codes[i] = (uint8_t)code;
+      }
     }
   }
 }
